@@ -1,0 +1,677 @@
+/* pvro.c — fp64 CPU ORACLE for the PVR super-resolution iteration.
+ *
+ * TEST INFRASTRUCTURE ONLY (see pvro.h): loaded by tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs; never by the product.
+ *
+ * Plain, slow, obviously-correct loops in fp64, in the order of SURVEY.md §8(c)
+ * (steps 0-11) and DESIGN.md §Readings. Every function cites the PAPER.md passage
+ * (P:line) it restates. No blocking, no factorisation of the PSF, no reordering:
+ * the forward model is a direct sum over (pixel, PSF sample, trilinear corner).
+ * OpenMP runs patches in parallel; the adjoint accumulates with atomic adds.
+ */
+#include "pvro.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define PVRO_MAX_STACKS 64
+#define PVRO_MAX_PSF 20000
+
+typedef struct {
+  int W, H, K;
+  double* y;          /* [K][H][W] */
+  double G[12];       /* index -> world, row-major 3x4 */
+  double theta;       /* slice thickness (through-plane FWHM) */
+  /* PSF lattice (built at extract time, step 0) */
+  double u[3], v[3], w[3];  /* in-plane unit axes and slice normal */
+  double h[3];              /* lattice steps h_u, h_v, h_w (mm) */
+  int S;
+  int32_t* abc;             /* [S][3] */
+  double* psi;              /* [S] */
+} ostack;
+
+struct pvro_ctx {
+  int n[3];
+  double s, o[3];
+  int n_stacks;
+  ostack st[PVRO_MAX_STACKS];
+  /* patches */
+  int64_t M, P;
+  int32_t* patch;    /* [M][7] stack, x0, y0, z0, sx, sy, sz */
+  int64_t* pix0;     /* [M+1] first pixel of each patch */
+  double* T;         /* [M][12] */
+  int state;         /* 0 created, 1 stacks, 2 patched, 3 ready */
+  /* parameters */
+  double delta, tau_patch, c0, tau_live, tau_C, tau_obs, clamp, psf_mode, s2floor, nsigma;
+  /* iteration state */
+  double* X;         /* [V] */
+  double *p, *e, *kappa, *yhat;  /* [P] */
+  double *pbar, *wpatch;         /* [M] */
+  double *A, *C;                 /* [V] */
+  double sigma2, c, m, lo, hi, s2min;
+  int64_t t;
+};
+
+/* ------------------------------------------------------------------ */
+/* Step 0: Taylor-series sinc: sinc(x) = 1 - x^2/3! + x^4/5! - ...
+ * Reading Q4: cut the series once the next term is below an ABSOLUTE bound 1e-16
+ * (the paper's "relative error" is undefined at the zero x = pi).               */
+double pvro_sinc_taylor(double x) {
+  double term = 1.0, sum = 1.0, x2 = x * x;
+  for (int n = 0; n < 200; ++n) {
+    double next = -term * x2 / ((2.0 * n + 2.0) * (2.0 * n + 3.0));
+    if (fabs(next) < 1e-16) break;
+    sum += next;
+    term = next;
+  }
+  return sum;
+}
+
+static int lattice_count(double pitch, double s) {
+  /* Reading Q5: lattice step <= the HR voxel size, at least 2 steps per pitch. */
+  int n = (int)ceil(pitch / s - 1e-9);
+  return n < 2 ? 2 : n;
+}
+
+/* Step 0: PSF lattice ("sinc function for the in-plane and the slice
+ * profile for the through-plane"). Readings Q1 (radial sinc(pi R)), Q2 (main
+ * lobe R < 1), Q3 (Gaussian slice profile, FWHM = thickness, cut at nsigma),
+ * Q5 (lattice discretisation). psi is normalised to sum 1.                     */
+int pvro_psf_table(double dx, double dy, double theta, double s, double nsigma, int cap,
+                   int32_t* abc, double* psi, double* hw_out) {
+  if (!(dx > 0) || !(dy > 0) || !(theta > 0) || !(s > 0)) return -1;
+  int nu = lattice_count(dx, s), nv = lattice_count(dy, s), nw = lattice_count(theta, s);
+  double hu = dx / nu, hv = dy / nv, hw = theta / nw;
+  double sigw = theta / (2.0 * sqrt(2.0 * log(2.0)));
+  int S = 0;
+  double total = 0.0;
+  for (int c = -1000; c <= 1000; ++c) {
+    if (fabs(c * hw) > nsigma * sigw) continue;
+    for (int b = -nv; b <= nv; ++b) {
+      for (int a = -nu; a <= nu; ++a) {
+        double R = sqrt((double)a * a / ((double)nu * nu) + (double)b * b / ((double)nv * nv));
+        if (!(R < 1.0)) continue;
+        if (S >= cap) return -2;
+        double val = pvro_sinc_taylor(M_PI * R) * exp(-(c * hw) * (c * hw) / (2.0 * sigw * sigw));
+        abc[3 * S + 0] = a;
+        abc[3 * S + 1] = b;
+        abc[3 * S + 2] = c;
+        psi[S] = val;
+        total += val;
+        ++S;
+      }
+    }
+  }
+  for (int q = 0; q < S; ++q) psi[q] /= total;
+  if (hw_out) {
+    hw_out[0] = nu; hw_out[1] = nv; hw_out[2] = nw;
+    hw_out[3] = hu; hw_out[4] = hv; hw_out[5] = hw; hw_out[6] = sigw;
+  }
+  return S;
+}
+
+/* Square patch windows along one axis ("size a and stride omega");
+ * reading Q22: a last window is clamped to the edge so every pixel is covered. */
+int pvro_windows(int dim, int size, int stride, int cap, int32_t* out) {
+  if (size < 1 || size > dim || stride < 1 || stride > size) return -1;
+  int n = 0, x = 0;
+  for (; x + size <= dim; x += stride) {
+    if (n >= cap) return -2;
+    out[n++] = x;
+  }
+  if (out[n - 1] + size < dim) {
+    if (n >= cap) return -2;
+    out[n++] = dim - size;
+  }
+  return n;
+}
+
+/* P:202 p = G c / (G c + m (1 - c)), G = N(e; 0, sigma^2), evaluated in the
+ * algebraically identical logistic form p = 1 / (1 + exp(z)),
+ * z = ln(m (1-c) / c) + e^2 / (2 sigma^2) + 0.5 ln(2 pi sigma^2).              */
+double pvro_posterior(double e, double sigma2, double c, double m) {
+  if (c >= 1.0 || m <= 0.0) return 1.0;
+  if (c <= 0.0) return 0.0;
+  double z = log(m * (1.0 - c) / c) + e * e / (2.0 * sigma2) + 0.5 * log(2.0 * M_PI * sigma2);
+  return 1.0 / (1.0 + exp(z));
+}
+
+/* One M-step + E-step (reading Q10/Q11). */
+int pvro_em_round(int64_t n, const double* e, const uint8_t* live, const double* p_prev,
+                  int64_t t, double c0, double sigma2_min, double* p_out, double* sigma2_out,
+                  double* c_out, double* m_out) {
+  double s_pe2 = 0.0, s_p = 0.0, emax = -INFINITY, emin = INFINITY;
+  int64_t nl = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (!live[j]) continue;
+    s_pe2 += p_prev[j] * e[j] * e[j];
+    s_p += p_prev[j];
+    if (e[j] > emax) emax = e[j];
+    if (e[j] < emin) emin = e[j];
+    ++nl;
+  }
+  double sigma2 = s_p > 0.0 ? s_pe2 / s_p : 0.0;
+  if (sigma2 < sigma2_min) sigma2 = sigma2_min;
+  double c = (t <= 1) ? c0 : (nl > 0 ? s_p / (double)nl : c0);
+  double spread = emax - emin;
+  int degenerate = (nl == 0) || !(spread > sqrt(sigma2_min));
+  double m = degenerate ? 0.0 : 1.0 / spread;  /* P:193 m = 1 / (max(e) - min(e)) */
+  for (int64_t j = 0; j < n; ++j)
+    p_out[j] = degenerate ? 1.0 : pvro_posterior(e[j], sigma2, c, m);
+  if (sigma2_out) *sigma2_out = sigma2;
+  if (c_out) *c_out = c;
+  if (m_out) *m_out = m;
+  return degenerate;
+}
+
+/* P:207 pbar = sqrt((sum p^2) / N), N = number of (live) pixels of the patch. */
+double pvro_patch_score(int64_t n, const double* p, const uint8_t* live) {
+  double s = 0.0;
+  int64_t N = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (!live[j]) continue;
+    s += p[j] * p[j];
+    ++N;
+  }
+  return N > 0 ? sqrt(s / (double)N) : 0.0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Steps 9-10: SR update and edge-preserving regularisation.                  */
+static const int D13[13][3] = {{1, 0, -1}, {0, 1, -1}, {1, 1, -1}, {1, -1, -1}, {1, 0, 0},
+                               {0, 1, 0},  {1, 1, 0},  {1, -1, 0}, {1, 0, 1},   {0, 1, 1},
+                               {1, 1, 1},  {1, -1, 1}, {0, 0, 1}};
+
+int pvro_update_regularise(int nx, int ny, int nz, const double* X0, const double* A,
+                           const double* C, double alpha, double lambda, double delta,
+                           double tau_C, int clamp, double lo, double hi, double* X1,
+                           double* X2) {
+  int64_t V = (int64_t)nx * ny * nz;
+  /* step 9: X1 = clip(X0 + alpha A / C) where C > tau_C, else X0 */
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < V; ++k) {
+    if (C[k] > tau_C) {
+      double x = X0[k] + alpha * A[k] / C[k];
+      if (clamp) x = x < lo ? lo : (x > hi ? hi : x);
+      X1[k] = x;
+    } else {
+      X1[k] = X0[k];
+    }
+  }
+  /* step 10: X2_k = X1_k + alpha lambda sum_d [b_d(k)(X1_{k+d} - X1_k)
+   *                                               + b_d(k-d)(X1_{k-d} - X1_k)],
+   * b_d(k) = phi_d / sqrt(1 + phi_d ((X0_{k+d} - X0_k) / delta)^2), phi_d = 1/|d|_1,
+   * b_d(k) = 0 unless k and k+d are both in the grid and both have C > tau_C.  */
+#pragma omp parallel for schedule(static)
+  for (int l = 0; l < nz; ++l) {
+    for (int j = 0; j < ny; ++j) {
+      for (int i = 0; i < nx; ++i) {
+        int64_t k = ((int64_t)l * ny + j) * nx + i;
+        if (!(C[k] > tau_C)) {
+          X2[k] = X1[k];
+          continue;
+        }
+        double sum = 0.0;
+        for (int d = 0; d < 13; ++d) {
+          double phi = 1.0 / (abs(D13[d][0]) + abs(D13[d][1]) + abs(D13[d][2]));
+          for (int sgn = -1; sgn <= 1; sgn += 2) {
+            int i2 = i + sgn * D13[d][0], j2 = j + sgn * D13[d][1], l2 = l + sgn * D13[d][2];
+            if (i2 < 0 || i2 >= nx || j2 < 0 || j2 >= ny || l2 < 0 || l2 >= nz) continue;
+            int64_t k2 = ((int64_t)l2 * ny + j2) * nx + i2;
+            if (!(C[k2] > tau_C)) continue;
+            /* b_d(k) for sgn = +1 uses (X0_{k+d} - X0_k); b_d(k-d) for sgn = -1 uses
+               (X0_k - X0_{k-d}); both square the same neighbour difference. */
+            double g = (X0[k2] - X0[k]) / delta;
+            double b = phi / sqrt(1.0 + phi * g * g);
+            sum += b * (X1[k2] - X1[k]);
+          }
+        }
+        X2[k] = X1[k] + alpha * lambda * sum;
+      }
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Problem-level API                                                           */
+pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin[3]) {
+  if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || !(spacing > 0)) return NULL;
+  pvro_ctx* x = (pvro_ctx*)calloc(1, sizeof(pvro_ctx));
+  for (int d = 0; d < 3; ++d) { x->n[d] = dims[d]; x->o[d] = origin[d]; }
+  x->s = spacing;
+  x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-6;
+  x->tau_obs = 0.01; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0;
+  int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
+  x->X = (double*)calloc(V, sizeof(double));
+  x->A = (double*)calloc(V, sizeof(double));
+  x->C = (double*)calloc(V, sizeof(double));
+  return x;
+}
+
+void pvro_destroy(pvro_ctx* x) {
+  if (!x) return;
+  for (int i = 0; i < x->n_stacks; ++i) { free(x->st[i].y); free(x->st[i].abc); free(x->st[i].psi); }
+  free(x->patch); free(x->pix0); free(x->T); free(x->X); free(x->A); free(x->C);
+  free(x->p); free(x->e); free(x->kappa); free(x->yhat); free(x->pbar); free(x->wpatch);
+  free(x);
+}
+
+int pvro_set_param(pvro_ctx* x, int key, double v) {
+  switch (key) {
+    case PVRO_DELTA: x->delta = v; break;
+    case PVRO_TAU_PATCH: x->tau_patch = v; break;
+    case PVRO_C0: x->c0 = v; break;
+    case PVRO_TAU_LIVE: x->tau_live = v; break;
+    case PVRO_TAU_C: x->tau_C = v; break;
+    case PVRO_TAU_OBS: x->tau_obs = v; break;
+    case PVRO_CLAMP: x->clamp = v; break;
+    case PVRO_PSF_MODE: x->psf_mode = v; break;
+    case PVRO_SIGMA2_FLOOR: x->s2floor = v; break;
+    case PVRO_PSF_NSIGMA: x->nsigma = v; break;
+    default: return -1;
+  }
+  return 0;
+}
+
+static double norm3(const double* a) { return sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+
+static int add_stack_impl(pvro_ctx* x, const float* sf, const double* sd, int W, int H, int K,
+                          const double G[12], double thickness) {
+  if (x->state > 1 || x->n_stacks >= PVRO_MAX_STACKS) return -1;
+  if (W < 1 || H < 1 || K < 1 || !(thickness > 0)) return -1;
+  ostack* st = &x->st[x->n_stacks];
+  memset(st, 0, sizeof(*st));
+  st->W = W; st->H = H; st->K = K; st->theta = thickness;
+  memcpy(st->G, G, sizeof(st->G));
+  int64_t L = (int64_t)W * H * K;
+  st->y = (double*)malloc(L * sizeof(double));
+  for (int64_t i = 0; i < L; ++i) st->y[i] = sf ? (double)sf[i] : sd[i];
+  x->n_stacks++;
+  x->state = 1;
+  return x->n_stacks - 1;
+}
+
+int pvro_add_stack(pvro_ctx* x, const float* slices, int W, int H, int K, const double G[12],
+                   double thickness) {
+  return add_stack_impl(x, slices, NULL, W, H, K, G, thickness);
+}
+
+int pvro_add_stack_f64(pvro_ctx* x, const double* slices, int W, int H, int K, const double G[12],
+                       double thickness) {
+  return add_stack_impl(x, NULL, slices, W, H, K, G, thickness);
+}
+
+/* Stack frame: u = G[:,0]/dx, v = G[:,1]/dy, w = u x v (normalised) and its PSF. */
+static int build_psf(pvro_ctx* x, ostack* st) {
+  double c0[3] = {st->G[0], st->G[4], st->G[8]}, c1[3] = {st->G[1], st->G[5], st->G[9]};
+  double dx = norm3(c0), dy = norm3(c1);
+  if (!(dx > 0) || !(dy > 0)) return -1;
+  for (int d = 0; d < 3; ++d) { st->u[d] = c0[d] / dx; st->v[d] = c1[d] / dy; }
+  st->w[0] = st->u[1] * st->v[2] - st->u[2] * st->v[1];
+  st->w[1] = st->u[2] * st->v[0] - st->u[0] * st->v[2];
+  st->w[2] = st->u[0] * st->v[1] - st->u[1] * st->v[0];
+  double nw = norm3(st->w);
+  if (!(nw > 1e-12)) return -1;
+  for (int d = 0; d < 3; ++d) st->w[d] /= nw;
+  st->abc = (int32_t*)malloc(3 * PVRO_MAX_PSF * sizeof(int32_t));
+  st->psi = (double*)malloc(PVRO_MAX_PSF * sizeof(double));
+  if (x->psf_mode == 1) { /* test-only delta PSF: one sample at the pixel centre */
+    st->S = 1;
+    st->abc[0] = st->abc[1] = st->abc[2] = 0;
+    st->psi[0] = 1.0;
+    st->h[0] = st->h[1] = st->h[2] = 0.0;
+    return 0;
+  }
+  double hw[7];
+  st->S = pvro_psf_table(dx, dy, st->theta, x->s, x->nsigma, PVRO_MAX_PSF, st->abc, st->psi, hw);
+  st->h[0] = hw[3]; st->h[1] = hw[4]; st->h[2] = hw[5];
+  return st->S > 0 ? 0 : -1;
+}
+
+int64_t pvro_extract_patches(pvro_ctx* x, int size, int stride, int depth, int stride_z) {
+  if (x->state != 1) return -1;
+  for (int i = 0; i < x->n_stacks; ++i)
+    if (build_psf(x, &x->st[i]) != 0) return -1;
+  int64_t M = 0;
+  int32_t *xs = (int32_t*)malloc(65536 * 4), *ys = (int32_t*)malloc(65536 * 4),
+          *zs = (int32_t*)malloc(65536 * 4);
+  for (int pass = 0; pass < 2; ++pass) {
+    M = 0;
+    for (int i = 0; i < x->n_stacks; ++i) {
+      ostack* st = &x->st[i];
+      int nxw = pvro_windows(st->W, size, stride, 65536, xs);
+      int nyw = pvro_windows(st->H, size, stride, 65536, ys);
+      int nzw = pvro_windows(st->K, depth, stride_z, 65536, zs);
+      if (nxw < 0 || nyw < 0 || nzw < 0) { free(xs); free(ys); free(zs); return -1; }
+      for (int a = 0; a < nzw; ++a)
+        for (int b = 0; b < nyw; ++b)
+          for (int c = 0; c < nxw; ++c) {
+            if (pass == 1) {
+              int32_t* pt = &x->patch[7 * M];
+              pt[0] = i; pt[1] = xs[c]; pt[2] = ys[b]; pt[3] = zs[a];
+              pt[4] = size; pt[5] = size; pt[6] = depth;
+            }
+            ++M;
+          }
+    }
+    if (pass == 0) x->patch = (int32_t*)malloc(7 * (M > 0 ? M : 1) * sizeof(int32_t));
+  }
+  free(xs); free(ys); free(zs);
+  x->M = M;
+  x->pix0 = (int64_t*)malloc((M + 1) * sizeof(int64_t));
+  x->pix0[0] = 0;
+  for (int64_t s = 0; s < M; ++s)
+    x->pix0[s + 1] = x->pix0[s] + (int64_t)x->patch[7 * s + 4] * x->patch[7 * s + 5] * x->patch[7 * s + 6];
+  x->P = x->pix0[M];
+  x->p = (double*)calloc(x->P, sizeof(double));
+  x->e = (double*)calloc(x->P, sizeof(double));
+  x->kappa = (double*)calloc(x->P, sizeof(double));
+  x->yhat = (double*)calloc(x->P, sizeof(double));
+  x->pbar = (double*)calloc(M, sizeof(double));
+  x->wpatch = (double*)calloc(M, sizeof(double));
+  x->T = (double*)calloc(12 * M, sizeof(double));
+  x->state = 2;
+  return M;
+}
+
+int64_t pvro_num_pixels(const pvro_ctx* x) { return x->P; }
+
+int pvro_get_patches(const pvro_ctx* x, int32_t* out) {
+  if (x->state < 2) return -1;
+  memcpy(out, x->patch, 7 * x->M * sizeof(int32_t));
+  return 0;
+}
+
+int pvro_get_psf(const pvro_ctx* x, int stack, int cap, int32_t* abc, double* psi) {
+  if (x->state < 2 || stack < 0 || stack >= x->n_stacks) return -1;
+  const ostack* st = &x->st[stack];
+  if (cap < st->S) return -2;
+  memcpy(abc, st->abc, 3 * st->S * sizeof(int32_t));
+  memcpy(psi, st->psi, st->S * sizeof(double));
+  return st->S;
+}
+
+/* Pixel j's observed value (stack view, not a copy). */
+static double pixel_y(const pvro_ctx* x, const int32_t* pt, int u, int v, int z) {
+  const ostack* st = &x->st[pt[0]];
+  return st->y[((int64_t)(pt[3] + z) * st->H + (pt[2] + v)) * st->W + (pt[1] + u)];
+}
+
+/* Step 1: sample position x_jq = g(T_s(c_j + delta_q)) in continuous voxel index,
+ * c_j = G (x0+u, y0+v, z0+z, 1), g(w) = (w - o) / s.                          */
+static void sample_pos(const pvro_ctx* x, const int32_t* pt, const double* T, int u, int v,
+                       int z, int q, double out[3]) {
+  const ostack* st = &x->st[pt[0]];
+  double col = pt[1] + u, row = pt[2] + v, sl = pt[3] + z;
+  const int32_t* abc = &st->abc[3 * q];
+  double c[3];
+  for (int d = 0; d < 3; ++d)
+    c[d] = st->G[4 * d + 0] * col + st->G[4 * d + 1] * row + st->G[4 * d + 2] * sl + st->G[4 * d + 3] +
+           abc[0] * st->h[0] * st->u[d] + abc[1] * st->h[1] * st->v[d] + abc[2] * st->h[2] * st->w[d];
+  for (int d = 0; d < 3; ++d) {
+    double wd = T[4 * d + 0] * c[0] + T[4 * d + 1] * c[1] + T[4 * d + 2] * c[2] + T[4 * d + 3];
+    out[d] = (wd - x->o[d]) / x->s;
+  }
+}
+
+/* Step 1 (reading Q6): trilinear corners of a continuous index; corners outside
+ * [0, n-1] are dropped. Returns the number of in-grid corners written.        */
+static int trilinear(const pvro_ctx* x, const double pos[3], int64_t idx[8], double wt[8]) {
+  int i0[3];
+  double f[3];
+  for (int d = 0; d < 3; ++d) {
+    double fl = floor(pos[d]);
+    i0[d] = (int)fl;
+    f[d] = pos[d] - fl;
+  }
+  int n = 0;
+  for (int cz = 0; cz < 2; ++cz)
+    for (int cy = 0; cy < 2; ++cy)
+      for (int cx = 0; cx < 2; ++cx) {
+        int i = i0[0] + cx, j = i0[1] + cy, l = i0[2] + cz;
+        if (i < 0 || i >= x->n[0] || j < 0 || j >= x->n[1] || l < 0 || l >= x->n[2]) continue;
+        idx[n] = ((int64_t)l * x->n[1] + j) * x->n[0] + i;
+        wt[n] = (cx ? f[0] : 1.0 - f[0]) * (cy ? f[1] : 1.0 - f[1]) * (cz ? f[2] : 1.0 - f[2]);
+        ++n;
+      }
+  return n;
+}
+
+int pvro_set_transforms(pvro_ctx* x, const double* T, int64_t n) {
+  if (x->state < 2) return -1;
+  if (n != x->M) return -2;
+  memcpy(x->T, T, 12 * n * sizeof(double));
+  x->state = 3;
+  /* coverage kappa (step 2) is geometry only: one forward pass on any volume */
+  pvro_forward(x, x->X, x->yhat, x->kappa);
+  /* EM reset: p_prev = 1, t = 0; live-y range for sigma2_min and the clamp (Q19) */
+  double ymin = INFINITY, ymax = -INFINITY;
+  for (int64_t s = 0; s < x->M; ++s) {
+    const int32_t* pt = &x->patch[7 * s];
+    int64_t j = x->pix0[s];
+    for (int z = 0; z < pt[6]; ++z)
+      for (int v = 0; v < pt[5]; ++v)
+        for (int u = 0; u < pt[4]; ++u, ++j) {
+          x->p[j] = 1.0;
+          if (x->kappa[j] >= x->tau_live) {
+            double yv = pixel_y(x, pt, u, v, z);
+            if (yv < ymin) ymin = yv;
+            if (yv > ymax) ymax = yv;
+          }
+        }
+  }
+  if (!(ymax >= ymin)) { ymin = 0.0; ymax = 0.0; }
+  x->lo = ymin - 0.1 * fabs(ymin);
+  x->hi = ymax + 0.1 * fabs(ymax);
+  x->s2min = x->s2floor * (ymax - ymin) * (ymax - ymin);
+  x->t = 0;
+  for (int64_t s = 0; s < x->M; ++s) { x->pbar[s] = 1.0; x->wpatch[s] = 1.0; }
+  return 0;
+}
+
+int pvro_set_volume(pvro_ctx* x, const double* X) {
+  memcpy(x->X, X, (size_t)x->n[0] * x->n[1] * x->n[2] * sizeof(double));
+  return 0;
+}
+
+int pvro_get_volume(const pvro_ctx* x, double* X) {
+  memcpy(X, x->X, (size_t)x->n[0] * x->n[1] * x->n[2] * sizeof(double));
+  return 0;
+}
+
+/* Steps 2-3 (Eq. 1): kappa_j = sum_q psi_q sum_{k in grid} t_k(x_jq);
+ * observed iff kappa_j >= tau_obs; yhat_j = sum_k W_jk X_k,
+ * W_jk = kappa_j^-1 sum_q psi_q t_k(x_jq) (each observed row sums to 1).      */
+int pvro_forward(const pvro_ctx* x, const double* X, double* yhat, double* kappa) {
+  if (x->state < 2) return -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = 0; s < x->M; ++s) {
+    const int32_t* pt = &x->patch[7 * s];
+    const ostack* st = &x->st[pt[0]];
+    const double* T = &x->T[12 * s];
+    int64_t j = x->pix0[s];
+    for (int z = 0; z < pt[6]; ++z)
+      for (int v = 0; v < pt[5]; ++v)
+        for (int u = 0; u < pt[4]; ++u, ++j) {
+          double kap = 0.0, acc = 0.0;
+          for (int q = 0; q < st->S; ++q) {
+            double pos[3], wt[8];
+            int64_t idx[8];
+            sample_pos(x, pt, T, u, v, z, q, pos);
+            int nc = trilinear(x, pos, idx, wt);
+            for (int c = 0; c < nc; ++c) {
+              kap += st->psi[q] * wt[c];
+              acc += st->psi[q] * wt[c] * X[idx[c]];
+            }
+          }
+          kappa[j] = kap;
+          yhat[j] = (kap >= x->tau_obs) ? acc / kap : 0.0;
+        }
+  }
+  return 0;
+}
+
+/* Adjoint of step 3 (north_star "backprojection"): out_k += sum_j W_jk r_j over the
+ * observed pixels of patches [first, first+count). Requires kappa (set_transforms). */
+int pvro_adjoint(const pvro_ctx* x, const double* r, int64_t first, int64_t count, double* out) {
+  if (x->state < 3 || first < 0 || first + count > x->M) return -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = first; s < first + count; ++s) {
+    const int32_t* pt = &x->patch[7 * s];
+    const ostack* st = &x->st[pt[0]];
+    const double* T = &x->T[12 * s];
+    int64_t j = x->pix0[s];
+    for (int z = 0; z < pt[6]; ++z)
+      for (int v = 0; v < pt[5]; ++v)
+        for (int u = 0; u < pt[4]; ++u, ++j) {
+          if (!(x->kappa[j] >= x->tau_obs) || r[j] == 0.0) continue;
+          for (int q = 0; q < st->S; ++q) {
+            double pos[3], wt[8];
+            int64_t idx[8];
+            sample_pos(x, pt, T, u, v, z, q, pos);
+            int nc = trilinear(x, pos, idx, wt);
+            for (int c = 0; c < nc; ++c) {
+              double add = st->psi[q] * wt[c] / x->kappa[j] * r[j];
+#pragma omp atomic
+              out[idx[c]] += add;
+            }
+          }
+        }
+  }
+  return 0;
+}
+
+/* Init (SURVEY §8(c) Init): X = W^T y / W^T 1 where C0 > tau_C, else the mean
+ * of the 26-neighbours with C0 > tau_C (one pass), else 0.                      */
+int pvro_init_volume(pvro_ctx* x) {
+  if (x->state < 3) return -1;
+  int64_t V = (int64_t)x->n[0] * x->n[1] * x->n[2];
+  double* r = (double*)malloc(x->P * sizeof(double));
+  double* ones = (double*)malloc(x->P * sizeof(double));
+  for (int64_t s = 0; s < x->M; ++s) {
+    const int32_t* pt = &x->patch[7 * s];
+    int64_t j = x->pix0[s];
+    for (int z = 0; z < pt[6]; ++z)
+      for (int v = 0; v < pt[5]; ++v)
+        for (int u = 0; u < pt[4]; ++u, ++j) { r[j] = pixel_y(x, pt, u, v, z); ones[j] = 1.0; }
+  }
+  memset(x->A, 0, V * sizeof(double));
+  memset(x->C, 0, V * sizeof(double));
+  pvro_adjoint(x, r, 0, x->M, x->A);
+  pvro_adjoint(x, ones, 0, x->M, x->C);
+  free(r); free(ones);
+  int nx = x->n[0], ny = x->n[1], nz = x->n[2];
+#pragma omp parallel for schedule(static)
+  for (int l = 0; l < nz; ++l)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        int64_t k = ((int64_t)l * ny + j) * nx + i;
+        if (x->C[k] > x->tau_C) { x->X[k] = x->A[k] / x->C[k]; continue; }
+        double sum = 0.0;
+        int cnt = 0;
+        for (int dl = -1; dl <= 1; ++dl)
+          for (int dj = -1; dj <= 1; ++dj)
+            for (int di = -1; di <= 1; ++di) {
+              if (!di && !dj && !dl) continue;
+              int i2 = i + di, j2 = j + dj, l2 = l + dl;
+              if (i2 < 0 || i2 >= nx || j2 < 0 || j2 >= ny || l2 < 0 || l2 >= nz) continue;
+              int64_t k2 = ((int64_t)l2 * ny + j2) * nx + i2;
+              if (x->C[k2] > x->tau_C) { sum += x->A[k2] / x->C[k2]; ++cnt; }
+            }
+        x->X[k] = cnt ? sum / cnt : 0.0;
+      }
+  return 0;
+}
+
+/* One SR iteration = SURVEY §8(c) steps 1-11, in order. */
+static int sr_step(pvro_ctx* x, double alpha, double lambda) {
+  int64_t V = (int64_t)x->n[0] * x->n[1] * x->n[2];
+  x->t += 1;
+  /* steps 1-4: forward model and residual e = y - yhat on observed pixels */
+  pvro_forward(x, x->X, x->yhat, x->kappa);
+  uint8_t* live = (uint8_t*)malloc(x->P);
+  for (int64_t s = 0; s < x->M; ++s) {
+    const int32_t* pt = &x->patch[7 * s];
+    int64_t j = x->pix0[s];
+    for (int z = 0; z < pt[6]; ++z)
+      for (int v = 0; v < pt[5]; ++v)
+        for (int u = 0; u < pt[4]; ++u, ++j) {
+          int obs = x->kappa[j] >= x->tau_obs;
+          x->e[j] = obs ? pixel_y(x, pt, u, v, z) - x->yhat[j] : 0.0;
+          live[j] = x->kappa[j] >= x->tau_live;
+        }
+  }
+  /* steps 5-6: M-step (p_prev = p of the previous E-step) then E-step */
+  double* pnew = (double*)malloc(x->P * sizeof(double));
+  pvro_em_round(x->P, x->e, live, x->p, x->t, x->c0, x->s2min, pnew, &x->sigma2, &x->c, &x->m);
+  for (int64_t j = 0; j < x->P; ++j) x->p[j] = (x->kappa[j] >= x->tau_obs) ? pnew[j] : 0.0;
+  free(pnew);
+  /* step 7: patch score and weight (reading Q13) */
+  for (int64_t s = 0; s < x->M; ++s) {
+    int64_t j0 = x->pix0[s], n = x->pix0[s + 1] - j0;
+    x->pbar[s] = pvro_patch_score(n, &x->p[j0], &live[j0]);
+    x->wpatch[s] = x->pbar[s] >= x->tau_patch ? x->pbar[s] : 0.0;
+  }
+  free(live);
+  /* step 8: A = W^T (w p e), C = W^T (w p) */
+  double* rA = (double*)malloc(x->P * sizeof(double));
+  double* rC = (double*)malloc(x->P * sizeof(double));
+  for (int64_t s = 0; s < x->M; ++s)
+    for (int64_t j = x->pix0[s]; j < x->pix0[s + 1]; ++j) {
+      rA[j] = x->wpatch[s] * x->p[j] * x->e[j];
+      rC[j] = x->wpatch[s] * x->p[j];
+    }
+  memset(x->A, 0, V * sizeof(double));
+  memset(x->C, 0, V * sizeof(double));
+  pvro_adjoint(x, rA, 0, x->M, x->A);
+  pvro_adjoint(x, rC, 0, x->M, x->C);
+  free(rA); free(rC);
+  /* steps 9-11: update, regularise, commit */
+  double* X1 = (double*)malloc(V * sizeof(double));
+  double* X2 = (double*)malloc(V * sizeof(double));
+  pvro_update_regularise(x->n[0], x->n[1], x->n[2], x->X, x->A, x->C, alpha, lambda, x->delta,
+                         x->tau_C, x->clamp != 0, x->lo, x->hi, X1, X2);
+  memcpy(x->X, X2, V * sizeof(double));
+  free(X1); free(X2);
+  return 0;
+}
+
+int pvro_sr_iterate(pvro_ctx* x, int n, double alpha, double lambda) {
+  if (x->state < 3 || n < 0 || alpha < 0 || lambda < 0) return -1;
+  for (int i = 0; i < n; ++i) sr_step(x, alpha, lambda);
+  return 0;
+}
+
+int pvro_get_weights(const pvro_ctx* x, double* p, double* pbar, double* w) {
+  if (x->state < 3) return -1;
+  if (p) memcpy(p, x->p, x->P * sizeof(double));
+  if (pbar) memcpy(pbar, x->pbar, x->M * sizeof(double));
+  if (w) memcpy(w, x->wpatch, x->M * sizeof(double));
+  return 0;
+}
+
+int pvro_get_taps(const pvro_ctx* x, double* e, double* kappa, double* A, double* C) {
+  if (x->state < 3) return -1;
+  int64_t V = (int64_t)x->n[0] * x->n[1] * x->n[2];
+  if (e) memcpy(e, x->e, x->P * sizeof(double));
+  if (kappa) memcpy(kappa, x->kappa, x->P * sizeof(double));
+  if (A) memcpy(A, x->A, V * sizeof(double));
+  if (C) memcpy(C, x->C, V * sizeof(double));
+  return 0;
+}
+
+int pvro_get_em_state(const pvro_ctx* x, double* sigma2, double* c, double* m, int64_t* t,
+                      double* lo, double* hi) {
+  if (sigma2) *sigma2 = x->sigma2;
+  if (c) *c = x->c;
+  if (m) *m = x->m;
+  if (t) *t = x->t;
+  if (lo) *lo = x->lo;
+  if (hi) *hi = x->hi;
+  return 0;
+}

@@ -1,0 +1,112 @@
+/* pvro.h — fp64 CPU ORACLE for the PVR super-resolution iteration.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product
+ * (libpvr.so, paper_1611_07289_b200/) never includes, links or calls it, and this
+ * tree includes nothing from the product: the two share no code, header, table or
+ * constant generator.
+ *
+ * What it computes: SURVEY.md §8(c) steps 0-11 and the init, written as plain
+ * fp64 loops in the paper's order (PAPER.md = /root/reference/PAPER.md):
+ *   PSF table ............ P:158-160 (sinc in-plane, slice profile through-plane,
+ *                          Taylor-series sinc); readings Q1-Q5 in DESIGN.md
+ *   forward model ........ Eq. 1, P:53-58 (x_i = W_i y + n_i, W_i = D B T_i)
+ *   residual, EM ......... P:189-209 (m = 1/(max e - min e), p = Gc/(Gc+m(1-c)),
+ *                          pbar = sqrt(sum p^2 / N), patch exclusion)
+ *   adjoint / SR update .. P:185 ("reintegrated into X using iterative
+ *                          super-resolution with gradient descent")
+ *   regulariser .......... P:97 (edge-preserving anisotropic diffusion; reading Q17)
+ *   init ................. P:89 (empty voxels filled with the mean of neighbours)
+ * Parity status per function is listed in DESIGN.md §Oracle; the PSF
+ * discretisation (Q1-Q5), regulariser form (Q17) and patch rule (Q13) are
+ * "parity unpinned" against the paper (the paper prints no numbers for them) and
+ * are pinned only by closed forms / invariants of the readings themselves.
+ *
+ * Conventions (independent restatement of DESIGN.md §Geometry):
+ *   volume voxel (i,j,l) -> world o + s*(i,j,l); data index (l*ny + j)*nx + i.
+ *   stack slices float/double [K][H][W]; G: row-major 3x4, world = G*(col,row,slice,1).
+ *   patch pixel order: patch-major, then slice z, row v, column u.
+ *   T: row-major 3x4 per patch, world -> world; sample = T(c_j + delta_q).
+ * All functions return 0 on success, a negative value on error.
+ */
+#ifndef PVRO_H
+#define PVRO_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pvro_ctx pvro_ctx;
+
+/* parameter keys (oracle-side numbering; the product has its own) */
+enum {
+  PVRO_DELTA = 0,        /* regulariser edge scale delta (default 150)              */
+  PVRO_TAU_PATCH = 1,    /* patch inlier threshold on pbar (0.5)                     */
+  PVRO_C0 = 2,           /* initial inlier proportion c at t = 1 (0.9)               */
+  PVRO_TAU_LIVE = 3,     /* live pixel: kappa >= tau_live (0.99)                     */
+  PVRO_TAU_C = 4,        /* voxel updated iff C > tau_C (1e-6)                       */
+  PVRO_TAU_OBS = 5,      /* observed pixel: kappa >= tau_obs (0.01)                  */
+  PVRO_CLAMP = 6,        /* 1: clamp X1 to [lo, hi] (default 1)                      */
+  PVRO_PSF_MODE = 7,     /* 0: PVR PSF; 1: delta PSF (S = 1, delta_q = 0), test only */
+  PVRO_SIGMA2_FLOOR = 9, /* sigma2_min = floor * (ymax - ymin)^2 (1e-6)              */
+  PVRO_PSF_NSIGMA = 10,  /* through-plane truncation in sigma_w (3)                  */
+};
+
+/* ---- scalar building blocks (pinned individually by tests/test_oracle_*.py) ---- */
+double pvro_sinc_taylor(double x);                       /* sin(x)/x by its Taylor series */
+/* PSF lattice of one stack. Writes up to cap entries: abc[3*q] = (a,b,c), psi[q].
+   Returns S (number of samples) or <0. hw_out (nullable) = {n_u,n_v,n_w,h_u,h_v,h_w,sigma_w}. */
+int pvro_psf_table(double dx, double dy, double theta, double s, double nsigma,
+                   int cap, int32_t* abc, double* psi, double* hw_out);
+/* Square-window extraction along one axis (clamp-last reading Q22).
+   Returns the number of windows, writes starts to out (cap entries). */
+int pvro_windows(int dim, int size, int stride, int cap, int32_t* out);
+/* EM: posterior of one residual (logistic form of P:202). */
+double pvro_posterior(double e, double sigma2, double c, double m);
+/* One EM round over n residuals: M-step with p_prev (t == 1 uses c = c0), then E-step.
+   live[j] != 0 marks pixels in the statistics; p_out gets the posterior for every j.
+   Returns 1 if the degenerate (zero-spread / no-live) path was taken, else 0. */
+int pvro_em_round(int64_t n, const double* e, const uint8_t* live, const double* p_prev,
+                  int64_t t, double c0, double sigma2_min, double* p_out,
+                  double* sigma2_out, double* c_out, double* m_out);
+/* pbar = sqrt(sum_{live} p^2 / N_live); 0 if N_live = 0. */
+double pvro_patch_score(int64_t n, const double* p, const uint8_t* live);
+/* SR update (step 9) + regulariser (step 10) on a bare grid, for the closed-form pins. */
+int pvro_update_regularise(int nx, int ny, int nz, const double* X0, const double* A,
+                           const double* C, double alpha, double lambda, double delta,
+                           double tau_C, int clamp, double lo, double hi, double* X1_out,
+                           double* X2_out);
+
+/* ---- problem-level API (mirrors the product's call sequence) ---- */
+pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin[3]);
+void pvro_destroy(pvro_ctx*);
+int pvro_set_param(pvro_ctx*, int key, double value);
+int pvro_add_stack(pvro_ctx*, const float* slices, int W, int H, int K,
+                   const double G[12], double thickness);
+/* fp64 slices, for the exact fixed-point pins (tests only) */
+int pvro_add_stack_f64(pvro_ctx*, const double* slices, int W, int H, int K,
+                       const double G[12], double thickness);
+int64_t pvro_extract_patches(pvro_ctx*, int size, int stride, int depth, int stride_z);
+int64_t pvro_num_pixels(const pvro_ctx*);
+/* patch table: 7 int32 per patch {stack, x0, y0, z0, sx, sy, sz} */
+int pvro_get_patches(const pvro_ctx*, int32_t* out);
+int pvro_get_psf(const pvro_ctx*, int stack, int cap, int32_t* abc, double* psi);
+int pvro_set_transforms(pvro_ctx*, const double* T, int64_t n);
+int pvro_set_volume(pvro_ctx*, const double* X);
+int pvro_get_volume(const pvro_ctx*, double* X);
+/* forward operator on an arbitrary volume: yhat[j] (0 if unobserved) and kappa[j] */
+int pvro_forward(const pvro_ctx*, const double* X, double* yhat, double* kappa);
+/* adjoint operator: out[k] = sum_j W_jk r[j] over observed pixels of patches
+   [first, first + count) (out is accumulated into, caller zeroes it) */
+int pvro_adjoint(const pvro_ctx*, const double* r, int64_t first, int64_t count, double* out);
+int pvro_init_volume(pvro_ctx*);
+int pvro_sr_iterate(pvro_ctx*, int n, double alpha, double lambda);
+/* state after the last iteration: per-pixel p and e, per-patch pbar and w */
+int pvro_get_weights(const pvro_ctx*, double* p, double* pbar, double* w);
+int pvro_get_taps(const pvro_ctx*, double* e, double* kappa, double* A, double* C);
+int pvro_get_em_state(const pvro_ctx*, double* sigma2, double* c, double* m, int64_t* t,
+                      double* lo, double* hi);
+#ifdef __cplusplus
+}
+#endif
+#endif
