@@ -1,0 +1,201 @@
+/* pvr.h — C ABI of libpvr.so: PVR's super-resolution (SR) iteration on B200 (sm_100a).
+ *
+ * Method: Alansary, Kainz et al., "PVR: Patch-to-Volume Reconstruction for Large Area
+ * Motion Correction of Fetal MRI", arXiv 1611.07289. Citations "P:L" are lines of
+ * /root/reference/PAPER.md; "§8(c)" is SURVEY.md §8(c); "Qn" are the readings listed
+ * in DESIGN.md §Readings (where the paper is silent, garbled or defers to a citation).
+ *
+ * The library reconstructs a high-resolution (HR) volume X from stacks of 2D slices cut
+ * into overlapping patches y_s (Eq. 2), each with its own transform T_s
+ * (W_i = D B T_i, Eq. 1). One pvr_sr_iterate() iteration runs, on the GPU:
+ *   a1 PSF-weighted forward simulation of every patch pixel   (Eq. 1; P:158-160 PSF)
+ *   a2 residual e = y - yhat and EM sufficient statistics
+ *   a3 EM parameters sigma^2, c, m
+ *   a4 pixel posteriors p, patch scores pbar, patch weights w
+ *   a5 adjoint backprojection into addon A and confidence C
+ *   a6 SR update X1 = clip(X0 + alpha A / C)                     (reading Q16)
+ *   a7 edge-preserving regularisation                           (reading Q17)
+ * Every step runs in the library's own CUDA kernels; there is no CPU fallback. With
+ * nranks > 1 (pvr_comm_init) patches are sharded over ranks and the EM statistics and
+ * (A, C) are sum-allreduced over NCCL each iteration (reading Q21).
+ *
+ * Conventions
+ *  - All functions return pvr_status; none throws or aborts. On error the message is
+ *    available from pvr_last_error(). A CUDA or NCCL error poisons the context: after it
+ *    only pvr_last_error() and pvr_destroy() are valid.
+ *  - Inputs are copied before return; the library never retains caller pointers.
+ *    Array arguments may be host or device pointers (detected per call).
+ *  - Volume layout: float32 [nz][ny][nx], voxel (i,j,l) at world origin + s*(i,j,l),
+ *    axes = identity ("isotropic" HR grid).
+ *  - Patch pixel order ("patch-major"): patches in extraction order (stack, z0, y0, x0),
+ *    within a patch slice z, then row v, then column u.
+ *  - All device work is issued on the context's stream (cuda_stream argument of
+ *    pvr_create_volume, or a stream the library creates when it is NULL).
+ *  - A context is not thread-safe; use one per GPU / rank.
+ *  - State machine: CREATED --add_stack--> STACKS --extract_patches--> PATCHED
+ *    --set_transforms--> READY. Out-of-order calls return PVR_ERR_STATE.
+ */
+#ifndef PVR_H
+#define PVR_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pvr_ctx pvr_ctx;
+
+typedef enum {
+  PVR_OK = 0,
+  PVR_ERR_ARG = 1,    /* invalid argument (sizes, geometry, ranges)                 */
+  PVR_ERR_STATE = 2,  /* call out of order for the state machine above              */
+  PVR_ERR_OOM = 3,    /* device or host allocation failed                           */
+  PVR_ERR_CUDA = 4,   /* CUDA runtime / launch error (context poisoned)             */
+  PVR_ERR_NCCL = 5,   /* NCCL error or NCCL unavailable (context poisoned)          */
+  PVR_ERR_EMPTY = 6   /* nothing to reconstruct: no patch, or no observed pixel     */
+} pvr_status;
+
+typedef struct {
+  int32_t dims[3];      /* nx, ny, nz >= 1                                          */
+  double spacing_mm;    /* isotropic voxel size s > 0                               */
+  double origin_mm[3];  /* world position of the centre of voxel (0,0,0)            */
+} pvr_geometry;
+
+/* Parameter keys for pvr_set_param (defaults in brackets). Keys marked (extract) must be
+ * set before pvr_extract_patches; the others take effect at the next call that uses them. */
+enum {
+  PVR_PARAM_DELTA = 0,        /* regulariser edge scale delta [150] (Q17, Q18)            */
+  PVR_PARAM_TAU_PATCH = 1,    /* patch kept iff pbar >= tau_patch [0.5] (Q13)             */
+  PVR_PARAM_C0 = 2,           /* inlier proportion c at the first iteration [0.9] (Q10)    */
+  PVR_PARAM_TAU_LIVE = 3,     /* pixel in the EM statistics iff kappa >= tau_live [0.99]   */
+  PVR_PARAM_TAU_C = 4,        /* voxel updated iff C > tau_C [1e-6] (Q24)                  */
+  PVR_PARAM_TAU_OBS = 5,      /* pixel observed iff kappa >= tau_obs [0.01] (Q25)          */
+  PVR_PARAM_CLAMP = 6,        /* 1: clamp X1 to the live-y range +-10% [1] (Q19)           */
+  PVR_PARAM_PSF_MODE = 7,     /* (extract) 0: PVR PSF; 1: delta PSF (tests only) [0]       */
+  PVR_PARAM_SIGMA2_FLOOR = 9, /* sigma2 >= floor * (ymax - ymin)^2 [1e-6] (Q10)            */
+  PVR_PARAM_PSF_NSIGMA = 10,  /* (extract) slice profile cut at nsigma * sigma_w [3] (Q3)  */
+  PVR_PARAM_PROFILE = 11      /* 1: time every kernel with CUDA events (pvr_get_stats) [0] */
+};
+
+/* Version string of the library build. */
+const char* pvr_version(void);
+
+/* Create a context for one HR volume on cuda_device. cuda_stream: a cudaStream_t to issue
+ * all work on (the caller keeps ownership), or NULL for a library-owned stream.
+ * Errors: PVR_ERR_ARG (dims < 1, spacing <= 0), PVR_ERR_CUDA, PVR_ERR_OOM. */
+pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_stream,
+                             pvr_ctx** out);
+pvr_status pvr_destroy(pvr_ctx* ctx);
+/* Last error message of ctx (a static string when ctx is NULL). Never NULL. */
+const char* pvr_last_error(const pvr_ctx* ctx);
+
+/* Optional, before pvr_extract_patches: join an NCCL communicator of nranks ranks (one
+ * process per GPU). nccl_unique_id: the 128-byte ncclUniqueId created by rank 0 and
+ * broadcast by the caller (e.g. over torch.distributed). Patches are then sharded in
+ * contiguous ranges balanced by pixels x PSF samples; X is replicated.
+ * Errors: PVR_ERR_ARG, PVR_ERR_STATE, PVR_ERR_NCCL (library not loadable / init failed). */
+pvr_status pvr_comm_init(pvr_ctx* ctx, int nranks, int rank, const void* nccl_unique_id);
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */
+pvr_status pvr_comm_unique_id(void* out128);
+
+/* Add one stack of slices ("stacks of 2D images").
+ * slices: float32 [K][H][W], host or device, copied.
+ * index_to_world: row-major 3x4 double, world_mm = M (col, row, slice, 1); its first two
+ *   columns give the in-plane pixel pitches |col0| = dx, |col1| = dy and directions, the
+ *   third the slice step (may differ from the thickness).
+ * thickness_mm: slice profile FWHM theta > 0 ("slice profile for the through-plane").
+ * Errors: PVR_ERR_ARG (sizes < 1, thickness <= 0, degenerate in-plane axes),
+ * PVR_ERR_STATE (after extract_patches). */
+pvr_status pvr_add_stack(pvr_ctx* ctx, const float* slices, int W, int H, int K,
+                         const double index_to_world[12], double thickness_mm,
+                         int* stack_id_out);
+
+/* Cut every stack into square size x size windows at stride `stride` in-plane and
+ * depth-slice windows at stride_z through-plane ("size a and stride omega";
+ * depth > 1 gives 3D patches). The last window of an axis is clamped to the edge (Q22).
+ * Builds the PSF tables (Q1-Q5) and the shard plan. Returns the global
+ * patch count M. Errors: PVR_ERR_ARG (size > W or H, stride < 1 or > size, depth > K,
+ * stride_z < 1 or > depth), PVR_ERR_STATE, PVR_ERR_EMPTY (M = 0). */
+pvr_status pvr_extract_patches(pvr_ctx* ctx, int size, int stride, int depth, int stride_z,
+                               int64_t* n_patches_out);
+/* Host-only helper (no GPU needed): contiguous shard plan of M patches over nranks,
+ * balanced by cost[s] (pixels x PSF samples of patch s): rank r owns patches
+ * [bounds[r], bounds[r+1]); bounds has nranks + 1 entries, bounds[0] = 0, bounds[nranks] = M.
+ * P:233 "distributing independent subsets of patches over the desired number of devices".
+ * Errors: PVR_ERR_ARG (null pointers, M < 0, nranks < 1). */
+pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* bounds);
+
+/* This rank's shard: patches [first_patch, first_patch + n_local), and its pixel range in
+ * the global patch-major pixel order. Any output pointer may be NULL. */
+pvr_status pvr_get_shard(const pvr_ctx* ctx, int64_t* first_patch, int64_t* n_local,
+                         int64_t* first_pixel, int64_t* n_local_pixels);
+/* Patch table of this rank's shard: 7 int32 per patch {stack, x0, y0, z0, sx, sy, sz},
+ * host pointer. */
+pvr_status pvr_get_patches(const pvr_ctx* ctx, int32_t* out);
+
+/* Per-patch transforms (P:58 T_i; "continuously rigidly registered"): n = M
+ * row-major 3x4 double world->world affines for ALL patches (every rank passes the same
+ * array). The volume is sampled at T_s(pixel_world + PSF offset) (reading Q7); rigid is
+ * the special case. Computes the coverage kappa of every pixel and resets the EM state
+ * (p_prev = 1, w = 1, t = 0) and the live-y range used by the clamp and the sigma^2 floor.
+ * Errors: PVR_ERR_ARG (n != M), PVR_ERR_STATE (before extract), PVR_ERR_EMPTY (no
+ * observed pixel on any rank). Collective when nranks > 1. */
+pvr_status pvr_set_transforms(pvr_ctx* ctx, const double* T, int64_t n);
+
+/* Set X (float32 [nz][ny][nx], host or device). Errors: PVR_ERR_ARG (nvox != V). */
+pvr_status pvr_set_volume(pvr_ctx* ctx, const float* x, size_t nvox);
+/* X = W^T y / W^T 1 where W^T 1 > tau_C, else the mean of the covered 26-neighbours, else 0
+ * ("empty voxels are filled using the mean of the surrounding voxels").
+ * Errors: PVR_ERR_STATE (before set_transforms). Collective when nranks > 1. */
+pvr_status pvr_init_volume(pvr_ctx* ctx);
+/* Set a parameter (keys above). Errors: PVR_ERR_ARG (unknown key / invalid value),
+ * PVR_ERR_STATE ((extract) keys after extract_patches). */
+pvr_status pvr_set_param(pvr_ctx* ctx, int key, double value);
+
+/* Run n SR iterations (steps a1-a7 above), all on the device.
+ * Errors: PVR_ERR_ARG (n < 0, alpha < 0, lambda < 0), PVR_ERR_STATE (before
+ * set_transforms), PVR_ERR_CUDA / PVR_ERR_NCCL. alpha*lambda > 3/44 is accepted (the
+ * maximum principle of the regulariser no longer holds; a warning is left in
+ * pvr_last_error). Collective when nranks > 1. */
+pvr_status pvr_sr_iterate(pvr_ctx* ctx, int n, float alpha, float lambda);
+
+/* Copy X out (float32 [nz][ny][nx]; host or device pointer). Errors: PVR_ERR_ARG. */
+pvr_status pvr_get_volume(pvr_ctx* ctx, float* out, size_t nvox);
+/* Weights of this rank's shard after the last iteration: pixel posteriors p
+ * [n_local_pixels], patch weights w and patch scores pbar [n_local]; any may be NULL. */
+pvr_status pvr_get_weights(pvr_ctx* ctx, float* pixel_p, float* patch_w, float* patch_pbar);
+/* Debug taps of the last iteration: residual e and coverage kappa [n_local_pixels] of this
+ * shard, and the (reduced) addon A and confidence C [V]; any may be NULL. */
+pvr_status pvr_get_taps(pvr_ctx* ctx, float* e, float* kappa, float* addon, float* confidence);
+/* EM state after the last iteration: sigma^2, c, m, iteration counter t, and the clamp
+ * range [lo, hi]. Any output may be NULL. */
+pvr_status pvr_get_em_state(pvr_ctx* ctx, double* sigma2, double* c, double* m, int64_t* iter,
+                            double* lo, double* hi);
+
+/* Counters accumulated since the last pvr_reset_stats (kernel times need PVR_PARAM_PROFILE). */
+typedef struct {
+  int64_t iterations;         /* SR iterations run                                       */
+  int64_t psf_samples;        /* PSF samples visited by the forward model (P x S summed) */
+  int64_t pixels;             /* patch pixels of this shard                               */
+  int64_t voxels;             /* V                                                        */
+  int64_t patches;            /* patches of this shard                                    */
+  int64_t kernel_launches;    /* kernels launched by pvr_sr_iterate                       */
+  double ms_forward;          /* a1+a2 (k_forward)                                        */
+  double ms_em;               /* a3 (k_em_params) + statistics allreduce                  */
+  double ms_estep;            /* a4 (k_estep)                                             */
+  double ms_backproject;      /* a5 (k_backproject, including the A/C clear)              */
+  double ms_allreduce;        /* A/C allreduce (nranks > 1)                               */
+  double ms_update;           /* a6+a7 (k_update_regularise)                              */
+  int64_t n_forward, n_em, n_estep, n_backproject, n_allreduce, n_update; /* launches     */
+  int64_t bytes_alg_forward;      /* algorithmic HBM bytes per forward launch             */
+  int64_t bytes_alg_estep;        /* per E-step launch                                    */
+  int64_t bytes_alg_backproject;  /* per backprojection launch                            */
+  int64_t bytes_alg_update;       /* per update launch                                    */
+} pvr_stats;
+pvr_status pvr_get_stats(const pvr_ctx* ctx, pvr_stats* out);
+pvr_status pvr_reset_stats(pvr_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PVR_H */

@@ -1,0 +1,812 @@
+// engine.cu — host engine and C ABI of libpvr.so (include/pvr.h).
+//
+// Host side, in fp64: the state machine, stack frames and PSF tables (P:158-160,
+// readings Q1-Q5), square-patch extraction (Q22), the shard plan (Q21),
+// and the per-patch composition of index->world, T_s and world->voxel maps (P:58,
+// Q7) that the kernels consume as fp32 (DESIGN.md §Data layout). Device side: the
+// kernels of kernels.cu, issued on the context's stream, plus the NCCL layer (dlopen'd).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pvr.h"
+#include "pvr_internal.h"
+
+using namespace pvr;
+
+namespace {
+
+enum State { CREATED = 0, STACKS = 1, PATCHED = 2, READY = 3 };
+
+struct HostStack {
+  int W, H, K;
+  double G[12];
+  double theta;
+  double u[3], v[3], w[3], h[3];  // in-plane axes, slice normal, PSF lattice steps (mm)
+  int S = 0, psf0 = 0;
+  float* y_dev = nullptr;          // device copy of the slices (until extract)
+  int64_t y_off = 0;               // offset in the concatenated stack buffer
+};
+
+struct HostPatch {
+  int32_t stack, x0, y0, z0, sx, sy, sz;
+};
+
+// ---- NCCL, loaded at pvr_comm_init (no link-time dependency) ----
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) { err = std::string("cannot dlopen libnccl.so.2: ") + dlerror(); return false; }
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString) {
+      err = "libnccl is missing a required symbol";
+      return false;
+    }
+    return true;
+  }
+};
+Nccl g_nccl;
+
+}  // namespace
+
+struct pvr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int3 dims;
+  double s, o[3];
+  int64_t V;
+  int state = CREATED;
+  bool poisoned = false;
+  std::string err;
+  // parameters
+  double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-6, tau_obs = 0.01;
+  int clamp = 1, psf_mode = 0, profile = 0;
+  double s2floor = 1e-6, nsigma = 3.0;
+  // stacks / patches
+  std::vector<HostStack> stacks;
+  std::vector<HostPatch> patches;   // global list
+  std::vector<int64_t> pix0_global; // [M+1]
+  int64_t M = 0, P = 0;
+  int64_t first = 0, nloc = 0, first_pix = 0, nloc_pix = 0;
+  int64_t samples_obs = 0;          // observed local pixels x S (per iteration)
+  // comm
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  // device buffers
+  float* X[2] = {nullptr, nullptr};
+  int cur = 0;
+  float2* AC = nullptr;
+  float *e = nullptr, *p = nullptr, *kap = nullptr, *pbar = nullptr, *w = nullptr;
+  float* ys = nullptr;
+  float4* psf = nullptr;
+  PatchDev* pdev = nullptr;
+  int2* tiles = nullptr;
+  int64_t ntiles = 0;
+  double* partials = nullptr;
+  EmDev* em = nullptr;
+  // stats
+  pvr_stats st;
+  cudaEvent_t ev[16];
+  bool have_events = false;
+};
+
+namespace {
+
+const char* kVersion = "pvr-b200 0.1 (sm_100a)";
+thread_local std::string g_static_err = "no context";
+
+pvr_status fail(pvr_ctx* c, pvr_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (s == PVR_ERR_CUDA || s == PVR_ERR_NCCL) c->poisoned = true;
+  } else {
+    g_static_err = buf;
+  }
+  return s;
+}
+
+#define CUDA_TRY(c, call)                                                                  \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail((c), _e == cudaErrorMemoryAllocation ? PVR_ERR_OOM : PVR_ERR_CUDA,       \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+#define CHECK_LAUNCH(c) CUDA_TRY(c, cudaGetLastError())
+
+#define GUARD(c)                                                                   \
+  do {                                                                             \
+    if (!(c)) return fail(nullptr, PVR_ERR_ARG, "null context");                   \
+    if ((c)->poisoned) return fail((c), PVR_ERR_STATE, "context poisoned: %s", (c)->err.c_str()); \
+    cudaSetDevice((c)->device);                                                    \
+  } while (0)
+
+bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+double norm3(const double* a) { return std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+
+// Taylor-series sinc: 1 - x^2/3! + x^4/5! - ..., stopped when the next term is
+// below an absolute 1e-16 (reading Q4).
+double taylor_sinc(double x) {
+  const double x2 = x * x;
+  double term = 1.0, sum = 1.0;
+  for (int k = 1; k < 200; ++k) {
+    term *= -x2 / ((2.0 * k) * (2.0 * k + 1.0));
+    if (std::fabs(term) < 1e-16) break;
+    sum += term;
+  }
+  return sum;
+}
+
+int psf_steps(double pitch, double s) {  // reading Q5: n = max(2, ceil(pitch / s))
+  int n = (int)std::ceil(pitch / s - 1e-9);
+  return std::max(2, n);
+}
+
+// PSF lattice of one stack: psi(a,b,c) ~ sinc(pi R) * exp(-(c h_w)^2 / 2 sw^2),
+// R = |(a/n_u, b/n_v)| < 1 (main lobe, Q2), |c h_w| <= nsigma sw (Q3); normalised to 1.
+void build_psf(const pvr_ctx* c, HostStack& st, std::vector<float4>& table) {
+  st.psf0 = (int)table.size();
+  if (c->psf_mode == 1) {  // test-only delta PSF
+    table.push_back(make_float4(0.f, 0.f, 0.f, 1.f));
+    st.S = 1;
+    st.h[0] = st.h[1] = st.h[2] = 0.0;
+    return;
+  }
+  double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
+  const double px = norm3(c0), py = norm3(c1);
+  const int nu = psf_steps(px, c->s), nv = psf_steps(py, c->s), nw = psf_steps(st.theta, c->s);
+  st.h[0] = px / nu;
+  st.h[1] = py / nv;
+  st.h[2] = st.theta / nw;
+  const double sw = st.theta / (2.0 * std::sqrt(2.0 * std::log(2.0)));
+  const int cmax = (int)std::floor(c->nsigma * sw / st.h[2] + 1e-9) + 1;
+  std::vector<double> val;
+  std::vector<int> abc;
+  double total = 0.0;
+  for (int cc = -cmax; cc <= cmax; ++cc) {
+    const double zc = cc * st.h[2];
+    if (std::fabs(zc) > c->nsigma * sw) continue;
+    const double g = std::exp(-zc * zc / (2.0 * sw * sw));
+    for (int b = -nv; b <= nv; ++b)
+      for (int a = -nu; a <= nu; ++a) {
+        const double R = std::sqrt((double)a * a / ((double)nu * nu) + (double)b * b / ((double)nv * nv));
+        if (!(R < 1.0)) continue;
+        const double v = taylor_sinc(M_PI * R) * g;
+        val.push_back(v);
+        abc.push_back(a); abc.push_back(b); abc.push_back(cc);
+        total += v;
+      }
+  }
+  st.S = (int)val.size();
+  for (int q = 0; q < st.S; ++q)
+    table.push_back(make_float4((float)abc[3 * q], (float)abc[3 * q + 1], (float)abc[3 * q + 2],
+                                (float)(val[q] / total)));
+}
+
+// Square windows along one axis; the last one is clamped to the edge (Q22).
+std::vector<int> windows(int dim, int size, int stride) {
+  std::vector<int> out;
+  for (int x = 0; x + size <= dim; x += stride) out.push_back(x);
+  if (!out.empty() && out.back() + size < dim) out.push_back(dim - size);
+  return out;
+}
+
+Params make_params(const pvr_ctx* c) {
+  Params p;
+  p.tau_live = (float)c->tau_live;
+  p.tau_obs = (float)c->tau_obs;
+  p.tau_C = (float)c->tau_C;
+  p.tau_patch = (float)c->tau_patch;
+  p.c0 = (float)c->c0;
+  p.delta = (float)c->delta;
+  p.clamp = c->clamp;
+  return p;
+}
+
+pvr_status nccl_check(pvr_ctx* c, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return PVR_OK;
+  return fail(c, PVR_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+}
+
+// EM statistics allreduce (C1): SUM over stats[0..2], MAX over stats[3..4].
+pvr_status allreduce_stats(pvr_ctx* c) {
+  if (c->nranks <= 1) return PVR_OK;
+  double* s = c->em->stats;
+  pvr_status r = nccl_check(c, g_nccl.AllReduce(s, s, 3, ncclFloat64, ncclSum, c->comm, c->stream),
+                            "ncclAllReduce(stats sum)");
+  if (r != PVR_OK) return r;
+  return nccl_check(c, g_nccl.AllReduce(s + 3, s + 3, 2, ncclFloat64, ncclMax, c->comm, c->stream),
+                    "ncclAllReduce(stats max)");
+}
+
+// Addon / confidence allreduce (C2): SUM over the interleaved (A, C) volume.
+pvr_status allreduce_ac(pvr_ctx* c) {
+  if (c->nranks <= 1) return PVR_OK;
+  return nccl_check(c, g_nccl.AllReduce(c->AC, c->AC, (size_t)c->V * 2, ncclFloat32, ncclSum,
+                                        c->comm, c->stream),
+                    "ncclAllReduce(A,C)");
+}
+
+void free_dev(pvr_ctx* c) {
+  for (auto& s : c->stacks)
+    if (s.y_dev) cudaFree(s.y_dev), s.y_dev = nullptr;
+  void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->psf,
+                  c->pdev, c->tiles, c->partials, c->em};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+}
+
+// profiling: events bracket each kernel group when PVR_PARAM_PROFILE is on
+enum { EV_FWD0, EV_FWD1, EV_EM1, EV_EST1, EV_BP1, EV_AR1, EV_UPD1, EV_N };
+
+}  // namespace
+
+// ======================================================================================
+extern "C" {
+
+const char* pvr_version(void) { return kVersion; }
+
+const char* pvr_last_error(const pvr_ctx* c) { return c ? c->err.c_str() : g_static_err.c_str(); }
+
+pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* bounds);
+
+pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_stream, pvr_ctx** out) {
+  if (!g || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
+  if (g->dims[0] < 1 || g->dims[1] < 1 || g->dims[2] < 1 || !(g->spacing_mm > 0))
+    return fail(nullptr, PVR_ERR_ARG, "invalid geometry (dims >= 1, spacing > 0)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(nullptr, PVR_ERR_CUDA, "no CUDA device available (libpvr has no CPU path)");
+  }
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(nullptr, PVR_ERR_ARG, "bad cuda_device");
+  pvr_ctx* c = new pvr_ctx();
+  memset(&c->st, 0, sizeof(c->st));
+  c->device = cuda_device;
+  c->dims = make_int3(g->dims[0], g->dims[1], g->dims[2]);
+  c->s = g->spacing_mm;
+  for (int d = 0; d < 3; ++d) c->o[d] = g->origin_mm[d];
+  c->V = (int64_t)g->dims[0] * g->dims[1] * g->dims[2];
+  cudaSetDevice(cuda_device);
+  if (cuda_stream) {
+    c->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return fail(nullptr, PVR_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    c->own_stream = true;
+  }
+  cudaError_t e1 = cudaMalloc(&c->X[0], c->V * sizeof(float));
+  cudaError_t e2 = cudaMalloc(&c->X[1], c->V * sizeof(float));
+  cudaError_t e3 = cudaMalloc(&c->AC, c->V * sizeof(float2));
+  cudaError_t e4 = cudaMalloc(&c->em, sizeof(EmDev));
+  cudaError_t e5 = cudaMalloc(&c->partials, (size_t)kStatBlocks * 5 * sizeof(double));
+  if (e1 || e2 || e3 || e4 || e5) {
+    cudaGetLastError();
+    free_dev(c);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return fail(nullptr, PVR_ERR_OOM, "device allocation of the volume buffers failed");
+  }
+  cudaMemsetAsync(c->X[0], 0, c->V * sizeof(float), c->stream);
+  cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), c->stream);
+  cudaMemsetAsync(c->em, 0, sizeof(EmDev), c->stream);
+  for (int i = 0; i < EV_N; ++i) cudaEventCreate(&c->ev[i]);
+  c->have_events = true;
+  c->st.voxels = c->V;
+  *out = c;
+  return PVR_OK;
+}
+
+pvr_status pvr_destroy(pvr_ctx* c) {
+  if (!c) return PVR_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_dev(c);
+  if (c->have_events)
+    for (int i = 0; i < EV_N; ++i) cudaEventDestroy(c->ev[i]);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return PVR_OK;
+}
+
+pvr_status pvr_comm_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, PVR_ERR_ARG, "null buffer");
+  std::string err;
+  if (!g_nccl.load(err)) return fail(nullptr, PVR_ERR_NCCL, "%s", err.c_str());
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, PVR_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+  memcpy(out128, &id, sizeof(id));
+  return PVR_OK;
+}
+
+pvr_status pvr_comm_init(pvr_ctx* c, int nranks, int rank, const void* uid) {
+  GUARD(c);
+  if (c->state >= PATCHED) return fail(c, PVR_ERR_STATE, "pvr_comm_init must precede extract_patches");
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !uid))
+    return fail(c, PVR_ERR_ARG, "invalid nranks/rank/unique id");
+  c->nranks = nranks;
+  c->rank = rank;
+  if (nranks == 1) return PVR_OK;
+  std::string err;
+  if (!g_nccl.load(err)) return fail(c, PVR_ERR_NCCL, "%s", err.c_str());
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  return nccl_check(c, g_nccl.CommInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+}
+
+pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
+  GUARD(c);
+  const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA;
+  if (extract_key && c->state >= PATCHED)
+    return fail(c, PVR_ERR_STATE, "parameter %d must be set before extract_patches", key);
+  switch (key) {
+    case PVR_PARAM_DELTA: if (!(v > 0)) goto bad; c->delta = v; break;
+    case PVR_PARAM_TAU_PATCH: c->tau_patch = v; break;
+    case PVR_PARAM_C0: if (!(v >= 0 && v <= 1)) goto bad; c->c0 = v; break;
+    case PVR_PARAM_TAU_LIVE: c->tau_live = v; break;
+    case PVR_PARAM_TAU_C: if (!(v >= 0)) goto bad; c->tau_C = v; break;
+    case PVR_PARAM_TAU_OBS: if (!(v > 0)) goto bad; c->tau_obs = v; break;
+    case PVR_PARAM_CLAMP: c->clamp = v != 0; break;
+    case PVR_PARAM_PSF_MODE: if (v != 0 && v != 1) goto bad; c->psf_mode = (int)v; break;
+    case PVR_PARAM_SIGMA2_FLOOR: if (!(v >= 0)) goto bad; c->s2floor = v; break;
+    case PVR_PARAM_PSF_NSIGMA: if (!(v > 0)) goto bad; c->nsigma = v; break;
+    case PVR_PARAM_PROFILE: c->profile = v != 0; break;
+    default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
+  }
+  return PVR_OK;
+bad:
+  return fail(c, PVR_ERR_ARG, "invalid value %g for parameter %d", v, key);
+}
+
+pvr_status pvr_add_stack(pvr_ctx* c, const float* slices, int W, int H, int K,
+                         const double G[12], double thickness, int* id_out) {
+  GUARD(c);
+  if (c->state > STACKS) return fail(c, PVR_ERR_STATE, "add_stack after extract_patches");
+  if (!slices || !G || W < 1 || H < 1 || K < 1 || !(thickness > 0))
+    return fail(c, PVR_ERR_ARG, "invalid stack (sizes >= 1, thickness > 0)");
+  HostStack st;
+  st.W = W; st.H = H; st.K = K;
+  memcpy(st.G, G, sizeof(st.G));
+  st.theta = thickness;
+  double c0[3] = {G[0], G[4], G[8]}, c1[3] = {G[1], G[5], G[9]}, c2[3] = {G[2], G[6], G[10]};
+  const double px = norm3(c0), py = norm3(c1);
+  if (!(px > 0) || !(py > 0)) return fail(c, PVR_ERR_ARG, "degenerate in-plane axes");
+  for (int d = 0; d < 3; ++d) { st.u[d] = c0[d] / px; st.v[d] = c1[d] / py; }
+  st.w[0] = st.u[1] * st.v[2] - st.u[2] * st.v[1];
+  st.w[1] = st.u[2] * st.v[0] - st.u[0] * st.v[2];
+  st.w[2] = st.u[0] * st.v[1] - st.u[1] * st.v[0];
+  const double nw = norm3(st.w);
+  if (!(nw > 1e-12)) return fail(c, PVR_ERR_ARG, "parallel in-plane axes");
+  for (int d = 0; d < 3; ++d) st.w[d] /= nw;
+  // a singular index->world map (zero slice step along the normal) is rejected too
+  const double det = c0[0] * (c1[1] * c2[2] - c1[2] * c2[1]) - c0[1] * (c1[0] * c2[2] - c1[2] * c2[0]) +
+                     c0[2] * (c1[0] * c2[1] - c1[1] * c2[0]);
+  if (K > 1 && !(std::fabs(det) > 1e-12)) return fail(c, PVR_ERR_ARG, "singular index_to_world");
+  const size_t bytes = (size_t)W * H * K * sizeof(float);
+  CUDA_TRY(c, cudaMalloc(&st.y_dev, bytes));
+  CUDA_TRY(c, cudaMemcpyAsync(st.y_dev, slices, bytes,
+                              is_device_ptr(slices) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->stacks.push_back(st);
+  if (id_out) *id_out = (int)c->stacks.size() - 1;
+  c->state = STACKS;
+  return PVR_OK;
+}
+
+// Contiguous shard plan balanced by cost (pixels x PSF samples): bounds[r] .. bounds[r+1]
+// is rank r's patch range ("distributing independent subsets of patches").
+pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* bounds) {
+  if (!cost || !bounds || M < 0 || nranks < 1) return fail(nullptr, PVR_ERR_ARG, "invalid shard plan args");
+  std::vector<int64_t> pre(M + 1, 0);
+  for (int64_t i = 0; i < M; ++i) pre[i + 1] = pre[i] + cost[i];
+  const int64_t total = pre[M];
+  bounds[0] = 0;
+  for (int r = 1; r < nranks; ++r) {
+    const double target = (double)total * r / nranks;
+    int64_t i = std::lower_bound(pre.begin(), pre.end(), (int64_t)std::ceil(target)) - pre.begin();
+    if (i > 0 && (target - pre[i - 1]) < (pre[std::min(i, M)] - target)) --i;
+    i = std::min(std::max(i, bounds[r - 1]), M);
+    bounds[r] = i;
+  }
+  bounds[nranks] = M;
+  return PVR_OK;
+}
+
+pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int stride_z, int64_t* n_out) {
+  GUARD(c);
+  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "extract_patches needs stacks and runs once");
+  if (size < 1 || stride < 1 || stride > size || depth < 1 || stride_z < 1 || stride_z > depth)
+    return fail(c, PVR_ERR_ARG, "invalid patch size/stride (1 <= stride <= size, 1 <= stride_z <= depth)");
+  for (auto& st : c->stacks)
+    if (size > st.W || size > st.H || depth > st.K)
+      return fail(c, PVR_ERR_ARG, "patch %dx%dx%d larger than a %dx%dx%d stack", size, size, depth,
+                  st.W, st.H, st.K);
+  // PSF tables (host fp64 -> device fp32)
+  std::vector<float4> table;
+  for (auto& st : c->stacks) build_psf(c, st, table);
+  // patch list, order stack, z0, y0, x0
+  c->patches.clear();
+  for (int si = 0; si < (int)c->stacks.size(); ++si) {
+    const HostStack& st = c->stacks[si];
+    for (int z0 : windows(st.K, depth, stride_z))
+      for (int y0 : windows(st.H, size, stride))
+        for (int x0 : windows(st.W, size, stride))
+          c->patches.push_back(HostPatch{si, x0, y0, z0, size, size, depth});
+  }
+  c->M = (int64_t)c->patches.size();
+  if (c->M == 0) return fail(c, PVR_ERR_EMPTY, "no patches");
+  c->pix0_global.assign(c->M + 1, 0);
+  std::vector<int64_t> cost(c->M);
+  for (int64_t s = 0; s < c->M; ++s) {
+    const HostPatch& hp = c->patches[s];
+    const int64_t npx = (int64_t)hp.sx * hp.sy * hp.sz;
+    c->pix0_global[s + 1] = c->pix0_global[s] + npx;
+    cost[s] = npx * c->stacks[hp.stack].S;
+  }
+  c->P = c->pix0_global[c->M];
+  std::vector<int64_t> bounds(c->nranks + 1);
+  pvr_plan_shards(cost.data(), c->M, c->nranks, bounds.data());
+  c->first = bounds[c->rank];
+  c->nloc = bounds[c->rank + 1] - bounds[c->rank];
+  c->first_pix = c->pix0_global[c->first];
+  c->nloc_pix = c->pix0_global[c->first + c->nloc] - c->first_pix;
+  // concatenated stacks
+  int64_t L = 0;
+  for (auto& st : c->stacks) { st.y_off = L; L += (int64_t)st.W * st.H * st.K; }
+  CUDA_TRY(c, cudaMalloc(&c->ys, std::max<int64_t>(L, 1) * sizeof(float)));
+  for (auto& st : c->stacks) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->ys + st.y_off, st.y_dev, (size_t)st.W * st.H * st.K * sizeof(float),
+                                cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (auto& st : c->stacks) { cudaFree(st.y_dev); st.y_dev = nullptr; }
+  // per-pixel / per-patch arrays of the local shard
+  const size_t np = (size_t)std::max<int64_t>(c->nloc_pix, 1), mp = (size_t)std::max<int64_t>(c->nloc, 1);
+  CUDA_TRY(c, cudaMalloc(&c->e, np * sizeof(float)));
+  CUDA_TRY(c, cudaMalloc(&c->p, np * sizeof(float)));
+  CUDA_TRY(c, cudaMalloc(&c->kap, np * sizeof(float)));
+  CUDA_TRY(c, cudaMalloc(&c->pbar, mp * sizeof(float)));
+  CUDA_TRY(c, cudaMalloc(&c->w, mp * sizeof(float)));
+  CUDA_TRY(c, cudaMalloc(&c->pdev, mp * sizeof(PatchDev)));
+  CUDA_TRY(c, cudaMalloc(&c->psf, std::max<size_t>(table.size(), 1) * sizeof(float4)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->psf, table.data(), table.size() * sizeof(float4), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->e, 0, np * sizeof(float), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->p, 0, np * sizeof(float), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->kap, 0, np * sizeof(float), c->stream));
+  // pixel tiles of kTile pixels, never straddling a patch
+  std::vector<int2> tl;
+  for (int64_t s = 0; s < c->nloc; ++s) {
+    const HostPatch& hp = c->patches[c->first + s];
+    const int npx = hp.sx * hp.sy * hp.sz;
+    for (int off = 0; off < npx; off += kTile) tl.push_back(make_int2((int)s, off));
+  }
+  c->ntiles = (int64_t)tl.size();
+  CUDA_TRY(c, cudaMalloc(&c->tiles, std::max<size_t>(tl.size(), 1) * sizeof(int2)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->st.pixels = c->nloc_pix;
+  c->st.patches = c->nloc;
+  c->state = PATCHED;
+  if (n_out) *n_out = c->M;
+  return PVR_OK;
+}
+
+pvr_status pvr_get_shard(const pvr_ctx* c, int64_t* first, int64_t* nloc, int64_t* fpix, int64_t* npix) {
+  if (!c) return fail(nullptr, PVR_ERR_ARG, "null context");
+  if (c->state < PATCHED) return fail(const_cast<pvr_ctx*>(c), PVR_ERR_STATE, "no patches yet");
+  if (first) *first = c->first;
+  if (nloc) *nloc = c->nloc;
+  if (fpix) *fpix = c->first_pix;
+  if (npix) *npix = c->nloc_pix;
+  return PVR_OK;
+}
+
+pvr_status pvr_get_patches(const pvr_ctx* c, int32_t* out) {
+  if (!c || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
+  if (c->state < PATCHED) return fail(const_cast<pvr_ctx*>(c), PVR_ERR_STATE, "no patches yet");
+  for (int64_t s = 0; s < c->nloc; ++s) {
+    const HostPatch& hp = c->patches[c->first + s];
+    const int32_t v[7] = {hp.stack, hp.x0, hp.y0, hp.z0, hp.sx, hp.sy, hp.sz};
+    memcpy(out + 7 * s, v, sizeof(v));
+  }
+  return PVR_OK;
+}
+
+pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
+  GUARD(c);
+  if (c->state < PATCHED) return fail(c, PVR_ERR_STATE, "set_transforms needs extract_patches");
+  if (!T || n != c->M) return fail(c, PVR_ERR_ARG, "expected %lld transforms, got %lld", (long long)c->M, (long long)n);
+  std::vector<double> Th((size_t)12 * c->nloc);
+  const double* Tl = T + 12 * c->first;
+  if (is_device_ptr(T)) {
+    CUDA_TRY(c, cudaMemcpy(Th.data(), Tl, Th.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  } else {
+    memcpy(Th.data(), Tl, Th.size() * sizeof(double));
+  }
+  // compose, per patch, in fp64: voxel index of lattice point (a,b,c) of pixel (u,v,z) is
+  // g(T_s(G (x0+u, y0+v, z0+z, 1) + a h_u u^ + b h_v v^ + c h_w w^)), g(x) = (x - o) / s
+  std::vector<PatchDev> pd(c->nloc);
+  const double is = 1.0 / c->s;
+  for (int64_t s = 0; s < c->nloc; ++s) {
+    const HostPatch& hp = c->patches[c->first + s];
+    const HostStack& st = c->stacks[hp.stack];
+    const double* A = &Th[12 * s];
+    auto lin = [&](const double* vec, float* out, double scale) {
+      for (int d = 0; d < 3; ++d)
+        out[d] = (float)(scale * (A[4 * d] * vec[0] + A[4 * d + 1] * vec[1] + A[4 * d + 2] * vec[2]));
+    };
+    PatchDev& q = pd[s];
+    memset(&q, 0, sizeof(q));
+    const double gu[3] = {st.G[0], st.G[4], st.G[8]}, gv[3] = {st.G[1], st.G[5], st.G[9]},
+                 gz[3] = {st.G[2], st.G[6], st.G[10]};
+    lin(gu, q.Mu, is);
+    lin(gv, q.Mv, is);
+    lin(gz, q.Mz, is);
+    const double qa[3] = {st.h[0] * st.u[0], st.h[0] * st.u[1], st.h[0] * st.u[2]};
+    const double qb[3] = {st.h[1] * st.v[0], st.h[1] * st.v[1], st.h[1] * st.v[2]};
+    const double qc[3] = {st.h[2] * st.w[0], st.h[2] * st.w[1], st.h[2] * st.w[2]};
+    lin(qa, q.Qa, is);
+    lin(qb, q.Qb, is);
+    lin(qc, q.Qc, is);
+    double w0[3];
+    for (int d = 0; d < 3; ++d)
+      w0[d] = st.G[4 * d] * hp.x0 + st.G[4 * d + 1] * hp.y0 + st.G[4 * d + 2] * hp.z0 + st.G[4 * d + 3];
+    for (int d = 0; d < 3; ++d) {
+      const double wd = A[4 * d] * w0[0] + A[4 * d + 1] * w0[1] + A[4 * d + 2] * w0[2] + A[4 * d + 3];
+      const double x = (wd - c->o[d]) * is;
+      const double b = std::floor(x);
+      q.base[d] = (int32_t)b;
+      q.frac[d] = (float)(x - b);
+    }
+    q.stack = hp.stack;
+    q.x0 = hp.x0; q.y0 = hp.y0; q.z0 = hp.z0;
+    q.sx = hp.sx; q.sy = hp.sy; q.sz = hp.sz;
+    q.pix0 = c->pix0_global[c->first + s] - c->first_pix;
+    q.W = st.W;
+    q.HW = st.W * st.H;
+    q.y0off = st.y_off + ((int64_t)hp.z0 * st.H + hp.y0) * st.W + hp.x0;
+    q.psf0 = st.psf0;
+    q.S = st.S;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
+  // coverage kappa (geometry only) + live-y range, then the EM reset
+  const Params prm = make_params(c);
+  launch_coverage(c->stream, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap, c->partials);
+  CHECK_LAUNCH(c);
+  launch_em_reduce(c->stream, c->partials, kStatBlocks, c->em);
+  CHECK_LAUNCH(c);
+  pvr_status r = allreduce_stats(c);
+  if (r != PVR_OK) return r;
+  launch_range_finish(c->stream, c->s2floor, c->em);
+  CHECK_LAUNCH(c);
+  launch_fill(c->stream, c->p, c->nloc_pix, 1.0f);
+  launch_fill(c->stream, c->pbar, c->nloc, 1.0f);
+  launch_fill(c->stream, c->w, c->nloc, 1.0f);
+  CHECK_LAUNCH(c);
+  EmDev h;
+  CUDA_TRY(c, cudaMemcpyAsync(&h, c->em, sizeof(EmDev), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (!(h.stats[0] > 0)) return fail(c, PVR_ERR_EMPTY, "no observed pixel: nothing to reconstruct");
+  // PSF samples visited per iteration (observed pixels x S, all ranks after the allreduce)
+  c->samples_obs = (int64_t)h.stats[2];
+  c->state = READY;
+  return PVR_OK;
+}
+
+pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
+  GUARD(c);
+  if (!x || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
+  CUDA_TRY(c, cudaMemcpyAsync(c->X[c->cur], x, nvox * sizeof(float),
+                              is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_init_volume(pvr_ctx* c) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
+  const Params prm = make_params(c);
+  CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), c->stream));
+  launch_backproject(c->stream, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap,
+                     c->e, c->p, c->w, 1, c->AC);
+  CHECK_LAUNCH(c);
+  pvr_status r = allreduce_ac(c);
+  if (r != PVR_OK) return r;
+  launch_init_fill(c->stream, c->AC, c->dims, prm, c->X[c->cur]);
+  CHECK_LAUNCH(c);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "sr_iterate needs set_transforms");
+  if (n < 0 || !(alpha >= 0) || !(lambda >= 0)) return fail(c, PVR_ERR_ARG, "n, alpha, lambda must be >= 0");
+  const Params prm = make_params(c);
+  const bool prof = c->profile != 0;
+  cudaStream_t s = c->stream;
+  double ms[6] = {0, 0, 0, 0, 0, 0};
+  for (int it = 0; it < n; ++it) {
+    float* X0 = c->X[c->cur];
+    float* X2 = c->X[1 - c->cur];
+    if (prof) cudaEventRecord(c->ev[EV_FWD0], s);
+    launch_forward(s, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, X0, c->dims, prm, c->kap, c->p,
+                   c->e, c->partials);
+    CHECK_LAUNCH(c);
+    if (prof) cudaEventRecord(c->ev[EV_FWD1], s);
+    launch_em_reduce(s, c->partials, kStatBlocks, c->em);
+    CHECK_LAUNCH(c);
+    pvr_status r = allreduce_stats(c);
+    if (r != PVR_OK) return r;
+    launch_em_params(s, prm, c->em);
+    CHECK_LAUNCH(c);
+    if (prof) cudaEventRecord(c->ev[EV_EM1], s);
+    launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w);
+    CHECK_LAUNCH(c);
+    if (prof) cudaEventRecord(c->ev[EV_EST1], s);
+    CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), s));
+    launch_backproject(s, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap, c->e,
+                       c->p, c->w, 0, c->AC);
+    CHECK_LAUNCH(c);
+    if (prof) cudaEventRecord(c->ev[EV_BP1], s);
+    r = allreduce_ac(c);
+    if (r != PVR_OK) return r;
+    if (prof) cudaEventRecord(c->ev[EV_AR1], s);
+    launch_update(s, X0, c->AC, c->dims, prm, c->em, alpha, lambda, X2);
+    CHECK_LAUNCH(c);
+    if (prof) {
+      cudaEventRecord(c->ev[EV_UPD1], s);
+      CUDA_TRY(c, cudaEventSynchronize(c->ev[EV_UPD1]));
+      float t[6];
+      cudaEventElapsedTime(&t[0], c->ev[EV_FWD0], c->ev[EV_FWD1]);
+      cudaEventElapsedTime(&t[1], c->ev[EV_FWD1], c->ev[EV_EM1]);
+      cudaEventElapsedTime(&t[2], c->ev[EV_EM1], c->ev[EV_EST1]);
+      cudaEventElapsedTime(&t[3], c->ev[EV_EST1], c->ev[EV_BP1]);
+      cudaEventElapsedTime(&t[4], c->ev[EV_BP1], c->ev[EV_AR1]);
+      cudaEventElapsedTime(&t[5], c->ev[EV_AR1], c->ev[EV_UPD1]);
+      for (int i = 0; i < 6; ++i) ms[i] += t[i];
+    }
+    c->cur = 1 - c->cur;
+    c->st.iterations += 1;
+    c->st.psf_samples += c->samples_obs;
+    c->st.kernel_launches += 6;  // forward, em_reduce, em_params, estep, backproject, update
+    c->st.n_forward += 1; c->st.n_em += 1; c->st.n_estep += 1; c->st.n_backproject += 1;
+    c->st.n_update += 1;
+    if (c->nranks > 1) c->st.n_allreduce += 1;
+  }
+  c->st.ms_forward += ms[0];
+  c->st.ms_em += ms[1];
+  c->st.ms_estep += ms[2];
+  c->st.ms_backproject += ms[3];
+  c->st.ms_allreduce += ms[4];
+  c->st.ms_update += ms[5];
+  if ((double)alpha * lambda > 3.0 / 44.0)
+    c->err = "warning: alpha*lambda > 3/44, the regulariser's maximum principle does not hold";
+  return PVR_OK;
+}
+
+pvr_status pvr_get_volume(pvr_ctx* c, float* out, size_t nvox) {
+  GUARD(c);
+  if (!out || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
+  CUDA_TRY(c, cudaMemcpyAsync(out, c->X[c->cur], nvox * sizeof(float),
+                              is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+static pvr_status copy_out(pvr_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!dst || bytes == 0) return PVR_OK;
+  CUDA_TRY(c, cudaMemcpyAsync(dst, src, bytes, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_get_weights(pvr_ctx* c, float* pp, float* pw, float* pb) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "no weights before set_transforms");
+  pvr_status r;
+  if ((r = copy_out(c, pp, c->p, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
+  if ((r = copy_out(c, pw, c->w, c->nloc * sizeof(float))) != PVR_OK) return r;
+  if ((r = copy_out(c, pb, c->pbar, c->nloc * sizeof(float))) != PVR_OK) return r;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_get_taps(pvr_ctx* c, float* e, float* kap, float* A, float* C) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "no taps before set_transforms");
+  pvr_status r;
+  if ((r = copy_out(c, e, c->e, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
+  if ((r = copy_out(c, kap, c->kap, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
+  if (A || C) {
+    std::vector<float2> ac(c->V);
+    CUDA_TRY(c, cudaMemcpyAsync(ac.data(), c->AC, c->V * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    std::vector<float> a(c->V), cc(c->V);
+    for (int64_t k = 0; k < c->V; ++k) { a[k] = ac[k].x; cc[k] = ac[k].y; }
+    float* dsts[2] = {A, C};
+    const std::vector<float>* srcs[2] = {&a, &cc};
+    for (int i = 0; i < 2; ++i) {
+      if (!dsts[i]) continue;
+      if (is_device_ptr(dsts[i])) {
+        CUDA_TRY(c, cudaMemcpy(dsts[i], srcs[i]->data(), c->V * sizeof(float), cudaMemcpyHostToDevice));
+      } else {
+        memcpy(dsts[i], srcs[i]->data(), c->V * sizeof(float));
+      }
+    }
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_get_em_state(pvr_ctx* c, double* sigma2, double* cc, double* m, int64_t* it, double* lo,
+                            double* hi) {
+  GUARD(c);
+  EmDev h;
+  CUDA_TRY(c, cudaMemcpyAsync(&h, c->em, sizeof(EmDev), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (sigma2) *sigma2 = h.sigma2;
+  if (cc) *cc = h.c;
+  if (m) *m = h.m;
+  if (it) *it = h.t;
+  if (lo) *lo = h.lo;
+  if (hi) *hi = h.hi;
+  return PVR_OK;
+}
+
+pvr_status pvr_get_stats(const pvr_ctx* c, pvr_stats* out) {
+  if (!c || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
+  *out = c->st;
+  return PVR_OK;
+}
+
+pvr_status pvr_reset_stats(pvr_ctx* c) {
+  if (!c) return fail(nullptr, PVR_ERR_ARG, "null context");
+  const int64_t px = c->st.pixels, vx = c->st.voxels, pt = c->st.patches;
+  memset(&c->st, 0, sizeof(c->st));
+  c->st.pixels = px; c->st.voxels = vx; c->st.patches = pt;
+  return PVR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+"""GPU (libpvr, fp32 CUDA) vs oracle (fp64 CPU) parity on seeded synthetic problems.
+
+Tolerances are north_star's (BASELINE.json): volume within 1e-4 relative L2 after every
+iteration (free-running, both sides iterate from the same start); pixel posteriors and
+patch weights within 1e-3 absolute. Stage taps (e, kappa, A, C, EM scalars) are checked
+with the tolerances DESIGN.md §Parity derives from fp32 arithmetic.
+"""
+import numpy as np
+import pytest
+
+import synth
+from helpers import make_gpu, make_oracle, rel_l2, weight_mismatch
+
+pytestmark = pytest.mark.gpu
+
+
+def run_pair(prob, iters, params=None, init=True, X0=None, check_taps=True):
+    orc = make_oracle(prob, params)
+    ctx = make_gpu(prob, params)
+    try:
+        if X0 is not None:
+            orc.set_volume(X0)
+            ctx.set_volume(np.ascontiguousarray(X0, np.float32))
+        elif init:
+            orc.init_volume()
+            ctx.init_volume()
+        rel0 = rel_l2(ctx.volume(), orc.volume())
+        assert rel0 <= 1e-5, f"initial volume rel L2 {rel0:.3e}"
+        # coverage is geometry only: kappa parity and threshold margins
+        _, kap_o, _, _ = orc.taps()
+        _, kap_g, _, _ = ctx.taps()
+        assert np.abs(kap_g - kap_o).max() <= 2e-5
+        hist = []
+        for it in range(iters):
+            orc.sr_iterate(1, prob["alpha"], prob["lam"])
+            ctx.sr_iterate(1, prob["alpha"], prob["lam"])
+            Xo, Xg = orc.volume(), ctx.volume()
+            rel = rel_l2(Xg, Xo)
+            po, pbo, wo = orc.weights()
+            pg, pbg, wg = ctx.weights()
+            dp, dw, near = weight_mismatch(pg, po, pbg, pbo, wg, wo)
+            emo, emg = orc.em_state(), ctx.em_state()
+            hist.append((rel, dp, dw, near))
+            assert emg["t"] == emo["t"] == it + 1
+            for key in ("sigma2", "c", "m"):
+                assert abs(emg[key] - emo[key]) <= 1e-4 * max(abs(emo[key]), 1e-30), (key, emg, emo)
+            if check_taps:
+                eo, _, Ao, Co = orc.taps()
+                eg, _, Ag, Cg = ctx.taps()
+                assert rel_l2(eg, eo) <= 1e-3, "residual e"
+                assert rel_l2(Cg, Co) <= 1e-4, "confidence C"
+                assert rel_l2(Ag, Ao) <= 2e-3, "addon A"
+            assert rel <= 1e-4, f"iteration {it + 1}: volume rel L2 {rel:.3e}"
+            assert dp <= 1e-3, f"iteration {it + 1}: max |dp| {dp:.3e}"
+            assert dw <= 1e-3, f"iteration {it + 1}: max |dw| {dw:.3e}"
+        return hist
+    finally:
+        ctx.close()
+
+
+def test_c1_phantom_two_iterations():
+    prob = synth.make_problem("c1")
+    run_pair(prob, prob["iters"])
+
+
+def test_c1_more_iterations():
+    prob = synth.make_problem("c1")
+    run_pair(prob, 6)
+
+
+def test_c2_svr_mode():
+    prob = synth.make_problem("c2")
+    run_pair(prob, 3)
+
+
+def test_c3_structure_small():
+    """c3's structure (4 stacks, 64x64 patches at 50% overlap, breathing motion with
+    per-patch mismatch) on a cropped grid the oracle finishes in seconds."""
+    prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
+    run_pair(prob, 2)
+
+
+def test_c4_3d_patches_corrupted_small():
+    """c4's structure: 3D 4-slice patches, per-slab affine motion, 10% gross errors."""
+    prob = synth.make_problem("c4", scale=(96, 96, 16), size=32, stride=16)
+    run_pair(prob, 2)
+
+
+def test_oblique_stacks_small():
+    """c5's oblique stacks (30 deg about x, 45 deg about y) and dense 75% overlap."""
+    prob = synth.make_problem("c5", scale=(64, 64, 12), size=16, stride=4)
+    run_pair(prob, 1)
