@@ -106,10 +106,10 @@ struct pvr_ctx {
   int64_t ntiles = 0;
   double* partials = nullptr;
   EmDev* em = nullptr;
-  // stats
+  // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of
+  // the pool, drained (synchronised) only by pvr_get_stats or when the pool is large
   pvr_stats st;
-  cudaEvent_t ev[16];
-  bool have_events = false;
+  std::vector<std::vector<cudaEvent_t>> prof_free, prof_pending;
 };
 
 namespace {
@@ -275,6 +275,33 @@ void free_dev(pvr_ctx* c) {
 // profiling: events bracket each kernel group when PVR_PARAM_PROFILE is on
 enum { EV_FWD0, EV_FWD1, EV_EM1, EV_EST1, EV_BP1, EV_AR1, EV_UPD1, EV_N };
 
+std::vector<cudaEvent_t>* prof_slot(pvr_ctx* c) {
+  if (c->prof_free.empty()) {
+    std::vector<cudaEvent_t> s(EV_N);
+    for (auto& e : s) cudaEventCreate(&e);
+    c->prof_free.push_back(s);
+  }
+  c->prof_pending.push_back(c->prof_free.back());
+  c->prof_free.pop_back();
+  return &c->prof_pending.back();
+}
+
+void prof_drain(pvr_ctx* c) {
+  for (auto& s : c->prof_pending) {
+    cudaEventSynchronize(s[EV_UPD1]);
+    float t[6];
+    for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&t[i], s[i], s[i + 1]);
+    c->st.ms_forward += t[0];
+    c->st.ms_em += t[1];
+    c->st.ms_estep += t[2];
+    c->st.ms_backproject += t[3];
+    c->st.ms_allreduce += t[4];
+    c->st.ms_update += t[5];
+    c->prof_free.push_back(s);
+  }
+  c->prof_pending.clear();
+}
+
 }  // namespace
 
 // ======================================================================================
@@ -328,8 +355,6 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   cudaMemsetAsync(c->X[0], 0, c->V * sizeof(float), c->stream);
   cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), c->stream);
   cudaMemsetAsync(c->em, 0, sizeof(EmDev), c->stream);
-  for (int i = 0; i < EV_N; ++i) cudaEventCreate(&c->ev[i]);
-  c->have_events = true;
   c->st.voxels = c->V;
   *out = c;
   return PVR_OK;
@@ -340,8 +365,9 @@ pvr_status pvr_destroy(pvr_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_dev(c);
-  if (c->have_events)
-    for (int i = 0; i < EV_N; ++i) cudaEventDestroy(c->ev[i]);
+  for (auto* pool : {&c->prof_free, &c->prof_pending})
+    for (auto& slot : *pool)
+      for (auto e : slot) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -630,6 +656,11 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   if (!(h.stats[0] > 0)) return fail(c, PVR_ERR_EMPTY, "no observed pixel: nothing to reconstruct");
   // PSF samples visited per iteration (observed pixels x S, all ranks after the allreduce)
   c->samples_obs = (int64_t)h.stats[2];
+  // algorithmic HBM bytes per launch: compulsory reads/writes only
+  c->st.bytes_alg_forward = 16 * c->nloc_pix + 4 * c->V + 48 * c->nloc;   // y,kap,p in; e out; X; T
+  c->st.bytes_alg_estep = 12 * c->nloc_pix + 8 * c->nloc;                  // kap,e in; p out; pbar,w
+  c->st.bytes_alg_backproject = 12 * c->nloc_pix + 8 * c->V + 4 * c->nloc; // kap,e,p in; A,C out
+  c->st.bytes_alg_update = 16 * c->V;                                      // X0,A,C in; X2 out
   c->state = READY;
   return PVR_OK;
 }
@@ -666,47 +697,36 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   const Params prm = make_params(c);
   const bool prof = c->profile != 0;
   cudaStream_t s = c->stream;
-  double ms[6] = {0, 0, 0, 0, 0, 0};
   for (int it = 0; it < n; ++it) {
     float* X0 = c->X[c->cur];
     float* X2 = c->X[1 - c->cur];
-    if (prof) cudaEventRecord(c->ev[EV_FWD0], s);
+    std::vector<cudaEvent_t>* ev = prof ? prof_slot(c) : nullptr;
+    if (prof) cudaEventRecord((*ev)[EV_FWD0], s);
     launch_forward(s, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, X0, c->dims, prm, c->kap, c->p,
                    c->e, c->partials);
     CHECK_LAUNCH(c);
-    if (prof) cudaEventRecord(c->ev[EV_FWD1], s);
+    if (prof) cudaEventRecord((*ev)[EV_FWD1], s);
     launch_em_reduce(s, c->partials, kStatBlocks, c->em);
     CHECK_LAUNCH(c);
     pvr_status r = allreduce_stats(c);
     if (r != PVR_OK) return r;
     launch_em_params(s, prm, c->em);
     CHECK_LAUNCH(c);
-    if (prof) cudaEventRecord(c->ev[EV_EM1], s);
+    if (prof) cudaEventRecord((*ev)[EV_EM1], s);
     launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w);
     CHECK_LAUNCH(c);
-    if (prof) cudaEventRecord(c->ev[EV_EST1], s);
+    if (prof) cudaEventRecord((*ev)[EV_EST1], s);
     CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), s));
     launch_backproject(s, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap, c->e,
                        c->p, c->w, 0, c->AC);
     CHECK_LAUNCH(c);
-    if (prof) cudaEventRecord(c->ev[EV_BP1], s);
+    if (prof) cudaEventRecord((*ev)[EV_BP1], s);
     r = allreduce_ac(c);
     if (r != PVR_OK) return r;
-    if (prof) cudaEventRecord(c->ev[EV_AR1], s);
+    if (prof) cudaEventRecord((*ev)[EV_AR1], s);
     launch_update(s, X0, c->AC, c->dims, prm, c->em, alpha, lambda, X2);
     CHECK_LAUNCH(c);
-    if (prof) {
-      cudaEventRecord(c->ev[EV_UPD1], s);
-      CUDA_TRY(c, cudaEventSynchronize(c->ev[EV_UPD1]));
-      float t[6];
-      cudaEventElapsedTime(&t[0], c->ev[EV_FWD0], c->ev[EV_FWD1]);
-      cudaEventElapsedTime(&t[1], c->ev[EV_FWD1], c->ev[EV_EM1]);
-      cudaEventElapsedTime(&t[2], c->ev[EV_EM1], c->ev[EV_EST1]);
-      cudaEventElapsedTime(&t[3], c->ev[EV_EST1], c->ev[EV_BP1]);
-      cudaEventElapsedTime(&t[4], c->ev[EV_BP1], c->ev[EV_AR1]);
-      cudaEventElapsedTime(&t[5], c->ev[EV_AR1], c->ev[EV_UPD1]);
-      for (int i = 0; i < 6; ++i) ms[i] += t[i];
-    }
+    if (prof) cudaEventRecord((*ev)[EV_UPD1], s);
     c->cur = 1 - c->cur;
     c->st.iterations += 1;
     c->st.psf_samples += c->samples_obs;
@@ -714,13 +734,8 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     c->st.n_forward += 1; c->st.n_em += 1; c->st.n_estep += 1; c->st.n_backproject += 1;
     c->st.n_update += 1;
     if (c->nranks > 1) c->st.n_allreduce += 1;
+    if (c->prof_pending.size() >= 512) prof_drain(c);
   }
-  c->st.ms_forward += ms[0];
-  c->st.ms_em += ms[1];
-  c->st.ms_estep += ms[2];
-  c->st.ms_backproject += ms[3];
-  c->st.ms_allreduce += ms[4];
-  c->st.ms_update += ms[5];
   if ((double)alpha * lambda > 3.0 / 44.0)
     c->err = "warning: alpha*lambda > 3/44, the regulariser's maximum principle does not hold";
   return PVR_OK;
@@ -795,17 +810,26 @@ pvr_status pvr_get_em_state(pvr_ctx* c, double* sigma2, double* cc, double* m, i
   return PVR_OK;
 }
 
-pvr_status pvr_get_stats(const pvr_ctx* c, pvr_stats* out) {
-  if (!c || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
+pvr_status pvr_get_stats(const pvr_ctx* cc, pvr_stats* out) {
+  if (!cc || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
+  pvr_ctx* c = const_cast<pvr_ctx*>(cc);
+  cudaSetDevice(c->device);
+  prof_drain(c);
   *out = c->st;
   return PVR_OK;
 }
 
 pvr_status pvr_reset_stats(pvr_ctx* c) {
   if (!c) return fail(nullptr, PVR_ERR_ARG, "null context");
-  const int64_t px = c->st.pixels, vx = c->st.voxels, pt = c->st.patches;
+  cudaSetDevice(c->device);
+  prof_drain(c);
+  pvr_stats keep = c->st;
   memset(&c->st, 0, sizeof(c->st));
-  c->st.pixels = px; c->st.voxels = vx; c->st.patches = pt;
+  c->st.pixels = keep.pixels; c->st.voxels = keep.voxels; c->st.patches = keep.patches;
+  c->st.bytes_alg_forward = keep.bytes_alg_forward;
+  c->st.bytes_alg_estep = keep.bytes_alg_estep;
+  c->st.bytes_alg_backproject = keep.bytes_alg_backproject;
+  c->st.bytes_alg_update = keep.bytes_alg_update;
   return PVR_OK;
 }
 
