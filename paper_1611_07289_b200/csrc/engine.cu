@@ -1,10 +1,11 @@
 // engine.cu — host engine and C ABI of libpvr.so (include/pvr.h).
 //
-// Host side, in fp64: the state machine, stack frames and PSF tables (P:158-160,
-// readings Q1-Q5), square-patch extraction (Q22), the shard plan (Q21),
-// and the per-patch composition of index->world, T_s and world->voxel maps (P:58,
-// Q7) that the kernels consume as fp32 (DESIGN.md §Data layout). Device side: the
-// kernels of kernels.cu, issued on the context's stream, plus the NCCL layer (dlopen'd).
+// Host side, in fp64: the state machine, stack frames and separable PSF tables (P:158-160,
+// readings Q1-Q5), square-patch extraction (Q22), the shard plan (Q21), the
+// per-patch composition of index->world, T_s and world->voxel maps (Q7), and the work
+// plan of the lattice kernels (member tiles grouped by shared stack pixels, each group with
+// its voxel bounding box). The kernels (kernels.cu, lattice.cu) consume fp32 copies. Device
+// work is issued on the context's stream; NCCL is dlopen'd at pvr_comm_init.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -14,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/pvr.h"
@@ -30,13 +32,20 @@ struct HostStack {
   double G[12];
   double theta;
   double u[3], v[3], w[3], h[3];  // in-plane axes, slice normal, PSF lattice steps (mm)
-  int S = 0, psf0 = 0;
+  int S = 0;                       // PSF samples (direct count)
+  StackPsf psf;                    // separable factors (offsets into the float table)
   float* y_dev = nullptr;          // device copy of the slices (until extract)
   int64_t y_off = 0;               // offset in the concatenated stack buffer
 };
 
 struct HostPatch {
   int32_t stack, x0, y0, z0, sx, sy, sz;
+};
+
+// fp64 geometry of one local patch: voxel index of lattice point (U, V, c) of slice z is
+// t0 + z Mz + U Qa + V Qb + c Qc
+struct PatchGeo {
+  double t0[3], Mz[3], Qa[3], Qb[3], Qc[3];
 };
 
 // ---- NCCL, loaded at pvr_comm_init (no link-time dependency) ----
@@ -75,8 +84,9 @@ struct pvr_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int3 dims;
+  int nxp = 0;  // (A, C) row pitch: nx rounded up to even (16-byte aligned voxel pairs)
   double s, o[3];
-  int64_t V;
+  int64_t V, Vp;  // voxels; padded (A, C) entries
   int state = CREATED;
   bool poisoned = false;
   std::string err;
@@ -86,11 +96,15 @@ struct pvr_ctx {
   double s2floor = 1e-6, nsigma = 3.0;
   // stacks / patches
   std::vector<HostStack> stacks;
-  std::vector<HostPatch> patches;   // global list
-  std::vector<int64_t> pix0_global; // [M+1]
+  std::vector<float> psf_tab;        // separable PSF factors of all stacks
+  std::vector<HostPatch> patches;    // global list
+  std::vector<int64_t> pix0_global;  // [M+1]
   int64_t M = 0, P = 0;
   int64_t first = 0, nloc = 0, first_pix = 0, nloc_pix = 0;
-  int64_t samples_obs = 0;          // observed local pixels x S (per iteration)
+  int64_t samples_obs = 0;           // observed pixels x S per iteration (all ranks)
+  // work plan of the lattice kernels
+  int TU = 16, TV = 16;
+  int ngroups = 0, nfallback = 0, tile_bytes = 0, r_bytes = 0, t_bytes = 0;
   // comm
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -100,21 +114,23 @@ struct pvr_ctx {
   float2* AC = nullptr;
   float *e = nullptr, *p = nullptr, *kap = nullptr, *pbar = nullptr, *w = nullptr;
   float* ys = nullptr;
-  float4* psf = nullptr;
+  float* tab = nullptr;
+  StackPsf* psf = nullptr;
   PatchDev* pdev = nullptr;
-  int2* tiles = nullptr;
-  int64_t ntiles = 0;
+  MemberDev* mem = nullptr;
+  GroupDev* grp = nullptr;
+  size_t mem_cap = 0, grp_cap = 0;
   double* partials = nullptr;
   EmDev* em = nullptr;
-  // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of
-  // the pool, drained (synchronised) only by pvr_get_stats or when the pool is large
+  // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of the
+  // pool, drained (synchronised) only by pvr_get_stats or when the pool is large
   pvr_stats st;
   std::vector<std::vector<cudaEvent_t>> prof_free, prof_pending;
 };
 
 namespace {
 
-const char* kVersion = "pvr-b200 0.1 (sm_100a)";
+const char* kVersion = "pvr-b200 0.2 (sm_100a, lattice kernels)";
 thread_local std::string g_static_err = "no context";
 
 pvr_status fail(pvr_ctx* c, pvr_status s, const char* fmt, ...) {
@@ -178,45 +194,73 @@ int psf_steps(double pitch, double s) {  // reading Q5: n = max(2, ceil(pitch / 
   return std::max(2, n);
 }
 
-// PSF lattice of one stack: psi(a,b,c) ~ sinc(pi R) * exp(-(c h_w)^2 / 2 sw^2),
-// R = |(a/n_u, b/n_v)| < 1 (main lobe, Q2), |c h_w| <= nsigma sw (Q3); normalised to 1.
-void build_psf(const pvr_ctx* c, HostStack& st, std::vector<float4>& table) {
-  st.psf0 = (int)table.size();
-  if (c->psf_mode == 1) {  // test-only delta PSF
-    table.push_back(make_float4(0.f, 0.f, 0.f, 1.f));
+// PSF of one stack: psi(a,b,c) ~ sinc(pi R) exp(-(c h_w)^2 / 2 sw^2) with
+// R = |(a/n_u, b/n_v)| < 1 (main lobe, Q2), |c h_w| <= nsigma sw (Q3), normalised to 1.
+// Stored as its two factors ip(a,b) = sinc / sum sinc and tp(c) = g / sum g, whose product is
+// psi; the product is checked in fp64 against the directly normalised table.
+pvr_status build_psf(pvr_ctx* c, HostStack& st) {
+  StackPsf& ps = st.psf;
+  if (c->psf_mode == 1) {  // test-only delta PSF: one sample at the pixel centre
+    ps.nu = ps.nv = 1; ps.ru = ps.rv = 0; ps.cmax = 0;
+    ps.ip0 = (int)c->psf_tab.size(); c->psf_tab.push_back(1.0f);
+    ps.tp0 = (int)c->psf_tab.size(); c->psf_tab.push_back(1.0f);
+    ps.tpmax = 1.0f;
     st.S = 1;
-    st.h[0] = st.h[1] = st.h[2] = 0.0;
-    return;
+    const double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
+    st.h[0] = norm3(c0); st.h[1] = norm3(c1); st.h[2] = 0.0;  // Qa = Mu, Qb = Mv
+    return PVR_OK;
   }
-  double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
+  const double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
   const double px = norm3(c0), py = norm3(c1);
   const int nu = psf_steps(px, c->s), nv = psf_steps(py, c->s), nw = psf_steps(st.theta, c->s);
   st.h[0] = px / nu;
   st.h[1] = py / nv;
   st.h[2] = st.theta / nw;
   const double sw = st.theta / (2.0 * std::sqrt(2.0 * std::log(2.0)));
-  const int cmax = (int)std::floor(c->nsigma * sw / st.h[2] + 1e-9) + 1;
-  std::vector<double> val;
-  std::vector<int> abc;
-  double total = 0.0;
+  int cmax = 0;
+  while (std::fabs((cmax + 1) * st.h[2]) <= c->nsigma * sw) ++cmax;
+  const int ru = nu - 1, rv = nv - 1;
+  if ((2 * ru + 1) * (2 * rv + 1) > 81 || 2 * cmax + 1 > 256)
+    return fail(c, PVR_ERR_ARG, "PSF lattice too large (in-plane %dx%d, through-plane %d)", 2 * ru + 1,
+                2 * rv + 1, 2 * cmax + 1);
+  std::vector<double> ip((2 * ru + 1) * (2 * rv + 1), 0.0), tp(2 * cmax + 1);
+  double sip = 0.0, stp = 0.0;
+  int disk = 0;
+  for (int b = -rv; b <= rv; ++b)
+    for (int a = -ru; a <= ru; ++a) {
+      const double R = std::sqrt((double)a * a / ((double)nu * nu) + (double)b * b / ((double)nv * nv));
+      if (!(R < 1.0)) continue;
+      const double v = taylor_sinc(M_PI * R);
+      ip[(b + rv) * (2 * ru + 1) + (a + ru)] = v;
+      sip += v;
+      ++disk;
+    }
   for (int cc = -cmax; cc <= cmax; ++cc) {
     const double zc = cc * st.h[2];
-    if (std::fabs(zc) > c->nsigma * sw) continue;
-    const double g = std::exp(-zc * zc / (2.0 * sw * sw));
-    for (int b = -nv; b <= nv; ++b)
-      for (int a = -nu; a <= nu; ++a) {
-        const double R = std::sqrt((double)a * a / ((double)nu * nu) + (double)b * b / ((double)nv * nv));
-        if (!(R < 1.0)) continue;
-        const double v = taylor_sinc(M_PI * R) * g;
-        val.push_back(v);
-        abc.push_back(a); abc.push_back(b); abc.push_back(cc);
-        total += v;
-      }
+    tp[cc + cmax] = std::exp(-zc * zc / (2.0 * sw * sw));
+    stp += tp[cc + cmax];
   }
-  st.S = (int)val.size();
-  for (int q = 0; q < st.S; ++q)
-    table.push_back(make_float4((float)abc[3 * q], (float)abc[3 * q + 1], (float)abc[3 * q + 2],
-                                (float)(val[q] / total)));
+  // separability check against the directly normalised psi (same support, same values)
+  double total = 0.0;
+  for (double a : ip)
+    for (double b : tp) total += a * b;
+  double worst = 0.0;
+  for (size_t i = 0; i < ip.size(); ++i)
+    for (size_t k = 0; k < tp.size(); ++k)
+      worst = std::max(worst, std::fabs(ip[i] * tp[k] / total - (ip[i] / sip) * (tp[k] / stp)));
+  if (worst > 1e-15) return fail(c, PVR_ERR_ARG, "PSF factorisation check failed (%g)", worst);
+  ps.nu = nu; ps.nv = nv; ps.ru = ru; ps.rv = rv; ps.cmax = cmax;
+  ps.ip0 = (int)c->psf_tab.size();
+  for (double v : ip) c->psf_tab.push_back((float)(v / sip));
+  ps.tp0 = (int)c->psf_tab.size();
+  double tpmax = 0.0;
+  for (double v : tp) {
+    c->psf_tab.push_back((float)(v / stp));
+    tpmax = std::max(tpmax, v / stp);
+  }
+  ps.tpmax = (float)tpmax;
+  st.S = disk * (2 * cmax + 1);
+  return PVR_OK;
 }
 
 // Square windows along one axis; the last one is clamped to the edge (Q22).
@@ -239,6 +283,21 @@ Params make_params(const pvr_ctx* c) {
   return p;
 }
 
+LatticeArgs lattice_args(const pvr_ctx* c) {
+  LatticeArgs a;
+  a.P = c->pdev;
+  a.psf = c->psf;
+  a.tab = c->tab;
+  a.mem = c->mem;
+  a.grp = c->grp;
+  a.ngroups = c->ngroups;
+  a.n = c->dims;
+  a.nxp = c->nxp;
+  a.ys = c->ys;
+  a.prm = make_params(c);
+  return a;
+}
+
 pvr_status nccl_check(pvr_ctx* c, ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return PVR_OK;
   return fail(c, PVR_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
@@ -255,10 +314,10 @@ pvr_status allreduce_stats(pvr_ctx* c) {
                     "ncclAllReduce(stats max)");
 }
 
-// Addon / confidence allreduce (C2): SUM over the interleaved (A, C) volume.
+// Addon / confidence allreduce (C2): SUM over the interleaved, row-padded (A, C) volume.
 pvr_status allreduce_ac(pvr_ctx* c) {
   if (c->nranks <= 1) return PVR_OK;
-  return nccl_check(c, g_nccl.AllReduce(c->AC, c->AC, (size_t)c->V * 2, ncclFloat32, ncclSum,
+  return nccl_check(c, g_nccl.AllReduce(c->AC, c->AC, (size_t)c->Vp * 2, ncclFloat32, ncclSum,
                                         c->comm, c->stream),
                     "ncclAllReduce(A,C)");
 }
@@ -266,10 +325,226 @@ pvr_status allreduce_ac(pvr_ctx* c) {
 void free_dev(pvr_ctx* c) {
   for (auto& s : c->stacks)
     if (s.y_dev) cudaFree(s.y_dev), s.y_dev = nullptr;
-  void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->psf,
-                  c->pdev, c->tiles, c->partials, c->em};
+  void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
+                  c->psf, c->pdev, c->mem, c->grp, c->partials, c->em};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+}
+
+// ---- work plan ------------------------------------------------------------------------
+struct PlanOut {
+  std::vector<MemberDev> mem;
+  std::vector<GroupDev> grp;
+  int tile_bytes = 0, r_bytes = 0, t_bytes = 0, nfallback = 0;
+  double fit_frac = 0.0;
+};
+
+struct MemberKey {
+  int64_t key[5];
+  int32_t idx;
+};
+
+// Owned fine-lattice range of a member (must match owned_range() in lattice.cu).
+void owned(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, int& Ulo, int& Uhi, int& Vlo,
+           int& Vhi) {
+  Ulo = ps.nu * m.u0 - ps.ru;
+  Uhi = (m.u0 + m.tu >= hp.sx) ? ps.nu * (hp.sx - 1) + ps.ru + 1 : ps.nu * (m.u0 + m.tu) - ps.ru;
+  Vlo = ps.nv * m.v0 - ps.rv;
+  Vhi = (m.v0 + m.tv >= hp.sy) ? ps.nv * (hp.sy - 1) + ps.rv + 1 : ps.nv * (m.v0 + m.tv) - ps.rv;
+}
+
+// Voxel bbox [lo, hi] (inclusive) of the trilinear corners of a member's owned lattice
+// points, clipped to the grid; returns false if it misses the grid.
+bool member_bbox(const pvr_ctx* c, const MemberDev& m, const HostPatch& hp, const StackPsf& ps,
+                 const PatchGeo& g, int lo[3], int hi[3]) {
+  int Ulo, Uhi, Vlo, Vhi;
+  owned(m, hp, ps, Ulo, Uhi, Vlo, Vhi);
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int iu = 0; iu < 2; ++iu)
+    for (int iv = 0; iv < 2; ++iv)
+      for (int ic = 0; ic < 2; ++ic) {
+        const double U = iu ? Uhi - 1 : Ulo, V = iv ? Vhi - 1 : Vlo, C = ic ? ps.cmax : -ps.cmax;
+        for (int d = 0; d < 3; ++d) {
+          const double x = g.t0[d] + m.z * g.Mz[d] + U * g.Qa[d] + V * g.Qb[d] + C * g.Qc[d];
+          mn[d] = std::min(mn[d], x);
+          mx[d] = std::max(mx[d], x);
+        }
+      }
+  const int n[3] = {c->dims.x, c->dims.y, c->dims.z};
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = std::max(0, (int)std::floor(mn[d] - 1e-3));
+    hi[d] = std::min(n[d] - 1, (int)std::floor(mx[d] + 1e-3) + 1);
+    if (lo[d] > hi[d]) return false;
+  }
+  return true;
+}
+
+void build_members(const pvr_ctx* c, int TU, int TV, const std::vector<int64_t>& which,
+                   std::vector<MemberDev>& mem) {
+  mem.clear();
+  for (int64_t s : which) {
+    const HostPatch& hp = c->patches[c->first + s];
+    for (int z = 0; z < hp.sz; ++z)
+      for (int v0 = 0; v0 < hp.sy; v0 += TV)
+        for (int u0 = 0; u0 < hp.sx; u0 += TU)
+          mem.push_back(MemberDev{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0)});
+  }
+}
+
+// Group members that cover the same stack pixels (stack, slice, row, column, size), then
+// size each group's shared (A, C) tile from the union of its members' voxel bboxes. Groups
+// over the budgets are split; a single member over the tile budget uses global atomics.
+void group_members(const pvr_ctx* c, const std::vector<PatchGeo>& geo, std::vector<MemberDev>& mem,
+                   PlanOut& out) {
+  std::vector<MemberKey> keys(mem.size());
+  for (size_t i = 0; i < mem.size(); ++i) {
+    const MemberDev& m = mem[i];
+    const HostPatch& hp = c->patches[c->first + m.patch];
+    keys[i] = MemberKey{{hp.stack, hp.z0 + m.z, hp.y0 + m.v0, hp.x0 + m.u0, (int64_t)m.tu * 64 + m.tv},
+                        (int32_t)i};
+  }
+  std::stable_sort(keys.begin(), keys.end(), [](const MemberKey& a, const MemberKey& b) {
+    return std::lexicographical_compare(a.key, a.key + 5, b.key, b.key + 5);
+  });
+  std::vector<MemberDev> sorted;
+  sorted.reserve(mem.size());
+  out.grp.clear();
+  out.tile_bytes = 0;
+  out.r_bytes = 0;
+  out.t_bytes = 0;
+  out.nfallback = 0;
+  int fit = 0, total = 0;
+  size_t i = 0;
+  auto rbytes_of = [&](const MemberDev& m) {
+    const HostPatch& hp = c->patches[c->first + m.patch];
+    const StackPsf& ps = c->stacks[hp.stack].psf;
+    // pixel range feeding the owned lattice (upper bound: tile + 2 on each side)
+    return (m.tu + 2 * ps.ru / ps.nu + 2) * (m.tv + 2 * ps.rv / ps.nv + 2) * 8;
+  };
+  auto tbytes_of = [&](const MemberDev& m) {
+    const HostPatch& hp = c->patches[c->first + m.patch];
+    const StackPsf& ps = c->stacks[hp.stack].psf;
+    return (ps.nu * (m.tu - 1) + 2 * ps.ru + 1) * (ps.nv * (m.tv - 1) + 2 * ps.rv + 1) * 4;
+  };
+  auto emit = [&](const std::vector<int>& ids) {
+    // union bbox of the members (those that touch the grid)
+    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-1, -1, -1};
+    bool any = false;
+    int rb = 0;
+    for (int id : ids) {
+      const MemberDev& m = mem[id];
+      const HostPatch& hp = c->patches[c->first + m.patch];
+      int l[3], h[3];
+      if (member_bbox(c, m, hp, c->stacks[hp.stack].psf, geo[m.patch], l, h)) {
+        any = true;
+        for (int d = 0; d < 3; ++d) { lo[d] = std::min(lo[d], l[d]); hi[d] = std::max(hi[d], h[d]); }
+      }
+      rb += rbytes_of(m);
+      out.t_bytes = std::max(out.t_bytes, tbytes_of(m));
+    }
+    GroupDev g;
+    g.m0 = (int32_t)sorted.size();
+    g.nm = (int32_t)ids.size();
+    for (int id : ids) sorted.push_back(mem[id]);
+    if (!any) {  // misses the grid entirely: nothing to splat, tiny tile
+      for (int d = 0; d < 3; ++d) { g.lo[d] = 0; g.dim[d] = 2; }
+      g.dim[1] = g.dim[2] = 1;
+    } else {
+      lo[0] &= ~1;  // even x origin and size: 16-byte aligned voxel pairs for the flush
+      for (int d = 0; d < 3; ++d) { g.lo[d] = lo[d]; g.dim[d] = hi[d] - lo[d] + 1; }
+      g.dim[0] += g.dim[0] & 1;
+    }
+    const int64_t bytes = (int64_t)g.dim[0] * g.dim[1] * g.dim[2] * 8;
+    if (bytes > kMaxTileBytes) {
+      g.dim[0] = g.dim[1] = g.dim[2] = 0;  // global-atomic fallback
+      out.nfallback += 1;
+    } else {
+      out.tile_bytes = std::max<int>(out.tile_bytes, (int)bytes);
+    }
+    out.r_bytes = std::max(out.r_bytes, rb);
+    out.grp.push_back(g);
+    return bytes;
+  };
+  while (i < keys.size()) {
+    size_t j = i;
+    while (j < keys.size() && std::equal(keys[i].key, keys[i].key + 5, keys[j].key)) ++j;
+    std::vector<int> ids;
+    int rb = 0;
+    for (size_t k = i; k < j; ++k) {
+      const int id = keys[k].idx;
+      if (!ids.empty() && rb + rbytes_of(mem[id]) > kRBytes) {  // R buffer budget
+        emit(ids);
+        ids.clear();
+        rb = 0;
+      }
+      ids.push_back(id);
+      rb += rbytes_of(mem[id]);
+    }
+    // try the whole group; if its tile is over budget, emit members one by one
+    const size_t g0 = out.grp.size(), s0 = sorted.size();
+    const int64_t bytes = emit(ids);
+    ++total;
+    if (bytes <= kMaxTileBytes) {
+      ++fit;
+    } else if (ids.size() > 1) {
+      out.grp.resize(g0);
+      sorted.resize(s0);
+      out.nfallback -= 1;
+      for (int id : ids) emit(std::vector<int>{id});
+    }
+    i = j;
+  }
+  out.fit_frac = total ? (double)fit / total : 1.0;
+  mem.swap(sorted);
+}
+
+pvr_status build_plan(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
+  // tile size: the largest candidate for which >= 90% of the groups of a sample of patches
+  // fit the shared tile budget (large tiles amortise the flush and the lattice halo)
+  const int cand[][2] = {{16, 16}, {16, 8}, {8, 8}, {8, 4}, {4, 4}, {2, 2}, {1, 1}};
+  std::vector<int64_t> sample, all(c->nloc);
+  for (int64_t s = 0; s < c->nloc; ++s) all[s] = s;
+  const int64_t step = std::max<int64_t>(1, c->nloc / 256);
+  for (int64_t s = 0; s < c->nloc; s += step) sample.push_back(s);
+  int TU = 1, TV = 1;
+  for (auto& cd : cand) {
+    std::vector<MemberDev> mem;
+    PlanOut po;
+    build_members(c, cd[0], cd[1], sample, mem);
+    group_members(c, geo, mem, po);
+    if (po.fit_frac >= 0.9) {
+      TU = cd[0];
+      TV = cd[1];
+      break;
+    }
+  }
+  c->TU = TU;
+  c->TV = TV;
+  std::vector<MemberDev> mem;
+  PlanOut po;
+  build_members(c, TU, TV, all, mem);
+  group_members(c, geo, mem, po);
+  c->ngroups = (int)po.grp.size();
+  c->nfallback = po.nfallback;
+  c->tile_bytes = (po.tile_bytes + 15) & ~15;
+  c->r_bytes = po.r_bytes;
+  c->t_bytes = std::max(po.t_bytes, 16);
+  if (mem.size() > c->mem_cap) {
+    if (c->mem) cudaFree(c->mem);
+    c->mem = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->mem, mem.size() * sizeof(MemberDev)));
+    c->mem_cap = mem.size();
+  }
+  if (po.grp.size() > c->grp_cap) {
+    if (c->grp) cudaFree(c->grp);
+    c->grp = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->grp, po.grp.size() * sizeof(GroupDev)));
+    c->grp_cap = po.grp.size();
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->mem, mem.data(), mem.size() * sizeof(MemberDev), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->grp, po.grp.data(), po.grp.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  return PVR_OK;
 }
 
 // profiling: events bracket each kernel group when PVR_PARAM_PROFILE is on
@@ -311,8 +586,6 @@ const char* pvr_version(void) { return kVersion; }
 
 const char* pvr_last_error(const pvr_ctx* c) { return c ? c->err.c_str() : g_static_err.c_str(); }
 
-pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* bounds);
-
 pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_stream, pvr_ctx** out) {
   if (!g || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
   if (g->dims[0] < 1 || g->dims[1] < 1 || g->dims[2] < 1 || !(g->spacing_mm > 0))
@@ -327,9 +600,11 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   memset(&c->st, 0, sizeof(c->st));
   c->device = cuda_device;
   c->dims = make_int3(g->dims[0], g->dims[1], g->dims[2]);
+  c->nxp = g->dims[0] + (g->dims[0] & 1);
   c->s = g->spacing_mm;
   for (int d = 0; d < 3; ++d) c->o[d] = g->origin_mm[d];
   c->V = (int64_t)g->dims[0] * g->dims[1] * g->dims[2];
+  c->Vp = (int64_t)c->nxp * g->dims[1] * g->dims[2];
   cudaSetDevice(cuda_device);
   if (cuda_stream) {
     c->stream = (cudaStream_t)cuda_stream;
@@ -342,7 +617,7 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   }
   cudaError_t e1 = cudaMalloc(&c->X[0], c->V * sizeof(float));
   cudaError_t e2 = cudaMalloc(&c->X[1], c->V * sizeof(float));
-  cudaError_t e3 = cudaMalloc(&c->AC, c->V * sizeof(float2));
+  cudaError_t e3 = cudaMalloc(&c->AC, (c->Vp + 2) * sizeof(float2));
   cudaError_t e4 = cudaMalloc(&c->em, sizeof(EmDev));
   cudaError_t e5 = cudaMalloc(&c->partials, (size_t)kStatBlocks * 5 * sizeof(double));
   if (e1 || e2 || e3 || e4 || e5) {
@@ -353,7 +628,7 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
     return fail(nullptr, PVR_ERR_OOM, "device allocation of the volume buffers failed");
   }
   cudaMemsetAsync(c->X[0], 0, c->V * sizeof(float), c->stream);
-  cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), c->stream);
+  cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream);
   cudaMemsetAsync(c->em, 0, sizeof(EmDev), c->stream);
   c->st.voxels = c->V;
   *out = c;
@@ -463,7 +738,8 @@ pvr_status pvr_add_stack(pvr_ctx* c, const float* slices, int W, int H, int K,
 // Contiguous shard plan balanced by cost (pixels x PSF samples): bounds[r] .. bounds[r+1]
 // is rank r's patch range ("distributing independent subsets of patches").
 pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* bounds) {
-  if (!cost || !bounds || M < 0 || nranks < 1) return fail(nullptr, PVR_ERR_ARG, "invalid shard plan args");
+  if (!bounds || M < 0 || nranks < 1 || (M > 0 && !cost))
+    return fail(nullptr, PVR_ERR_ARG, "invalid shard plan args");
   std::vector<int64_t> pre(M + 1, 0);
   for (int64_t i = 0; i < M; ++i) pre[i + 1] = pre[i] + cost[i];
   const int64_t total = pre[M];
@@ -488,9 +764,12 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
     if (size > st.W || size > st.H || depth > st.K)
       return fail(c, PVR_ERR_ARG, "patch %dx%dx%d larger than a %dx%dx%d stack", size, size, depth,
                   st.W, st.H, st.K);
-  // PSF tables (host fp64 -> device fp32)
-  std::vector<float4> table;
-  for (auto& st : c->stacks) build_psf(c, st, table);
+  // PSF tables (host fp64 -> device fp32 factors)
+  c->psf_tab.clear();
+  for (auto& st : c->stacks) {
+    pvr_status r = build_psf(c, st);
+    if (r != PVR_OK) return r;
+  }
   // patch list, order stack, z0, y0, x0
   c->patches.clear();
   for (int si = 0; si < (int)c->stacks.size(); ++si) {
@@ -521,10 +800,9 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
   int64_t L = 0;
   for (auto& st : c->stacks) { st.y_off = L; L += (int64_t)st.W * st.H * st.K; }
   CUDA_TRY(c, cudaMalloc(&c->ys, std::max<int64_t>(L, 1) * sizeof(float)));
-  for (auto& st : c->stacks) {
+  for (auto& st : c->stacks)
     CUDA_TRY(c, cudaMemcpyAsync(c->ys + st.y_off, st.y_dev, (size_t)st.W * st.H * st.K * sizeof(float),
                                 cudaMemcpyDeviceToDevice, c->stream));
-  }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   for (auto& st : c->stacks) { cudaFree(st.y_dev); st.y_dev = nullptr; }
   // per-pixel / per-patch arrays of the local shard
@@ -535,21 +813,16 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
   CUDA_TRY(c, cudaMalloc(&c->pbar, mp * sizeof(float)));
   CUDA_TRY(c, cudaMalloc(&c->w, mp * sizeof(float)));
   CUDA_TRY(c, cudaMalloc(&c->pdev, mp * sizeof(PatchDev)));
-  CUDA_TRY(c, cudaMalloc(&c->psf, std::max<size_t>(table.size(), 1) * sizeof(float4)));
-  CUDA_TRY(c, cudaMemcpyAsync(c->psf, table.data(), table.size() * sizeof(float4), cudaMemcpyHostToDevice, c->stream));
+  std::vector<StackPsf> psd;
+  for (auto& st : c->stacks) psd.push_back(st.psf);
+  CUDA_TRY(c, cudaMalloc(&c->psf, psd.size() * sizeof(StackPsf)));
+  CUDA_TRY(c, cudaMalloc(&c->tab, c->psf_tab.size() * sizeof(float)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->psf, psd.data(), psd.size() * sizeof(StackPsf), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->tab, c->psf_tab.data(), c->psf_tab.size() * sizeof(float),
+                              cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->e, 0, np * sizeof(float), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->p, 0, np * sizeof(float), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->kap, 0, np * sizeof(float), c->stream));
-  // pixel tiles of kTile pixels, never straddling a patch
-  std::vector<int2> tl;
-  for (int64_t s = 0; s < c->nloc; ++s) {
-    const HostPatch& hp = c->patches[c->first + s];
-    const int npx = hp.sx * hp.sy * hp.sz;
-    for (int off = 0; off < npx; off += kTile) tl.push_back(make_int2((int)s, off));
-  }
-  c->ntiles = (int64_t)tl.size();
-  CUDA_TRY(c, cudaMalloc(&c->tiles, std::max<size_t>(tl.size(), 1) * sizeof(int2)));
-  CUDA_TRY(c, cudaMemcpyAsync(c->tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->st.pixels = c->nloc_pix;
   c->st.patches = c->nloc;
@@ -593,37 +866,41 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   // compose, per patch, in fp64: voxel index of lattice point (a,b,c) of pixel (u,v,z) is
   // g(T_s(G (x0+u, y0+v, z0+z, 1) + a h_u u^ + b h_v v^ + c h_w w^)), g(x) = (x - o) / s
   std::vector<PatchDev> pd(c->nloc);
+  std::vector<PatchGeo> geo(c->nloc);
   const double is = 1.0 / c->s;
   for (int64_t s = 0; s < c->nloc; ++s) {
     const HostPatch& hp = c->patches[c->first + s];
     const HostStack& st = c->stacks[hp.stack];
     const double* A = &Th[12 * s];
-    auto lin = [&](const double* vec, float* out, double scale) {
-      for (int d = 0; d < 3; ++d)
-        out[d] = (float)(scale * (A[4 * d] * vec[0] + A[4 * d + 1] * vec[1] + A[4 * d + 2] * vec[2]));
+    PatchGeo& g = geo[s];
+    auto lin = [&](const double* vec, double* out) {
+      for (int d = 0; d < 3; ++d) out[d] = is * (A[4 * d] * vec[0] + A[4 * d + 1] * vec[1] + A[4 * d + 2] * vec[2]);
     };
-    PatchDev& q = pd[s];
-    memset(&q, 0, sizeof(q));
     const double gu[3] = {st.G[0], st.G[4], st.G[8]}, gv[3] = {st.G[1], st.G[5], st.G[9]},
                  gz[3] = {st.G[2], st.G[6], st.G[10]};
-    lin(gu, q.Mu, is);
-    lin(gv, q.Mv, is);
-    lin(gz, q.Mz, is);
     const double qa[3] = {st.h[0] * st.u[0], st.h[0] * st.u[1], st.h[0] * st.u[2]};
     const double qb[3] = {st.h[1] * st.v[0], st.h[1] * st.v[1], st.h[1] * st.v[2]};
     const double qc[3] = {st.h[2] * st.w[0], st.h[2] * st.w[1], st.h[2] * st.w[2]};
-    lin(qa, q.Qa, is);
-    lin(qb, q.Qb, is);
-    lin(qc, q.Qc, is);
+    double Mu[3], Mv[3];
+    lin(gu, Mu);
+    lin(gv, Mv);
+    lin(gz, g.Mz);
+    lin(qa, g.Qa);
+    lin(qb, g.Qb);
+    lin(qc, g.Qc);
     double w0[3];
     for (int d = 0; d < 3; ++d)
       w0[d] = st.G[4 * d] * hp.x0 + st.G[4 * d + 1] * hp.y0 + st.G[4 * d + 2] * hp.z0 + st.G[4 * d + 3];
+    for (int d = 0; d < 3; ++d)
+      g.t0[d] = ((A[4 * d] * w0[0] + A[4 * d + 1] * w0[1] + A[4 * d + 2] * w0[2] + A[4 * d + 3]) - c->o[d]) * is;
+    PatchDev& q = pd[s];
+    memset(&q, 0, sizeof(q));
     for (int d = 0; d < 3; ++d) {
-      const double wd = A[4 * d] * w0[0] + A[4 * d + 1] * w0[1] + A[4 * d + 2] * w0[2] + A[4 * d + 3];
-      const double x = (wd - c->o[d]) * is;
-      const double b = std::floor(x);
+      q.Mu[d] = (float)Mu[d]; q.Mv[d] = (float)Mv[d]; q.Mz[d] = (float)g.Mz[d];
+      q.Qa[d] = (float)g.Qa[d]; q.Qb[d] = (float)g.Qb[d]; q.Qc[d] = (float)g.Qc[d];
+      const double b = std::floor(g.t0[d]);
       q.base[d] = (int32_t)b;
-      q.frac[d] = (float)(x - b);
+      q.frac[d] = (float)(g.t0[d] - b);
     }
     q.stack = hp.stack;
     q.x0 = hp.x0; q.y0 = hp.y0; q.z0 = hp.z0;
@@ -632,17 +909,25 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
     q.W = st.W;
     q.HW = st.W * st.H;
     q.y0off = st.y_off + ((int64_t)hp.z0 * st.H + hp.y0) * st.W + hp.x0;
-    q.psf0 = st.psf0;
     q.S = st.S;
+    for (int d = 0; d < 3; ++d) {
+      q.t0d[d] = g.t0[d];
+      q.Mzd[d] = g.Mz[d];
+      q.Qad[d] = g.Qa[d];
+      q.Qbd[d] = g.Qb[d];
+      q.Qcd[d] = g.Qc[d];
+    }
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
+  pvr_status r = build_plan(c, geo);
+  if (r != PVR_OK) return r;
   // coverage kappa (geometry only) + live-y range, then the EM reset
-  const Params prm = make_params(c);
-  launch_coverage(c->stream, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap, c->partials);
+  const LatticeArgs la = lattice_args(c);
+  launch_coverage(c->stream, la, c->t_bytes, c->kap, c->partials);
   CHECK_LAUNCH(c);
   launch_em_reduce(c->stream, c->partials, kStatBlocks, c->em);
   CHECK_LAUNCH(c);
-  pvr_status r = allreduce_stats(c);
+  r = allreduce_stats(c);
   if (r != PVR_OK) return r;
   launch_range_finish(c->stream, c->s2floor, c->em);
   CHECK_LAUNCH(c);
@@ -657,10 +942,10 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   // PSF samples visited per iteration (observed pixels x S, all ranks after the allreduce)
   c->samples_obs = (int64_t)h.stats[2];
   // algorithmic HBM bytes per launch: compulsory reads/writes only
-  c->st.bytes_alg_forward = 16 * c->nloc_pix + 4 * c->V + 48 * c->nloc;   // y,kap,p in; e out; X; T
-  c->st.bytes_alg_estep = 12 * c->nloc_pix + 8 * c->nloc;                  // kap,e in; p out; pbar,w
-  c->st.bytes_alg_backproject = 12 * c->nloc_pix + 8 * c->V + 4 * c->nloc; // kap,e,p in; A,C out
-  c->st.bytes_alg_update = 16 * c->V;                                      // X0,A,C in; X2 out
+  c->st.bytes_alg_forward = 16 * c->nloc_pix + 4 * c->V + 48 * c->nloc;    // y,kap,p in; e out; X; T
+  c->st.bytes_alg_estep = 12 * c->nloc_pix + 8 * c->nloc;                   // kap,e in; p out; pbar,w
+  c->st.bytes_alg_backproject = 12 * c->nloc_pix + 8 * c->V + 4 * c->nloc;  // kap,e,p in; A,C out
+  c->st.bytes_alg_update = 16 * c->V;                                       // X0,A,C in; X2 out
   c->state = READY;
   return PVR_OK;
 }
@@ -677,14 +962,13 @@ pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
 pvr_status pvr_init_volume(pvr_ctx* c) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
-  const Params prm = make_params(c);
-  CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), c->stream));
-  launch_backproject(c->stream, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap,
-                     c->e, c->p, c->w, 1, c->AC);
+  const LatticeArgs la = lattice_args(c);
+  CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
+  launch_backproject(c->stream, la, c->tile_bytes, c->r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);
   CHECK_LAUNCH(c);
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;
-  launch_init_fill(c->stream, c->AC, c->dims, prm, c->X[c->cur]);
+  launch_init_fill(c->stream, c->AC, c->dims, c->nxp, la.prm, c->X[c->cur]);
   CHECK_LAUNCH(c);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
@@ -694,7 +978,8 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "sr_iterate needs set_transforms");
   if (n < 0 || !(alpha >= 0) || !(lambda >= 0)) return fail(c, PVR_ERR_ARG, "n, alpha, lambda must be >= 0");
-  const Params prm = make_params(c);
+  const LatticeArgs la = lattice_args(c);
+  const Params prm = la.prm;
   const bool prof = c->profile != 0;
   cudaStream_t s = c->stream;
   for (int it = 0; it < n; ++it) {
@@ -702,8 +987,7 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     float* X2 = c->X[1 - c->cur];
     std::vector<cudaEvent_t>* ev = prof ? prof_slot(c) : nullptr;
     if (prof) cudaEventRecord((*ev)[EV_FWD0], s);
-    launch_forward(s, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, X0, c->dims, prm, c->kap, c->p,
-                   c->e, c->partials);
+    launch_forward(s, la, c->t_bytes, X0, c->kap, c->p, c->e, c->partials);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_FWD1], s);
     launch_em_reduce(s, c->partials, kStatBlocks, c->em);
@@ -716,15 +1000,14 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_EST1], s);
-    CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, c->V * sizeof(float2), s));
-    launch_backproject(s, c->pdev, c->psf, c->tiles, c->ntiles, c->ys, c->dims, prm, c->kap, c->e,
-                       c->p, c->w, 0, c->AC);
+    CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
+    launch_backproject(s, la, c->tile_bytes, c->r_bytes, c->kap, c->e, c->p, c->w, 0, c->AC);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_BP1], s);
     r = allreduce_ac(c);
     if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_AR1], s);
-    launch_update(s, X0, c->AC, c->dims, prm, c->em, alpha, lambda, X2);
+    launch_update(s, X0, c->AC, c->dims, c->nxp, prm, c->em, alpha, lambda, X2);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_UPD1], s);
     c->cur = 1 - c->cur;
@@ -775,11 +1058,16 @@ pvr_status pvr_get_taps(pvr_ctx* c, float* e, float* kap, float* A, float* C) {
   if ((r = copy_out(c, e, c->e, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
   if ((r = copy_out(c, kap, c->kap, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
   if (A || C) {
-    std::vector<float2> ac(c->V);
-    CUDA_TRY(c, cudaMemcpyAsync(ac.data(), c->AC, c->V * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<float2> ac(c->Vp);
+    CUDA_TRY(c, cudaMemcpyAsync(ac.data(), c->AC, c->Vp * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     std::vector<float> a(c->V), cc(c->V);
-    for (int64_t k = 0; k < c->V; ++k) { a[k] = ac[k].x; cc[k] = ac[k].y; }
+    const int nx = c->dims.x;
+    for (int64_t row = 0; row < (int64_t)c->dims.y * c->dims.z; ++row)
+      for (int i = 0; i < nx; ++i) {
+        a[row * nx + i] = ac[row * c->nxp + i].x;
+        cc[row * nx + i] = ac[row * c->nxp + i].y;
+      }
     float* dsts[2] = {A, C};
     const std::vector<float>* srcs[2] = {&a, &cc};
     for (int i = 0; i < 2; ++i) {

@@ -1,16 +1,18 @@
 // pvr_internal.h — device-side data layout and kernel launchers of libpvr.so.
-// Private to the product (engine.cu + kernels.cu); see DESIGN.md §Data layout.
+// Private to the product (engine.cu, kernels.cu, lattice.cu); see DESIGN.md §Data layout.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace pvr {
 
-// One patch of the local shard, composed on the host in fp64 (engine.cu) and uploaded
-// as fp32. Continuous voxel index of PSF lattice point (a, b, c) of pixel (u, v, z):
-//   x = base + frac + u*Mu + v*Mv + z*Mz + a*Qa + b*Qb + c*Qc
-// with Mu = n_u*Qa and Mv = n_v*Qb (the in-plane PSF lattice is commensurate with the
-// pixel pitch, reading Q5). `base` is an integer voxel so the fp32 part stays small.
+// One patch of the local shard, composed on the host in fp64 (engine.cu) and uploaded as
+// fp32. Continuous voxel index of PSF lattice point (a, b, c) of pixel (u, v, z):
+//   x = base + frac + u*Mu + v*Mv + z*Mz + a*Qa + b*Qb + c*Qc,
+// with Mu = n_u*Qa and Mv = n_v*Qb (the in-plane PSF lattice is commensurate with the pixel
+// pitch, reading Q5), so the fine in-plane lattice index U = n_u*u + a addresses it as
+//   x = base + frac + z*Mz + U*Qa + V*Qb + c*Qc.
+// `base` is an integer voxel so the fp32 part stays small (|frac + ...| <~ patch extent).
 struct PatchDev {
   float Mu[3], Mv[3], Mz[3];  // voxel-index step per pixel column / row / slice
   float Qa[3], Qb[3], Qc[3];  // voxel-index step per PSF lattice step a / b / c
@@ -21,11 +23,37 @@ struct PatchDev {
   int64_t pix0;               // first pixel of the patch in the local pixel arrays
   int64_t y0off;              // offset of pixel (x0, y0, z0) in the concatenated stacks
   int32_t W, HW;              // row / slice pitch of the patch's stack (elements)
-  int32_t psf0, S;            // this stack's PSF samples: psf[psf0 .. psf0+S)
-  int32_t pad[2];
+  int32_t S, pad0;            // PSF samples per pixel (direct count)
+  // fp64 copies: each CTA forms its tile origin in fp64, then steps in small fp32 offsets
+  double t0d[3], Mzd[3], Qad[3], Qbd[3], Qcd[3];
 };
 
-// EM state on the device (written by k_em_params / k_range, read by later kernels).
+// Separable PSF of one stack (in-plane sinc x through-plane slice profile):
+// psi(a, b, c) = ip[(b + rv) * (2 ru + 1) + (a + ru)] * tp[c + cmax],
+// a in [-ru, ru] (ru = n_u - 1), b in [-rv, rv], c in [-cmax, cmax]; ip is zero outside
+// the main-lobe disk R < 1 (reading Q2). Both factors sum to 1.
+struct StackPsf {
+  int32_t nu, nv, ru, rv, cmax;
+  int32_t ip0, tp0;  // offsets into the float table
+  float tpmax;       // max over c of tp
+};
+
+// Work decomposition of the lattice kernels (engine.cu: build_plan). A member is a tile of
+// tu x tv pixels of one slice z of one patch. Members whose pixels cover the same stack
+// pixels (overlapping patches of one stack) form a group: one CTA per group, sharing one
+// shared-memory accumulation tile of the group's voxel bounding box (backprojection) and the
+// same volume footprint in L1 (forward).
+struct MemberDev {
+  int32_t patch;            // local patch index
+  int32_t z, u0, v0, tu, tv;
+};
+struct GroupDev {
+  int32_t m0, nm;           // members [m0, m0 + nm)
+  int32_t lo[3];            // voxel bbox origin (lo[0] even)
+  int32_t dim[3];           // voxel bbox size (dim[0] even); 0 => global-atomic fallback
+};
+
+// EM state on the device (written by k_em_params / k_range_finish, read by later kernels).
 struct EmDev {
   double sigma2, c, m;
   double s2min, lo, hi;        // from the live-y range at set_transforms
@@ -44,28 +72,44 @@ struct Params {
   int clamp;
 };
 
-constexpr int kTile = 256;        // pixels per forward / backprojection tile
-constexpr int kStatBlocks = 1184; // 148 SMs x 8: fixed grid of the statistics kernels
+// Everything a lattice kernel needs about the problem (passed by value).
+struct LatticeArgs {
+  const PatchDev* P;
+  const StackPsf* psf;
+  const float* tab;        // PSF factor tables
+  const MemberDev* mem;
+  const GroupDev* grp;
+  int32_t ngroups;
+  int3 n;                  // volume dims
+  int32_t nxp;             // row pitch of the (A, C) volume (nx rounded up to even)
+  const float* ys;         // concatenated stacks
+  Params prm;
+};
 
-// ---- launchers (kernels.cu); all asynchronous on `st` ----
-void launch_coverage(cudaStream_t st, const PatchDev* P, const float4* psf, const int2* tiles,
-                     int64_t ntiles, const float* ystack, const int3 dims, Params prm, float* kap,
+constexpr int kThreads = 256;      // CTA size of the lattice kernels
+constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
+constexpr int kMaxTileBytes = 96 * 1024;   // shared (A, C) fixed-point tile budget per group
+constexpr int kRBytes = 12 * 1024;         // shared per-pixel (rA, rC) buffer budget per group
+
+// ---- launchers; all asynchronous on `st` ----
+// lattice.cu
+void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_bytes, float* kap,
                      double* partials);
+void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_bytes, const float* X,
+                    const float* kap, const float* p, float* e, double* partials);
+void launch_backproject(cudaStream_t st, const LatticeArgs& a, int smem_tile_bytes,
+                        int r_bytes, const float* kap, const float* e, const float* p,
+                        const float* w, int init, float2* AC);
+// kernels.cu
 void launch_range_finish(cudaStream_t st, double s2floor, EmDev* em);
 void launch_fill(cudaStream_t st, float* x, int64_t n, float v);
-void launch_forward(cudaStream_t st, const PatchDev* P, const float4* psf, const int2* tiles,
-                    int64_t ntiles, const float* ystack, const float* X, const int3 dims,
-                    Params prm, const float* kap, const float* p, float* e, double* partials);
 void launch_em_reduce(cudaStream_t st, const double* partials, int nblk, EmDev* em);
 void launch_em_params(cudaStream_t st, Params prm, EmDev* em);
 void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, const EmDev* em,
                   const float* kap, const float* e, float* p, float* pbar, float* w);
-void launch_backproject(cudaStream_t st, const PatchDev* P, const float4* psf, const int2* tiles,
-                        int64_t ntiles, const float* ystack, const int3 dims, Params prm,
-                        const float* kap, const float* e, const float* p, const float* w, int init,
-                        float2* AC);
-void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, Params prm,
-                   const EmDev* em, float alpha, float lambda, float* X2);
-void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, Params prm, float* X);
+void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
+                   Params prm, const EmDev* em, float alpha, float lambda, float* X2);
+void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, int nxp, Params prm,
+                      float* X);
 
 }  // namespace pvr
