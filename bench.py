@@ -130,7 +130,7 @@ def time_oracle(cfg, steps, warmup, slices):
     orc.set_volume(np.full(orc.V, 300.0))
     _, kap, _, _ = orc.taps()
     S = len(orc.psf(0)[1])
-    samples = int((kap >= 0.01).sum()) * S
+    samples = int((kap >= 0.5).sum()) * S  # observed pixels (tau_obs, Q25)
     for _ in range(warmup):
         orc.sr_iterate(1, prob["alpha"], prob["lam"])
     ts = []

@@ -68,8 +68,8 @@ enum {
   PVR_PARAM_TAU_PATCH = 1,    /* patch kept iff pbar >= tau_patch [0.5] (Q13)             */
   PVR_PARAM_C0 = 2,           /* inlier proportion c at the first iteration [0.9] (Q10)    */
   PVR_PARAM_TAU_LIVE = 3,     /* pixel in the EM statistics iff kappa >= tau_live [0.99]   */
-  PVR_PARAM_TAU_C = 4,        /* voxel updated iff C > tau_C [1e-6] (Q24)                  */
-  PVR_PARAM_TAU_OBS = 5,      /* pixel observed iff kappa >= tau_obs [0.01] (Q25)          */
+  PVR_PARAM_TAU_C = 4,        /* voxel updated iff C > tau_C [1e-3] (Q24)                  */
+  PVR_PARAM_TAU_OBS = 5,      /* pixel observed iff kappa >= tau_obs [0.5] (Q25)           */
   PVR_PARAM_CLAMP = 6,        /* 1: clamp X1 to the live-y range +-10% [1] (Q19)           */
   PVR_PARAM_PSF_MODE = 7,     /* (extract) 0: PVR PSF; 1: delta PSF (tests only) [0]       */
   PVR_PARAM_SIGMA2_FLOOR = 9, /* sigma2 >= floor * (ymax - ymin)^2 [1e-6] (Q10)            */
@@ -191,6 +191,11 @@ typedef struct {
   int64_t bytes_alg_estep;        /* per E-step launch                                    */
   int64_t bytes_alg_backproject;  /* per backprojection launch                            */
   int64_t bytes_alg_update;       /* per update launch                                    */
+  int32_t fwd_tile[3];            /* forward plan: tile TU, TV (pixels), 1                 */
+  int32_t bp_tile[3];             /* backprojection plan: TU, TV, through-plane segments   */
+  int64_t fwd_groups, bp_groups;  /* CTAs' work items (groups of overlapping member tiles) */
+  int64_t fwd_members, bp_members;
+  int64_t fwd_smem, bp_smem;      /* dynamic shared memory per CTA (bytes)                 */
 } pvr_stats;
 pvr_status pvr_get_stats(const pvr_ctx* ctx, pvr_stats* out);
 pvr_status pvr_reset_stats(pvr_ctx* ctx);

@@ -244,8 +244,8 @@ pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin
   pvro_ctx* x = (pvro_ctx*)calloc(1, sizeof(pvro_ctx));
   for (int d = 0; d < 3; ++d) { x->n[d] = dims[d]; x->o[d] = origin[d]; }
   x->s = spacing;
-  x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-6;
-  x->tau_obs = 0.01; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0;
+  x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-3;
+  x->tau_obs = 0.5; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0;
   int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
   x->X = (double*)calloc(V, sizeof(double));
   x->A = (double*)calloc(V, sizeof(double));

@@ -44,8 +44,8 @@ enum {
   PVRO_TAU_PATCH = 1,    /* patch inlier threshold on pbar (0.5)                     */
   PVRO_C0 = 2,           /* initial inlier proportion c at t = 1 (0.9)               */
   PVRO_TAU_LIVE = 3,     /* live pixel: kappa >= tau_live (0.99)                     */
-  PVRO_TAU_C = 4,        /* voxel updated iff C > tau_C (1e-6)                       */
-  PVRO_TAU_OBS = 5,      /* observed pixel: kappa >= tau_obs (0.01)                  */
+  PVRO_TAU_C = 4,        /* voxel updated iff C > tau_C (1e-3)                       */
+  PVRO_TAU_OBS = 5,      /* observed pixel: kappa >= tau_obs (0.5)                   */
   PVRO_CLAMP = 6,        /* 1: clamp X1 to [lo, hi] (default 1)                      */
   PVRO_PSF_MODE = 7,     /* 0: PVR PSF; 1: delta PSF (S = 1, delta_q = 0), test only */
   PVRO_SIGMA2_FLOOR = 9, /* sigma2_min = floor * (ymax - ymin)^2 (1e-6)              */

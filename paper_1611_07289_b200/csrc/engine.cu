@@ -91,7 +91,7 @@ struct pvr_ctx {
   bool poisoned = false;
   std::string err;
   // parameters
-  double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-6, tau_obs = 0.01;
+  double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-3, tau_obs = 0.5;
   int clamp = 1, psf_mode = 0, profile = 0;
   double s2floor = 1e-6, nsigma = 3.0;
   // stacks / patches
@@ -102,9 +102,15 @@ struct pvr_ctx {
   int64_t M = 0, P = 0;
   int64_t first = 0, nloc = 0, first_pix = 0, nloc_pix = 0;
   int64_t samples_obs = 0;           // observed pixels x S per iteration (all ranks)
-  // work plan of the lattice kernels
-  int TU = 16, TV = 16;
-  int ngroups = 0, nfallback = 0, tile_bytes = 0, r_bytes = 0, t_bytes = 0;
+  // work plans of the lattice kernels (forward / coverage, and backprojection)
+  struct Plan {
+    int TU = 16, TV = 16, nseg = 1;
+    int ngroups = 0, nsplit = 0;
+    int tile_words = 0, r_bytes = 0, t_floats = 0;
+    MemberDev* mem = nullptr;
+    GroupDev* grp = nullptr;
+    size_t mem_cap = 0, grp_cap = 0;
+  } fplan, bplan;
   // comm
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -117,9 +123,6 @@ struct pvr_ctx {
   float* tab = nullptr;
   StackPsf* psf = nullptr;
   PatchDev* pdev = nullptr;
-  MemberDev* mem = nullptr;
-  GroupDev* grp = nullptr;
-  size_t mem_cap = 0, grp_cap = 0;
   double* partials = nullptr;
   EmDev* em = nullptr;
   // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of the
@@ -283,14 +286,14 @@ Params make_params(const pvr_ctx* c) {
   return p;
 }
 
-LatticeArgs lattice_args(const pvr_ctx* c) {
+LatticeArgs lattice_args(const pvr_ctx* c, const pvr_ctx::Plan& pl) {
   LatticeArgs a;
   a.P = c->pdev;
   a.psf = c->psf;
   a.tab = c->tab;
-  a.mem = c->mem;
-  a.grp = c->grp;
-  a.ngroups = c->ngroups;
+  a.mem = pl.mem;
+  a.grp = pl.grp;
+  a.ngroups = pl.ngroups;
   a.n = c->dims;
   a.nxp = c->nxp;
   a.ys = c->ys;
@@ -326,25 +329,22 @@ void free_dev(pvr_ctx* c) {
   for (auto& s : c->stacks)
     if (s.y_dev) cudaFree(s.y_dev), s.y_dev = nullptr;
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
-                  c->psf, c->pdev, c->mem, c->grp, c->partials, c->em};
+                  c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
+                  c->partials, c->em};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
 
-// ---- work plan ------------------------------------------------------------------------
-struct PlanOut {
-  std::vector<MemberDev> mem;
-  std::vector<GroupDev> grp;
-  int tile_bytes = 0, r_bytes = 0, t_bytes = 0, nfallback = 0;
-  double fit_frac = 0.0;
-};
-
+// ---- work plans ----------------------------------------------------------------------
+// A member is a tile of tu x tv pixels of one slice of one patch (backprojection members also
+// carry a through-plane lattice segment [c0, c1]). Members that cover the same stack pixels
+// (overlapping patches of one stack) form a group: one CTA, one shared voxel tile.
 struct MemberKey {
-  int64_t key[5];
+  int64_t key[6];
   int32_t idx;
 };
 
-// Owned fine-lattice range of a member (must match owned_range() in lattice.cu).
+// Owned fine-lattice range of a backprojection member (must match owned_range() in lattice.cu).
 void owned(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, int& Ulo, int& Uhi, int& Vlo,
            int& Vhi) {
   Ulo = ps.nu * m.u0 - ps.ru;
@@ -353,197 +353,225 @@ void owned(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, int& Ulo
   Vhi = (m.v0 + m.tv >= hp.sy) ? ps.nv * (hp.sy - 1) + ps.rv + 1 : ps.nv * (m.v0 + m.tv) - ps.rv;
 }
 
-// Voxel bbox [lo, hi] (inclusive) of the trilinear corners of a member's owned lattice
-// points, clipped to the grid; returns false if it misses the grid.
-bool member_bbox(const pvr_ctx* c, const MemberDev& m, const HostPatch& hp, const StackPsf& ps,
-                 const PatchGeo& g, int lo[3], int hi[3]) {
+// Lattice range a member touches: forward = all lattice points its pixels read (halo'd),
+// backprojection = its owned points and c segment.
+void member_range(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, bool fwd, int& Ulo,
+                  int& Uhi, int& Vlo, int& Vhi) {
+  if (fwd) {
+    Ulo = ps.nu * m.u0 - ps.ru;
+    Uhi = ps.nu * (m.u0 + m.tu - 1) + ps.ru + 1;
+    Vlo = ps.nv * m.v0 - ps.rv;
+    Vhi = ps.nv * (m.v0 + m.tv - 1) + ps.rv + 1;
+  } else {
+    owned(m, hp, ps, Ulo, Uhi, Vlo, Vhi);
+  }
+}
+
+// Voxel bbox [lo, hi] (inclusive, not clipped to the grid) of every trilinear corner the
+// member's lattice points touch, from the fp64 geometry (margin 1e-3 voxel >> fp32 error).
+void member_bbox(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, const PatchGeo& g,
+                 bool fwd, int lo[3], int hi[3]) {
   int Ulo, Uhi, Vlo, Vhi;
-  owned(m, hp, ps, Ulo, Uhi, Vlo, Vhi);
+  member_range(m, hp, ps, fwd, Ulo, Uhi, Vlo, Vhi);
   double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
   for (int iu = 0; iu < 2; ++iu)
     for (int iv = 0; iv < 2; ++iv)
       for (int ic = 0; ic < 2; ++ic) {
-        const double U = iu ? Uhi - 1 : Ulo, V = iv ? Vhi - 1 : Vlo, C = ic ? ps.cmax : -ps.cmax;
+        const double U = iu ? Uhi - 1 : Ulo, V = iv ? Vhi - 1 : Vlo, C = ic ? m.c1 : m.c0;
         for (int d = 0; d < 3; ++d) {
           const double x = g.t0[d] + m.z * g.Mz[d] + U * g.Qa[d] + V * g.Qb[d] + C * g.Qc[d];
           mn[d] = std::min(mn[d], x);
           mx[d] = std::max(mx[d], x);
         }
       }
-  const int n[3] = {c->dims.x, c->dims.y, c->dims.z};
   for (int d = 0; d < 3; ++d) {
-    lo[d] = std::max(0, (int)std::floor(mn[d] - 1e-3));
-    hi[d] = std::min(n[d] - 1, (int)std::floor(mx[d] + 1e-3) + 1);
-    if (lo[d] > hi[d]) return false;
+    lo[d] = (int)std::floor(mn[d] - 1e-3);
+    hi[d] = (int)std::floor(mx[d] + 1e-3) + 1;
   }
-  return true;
 }
 
-void build_members(const pvr_ctx* c, int TU, int TV, const std::vector<int64_t>& which,
-                   std::vector<MemberDev>& mem) {
-  mem.clear();
+struct PlanBuild {
+  std::vector<MemberDev> mem;  // group-sorted
+  std::vector<GroupDev> grp;
+  int64_t max_tile_vox = 0, max_r_bytes = 0, max_t_floats = 0;
+  int nsplit = 0;              // groups that had to be split into single members
+  bool all_fit = true;         // every single member fits the tile budget
+  double fit_frac = 0.0;       // fraction of natural groups that fit whole
+};
+
+int64_t r_bytes_of(const MemberDev& m, const StackPsf& ps) {
+  return (int64_t)(m.tu + 2 * ps.ru / ps.nu + 2) * (m.tv + 2 * ps.rv / ps.nv + 2) * 8;
+}
+
+void build_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const std::vector<int64_t>& which,
+                  int TU, int TV, int nseg, bool fwd, PlanBuild& out) {
+  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kBpTileBytes / 16;
+  std::vector<MemberDev> mem;
   for (int64_t s : which) {
     const HostPatch& hp = c->patches[c->first + s];
+    const StackPsf& ps = c->stacks[hp.stack].psf;
+    const int ntp = 2 * ps.cmax + 1, seg = (ntp + nseg - 1) / nseg;
     for (int z = 0; z < hp.sz; ++z)
       for (int v0 = 0; v0 < hp.sy; v0 += TV)
         for (int u0 = 0; u0 < hp.sx; u0 += TU)
-          mem.push_back(MemberDev{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0)});
+          for (int k = 0; k < (fwd ? 1 : nseg); ++k) {
+            const int c0 = -ps.cmax + k * seg, c1 = fwd ? ps.cmax : std::min(ps.cmax, c0 + seg - 1);
+            if (c0 > c1) continue;
+            mem.push_back(MemberDev{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0),
+                                    c0, c1});
+          }
   }
-}
-
-// Group members that cover the same stack pixels (stack, slice, row, column, size), then
-// size each group's shared (A, C) tile from the union of its members' voxel bboxes. Groups
-// over the budgets are split; a single member over the tile budget uses global atomics.
-void group_members(const pvr_ctx* c, const std::vector<PatchGeo>& geo, std::vector<MemberDev>& mem,
-                   PlanOut& out) {
   std::vector<MemberKey> keys(mem.size());
   for (size_t i = 0; i < mem.size(); ++i) {
     const MemberDev& m = mem[i];
     const HostPatch& hp = c->patches[c->first + m.patch];
-    keys[i] = MemberKey{{hp.stack, hp.z0 + m.z, hp.y0 + m.v0, hp.x0 + m.u0, (int64_t)m.tu * 64 + m.tv},
+    keys[i] = MemberKey{{hp.stack, hp.z0 + m.z, m.c0, hp.y0 + m.v0, hp.x0 + m.u0, (int64_t)m.tu * 64 + m.tv},
                         (int32_t)i};
   }
   std::stable_sort(keys.begin(), keys.end(), [](const MemberKey& a, const MemberKey& b) {
-    return std::lexicographical_compare(a.key, a.key + 5, b.key, b.key + 5);
+    return std::lexicographical_compare(a.key, a.key + 6, b.key, b.key + 6);
   });
-  std::vector<MemberDev> sorted;
-  sorted.reserve(mem.size());
+  out.mem.clear();
   out.grp.clear();
-  out.tile_bytes = 0;
-  out.r_bytes = 0;
-  out.t_bytes = 0;
-  out.nfallback = 0;
-  int fit = 0, total = 0;
-  size_t i = 0;
-  auto rbytes_of = [&](const MemberDev& m) {
-    const HostPatch& hp = c->patches[c->first + m.patch];
-    const StackPsf& ps = c->stacks[hp.stack].psf;
-    // pixel range feeding the owned lattice (upper bound: tile + 2 on each side)
-    return (m.tu + 2 * ps.ru / ps.nu + 2) * (m.tv + 2 * ps.rv / ps.nv + 2) * 8;
-  };
-  auto tbytes_of = [&](const MemberDev& m) {
-    const HostPatch& hp = c->patches[c->first + m.patch];
-    const StackPsf& ps = c->stacks[hp.stack].psf;
-    return (ps.nu * (m.tu - 1) + 2 * ps.ru + 1) * (ps.nv * (m.tv - 1) + 2 * ps.rv + 1) * 4;
-  };
-  auto emit = [&](const std::vector<int>& ids) {
-    // union bbox of the members (those that touch the grid)
-    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-1, -1, -1};
-    bool any = false;
-    int rb = 0;
+  out.max_tile_vox = out.max_r_bytes = out.max_t_floats = 0;
+  out.nsplit = 0;
+  out.all_fit = true;
+  int natural = 0, fit = 0;
+  auto bbox_of = [&](const std::vector<int>& ids, int lo[3], int hi[3]) {
+    for (int d = 0; d < 3; ++d) { lo[d] = 1 << 30; hi[d] = -(1 << 30); }
     for (int id : ids) {
       const MemberDev& m = mem[id];
       const HostPatch& hp = c->patches[c->first + m.patch];
       int l[3], h[3];
-      if (member_bbox(c, m, hp, c->stacks[hp.stack].psf, geo[m.patch], l, h)) {
-        any = true;
-        for (int d = 0; d < 3; ++d) { lo[d] = std::min(lo[d], l[d]); hi[d] = std::max(hi[d], h[d]); }
-      }
-      rb += rbytes_of(m);
-      out.t_bytes = std::max(out.t_bytes, tbytes_of(m));
+      member_bbox(m, hp, c->stacks[hp.stack].psf, geo[m.patch], fwd, l, h);
+      for (int d = 0; d < 3; ++d) { lo[d] = std::min(lo[d], l[d]); hi[d] = std::max(hi[d], h[d]); }
     }
-    GroupDev g;
-    g.m0 = (int32_t)sorted.size();
-    g.nm = (int32_t)ids.size();
-    for (int id : ids) sorted.push_back(mem[id]);
-    if (!any) {  // misses the grid entirely: nothing to splat, tiny tile
-      for (int d = 0; d < 3; ++d) { g.lo[d] = 0; g.dim[d] = 2; }
-      g.dim[1] = g.dim[2] = 1;
-    } else {
-      lo[0] &= ~1;  // even x origin and size: 16-byte aligned voxel pairs for the flush
-      for (int d = 0; d < 3; ++d) { g.lo[d] = lo[d]; g.dim[d] = hi[d] - lo[d] + 1; }
-      g.dim[0] += g.dim[0] & 1;
-    }
-    const int64_t bytes = (int64_t)g.dim[0] * g.dim[1] * g.dim[2] * 8;
-    if (bytes > kMaxTileBytes) {
-      g.dim[0] = g.dim[1] = g.dim[2] = 0;  // global-atomic fallback
-      out.nfallback += 1;
-    } else {
-      out.tile_bytes = std::max<int>(out.tile_bytes, (int)bytes);
-    }
-    out.r_bytes = std::max(out.r_bytes, rb);
-    out.grp.push_back(g);
-    return bytes;
+    lo[0] = lo[0] - (((lo[0] % 2) + 2) % 2);  // even x origin: 16-byte aligned flush pairs
+    const int64_t dx = (hi[0] - lo[0] + 1) | 1, dy = (hi[1] - lo[1] + 1) | 1;
+    return dx * dy * (hi[2] - lo[2] + 1);
   };
+  auto emit = [&](const std::vector<int>& ids) {
+    int lo[3], hi[3];
+    const int64_t vox = bbox_of(ids, lo, hi);
+    GroupDev g;
+    g.m0 = (int32_t)out.mem.size();
+    g.nm = (int32_t)ids.size();
+    for (int d = 0; d < 3; ++d) g.lo[d] = lo[d];
+    g.dim[0] = hi[0] - lo[0] + 1;
+    // odd row and plane pitches: lanes stepping along x, y or z hit different banks
+    g.dim[0] |= 1;
+    g.dim[1] = (hi[1] - lo[1] + 1) | 1;
+    g.dim[2] = hi[2] - lo[2] + 1;
+    int64_t rb = 0;
+    for (int id : ids) {
+      const MemberDev& m = mem[id];
+      const HostPatch& hp = c->patches[c->first + m.patch];
+      const StackPsf& ps = c->stacks[hp.stack].psf;
+      out.mem.push_back(m);
+      rb += r_bytes_of(m, ps);
+      out.max_t_floats = std::max<int64_t>(out.max_t_floats, (int64_t)(ps.nu * (m.tu - 1) + 2 * ps.ru + 1) *
+                                                               (ps.nv * (m.tv - 1) + 2 * ps.rv + 1));
+    }
+    out.max_tile_vox = std::max(out.max_tile_vox, vox);
+    out.max_r_bytes = std::max(out.max_r_bytes, rb);
+    out.grp.push_back(g);
+    if (vox > vox_budget) out.all_fit = false;
+  };
+  size_t i = 0;
   while (i < keys.size()) {
     size_t j = i;
-    while (j < keys.size() && std::equal(keys[i].key, keys[i].key + 5, keys[j].key)) ++j;
-    std::vector<int> ids;
-    int rb = 0;
+    while (j < keys.size() && std::equal(keys[i].key, keys[i].key + 6, keys[j].key)) ++j;
+    // split natural groups by the R buffer budget (backprojection), then by the tile budget
+    std::vector<std::vector<int>> parts(1);
+    int64_t rb = 0;
     for (size_t k = i; k < j; ++k) {
       const int id = keys[k].idx;
-      if (!ids.empty() && rb + rbytes_of(mem[id]) > kRBytes) {  // R buffer budget
-        emit(ids);
-        ids.clear();
+      const MemberDev& m = mem[id];
+      const StackPsf& ps = c->stacks[c->patches[c->first + m.patch].stack].psf;
+      const int64_t b = r_bytes_of(m, ps);
+      if (!fwd && !parts.back().empty() && rb + b > kRBytes) {
+        parts.emplace_back();
         rb = 0;
       }
-      ids.push_back(id);
-      rb += rbytes_of(mem[id]);
+      parts.back().push_back(id);
+      rb += b;
     }
-    // try the whole group; if its tile is over budget, emit members one by one
-    const size_t g0 = out.grp.size(), s0 = sorted.size();
-    const int64_t bytes = emit(ids);
-    ++total;
-    if (bytes <= kMaxTileBytes) {
-      ++fit;
-    } else if (ids.size() > 1) {
-      out.grp.resize(g0);
-      sorted.resize(s0);
-      out.nfallback -= 1;
-      for (int id : ids) emit(std::vector<int>{id});
+    for (auto& part : parts) {
+      int lo[3], hi[3];
+      ++natural;
+      if (bbox_of(part, lo, hi) <= vox_budget) {
+        ++fit;
+        emit(part);
+      } else {
+        if (part.size() > 1) ++out.nsplit;
+        for (int id : part) emit(std::vector<int>{id});
+      }
     }
     i = j;
   }
-  out.fit_frac = total ? (double)fit / total : 1.0;
-  mem.swap(sorted);
+  out.fit_frac = natural ? (double)fit / natural : 1.0;
 }
 
-pvr_status build_plan(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
-  // tile size: the largest candidate for which >= 90% of the groups of a sample of patches
-  // fit the shared tile budget (large tiles amortise the flush and the lattice halo)
-  const int cand[][2] = {{16, 16}, {16, 8}, {8, 8}, {8, 4}, {4, 4}, {2, 2}, {1, 1}};
+pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
+  if (pb.mem.size() > pl.mem_cap) {
+    if (pl.mem) cudaFree(pl.mem);
+    pl.mem = nullptr;
+    CUDA_TRY(c, cudaMalloc(&pl.mem, pb.mem.size() * sizeof(MemberDev)));
+    pl.mem_cap = pb.mem.size();
+  }
+  if (pb.grp.size() > pl.grp_cap) {
+    if (pl.grp) cudaFree(pl.grp);
+    pl.grp = nullptr;
+    CUDA_TRY(c, cudaMalloc(&pl.grp, pb.grp.size() * sizeof(GroupDev)));
+    pl.grp_cap = pb.grp.size();
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(pl.mem, pb.mem.data(), pb.mem.size() * sizeof(MemberDev), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(pl.grp, pb.grp.data(), pb.grp.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // the host vectors go out of scope
+  pl.ngroups = (int)pb.grp.size();
+  pl.nsplit = pb.nsplit;
+  pl.tile_words = (int)((pb.max_tile_vox + 3) & ~int64_t(3));
+  pl.r_bytes = (int)((pb.max_r_bytes + 15) & ~int64_t(15));
+  pl.t_floats = (int)((pb.max_t_floats + 3) & ~int64_t(3));
+  return PVR_OK;
+}
+
+// Tile size (and backprojection c segments): the largest candidate for which >= 90% of the
+// natural groups of a sample of patches fit whole and every single member fits; large tiles
+// amortise the flush, the staging and the lattice halo.
+pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
   std::vector<int64_t> sample, all(c->nloc);
   for (int64_t s = 0; s < c->nloc; ++s) all[s] = s;
-  const int64_t step = std::max<int64_t>(1, c->nloc / 256);
+  const int64_t step = std::max<int64_t>(1, c->nloc / 128);
   for (int64_t s = 0; s < c->nloc; s += step) sample.push_back(s);
-  int TU = 1, TV = 1;
-  for (auto& cd : cand) {
-    std::vector<MemberDev> mem;
-    PlanOut po;
-    build_members(c, cd[0], cd[1], sample, mem);
-    group_members(c, geo, mem, po);
-    if (po.fit_frac >= 0.9) {
-      TU = cd[0];
-      TV = cd[1];
-      break;
+  const int fcand[][3] = {{16, 16, 1}, {16, 8, 1}, {8, 8, 1}, {8, 4, 1}, {4, 4, 1}, {2, 2, 1}, {1, 1, 1}};
+  const int bcand[][3] = {{16, 16, 1}, {16, 8, 1}, {16, 8, 2}, {8, 8, 1}, {8, 8, 2}, {8, 4, 2},
+                          {4, 4, 2},   {4, 4, 4},  {2, 2, 4},  {2, 2, 8}, {1, 1, 8}, {1, 1, 32}};
+  for (int fwd = 1; fwd >= 0; --fwd) {
+    pvr_ctx::Plan& pl = fwd ? c->fplan : c->bplan;
+    const int(*cand)[3] = fwd ? fcand : bcand;
+    const int ncand = fwd ? (int)(sizeof(fcand) / sizeof(fcand[0])) : (int)(sizeof(bcand) / sizeof(bcand[0]));
+    int pick = -1;
+    PlanBuild pb;
+    for (int k = 0; k < ncand; ++k) {
+      build_groups(c, geo, sample, cand[k][0], cand[k][1], cand[k][2], fwd, pb);  // quick reject
+      if (!(pb.all_fit && pb.fit_frac >= 0.9)) continue;
+      build_groups(c, geo, all, cand[k][0], cand[k][1], cand[k][2], fwd, pb);
+      if (pb.all_fit) { pick = k; break; }
     }
+    if (pick < 0) return fail(c, PVR_ERR_ARG, "no tiling fits the shared-memory budget (extreme transforms?)");
+    pl.TU = cand[pick][0];
+    pl.TV = cand[pick][1];
+    pl.nseg = cand[pick][2];
+    pvr_status r = upload_plan(c, pl, pb);
+    if (r != PVR_OK) return r;
+    int32_t* tile = fwd ? c->st.fwd_tile : c->st.bp_tile;
+    tile[0] = pl.TU; tile[1] = pl.TV; tile[2] = pl.nseg;
+    (fwd ? c->st.fwd_groups : c->st.bp_groups) = pl.ngroups;
+    (fwd ? c->st.fwd_members : c->st.bp_members) = (int64_t)pb.mem.size();
+    (fwd ? c->st.fwd_smem : c->st.bp_smem) =
+        fwd ? (int64_t)(pl.t_floats + pl.tile_words) * 4 : (int64_t)pl.tile_words * 16 + pl.r_bytes;
   }
-  c->TU = TU;
-  c->TV = TV;
-  std::vector<MemberDev> mem;
-  PlanOut po;
-  build_members(c, TU, TV, all, mem);
-  group_members(c, geo, mem, po);
-  c->ngroups = (int)po.grp.size();
-  c->nfallback = po.nfallback;
-  c->tile_bytes = (po.tile_bytes + 15) & ~15;
-  c->r_bytes = po.r_bytes;
-  c->t_bytes = std::max(po.t_bytes, 16);
-  if (mem.size() > c->mem_cap) {
-    if (c->mem) cudaFree(c->mem);
-    c->mem = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->mem, mem.size() * sizeof(MemberDev)));
-    c->mem_cap = mem.size();
-  }
-  if (po.grp.size() > c->grp_cap) {
-    if (c->grp) cudaFree(c->grp);
-    c->grp = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->grp, po.grp.size() * sizeof(GroupDev)));
-    c->grp_cap = po.grp.size();
-  }
-  CUDA_TRY(c, cudaMemcpyAsync(c->mem, mem.data(), mem.size() * sizeof(MemberDev), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->grp, po.grp.data(), po.grp.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // host vectors go out of scope
   return PVR_OK;
 }
 
@@ -919,11 +947,11 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
     }
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
-  pvr_status r = build_plan(c, geo);
+  pvr_status r = build_plans(c, geo);
   if (r != PVR_OK) return r;
   // coverage kappa (geometry only) + live-y range, then the EM reset
-  const LatticeArgs la = lattice_args(c);
-  launch_coverage(c->stream, la, c->t_bytes, c->kap, c->partials);
+  const LatticeArgs la = lattice_args(c, c->fplan);
+  launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
   CHECK_LAUNCH(c);
   launch_em_reduce(c->stream, c->partials, kStatBlocks, c->em);
   CHECK_LAUNCH(c);
@@ -962,13 +990,13 @@ pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
 pvr_status pvr_init_volume(pvr_ctx* c) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
-  const LatticeArgs la = lattice_args(c);
+  const LatticeArgs lb = lattice_args(c, c->bplan);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
-  launch_backproject(c->stream, la, c->tile_bytes, c->r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);
+  launch_backproject(c->stream, lb, c->bplan.tile_words, c->bplan.r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);
   CHECK_LAUNCH(c);
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;
-  launch_init_fill(c->stream, c->AC, c->dims, c->nxp, la.prm, c->X[c->cur]);
+  launch_init_fill(c->stream, c->AC, c->dims, c->nxp, lb.prm, c->X[c->cur]);
   CHECK_LAUNCH(c);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
@@ -978,7 +1006,7 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "sr_iterate needs set_transforms");
   if (n < 0 || !(alpha >= 0) || !(lambda >= 0)) return fail(c, PVR_ERR_ARG, "n, alpha, lambda must be >= 0");
-  const LatticeArgs la = lattice_args(c);
+  const LatticeArgs la = lattice_args(c, c->fplan), lb = lattice_args(c, c->bplan);
   const Params prm = la.prm;
   const bool prof = c->profile != 0;
   cudaStream_t s = c->stream;
@@ -987,7 +1015,7 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     float* X2 = c->X[1 - c->cur];
     std::vector<cudaEvent_t>* ev = prof ? prof_slot(c) : nullptr;
     if (prof) cudaEventRecord((*ev)[EV_FWD0], s);
-    launch_forward(s, la, c->t_bytes, X0, c->kap, c->p, c->e, c->partials);
+    launch_forward(s, la, c->fplan.t_floats, c->fplan.tile_words, X0, c->kap, c->p, c->e, c->partials);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_FWD1], s);
     launch_em_reduce(s, c->partials, kStatBlocks, c->em);
@@ -1001,7 +1029,7 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_EST1], s);
     CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
-    launch_backproject(s, la, c->tile_bytes, c->r_bytes, c->kap, c->e, c->p, c->w, 0, c->AC);
+    launch_backproject(s, lb, c->bplan.tile_words, c->bplan.r_bytes, c->kap, c->e, c->p, c->w, 0, c->AC);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_BP1], s);
     r = allreduce_ac(c);
@@ -1118,6 +1146,11 @@ pvr_status pvr_reset_stats(pvr_ctx* c) {
   c->st.bytes_alg_estep = keep.bytes_alg_estep;
   c->st.bytes_alg_backproject = keep.bytes_alg_backproject;
   c->st.bytes_alg_update = keep.bytes_alg_update;
+  memcpy(c->st.fwd_tile, keep.fwd_tile, sizeof(keep.fwd_tile));
+  memcpy(c->st.bp_tile, keep.bp_tile, sizeof(keep.bp_tile));
+  c->st.fwd_groups = keep.fwd_groups; c->st.bp_groups = keep.bp_groups;
+  c->st.fwd_members = keep.fwd_members; c->st.bp_members = keep.bp_members;
+  c->st.fwd_smem = keep.fwd_smem; c->st.bp_smem = keep.bp_smem;
   return PVR_OK;
 }
 

@@ -12,14 +12,22 @@
 //   adjoint:   A += sum_{U,V,c} tp(c) L_A(U, V) splat(x(U, V, c)),
 //              L_A(U, V) = sum_{(a,b): U = n_u u + a} ip(a,b) w p_j e_j / kappa_j
 // which is exactly W (resp. W^T) of the direct sum over (pixel, sample), summed in another
-// order; each lattice point is interpolated / splatted once instead of once per pixel that
-// shares it (c3: 2.9e9 lattice points instead of 6.5e9 samples per pass).
+// order: each lattice point is interpolated / splatted once instead of once per pixel sharing
+// it (c3: 2.9e9 lattice points instead of 6.5e9 samples per pass).
 //
-// Backprojection accumulates a group's splats in a shared-memory fp32 (A, C) tile of the
-// group's voxel bounding box, then flushes it with one coalesced red.global.add.v4.f32 per
-// voxel pair. (A per-group int32 fixed-point tile was tried: native
-// ATOMS.ADD is ~3x faster than the fp32 CAS loop, but the tile's dynamic range -- small-kappa
-// pixels, trilinear tails -- cost ~4e-4 relative L2 on X, over the 1e-4 parity bar.)
+// Forward: one CTA per group (tiles of overlapping patches over the same stack pixels). The
+// group's voxel footprint of X is staged once in shared memory, zero outside the grid, so the
+// inner loop is 8 shared loads + 7 lerps with 32-bit addressing and no bounds logic (dropping
+// out-of-grid corners == reading zeros there). Coverage is the same pass over the grid's
+// indicator function.
+//
+// Backprojection: one CTA per group. Splats accumulate in a shared tile of the group's voxel
+// bounding box as int32 fixed point on a per-group grid (one word per quantity on a 2^-21
+// grid in the iterations; exact hi/lo word pairs, 2^-41, in the init pass) with native
+// ATOMS.ADD: fp32 shared atomics are CAS loops on sm_100a (5-10x slower under contention,
+// profiles/r01_ubench_atomics2.txt). Precision and thresholds: DESIGN.md §7. Each thread walks
+// a lattice line along c. The tile is flushed with
+// coalesced red.global.add.v4.f32 (voxel pairs), skipping cells outside the grid.
 #include <cfloat>
 #include <cmath>
 
@@ -32,27 +40,10 @@ namespace {
 
 constexpr int kMaxIp = 81;   // (2 ru + 1)(2 rv + 1) <= 81 (n <= 5)
 constexpr int kMaxTp = 256;  // 2 cmax + 1
-
-struct Axis {
-  int i0, i1;
-  float w0, w1;
-};
-
-// Trilinear axis weights at continuous index off + r (grid [0, n)), with r a small fp32 local
-// coordinate and off an integer origin (keeps the fractional part exact to ~1e-6 voxel).
-// Out-of-grid corners get weight 0 and an in-grid (clamped) index (reading Q6: dropped, not
-// redistributed).
-__device__ __forceinline__ Axis axis_weights(float r, int off, int n) {
-  float fl;
-  const int i = mfloor(r, fl) + off;
-  const float f = r - fl;
-  Axis a;
-  a.w0 = (i >= 0 && i < n) ? 1.0f - f : 0.0f;
-  a.w1 = (i + 1 >= 0 && i + 1 < n) ? f : 0.0f;
-  a.i0 = min(max(i, 0), n - 1);
-  a.i1 = min(max(i + 1, 0), n - 1);
-  return a;
-}
+constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+constexpr float kLoScale = 1048576.0f;  // 2^20: resolution of the lo word in hi units
+constexpr float kTermMax = 1048576.0f;  // 2^20: largest splat term in hi units
 
 // Member geometry shared by both kernels.
 struct MemberGeom {
@@ -60,23 +51,9 @@ struct MemberGeom {
   int nu, nv, ru, rv, cmax, ntp, ip0, tp0;
 };
 
-// Voxel index of lattice point (U0, V0, c0) of slice z, formed in fp64 and split into an
-// integer base and an fp32 fraction; the kernels then add small fp32 lattice offsets.
-__device__ __forceinline__ void lattice_origin(const PatchDev& pt, int z, int U0, int V0, int c0,
-                                               int (&base)[3], float (&frac)[3]) {
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double x = pt.t0d[d] + z * pt.Mzd[d] + U0 * pt.Qad[d] + V0 * pt.Qbd[d] + c0 * pt.Qcd[d];
-    const double f = floor(x);
-    base[d] = (int)f;
-    frac[d] = (float)(x - f);
-  }
-}
-
-__device__ __forceinline__ MemberGeom member_geom(const LatticeArgs& a, const PatchDev& pt, int z) {
+__device__ __forceinline__ MemberGeom member_geom(const LatticeArgs& a, const PatchDev& pt) {
   MemberGeom g;
   const StackPsf ps = a.psf[pt.stack];
-  (void)z;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     g.qa[d] = pt.Qa[d];
@@ -88,29 +65,57 @@ __device__ __forceinline__ MemberGeom member_geom(const LatticeArgs& a, const Pa
   return g;
 }
 
+// Voxel index of lattice point (U0, V0, c0) of slice z, formed in fp64 and split into an
+// integer part relative to `lo` and an fp32 fraction; kernels then add small fp32 offsets.
+__device__ __forceinline__ void lattice_origin(const PatchDev& pt, int z, int U0, int V0, int c0,
+                                               const int32_t* lo, int (&base)[3], float (&frac)[3]) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double x = pt.t0d[d] + z * pt.Mzd[d] + U0 * pt.Qad[d] + V0 * pt.Qbd[d] + c0 * pt.Qcd[d];
+    const double f = floor(x);
+    base[d] = (int)f - lo[d];
+    frac[d] = (float)(x - f);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Forward (MODE 0) and coverage (MODE 1).
 //   MODE 0: out = e (residual, 0 if unobserved); stats {sum p e^2, sum p, n_live | max e, -min e}
 //   MODE 1: out = kappa;                         stats {n_obs, n_live, samples | max y, -min y}
+// Dynamic shared memory: [t_floats] lattice values T of one member, then the X tile.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, const float* __restrict__ X,
+__global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_floats,
+                                                          const float* __restrict__ X,
                                                           const float* __restrict__ kap,
                                                           const float* __restrict__ pprev,
                                                           float* __restrict__ out,
                                                           double* __restrict__ partials) {
-  extern __shared__ float sT[];  // lattice values T(U, V) of the current member
+  extern __shared__ float4 fsm4[];
+  float* sT = reinterpret_cast<float*>(fsm4);
+  float* sX = sT + t_floats;
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
   double acc_s[3] = {0.0, 0.0, 0.0};
   float acc_m[2] = {-FLT_MAX, -FLT_MAX};
   const int3 n = a.n;
-  const size_t nxy = (size_t)n.x * n.y;
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
+    const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
+    __syncthreads();  // the previous group's readers of sX / sT / tables are done
+    // stage X (or the grid indicator) over the group footprint, zero outside the grid
+    for (int i = threadIdx.x; i < dx * dy * dz; i += kThreads) {
+      const int lx = i % dx, r = i / dx;
+      const int ly = r % dy, lz = r / dy;
+      const int gx = G.lo[0] + lx, gy = G.lo[1] + ly, gz = G.lo[2] + lz;
+      float v = 0.0f;
+      if (gx >= 0 && gx < n.x && gy >= 0 && gy < n.y && gz >= 0 && gz < n.z)
+        v = MODE == 1 ? 1.0f : __ldg(X + ((size_t)gz * n.y + gy) * n.x + gx);
+      sX[i] = v;
+    }
     for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
       const MemberDev m = a.mem[mi];
       const PatchDev& pt = a.P[m.patch];
-      const MemberGeom mg = member_geom(a, pt, m.z);
+      const MemberGeom mg = member_geom(a, pt);
       const int nip = (2 * mg.ru + 1) * (2 * mg.rv + 1);
       __syncthreads();  // previous member's readers of sT / tables are done
       for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[mg.ip0 + i];
@@ -121,8 +126,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, const f
       const int U0 = mg.nu * m.u0 - mg.ru, V0 = mg.nv * m.v0 - mg.rv;
       int ob[3];
       float of[3];
-      lattice_origin(pt, m.z, U0, V0, -mg.cmax, ob, of);
-      const int bx = ob[0], by = ob[1], bz = ob[2];
+      lattice_origin(pt, m.z, U0, V0, -mg.cmax, G.lo, ob, of);
       __syncthreads();
       for (int i = threadIdx.x; i < LU * LV; i += kThreads) {
         const float U = (float)(i % LU), V = (float)(i / LU);
@@ -131,24 +135,18 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, const f
         float rz = of[2] + U * mg.qa[2] + V * mg.qb[2];
         float acc = 0.0f;
         for (int c = 0; c < mg.ntp; ++c) {
-          const Axis ax = axis_weights(rx, bx, n.x);
-          const Axis ay = axis_weights(ry, by, n.y);
-          const Axis az = axis_weights(rz, bz, n.z);
-          float v;
-          if (MODE == 1) {
-            v = (ax.w0 + ax.w1) * (ay.w0 + ay.w1) * (az.w0 + az.w1);
-          } else {
-            const float* p00 = X + az.i0 * nxy + (size_t)ay.i0 * n.x;
-            const float* p01 = X + az.i0 * nxy + (size_t)ay.i1 * n.x;
-            const float* p10 = X + az.i1 * nxy + (size_t)ay.i0 * n.x;
-            const float* p11 = X + az.i1 * nxy + (size_t)ay.i1 * n.x;
-            const float c00 = ax.w0 * __ldg(p00 + ax.i0) + ax.w1 * __ldg(p00 + ax.i1);
-            const float c01 = ax.w0 * __ldg(p01 + ax.i0) + ax.w1 * __ldg(p01 + ax.i1);
-            const float c10 = ax.w0 * __ldg(p10 + ax.i0) + ax.w1 * __ldg(p10 + ax.i1);
-            const float c11 = ax.w0 * __ldg(p11 + ax.i0) + ax.w1 * __ldg(p11 + ax.i1);
-            v = az.w0 * (ay.w0 * c00 + ay.w1 * c01) + az.w1 * (ay.w0 * c10 + ay.w1 * c11);
-          }
-          acc += s_tp[c] * v;
+          float flx, fly, flz;
+          const int ix = mfloor(rx, flx) + ob[0];
+          const int iy = mfloor(ry, fly) + ob[1];
+          const int iz = mfloor(rz, flz) + ob[2];
+          const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
+          const float* p = sX + (iz * dy + iy) * dx + ix;
+          const float x000 = p[0], x100 = p[1], x010 = p[dx], x110 = p[dx + 1];
+          const float x001 = p[dx * dy], x101 = p[dx * dy + 1], x011 = p[dx * dy + dx], x111 = p[dx * dy + dx + 1];
+          const float c00 = fmaf(fx, x100 - x000, x000), c10 = fmaf(fx, x110 - x010, x010);
+          const float c01 = fmaf(fx, x101 - x001, x001), c11 = fmaf(fx, x111 - x011, x011);
+          const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
+          acc = fmaf(s_tp[c], fmaf(fz, c1 - c0, c0), acc);
           rx += mg.qc[0];
           ry += mg.qc[1];
           rz += mg.qc[2];
@@ -209,7 +207,7 @@ struct Owned {  // a member's owned lattice range and the pixel range it reads
 
 __device__ __forceinline__ Owned owned_range(const MemberDev& m, const PatchDev& pt, const MemberGeom& g) {
   // tiles partition U in [-ru, nu (sx - 1) + ru]: a tile owns [nu u0 - ru, nu (u0 + tu) - ru),
-  // the last one up to nu (sx - 1) + ru inclusive
+  // the last one up to nu (sx - 1) + ru inclusive (engine.cu: owned() matches)
   Owned o;
   o.Ulo = g.nu * m.u0 - g.ru;
   o.Uhi = (m.u0 + m.tu >= pt.sx) ? g.nu * (pt.sx - 1) + g.ru + 1 : g.nu * (m.u0 + m.tu) - g.ru;
@@ -222,15 +220,88 @@ __device__ __forceinline__ Owned owned_range(const MemberDev& m, const PatchDev&
   return o;
 }
 
+// value (hi units, |v| < 2^22) -> exact hi/lo int32 pair: v = hi + lo 2^-20 (+ < 2^-21)
+__device__ __forceinline__ void split_hilo(float v, int& hi, int& lo) {
+  const float t = __fadd_rn(v, kMagic);
+  hi = __float_as_int(t) - kMagicBits;
+  const float r = __fsub_rn(v, __fsub_rn(t, kMagic));  // exact (Sterbenz)
+  lo = __float_as_int(__fmaf_rn(r, kLoScale, kMagic)) - kMagicBits;
+}
+
+struct Tile {  // planar int32 accumulators of the group bbox: A, C (+ lo words for HILO)
+  int *ah, *ch, *al, *cl;
+  int dx, dy;
+};
+
+// Add one (A, C) term to tile cell idx. HILO: exact hi/lo words (init pass: raw intensities,
+// the widest dynamic range); otherwise one int32 word per quantity, round-to-nearest on the
+// group's 2^-21 grid (iterations: residual-weighted terms; bounded dynamic range).
+template <bool HILO>
+__device__ __forceinline__ void tile_add(const Tile& T, int idx, float vA, float vC) {
+  if (HILO) {
+    int h, l;
+    split_hilo(vA, h, l);
+    atomicAdd(T.ah + idx, h);
+    atomicAdd(T.al + idx, l);
+    split_hilo(vC, h, l);
+    atomicAdd(T.ch + idx, h);
+    atomicAdd(T.cl + idx, l);
+  } else {
+    atomicAdd(T.ah + idx, __float_as_int(__fadd_rn(vA, kMagic)) - kMagicBits);
+    atomicAdd(T.ch + idx, __float_as_int(__fadd_rn(vC, kMagic)) - kMagicBits);
+  }
+}
+
+// Splat one lattice line (fixed U, V; c over [c0, c1]) into the tile: 8 trilinear corners per
+// sample, each (A, C) term split into exact hi/lo int32 words. Uniform control flow: every
+// lane of a warp issues the same atomics (a register window along c was tried: lanes cross
+// voxel planes at different steps, so the warp serialised the flush branches).
+template <bool HILO>
+__device__ __forceinline__ void splat_line(const Tile& T, const float* s_tp, float rx, float ry,
+                                           float rz, const float* qc, const int* ob, int c0,
+                                           int c1, int cmax, float LA, float LC) {
+  rx += c0 * qc[0];
+  ry += c0 * qc[1];
+  rz += c0 * qc[2];
+  const int dxy = T.dx * T.dy;
+  for (int c = c0; c <= c1; ++c) {
+    const float t = s_tp[c + cmax];
+    float flx, fly, flz;
+    const int ix = mfloor(rx, flx) + ob[0];
+    const int iy = mfloor(ry, fly) + ob[1];
+    const int iz = mfloor(rz, flz) + ob[2];
+    const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
+    const float vA = LA * t, vC = LC * t;
+    const int k000 = (iz * T.dy + iy) * T.dx + ix;
+    const float wy0z0 = (1.0f - fy) * (1.0f - fz), wy1z0 = fy * (1.0f - fz);
+    const float wy0z1 = (1.0f - fy) * fz, wy1z1 = fy * fz;
+    const float a0 = vA * (1.0f - fx), a1 = vA * fx, g0 = vC * (1.0f - fx), g1 = vC * fx;
+    tile_add<HILO>(T, k000, a0 * wy0z0, g0 * wy0z0);
+    tile_add<HILO>(T, k000 + 1, a1 * wy0z0, g1 * wy0z0);
+    tile_add<HILO>(T, k000 + T.dx, a0 * wy1z0, g0 * wy1z0);
+    tile_add<HILO>(T, k000 + T.dx + 1, a1 * wy1z0, g1 * wy1z0);
+    tile_add<HILO>(T, k000 + dxy, a0 * wy0z1, g0 * wy0z1);
+    tile_add<HILO>(T, k000 + dxy + 1, a1 * wy0z1, g1 * wy0z1);
+    tile_add<HILO>(T, k000 + dxy + T.dx, a0 * wy1z1, g0 * wy1z1);
+    tile_add<HILO>(T, k000 + dxy + T.dx + 1, a1 * wy1z1, g1 * wy1z1);
+    rx += qc[0];
+    ry += qc[1];
+    rz += qc[2];
+  }
+}
+
+// Dynamic shared memory: (HILO ? 4 : 2) x tile_words int32 (A, C [, A_lo, C_lo]), then R.
+template <bool HILO>
 __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile_words,
                                                          const float* __restrict__ kap,
                                                          const float* __restrict__ e,
                                                          const float* __restrict__ p,
                                                          const float* __restrict__ w, int init,
                                                          float2* __restrict__ AC) {
-  extern __shared__ float4 smem4[];
-  float* acc = reinterpret_cast<float*>(smem4);                   // [tile_words] (A, C) fp32
-  float2* R = reinterpret_cast<float2*>(acc + tile_words);        // per-pixel (rA, rC)
+  extern __shared__ int4 bsm4[];
+  int* base = reinterpret_cast<int*>(bsm4);
+  constexpr int NW = HILO ? 4 : 2;
+  float2* R = reinterpret_cast<float2*>(base + NW * tile_words);
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
   __shared__ float s_red[2][32];
   __shared__ float s_scale[2];
@@ -239,17 +310,16 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
-    const bool tiled = G.dim[0] > 0;
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
-    __syncthreads();  // previous group's flush is done with acc / R / tables
+    __syncthreads();  // previous group's flush is done with the tile / R / tables
     // ---- phase A: per-pixel (rA, rC) of every member into R; group maxima for the scale
     float mA = 0.0f, mC = 0.0f;
     int roff = 0;
     for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
       const MemberDev m = a.mem[mi];
       const PatchDev& pt = a.P[m.patch];
-      const MemberGeom mg = member_geom(a, pt, m.z);
+      const MemberGeom mg = member_geom(a, pt);
       const Owned o = owned_range(m, pt, mg);
       const int rw = o.phu - o.plu + 1, rh = o.phv - o.plv + 1;
       const float ws = init ? 1.0f : w[m.patch];
@@ -277,13 +347,14 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
       s_red[1][wid] = mC;
     }
     {  // PSF tables of the group's stack (all members share it) and the tile reset
-      const PatchDev& pt0 = a.P[a.mem[G.m0].patch];
-      const MemberGeom mg = member_geom(a, pt0, 0);
+      const MemberGeom mg = member_geom(a, a.P[a.mem[G.m0].patch]);
       const int nip = (2 * mg.ru + 1) * (2 * mg.rv + 1);
       for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[mg.ip0 + i];
       for (int i = threadIdx.x; i < mg.ntp; i += kThreads) s_tp[i] = a.tab[mg.tp0 + i];
-      if (tiled)
-        for (int i = threadIdx.x; i < (nvox >> 1); i += kThreads) smem4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = threadIdx.x; i < nvox; i += kThreads) {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) base[q * tile_words + i] = 0;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -292,35 +363,35 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         xA = fmaxf(xA, s_red[0][i]);
         xC = fmaxf(xC, s_red[1][i]);
       }
-      s_scale[0] = xA;
-      s_scale[1] = xC;
+      const float tpmax = a.psf[a.P[a.mem[G.m0].patch].stack].tpmax;
+      // every splat term |L tp w| <= max|r| tpmax  ->  < 2^20 (HILO) / 2^21 units
+      const float tmax = HILO ? kTermMax : 2.0f * kTermMax;
+      s_scale[0] = xA > 0.0f ? tmax / (xA * tpmax) : 0.0f;
+      s_scale[1] = xC > 0.0f ? tmax / (xC * tpmax) : 0.0f;
     }
     __syncthreads();
-    if (s_scale[0] == 0.0f && s_scale[1] == 0.0f) continue;  // nothing to splat (excluded patches)
-    // ---- phase B: splat every owned lattice point of every member
+    const float scA = s_scale[0], scC = s_scale[1];
+    if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
+    const Tile T{base, base + tile_words, HILO ? base + 2 * tile_words : nullptr,
+                 HILO ? base + 3 * tile_words : nullptr, dx, dy};
+
+    // ---- phase B: splat every owned lattice line of every member
     roff = 0;
     for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
       const MemberDev m = a.mem[mi];
       const PatchDev& pt = a.P[m.patch];
-      const MemberGeom mg = member_geom(a, pt, m.z);
+      const MemberGeom mg = member_geom(a, pt);
       const Owned o = owned_range(m, pt, mg);
       const int rw = o.phu - o.plu + 1, rh = o.phv - o.plv + 1;
       const int nU = o.Uhi - o.Ulo, nV = o.Vhi - o.Vlo;
       const int w2 = 2 * mg.ru + 1;
-      // local origin: tiled -> relative to the group bbox; global -> relative to voxel 0
       int ob[3];
       float of[3];
-      lattice_origin(pt, m.z, o.Ulo, o.Vlo, -mg.cmax, ob, of);
-      const int ox = ob[0] - (tiled ? G.lo[0] : 0);
-      const int oy = ob[1] - (tiled ? G.lo[1] : 0);
-      const int oz = ob[2] - (tiled ? G.lo[2] : 0);
-      // lanes of a warp take lattice columns P apart (P coprime to nU) so that their
-      // trilinear corners do not collide in the shared atomics
-      int P = 5;
-      while (nU % P == 0) P += 2;
-      const int ex = tiled ? dx : n.x, ey = tiled ? dy : n.y, ez = tiled ? dz : n.z;
+      lattice_origin(pt, m.z, o.Ulo, o.Vlo, 0, G.lo, ob, of);
+      // consecutive lanes take consecutive lines: their corners fall in consecutive cells of
+      // one tile row (distinct banks), or rows an odd pitch apart (engine.cu: odd dx, dy)
       for (int i = threadIdx.x; i < nU * nV; i += kThreads) {
-        const int iu = ((i % nU) * P) % nU, iv = i / nU;
+        const int iu = i % nU, iv = i / nU;
         const int U = o.Ulo + iu, V = o.Vlo + iv;
         float LA = 0.0f, LC = 0.0f;
         for (int b = -mg.rv; b <= mg.rv; ++b) {
@@ -332,75 +403,45 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
             if (un < mg.nu * o.plu || un > mg.nu * o.phu || (un - mg.nu * o.plu) % mg.nu) continue;
             const int u = un / mg.nu;
             const float wt = s_ip[(b + mg.rv) * w2 + (aa + mg.ru)];
-            const float2 r = R[roff + (v - o.plv) * rw + (u - o.plu)];
-            LA += wt * r.x;
-            LC += wt * r.y;
+            const float2 rr = R[roff + (v - o.plv) * rw + (u - o.plu)];
+            LA += wt * rr.x;
+            LC += wt * rr.y;
           }
         }
         if (LA == 0.0f && LC == 0.0f) continue;
+        LA *= scA;
+        LC *= scC;
         const float fU = (float)iu, fV = (float)iv;
-        float rx = of[0] + fU * mg.qa[0] + fV * mg.qb[0];
-        float ry = of[1] + fU * mg.qa[1] + fV * mg.qb[1];
-        float rz = of[2] + fU * mg.qa[2] + fV * mg.qb[2];
-        for (int c = 0; c < mg.ntp; ++c) {
-          const float t = s_tp[c];
-          const float vA = LA * t, vC = LC * t;
-          // validity against the grid: in tiled mode the bbox is clipped to the grid and
-          // contains every in-grid corner, so "in [0, e)" is the same test
-          const Axis ax = axis_weights(rx, ox, ex);
-          const Axis ay = axis_weights(ry, oy, ey);
-          const Axis az = axis_weights(rz, oz, ez);
-          if (tiled) {
-            const int r00 = (az.i0 * dy + ay.i0) * dx, r01 = (az.i0 * dy + ay.i1) * dx;
-            const int r10 = (az.i1 * dy + ay.i0) * dx, r11 = (az.i1 * dy + ay.i1) * dx;
-            const float w00 = az.w0 * ay.w0, w01 = az.w0 * ay.w1, w10 = az.w1 * ay.w0, w11 = az.w1 * ay.w1;
-            const float a0 = vA * ax.w0, a1 = vA * ax.w1, c0 = vC * ax.w0, c1 = vC * ax.w1;
-#define PVR_SPLAT(ROW, WYZ)                                          \
-  {                                                                  \
-    float* q0 = acc + 2 * ((ROW) + ax.i0);                           \
-    float* q1 = acc + 2 * ((ROW) + ax.i1);                           \
-    atomicAdd(q0, a0 * (WYZ));                                       \
-    atomicAdd(q0 + 1, c0 * (WYZ));                                   \
-    atomicAdd(q1, a1 * (WYZ));                                       \
-    atomicAdd(q1 + 1, c1 * (WYZ));                                   \
-  }
-            PVR_SPLAT(r00, w00)
-            PVR_SPLAT(r01, w01)
-            PVR_SPLAT(r10, w10)
-            PVR_SPLAT(r11, w11)
-#undef PVR_SPLAT
-          } else {
-            const size_t sy = (size_t)a.nxp, sz = (size_t)a.nxp * n.y;
-            const float wz[2] = {az.w0, az.w1}, wy[2] = {ay.w0, ay.w1}, wx[2] = {ax.w0, ax.w1};
-            const int iz[2] = {az.i0, az.i1}, iy[2] = {ay.i0, ay.i1}, ix[2] = {ax.i0, ax.i1};
-#pragma unroll
-            for (int cz = 0; cz < 2; ++cz)
-#pragma unroll
-              for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-                for (int cx = 0; cx < 2; ++cx) {
-                  const float wt = wz[cz] * wy[cy] * wx[cx];
-                  if (wt != 0.0f) red_v2(AC + iz[cz] * sz + iy[cy] * sy + ix[cx], vA * wt, vC * wt);
-                }
-          }
-          rx += mg.qc[0];
-          ry += mg.qc[1];
-          rz += mg.qc[2];
-        }
+        const float r0x = of[0] + fU * mg.qa[0] + fV * mg.qb[0];
+        const float r0y = of[1] + fU * mg.qa[1] + fV * mg.qb[1];
+        const float r0z = of[2] + fU * mg.qa[2] + fV * mg.qb[2];
+        splat_line<HILO>(T, s_tp, r0x, r0y, r0z, mg.qc, ob, m.c0, m.c1, mg.cmax, LA, LC);
       }
       roff += rw * rh;
     }
-    if (!tiled) continue;
     __syncthreads();
-    // ---- phase C: flush the tile, one red.v4 per (even, odd) voxel pair along x
-    const int hx = dx >> 1;
+    // ---- phase C: flush the tile, one red.v4 per in-grid (even, odd) voxel pair along x
+    const double iA = scA > 0.0f ? 1.0 / scA : 0.0, iC = scC > 0.0f ? 1.0 / scC : 0.0;
+    const int hx = (dx + 1) >> 1;
     for (int i = threadIdx.x; i < hx * dy * dz; i += kThreads) {
       const int px = i % hx, rest = i / hx;
       const int yy = rest % dy, zz = rest / dy;
-      const float4 q = smem4[(zz * dy + yy) * hx + px];
-      if (q.x == 0.0f && q.y == 0.0f && q.z == 0.0f && q.w == 0.0f) continue;
-      float2* dst = AC + ((size_t)(G.lo[2] + zz) * n.y + (G.lo[1] + yy)) * a.nxp + G.lo[0] + 2 * px;
-      red_v4(dst, q.x, q.y, q.z, q.w);
+      const int gy = G.lo[1] + yy, gz = G.lo[2] + zz, gx = G.lo[0] + 2 * px;
+      if (gy < 0 || gy >= n.y || gz < 0 || gz >= n.z || gx < 0 || gx >= a.nxp) continue;
+      const int k = (zz * dy + yy) * dx + 2 * px;
+      const bool two = 2 * px + 1 < dx;  // odd pitch: the last pair has one tile cell
+      const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
+      int al0 = 0, al1 = 0, cl0 = 0, cl1 = 0;
+      if (HILO) {
+        al0 = T.al[k]; al1 = two ? T.al[k + 1] : 0;
+        cl0 = T.cl[k]; cl1 = two ? T.cl[k + 1] : 0;
+      }
+      if ((ah0 | ah1 | ch0 | ch1 | al0 | al1 | cl0 | cl1) == 0) continue;
+      const float A0 = (float)(((double)ah0 + (double)al0 * (1.0 / kLoScale)) * iA);
+      const float A1 = (float)(((double)ah1 + (double)al1 * (1.0 / kLoScale)) * iA);
+      const float C0 = (float)(((double)ch0 + (double)cl0 * (1.0 / kLoScale)) * iC);
+      const float C1 = (float)(((double)ch1 + (double)cl1 * (1.0 / kLoScale)) * iC);
+      red_v4(AC + ((size_t)gz * n.y + gy) * a.nxp + gx, A0, C0, A1, C1);
     }
   }
 }
@@ -411,32 +452,39 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
 static void configure() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(k_lattice_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_lattice_fwd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  cudaFuncSetAttribute(k_lattice_fwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k_lattice_bp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_lattice_bp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_lattice_fwd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_lattice_fwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   done = true;
 }
 
-// t_bytes: shared T buffer of one member (LU x LV floats, from the plan)
-void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_bytes, float* kap, double* partials) {
+void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, float* kap,
+                     double* partials) {
   configure();
-  k_lattice_fwd<1><<<kStatBlocks, kThreads, t_bytes, st>>>(a, nullptr, nullptr, nullptr, kap, partials);
+  const int smem = (t_floats + x_floats) * 4;
+  k_lattice_fwd<1><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, nullptr, nullptr, nullptr, kap,
+                                                        partials);
 }
 
-void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_bytes, const float* X, const float* kap,
-                    const float* p, float* e, double* partials) {
+void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, const float* X,
+                    const float* kap, const float* p, float* e, double* partials) {
   configure();
-  k_lattice_fwd<0><<<kStatBlocks, kThreads, t_bytes, st>>>(a, X, kap, p, e, partials);
+  const int smem = (t_floats + x_floats) * 4;
+  k_lattice_fwd<0><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, X, kap, p, e, partials);
 }
 
-void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_bytes, int r_bytes,
+void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         const float* kap, const float* e, const float* p, const float* w, int init,
                         float2* AC) {
   if (a.ngroups <= 0) return;
   configure();
-  const int smem = tile_bytes + r_bytes;
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
-  k_lattice_bp<<<grid, kThreads, smem, st>>>(a, tile_bytes / 4, kap, e, p, w, init, AC);
+  if (init) {  // raw intensities: exact hi/lo words
+    k_lattice_bp<true><<<grid, kThreads, tile_words * 16 + r_bytes, st>>>(a, tile_words, kap, e, p, w, 1, AC);
+  } else {
+    k_lattice_bp<false><<<grid, kThreads, tile_words * 8 + r_bytes, st>>>(a, tile_words, kap, e, p, w, 0, AC);
+  }
 }
 
 }  // namespace pvr

@@ -46,11 +46,12 @@ struct StackPsf {
 struct MemberDev {
   int32_t patch;            // local patch index
   int32_t z, u0, v0, tu, tv;
+  int32_t c0, c1;           // through-plane lattice range [c0, c1] (backprojection segments)
 };
 struct GroupDev {
   int32_t m0, nm;           // members [m0, m0 + nm)
-  int32_t lo[3];            // voxel bbox origin (lo[0] even)
-  int32_t dim[3];           // voxel bbox size (dim[0] even); 0 => global-atomic fallback
+  int32_t lo[3];            // voxel bbox origin (not clipped to the grid; lo[0] even)
+  int32_t dim[3];           // voxel bbox size (dim[0] even)
 };
 
 // EM state on the device (written by k_em_params / k_range_finish, read by later kernels).
@@ -88,18 +89,20 @@ struct LatticeArgs {
 
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
 constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
-constexpr int kMaxTileBytes = 96 * 1024;   // shared (A, C) fixed-point tile budget per group
-constexpr int kRBytes = 12 * 1024;         // shared per-pixel (rA, rC) buffer budget per group
+constexpr int kBpTileBytes = 96 * 1024;   // backprojection: 16 B/voxel hi/lo (A, C) tile budget
+constexpr int kRBytes = 12 * 1024;         // backprojection: per-pixel (rA, rC) buffer budget
+constexpr int kFwdTileBytes = 56 * 1024;  // forward: 4 B/voxel X tile budget (3 CTAs/SM)
 
 // ---- launchers; all asynchronous on `st` ----
 // lattice.cu
-void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_bytes, float* kap,
-                     double* partials);
-void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_bytes, const float* X,
-                    const float* kap, const float* p, float* e, double* partials);
-void launch_backproject(cudaStream_t st, const LatticeArgs& a, int smem_tile_bytes,
-                        int r_bytes, const float* kap, const float* e, const float* p,
-                        const float* w, int init, float2* AC);
+void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
+                     float* kap, double* partials);
+void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
+                    const float* X, const float* kap, const float* p, float* e,
+                    double* partials);
+void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
+                        const float* kap, const float* e, const float* p, const float* w,
+                        int init, float2* AC);
 // kernels.cu
 void launch_range_finish(cudaStream_t st, double s2floor, EmDev* em);
 void launch_fill(cudaStream_t st, float* x, int64_t n, float v);

@@ -48,10 +48,17 @@ class pvr_stats(C.Structure):
                [(n, C.c_int64) for n in ("n_forward", "n_em", "n_estep", "n_backproject",
                                           "n_allreduce", "n_update", "bytes_alg_forward",
                                           "bytes_alg_estep", "bytes_alg_backproject",
-                                          "bytes_alg_update")]
+                                          "bytes_alg_update")] + \
+               [("fwd_tile", C.c_int32 * 3), ("bp_tile", C.c_int32 * 3)] + \
+               [(n, C.c_int64) for n in ("fwd_groups", "bp_groups", "fwd_members", "bp_members",
+                                          "fwd_smem", "bp_smem")]
 
     def as_dict(self):
-        return {n: getattr(self, n) for n, _ in self._fields_}
+        d = {}
+        for n, _ in self._fields_:
+            v = getattr(self, n)
+            d[n] = list(v) if n.endswith("_tile") else v
+        return d
 
 
 _lib = None

@@ -1,0 +1,15 @@
+"""Print the lattice-kernel plans and per-kernel times for a config (GPU)."""
+import sys, json
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import synth
+from helpers import make_gpu
+cfg = sys.argv[1]
+kw = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
+if "scale" in kw: kw["scale"] = tuple(kw["scale"])
+prob = synth.make_problem(cfg, **kw)
+ctx = make_gpu(prob, {"profile": 1})
+ctx.init_volume()
+ctx.sr_iterate(2, 1.0, 0.02)
+s = ctx.stats()
+print(cfg, {k: s[k] for k in ("fwd_tile", "bp_tile", "fwd_groups", "bp_groups", "fwd_members", "bp_members", "fwd_smem", "bp_smem")})
+print("ms/iter", {k: round(s[k] / 2, 3) for k in ("ms_forward", "ms_backproject", "ms_update", "ms_estep")})
