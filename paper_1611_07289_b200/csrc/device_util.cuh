@@ -61,12 +61,11 @@ __device__ __forceinline__ void red_v4(float2* addr, float a0, float c0, float a
                : "memory");
 }
 
-// floor(x) for |x| < 2^22 without the conversion pipe: round-to-nearest of x - 1/2 via the
-// 1.5 * 2^23 magic. At exact integers it may return x - 1 with fraction 1, which gives the
-// same trilinear value and the same splat (the weight 0 corner is the dropped one).
+// floor(x) for |x| < 2^22 without the conversion pipe: x + 1.5 * 2^23 rounded toward -inf
+// (FADD.RM) holds floor(x) in its low mantissa bits; fl = float(floor(x)) exactly.
 __device__ __forceinline__ int mfloor(float x, float& fl) {
-  const float t = __fadd_rn(__fadd_rn(x, -0.5f), 12582912.0f);
-  fl = __fadd_rn(t, -12582912.0f);
+  const float t = __fadd_rd(x, 12582912.0f);
+  fl = __fsub_rn(t, 12582912.0f);
   return __float_as_int(t) - 0x4B400000;
 }
 

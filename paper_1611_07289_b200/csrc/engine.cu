@@ -110,7 +110,7 @@ struct pvr_ctx {
     MemberDev* mem = nullptr;
     GroupDev* grp = nullptr;
     size_t mem_cap = 0, grp_cap = 0;
-  } fplan, bplan;
+  } fplan, bplan, iplan;  // forward/coverage, backprojection, init backprojection (hi/lo)
   // comm
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -330,6 +330,7 @@ void free_dev(pvr_ctx* c) {
     if (s.y_dev) cudaFree(s.y_dev), s.y_dev = nullptr;
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
+                  c->iplan.mem, c->iplan.grp,
                   c->partials, c->em};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -403,9 +404,12 @@ int64_t r_bytes_of(const MemberDev& m, const StackPsf& ps) {
   return (int64_t)(m.tu + 2 * ps.ru / ps.nu + 2) * (m.tv + 2 * ps.rv / ps.nv + 2) * 8;
 }
 
+// kind 0: forward / coverage (4 B per voxel of staged X), 1: backprojection in the iterations
+// (8 B: one int32 per quantity), 2: init backprojection (16 B: hi/lo pairs)
 void build_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const std::vector<int64_t>& which,
-                  int TU, int TV, int nseg, bool fwd, PlanBuild& out) {
-  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kBpTileBytes / 16;
+                  int TU, int TV, int nseg, int kind, PlanBuild& out) {
+  const bool fwd = kind == 0;
+  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 : kInitTileBytes / 16;
   std::vector<MemberDev> mem;
   for (int64_t s : which) {
     const HostPatch& hp = c->patches[c->first + s];
@@ -547,16 +551,17 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
   const int fcand[][3] = {{16, 16, 1}, {16, 8, 1}, {8, 8, 1}, {8, 4, 1}, {4, 4, 1}, {2, 2, 1}, {1, 1, 1}};
   const int bcand[][3] = {{16, 16, 1}, {16, 8, 1}, {16, 8, 2}, {8, 8, 1}, {8, 8, 2}, {8, 4, 2},
                           {4, 4, 2},   {4, 4, 4},  {2, 2, 4},  {2, 2, 8}, {1, 1, 8}, {1, 1, 32}};
-  for (int fwd = 1; fwd >= 0; --fwd) {
-    pvr_ctx::Plan& pl = fwd ? c->fplan : c->bplan;
+  for (int kind = 0; kind < 3; ++kind) {
+    const bool fwd = kind == 0;
+    pvr_ctx::Plan& pl = kind == 0 ? c->fplan : kind == 1 ? c->bplan : c->iplan;
     const int(*cand)[3] = fwd ? fcand : bcand;
     const int ncand = fwd ? (int)(sizeof(fcand) / sizeof(fcand[0])) : (int)(sizeof(bcand) / sizeof(bcand[0]));
     int pick = -1;
     PlanBuild pb;
     for (int k = 0; k < ncand; ++k) {
-      build_groups(c, geo, sample, cand[k][0], cand[k][1], cand[k][2], fwd, pb);  // quick reject
+      build_groups(c, geo, sample, cand[k][0], cand[k][1], cand[k][2], kind, pb);  // quick reject
       if (!(pb.all_fit && pb.fit_frac >= 0.9)) continue;
-      build_groups(c, geo, all, cand[k][0], cand[k][1], cand[k][2], fwd, pb);
+      build_groups(c, geo, all, cand[k][0], cand[k][1], cand[k][2], kind, pb);
       if (pb.all_fit) { pick = k; break; }
     }
     if (pick < 0) return fail(c, PVR_ERR_ARG, "no tiling fits the shared-memory budget (extreme transforms?)");
@@ -565,12 +570,13 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
     pl.nseg = cand[pick][2];
     pvr_status r = upload_plan(c, pl, pb);
     if (r != PVR_OK) return r;
+    if (kind == 2) continue;
     int32_t* tile = fwd ? c->st.fwd_tile : c->st.bp_tile;
     tile[0] = pl.TU; tile[1] = pl.TV; tile[2] = pl.nseg;
     (fwd ? c->st.fwd_groups : c->st.bp_groups) = pl.ngroups;
     (fwd ? c->st.fwd_members : c->st.bp_members) = (int64_t)pb.mem.size();
     (fwd ? c->st.fwd_smem : c->st.bp_smem) =
-        fwd ? (int64_t)(pl.t_floats + pl.tile_words) * 4 : (int64_t)pl.tile_words * 16 + pl.r_bytes;
+        fwd ? (int64_t)(pl.t_floats + pl.tile_words) * 4 : (int64_t)pl.tile_words * 8 + pl.r_bytes;
   }
   return PVR_OK;
 }
@@ -990,9 +996,9 @@ pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
 pvr_status pvr_init_volume(pvr_ctx* c) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
-  const LatticeArgs lb = lattice_args(c, c->bplan);
+  const LatticeArgs lb = lattice_args(c, c->iplan);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
-  launch_backproject(c->stream, lb, c->bplan.tile_words, c->bplan.r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);
+  launch_backproject(c->stream, lb, c->iplan.tile_words, c->iplan.r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);
   CHECK_LAUNCH(c);
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;

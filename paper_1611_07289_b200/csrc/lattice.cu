@@ -100,18 +100,30 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
-    const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
+    const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = dx * dy;
     __syncthreads();  // the previous group's readers of sX / sT / tables are done
-    // stage X (or the grid indicator) over the group footprint, zero outside the grid
-    for (int i = threadIdx.x; i < dx * dy * dz; i += kThreads) {
-      const int lx = i % dx, r = i / dx;
-      const int ly = r % dy, lz = r / dy;
-      const int gx = G.lo[0] + lx, gy = G.lo[1] + ly, gz = G.lo[2] + lz;
-      float v = 0.0f;
-      if (gx >= 0 && gx < n.x && gy >= 0 && gy < n.y && gz >= 0 && gz < n.z)
-        v = MODE == 1 ? 1.0f : __ldg(X + ((size_t)gz * n.y + gy) * n.x + gx);
-      sX[i] = v;
+    // stage X (or the grid indicator) over the group footprint, zero outside the grid: one
+    // warp per tile row, lanes along x, asynchronous copies (cp.async, zero-fill out of grid)
+    for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
+      const int ly = row % dy, lz = row / dy;
+      const int gy = G.lo[1] + ly, gz = G.lo[2] + lz;
+      const bool rin = gy >= 0 && gy < n.y && gz >= 0 && gz < n.z;
+      const size_t rowoff = ((size_t)(rin ? gz : 0) * n.y + (rin ? gy : 0)) * n.x;
+      float* dst = sX + row * dx;
+      for (int lx = threadIdx.x & 31; lx < dx; lx += 32) {
+        const int gx = G.lo[0] + lx;
+        const bool in = rin && gx >= 0 && gx < n.x;
+        if (MODE == 1) {
+          dst[lx] = in ? 1.0f : 0.0f;
+        } else {
+          const unsigned s = (unsigned)__cvta_generic_to_shared(dst + lx);
+          const float* src = X + (in ? rowoff + gx : 0);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(src), "r"(in ? 4 : 0)
+                       : "memory");
+        }
+      }
     }
+    if (MODE == 0) asm volatile("cp.async.wait_all;" ::: "memory");
     for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
       const MemberDev m = a.mem[mi];
       const PatchDev& pt = a.P[m.patch];
@@ -140,9 +152,9 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
           const int iy = mfloor(ry, fly) + ob[1];
           const int iz = mfloor(rz, flz) + ob[2];
           const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
-          const float* p = sX + (iz * dy + iy) * dx + ix;
+          const float* p = sX + iz * dxy + iy * dx + ix;
           const float x000 = p[0], x100 = p[1], x010 = p[dx], x110 = p[dx + 1];
-          const float x001 = p[dx * dy], x101 = p[dx * dy + 1], x011 = p[dx * dy + dx], x111 = p[dx * dy + dx + 1];
+          const float x001 = p[dxy], x101 = p[dxy + 1], x011 = p[dxy + dx], x111 = p[dxy + dx + 1];
           const float c00 = fmaf(fx, x100 - x000, x000), c10 = fmaf(fx, x110 - x010, x010);
           const float c01 = fmaf(fx, x101 - x001, x001), c11 = fmaf(fx, x111 - x011, x011);
           const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
@@ -236,19 +248,21 @@ struct Tile {  // planar int32 accumulators of the group bbox: A, C (+ lo words 
 // Add one (A, C) term to tile cell idx. HILO: exact hi/lo words (init pass: raw intensities,
 // the widest dynamic range); otherwise one int32 word per quantity, round-to-nearest on the
 // group's 2^-21 grid (iterations: residual-weighted terms; bounded dynamic range).
+// Term (a w, c w) for corner weight w: one FFMA per quantity forms round(a w) in the magic's
+// mantissa (|a w| < 2^22).
 template <bool HILO>
-__device__ __forceinline__ void tile_add(const Tile& T, int idx, float vA, float vC) {
+__device__ __forceinline__ void tile_add(const Tile& T, int idx, float a, float c, float w) {
   if (HILO) {
     int h, l;
-    split_hilo(vA, h, l);
+    split_hilo(a * w, h, l);
     atomicAdd(T.ah + idx, h);
     atomicAdd(T.al + idx, l);
-    split_hilo(vC, h, l);
+    split_hilo(c * w, h, l);
     atomicAdd(T.ch + idx, h);
     atomicAdd(T.cl + idx, l);
   } else {
-    atomicAdd(T.ah + idx, __float_as_int(__fadd_rn(vA, kMagic)) - kMagicBits);
-    atomicAdd(T.ch + idx, __float_as_int(__fadd_rn(vC, kMagic)) - kMagicBits);
+    atomicAdd(T.ah + idx, __float_as_int(__fmaf_rn(a, w, kMagic)) - kMagicBits);
+    atomicAdd(T.ch + idx, __float_as_int(__fmaf_rn(c, w, kMagic)) - kMagicBits);
   }
 }
 
@@ -258,35 +272,36 @@ __device__ __forceinline__ void tile_add(const Tile& T, int idx, float vA, float
 // voxel planes at different steps, so the warp serialised the flush branches).
 template <bool HILO>
 __device__ __forceinline__ void splat_line(const Tile& T, const float* s_tp, float rx, float ry,
-                                           float rz, const float* qc, const int* ob, int c0,
-                                           int c1, int cmax, float LA, float LC) {
-  rx += c0 * qc[0];
-  ry += c0 * qc[1];
-  rz += c0 * qc[2];
-  const int dxy = T.dx * T.dy;
+                                           float rz, float qcx, float qcy, float qcz, int obx,
+                                           int oby, int obz, int c0, int c1, int cmax, float LA,
+                                           float LC) {
+  rx += c0 * qcx;
+  ry += c0 * qcy;
+  rz += c0 * qcz;
+  const int dx = T.dx, dxy = T.dx * T.dy;
   for (int c = c0; c <= c1; ++c) {
     const float t = s_tp[c + cmax];
     float flx, fly, flz;
-    const int ix = mfloor(rx, flx) + ob[0];
-    const int iy = mfloor(ry, fly) + ob[1];
-    const int iz = mfloor(rz, flz) + ob[2];
+    const int ix = mfloor(rx, flx) + obx;
+    const int iy = mfloor(ry, fly) + oby;
+    const int iz = mfloor(rz, flz) + obz;
     const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
     const float vA = LA * t, vC = LC * t;
-    const int k000 = (iz * T.dy + iy) * T.dx + ix;
+    const int k000 = iz * dxy + iy * dx + ix;
     const float wy0z0 = (1.0f - fy) * (1.0f - fz), wy1z0 = fy * (1.0f - fz);
     const float wy0z1 = (1.0f - fy) * fz, wy1z1 = fy * fz;
     const float a0 = vA * (1.0f - fx), a1 = vA * fx, g0 = vC * (1.0f - fx), g1 = vC * fx;
-    tile_add<HILO>(T, k000, a0 * wy0z0, g0 * wy0z0);
-    tile_add<HILO>(T, k000 + 1, a1 * wy0z0, g1 * wy0z0);
-    tile_add<HILO>(T, k000 + T.dx, a0 * wy1z0, g0 * wy1z0);
-    tile_add<HILO>(T, k000 + T.dx + 1, a1 * wy1z0, g1 * wy1z0);
-    tile_add<HILO>(T, k000 + dxy, a0 * wy0z1, g0 * wy0z1);
-    tile_add<HILO>(T, k000 + dxy + 1, a1 * wy0z1, g1 * wy0z1);
-    tile_add<HILO>(T, k000 + dxy + T.dx, a0 * wy1z1, g0 * wy1z1);
-    tile_add<HILO>(T, k000 + dxy + T.dx + 1, a1 * wy1z1, g1 * wy1z1);
-    rx += qc[0];
-    ry += qc[1];
-    rz += qc[2];
+    tile_add<HILO>(T, k000, a0, g0, wy0z0);
+    tile_add<HILO>(T, k000 + 1, a1, g1, wy0z0);
+    tile_add<HILO>(T, k000 + dx, a0, g0, wy1z0);
+    tile_add<HILO>(T, k000 + dx + 1, a1, g1, wy1z0);
+    tile_add<HILO>(T, k000 + dxy, a0, g0, wy0z1);
+    tile_add<HILO>(T, k000 + dxy + 1, a1, g1, wy0z1);
+    tile_add<HILO>(T, k000 + dxy + dx, a0, g0, wy1z1);
+    tile_add<HILO>(T, k000 + dxy + dx + 1, a1, g1, wy1z1);
+    rx += qcx;
+    ry += qcy;
+    rz += qcz;
   }
 }
 
@@ -393,15 +408,19 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
       for (int i = threadIdx.x; i < nU * nV; i += kThreads) {
         const int iu = i % nU, iv = i / nU;
         const int U = o.Ulo + iu, V = o.Vlo + iv;
+        // pixels feeding lattice point U: u = (U - a) / nu with a = U mod nu (and a - nu when
+        // that is within [-ru, ru]); same along V
+        const int ub = floor_div(U, mg.nu), ra = U - ub * mg.nu;
+        const int vb = floor_div(V, mg.nv), rb = V - vb * mg.nv;
         float LA = 0.0f, LC = 0.0f;
-        for (int b = -mg.rv; b <= mg.rv; ++b) {
-          const int vn = V - b;
-          if (vn < mg.nv * o.plv || vn > mg.nv * o.phv || (vn - mg.nv * o.plv) % mg.nv) continue;
-          const int v = vn / mg.nv;
-          for (int aa = -mg.ru; aa <= mg.ru; ++aa) {
-            const int un = U - aa;
-            if (un < mg.nu * o.plu || un > mg.nu * o.phu || (un - mg.nu * o.plu) % mg.nu) continue;
-            const int u = un / mg.nu;
+#pragma unroll
+        for (int jb = 0; jb < 2; ++jb) {
+          const int b = jb ? rb - mg.nv : rb, v = vb + jb;
+          if (b < -mg.rv || b > mg.rv || v < o.plv || v > o.phv) continue;
+#pragma unroll
+          for (int ja = 0; ja < 2; ++ja) {
+            const int aa = ja ? ra - mg.nu : ra, u = ub + ja;
+            if (aa < -mg.ru || aa > mg.ru || u < o.plu || u > o.phu) continue;
             const float wt = s_ip[(b + mg.rv) * w2 + (aa + mg.ru)];
             const float2 rr = R[roff + (v - o.plv) * rw + (u - o.plu)];
             LA += wt * rr.x;
@@ -415,13 +434,15 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         const float r0x = of[0] + fU * mg.qa[0] + fV * mg.qb[0];
         const float r0y = of[1] + fU * mg.qa[1] + fV * mg.qb[1];
         const float r0z = of[2] + fU * mg.qa[2] + fV * mg.qb[2];
-        splat_line<HILO>(T, s_tp, r0x, r0y, r0z, mg.qc, ob, m.c0, m.c1, mg.cmax, LA, LC);
+        splat_line<HILO>(T, s_tp, r0x, r0y, r0z, mg.qc[0], mg.qc[1], mg.qc[2], ob[0], ob[1], ob[2], m.c0,
+                         m.c1, mg.cmax, LA, LC);
       }
       roff += rw * rh;
     }
     __syncthreads();
     // ---- phase C: flush the tile, one red.v4 per in-grid (even, odd) voxel pair along x
     const double iA = scA > 0.0f ? 1.0 / scA : 0.0, iC = scC > 0.0f ? 1.0 / scC : 0.0;
+    const float fA = (float)iA, fC = (float)iC;
     const int hx = (dx + 1) >> 1;
     for (int i = threadIdx.x; i < hx * dy * dz; i += kThreads) {
       const int px = i % hx, rest = i / hx;
@@ -437,10 +458,16 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         cl0 = T.cl[k]; cl1 = two ? T.cl[k + 1] : 0;
       }
       if ((ah0 | ah1 | ch0 | ch1 | al0 | al1 | cl0 | cl1) == 0) continue;
-      const float A0 = (float)(((double)ah0 + (double)al0 * (1.0 / kLoScale)) * iA);
-      const float A1 = (float)(((double)ah1 + (double)al1 * (1.0 / kLoScale)) * iA);
-      const float C0 = (float)(((double)ch0 + (double)cl0 * (1.0 / kLoScale)) * iC);
-      const float C1 = (float)(((double)ch1 + (double)cl1 * (1.0 / kLoScale)) * iC);
+      float A0, A1, C0, C1;
+      if (HILO) {
+        A0 = (float)(((double)ah0 + (double)al0 * (1.0 / kLoScale)) * iA);
+        A1 = (float)(((double)ah1 + (double)al1 * (1.0 / kLoScale)) * iA);
+        C0 = (float)(((double)ch0 + (double)cl0 * (1.0 / kLoScale)) * iC);
+        C1 = (float)(((double)ch1 + (double)cl1 * (1.0 / kLoScale)) * iC);
+      } else {
+        A0 = (float)ah0 * fA; A1 = (float)ah1 * fA;
+        C0 = (float)ch0 * fC; C1 = (float)ch1 * fC;
+      }
       red_v4(AC + ((size_t)gz * n.y + gy) * a.nxp + gx, A0, C0, A1, C1);
     }
   }
