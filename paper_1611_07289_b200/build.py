@@ -9,13 +9,13 @@ SRCS = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "kernels.cu", "latt
 DEPS = SRCS + [os.path.join(HERE, "csrc", "pvr_internal.h"), os.path.join(HERE, "csrc", "device_util.cuh"), os.path.join(ROOT, "include", "pvr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xlinker", "--no-undefined", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC,-fopenmp", "-shared", "-Xlinker", "--no-undefined", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
 def build(force=False, verbose=False):
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in DEPS):
         return SO
-    cmd = [NVCC] + FLAGS + ["-I" + os.path.join(ROOT, "include"), "-o", SO] + SRCS + ["-ldl"]
+    cmd = [NVCC] + FLAGS + ["-I" + os.path.join(ROOT, "include"), "-o", SO] + SRCS + ["-ldl", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <memory>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -40,6 +41,16 @@ struct HostStack {
 
 struct HostPatch {
   int32_t stack, x0, y0, z0, sx, sy, sz;
+};
+
+// Natural groups of one tiling candidate: geometry independent, built once per candidate and
+// cached (keyed by TU, TV, nseg, forward/backprojection); only bounding boxes depend on T.
+struct NaturalGroups {
+  int TU = 0, TV = 0, nseg = 0;
+  bool fwd = false, sample = false;
+  std::vector<MemberDev> mem;  // sorted by group
+  std::vector<int32_t> start;  // group g = mem[start[g], start[g+1])
+  int64_t max_r_bytes = 0, max_t_floats = 0;
 };
 
 // fp64 geometry of one local patch: voxel index of lattice point (U, V, c) of slice z is
@@ -111,6 +122,7 @@ struct pvr_ctx {
     GroupDev* grp = nullptr;
     size_t mem_cap = 0, grp_cap = 0;
   } fplan, bplan, iplan;  // forward/coverage, backprojection, init backprojection (hi/lo)
+  std::vector<std::unique_ptr<NaturalGroups>> ngcache;  // geometry-free group lists
   // comm
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -340,11 +352,6 @@ void free_dev(pvr_ctx* c) {
 // A member is a tile of tu x tv pixels of one slice of one patch (backprojection members also
 // carry a through-plane lattice segment [c0, c1]). Members that cover the same stack pixels
 // (overlapping patches of one stack) form a group: one CTA, one shared voxel tile.
-struct MemberKey {
-  int64_t key[6];
-  int32_t idx;
-};
-
 // Owned fine-lattice range of a backprojection member (must match owned_range() in lattice.cu).
 void owned(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, int& Ulo, int& Uhi, int& Vlo,
            int& Vhi) {
@@ -391,26 +398,15 @@ void member_bbox(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, co
   }
 }
 
-struct PlanBuild {
-  std::vector<MemberDev> mem;  // group-sorted
-  std::vector<GroupDev> grp;
-  int64_t max_tile_vox = 0, max_r_bytes = 0, max_t_floats = 0;
-  int nsplit = 0;              // groups that had to be split into single members
-  bool all_fit = true;         // every single member fits the tile budget
-  double fit_frac = 0.0;       // fraction of natural groups that fit whole
-};
-
 int64_t r_bytes_of(const MemberDev& m, const StackPsf& ps) {
   return (int64_t)(m.tu + 2 * ps.ru / ps.nu + 2) * (m.tv + 2 * ps.rv / ps.nv + 2) * 8;
 }
 
-// kind 0: forward / coverage (4 B per voxel of staged X), 1: backprojection in the iterations
-// (8 B: one int32 per quantity), 2: init backprojection (16 B: hi/lo pairs)
-void build_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const std::vector<int64_t>& which,
-                  int TU, int TV, int nseg, int kind, PlanBuild& out) {
-  const bool fwd = kind == 0;
-  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 : kInitTileBytes / 16;
+void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, int TV, int nseg, bool fwd,
+                   NaturalGroups& ng) {
+  ng.TU = TU; ng.TV = TV; ng.nseg = nseg; ng.fwd = fwd;
   std::vector<MemberDev> mem;
+  std::vector<std::pair<uint64_t, int32_t>> keys;
   for (int64_t s : which) {
     const HostPatch& hp = c->patches[c->first + s];
     const StackPsf& ps = c->stacks[hp.stack].psf;
@@ -421,99 +417,118 @@ void build_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const std:
           for (int k = 0; k < (fwd ? 1 : nseg); ++k) {
             const int c0 = -ps.cmax + k * seg, c1 = fwd ? ps.cmax : std::min(ps.cmax, c0 + seg - 1);
             if (c0 > c1) continue;
-            mem.push_back(MemberDev{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0),
-                                    c0, c1});
+            const MemberDev m{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0), c0, c1};
+            // group key: stack | slice | c segment | stack row | stack column | tile shape
+            const uint64_t key = ((uint64_t)hp.stack << 58) | ((uint64_t)(hp.z0 + z) << 44) |
+                                 ((uint64_t)k << 38) | ((uint64_t)(hp.y0 + v0) << 24) |
+                                 ((uint64_t)(hp.x0 + u0) << 10) | ((uint64_t)m.tu << 5) | (uint64_t)m.tv;
+            keys.emplace_back(key, (int32_t)mem.size());
+            mem.push_back(m);
           }
   }
-  std::vector<MemberKey> keys(mem.size());
-  for (size_t i = 0; i < mem.size(); ++i) {
-    const MemberDev& m = mem[i];
-    const HostPatch& hp = c->patches[c->first + m.patch];
-    keys[i] = MemberKey{{hp.stack, hp.z0 + m.z, m.c0, hp.y0 + m.v0, hp.x0 + m.u0, (int64_t)m.tu * 64 + m.tv},
-                        (int32_t)i};
-  }
-  std::stable_sort(keys.begin(), keys.end(), [](const MemberKey& a, const MemberKey& b) {
-    return std::lexicographical_compare(a.key, a.key + 6, b.key, b.key + 6);
-  });
-  out.mem.clear();
-  out.grp.clear();
-  out.max_tile_vox = out.max_r_bytes = out.max_t_floats = 0;
-  out.nsplit = 0;
-  out.all_fit = true;
-  int natural = 0, fit = 0;
-  auto bbox_of = [&](const std::vector<int>& ids, int lo[3], int hi[3]) {
-    for (int d = 0; d < 3; ++d) { lo[d] = 1 << 30; hi[d] = -(1 << 30); }
-    for (int id : ids) {
-      const MemberDev& m = mem[id];
-      const HostPatch& hp = c->patches[c->first + m.patch];
-      int l[3], h[3];
-      member_bbox(m, hp, c->stacks[hp.stack].psf, geo[m.patch], fwd, l, h);
-      for (int d = 0; d < 3; ++d) { lo[d] = std::min(lo[d], l[d]); hi[d] = std::max(hi[d], h[d]); }
-    }
-    lo[0] = lo[0] - (((lo[0] % 2) + 2) % 2);  // even x origin: 16-byte aligned flush pairs
-    const int64_t dx = (hi[0] - lo[0] + 1) | 1, dy = (hi[1] - lo[1] + 1) | 1;
-    return dx * dy * (hi[2] - lo[2] + 1);
-  };
-  auto emit = [&](const std::vector<int>& ids) {
-    int lo[3], hi[3];
-    const int64_t vox = bbox_of(ids, lo, hi);
-    GroupDev g;
-    g.m0 = (int32_t)out.mem.size();
-    g.nm = (int32_t)ids.size();
-    for (int d = 0; d < 3; ++d) g.lo[d] = lo[d];
-    g.dim[0] = hi[0] - lo[0] + 1;
-    // odd row and plane pitches: lanes stepping along x, y or z hit different banks
-    g.dim[0] |= 1;
-    g.dim[1] = (hi[1] - lo[1] + 1) | 1;
-    g.dim[2] = hi[2] - lo[2] + 1;
-    int64_t rb = 0;
-    for (int id : ids) {
-      const MemberDev& m = mem[id];
-      const HostPatch& hp = c->patches[c->first + m.patch];
-      const StackPsf& ps = c->stacks[hp.stack].psf;
-      out.mem.push_back(m);
-      rb += r_bytes_of(m, ps);
-      out.max_t_floats = std::max<int64_t>(out.max_t_floats, (int64_t)(ps.nu * (m.tu - 1) + 2 * ps.ru + 1) *
-                                                               (ps.nv * (m.tv - 1) + 2 * ps.rv + 1));
-    }
-    out.max_tile_vox = std::max(out.max_tile_vox, vox);
-    out.max_r_bytes = std::max(out.max_r_bytes, rb);
-    out.grp.push_back(g);
-    if (vox > vox_budget) out.all_fit = false;
-  };
+  std::sort(keys.begin(), keys.end());
+  ng.mem.clear();
+  ng.start.clear();
+  ng.max_r_bytes = ng.max_t_floats = 0;
   size_t i = 0;
   while (i < keys.size()) {
     size_t j = i;
-    while (j < keys.size() && std::equal(keys[i].key, keys[i].key + 6, keys[j].key)) ++j;
-    // split natural groups by the R buffer budget (backprojection), then by the tile budget
-    std::vector<std::vector<int>> parts(1);
+    while (j < keys.size() && keys[j].first == keys[i].first) ++j;
     int64_t rb = 0;
+    ng.start.push_back((int32_t)ng.mem.size());
     for (size_t k = i; k < j; ++k) {
-      const int id = keys[k].idx;
-      const MemberDev& m = mem[id];
+      const MemberDev& m = mem[keys[k].second];
       const StackPsf& ps = c->stacks[c->patches[c->first + m.patch].stack].psf;
       const int64_t b = r_bytes_of(m, ps);
-      if (!fwd && !parts.back().empty() && rb + b > kRBytes) {
-        parts.emplace_back();
+      if (!fwd && k > i && rb + b > kRBytes) {  // split by the R buffer budget
+        ng.max_r_bytes = std::max(ng.max_r_bytes, rb);
+        ng.start.push_back((int32_t)ng.mem.size());
         rb = 0;
       }
-      parts.back().push_back(id);
       rb += b;
+      ng.max_t_floats = std::max<int64_t>(ng.max_t_floats, (int64_t)(ps.nu * (m.tu - 1) + 2 * ps.ru + 1) *
+                                                             (ps.nv * (m.tv - 1) + 2 * ps.rv + 1));
+      ng.mem.push_back(m);
     }
-    for (auto& part : parts) {
-      int lo[3], hi[3];
-      ++natural;
-      if (bbox_of(part, lo, hi) <= vox_budget) {
-        ++fit;
-        emit(part);
-      } else {
-        if (part.size() > 1) ++out.nsplit;
-        for (int id : part) emit(std::vector<int>{id});
-      }
-    }
+    ng.max_r_bytes = std::max(ng.max_r_bytes, rb);
     i = j;
   }
-  out.fit_frac = natural ? (double)fit / natural : 1.0;
+  ng.start.push_back((int32_t)ng.mem.size());
+}
+
+struct PlanBuild {
+  std::vector<MemberDev> mem;  // group-sorted (groups over the budget are split into singles)
+  std::vector<GroupDev> grp;
+  int64_t max_tile_vox = 0, max_r_bytes = 0, max_t_floats = 0;
+  int nsplit = 0;              // natural groups split into single members
+  bool all_fit = true;         // every single member fits the tile budget
+  double fit_frac = 0.0;       // fraction of natural groups that fit whole
+};
+
+// Bounding boxes for the current transforms and the final group list of one plan.
+// kind 0: forward / coverage (4 B per voxel of staged X), 1: backprojection in the iterations
+// (8 B: one int32 per quantity), 2: init backprojection (16 B: hi/lo pairs).
+void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const NaturalGroups& ng, int kind,
+                 PlanBuild& out) {
+  const bool fwd = kind == 0;
+  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 : kInitTileBytes / 16;
+  const size_t nm = ng.mem.size();
+  std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)nm; ++i) {
+    const MemberDev& m = ng.mem[i];
+    const HostPatch& hp = c->patches[c->first + m.patch];
+    int lo[3], hi[3];
+    member_bbox(m, hp, c->stacks[hp.stack].psf, geo[m.patch], fwd, lo, hi);
+    for (int d = 0; d < 3; ++d) { mlo[3 * i + d] = lo[d]; mhi[3 * i + d] = hi[d]; }
+  }
+  out.mem.clear();
+  out.grp.clear();
+  out.max_tile_vox = 0;
+  out.max_r_bytes = ng.max_r_bytes;
+  out.max_t_floats = ng.max_t_floats;
+  out.nsplit = 0;
+  out.all_fit = true;
+  int fit = 0;
+  const int ngrp = (int)ng.start.size() - 1;
+  auto group = [&](int a, int b, GroupDev& g) {  // union bbox of members [a, b)
+    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+    for (int i = a; i < b; ++i)
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = std::min(lo[d], mlo[3 * i + d]);
+        hi[d] = std::max(hi[d], mhi[3 * i + d]);
+      }
+    lo[0] -= ((lo[0] % 2) + 2) % 2;  // even x origin: 16-byte aligned flush pairs
+    g.m0 = (int32_t)out.mem.size();
+    g.nm = b - a;
+    for (int d = 0; d < 3; ++d) g.lo[d] = lo[d];
+    // odd row and plane pitches: lanes stepping along x, y or z hit different banks
+    g.dim[0] = (hi[0] - lo[0] + 1) | 1;
+    g.dim[1] = (hi[1] - lo[1] + 1) | 1;
+    g.dim[2] = hi[2] - lo[2] + 1;
+    return (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
+  };
+  for (int gi = 0; gi < ngrp; ++gi) {
+    const int a = ng.start[gi], b = ng.start[gi + 1];
+    GroupDev g;
+    int64_t vox = group(a, b, g);
+    if (vox <= vox_budget) {
+      ++fit;
+      for (int i = a; i < b; ++i) out.mem.push_back(ng.mem[i]);
+      out.grp.push_back(g);
+      out.max_tile_vox = std::max(out.max_tile_vox, vox);
+      continue;
+    }
+    if (b - a > 1) ++out.nsplit;
+    for (int i = a; i < b; ++i) {
+      vox = group(i, i + 1, g);
+      if (vox > vox_budget) out.all_fit = false;
+      out.mem.push_back(ng.mem[i]);
+      out.grp.push_back(g);
+      out.max_tile_vox = std::max(out.max_tile_vox, vox);
+    }
+  }
+  out.fit_frac = ngrp ? (double)fit / ngrp : 1.0;
 }
 
 pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
@@ -541,28 +556,45 @@ pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
 }
 
 // Tile size (and backprojection c segments): the largest candidate for which >= 90% of the
-// natural groups of a sample of patches fit whole and every single member fits; large tiles
-// amortise the flush, the staging and the lattice halo.
+// natural groups fit whole and every single member fits; large tiles amortise the flush, the
+// staging and the lattice halo. Candidates are first screened on a sample of patches; the last
+// choice is tried first, so repeated set_transforms with similar motion only resize bboxes.
 pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
   std::vector<int64_t> sample, all(c->nloc);
   for (int64_t s = 0; s < c->nloc; ++s) all[s] = s;
   const int64_t step = std::max<int64_t>(1, c->nloc / 128);
   for (int64_t s = 0; s < c->nloc; s += step) sample.push_back(s);
-  const int fcand[][3] = {{16, 16, 1}, {16, 8, 1}, {8, 8, 1}, {8, 4, 1}, {4, 4, 1}, {2, 2, 1}, {1, 1, 1}};
-  const int bcand[][3] = {{16, 16, 1}, {16, 8, 1}, {16, 8, 2}, {8, 8, 1}, {8, 8, 2}, {8, 4, 2},
-                          {4, 4, 2},   {4, 4, 4},  {2, 2, 4},  {2, 2, 8}, {1, 1, 8}, {1, 1, 32}};
+  static const int fcand[][3] = {{16, 16, 1}, {16, 8, 1}, {8, 8, 1}, {8, 4, 1}, {4, 4, 1}, {2, 2, 1}, {1, 1, 1}};
+  static const int bcand[][3] = {{16, 16, 1}, {16, 8, 1}, {16, 8, 2}, {8, 8, 1}, {8, 8, 2}, {8, 4, 2},
+                                 {4, 4, 2},   {4, 4, 4},  {2, 2, 4},  {2, 2, 8}, {1, 1, 8}, {1, 1, 32}};
+  auto natural = [&](int TU, int TV, int nseg, bool fwd, bool smp) -> const NaturalGroups& {
+    for (auto& ng : c->ngcache)
+      if (ng->TU == TU && ng->TV == TV && ng->nseg == nseg && ng->fwd == fwd && ng->sample == smp) return *ng;
+    c->ngcache.emplace_back(new NaturalGroups());
+    NaturalGroups& ng = *c->ngcache.back();
+    build_natural(c, smp ? sample : all, TU, TV, nseg, fwd, ng);
+    ng.sample = smp;
+    return ng;
+  };
   for (int kind = 0; kind < 3; ++kind) {
     const bool fwd = kind == 0;
     pvr_ctx::Plan& pl = kind == 0 ? c->fplan : kind == 1 ? c->bplan : c->iplan;
     const int(*cand)[3] = fwd ? fcand : bcand;
     const int ncand = fwd ? (int)(sizeof(fcand) / sizeof(fcand[0])) : (int)(sizeof(bcand) / sizeof(bcand[0]));
+    std::vector<int> order;
+    for (int k = 0; k < ncand; ++k)
+      if (cand[k][0] == pl.TU && cand[k][1] == pl.TV && cand[k][2] == pl.nseg && pl.ngroups > 0) order.push_back(k);
+    for (int k = 0; k < ncand; ++k) order.push_back(k);
     int pick = -1;
     PlanBuild pb;
-    for (int k = 0; k < ncand; ++k) {
-      build_groups(c, geo, sample, cand[k][0], cand[k][1], cand[k][2], kind, pb);  // quick reject
-      if (!(pb.all_fit && pb.fit_frac >= 0.9)) continue;
-      build_groups(c, geo, all, cand[k][0], cand[k][1], cand[k][2], kind, pb);
-      if (pb.all_fit) { pick = k; break; }
+    for (int k : order) {
+      const bool previous = pl.ngroups > 0 && k == order[0] && order.size() > (size_t)ncand;
+      if (!previous) {  // quick reject on the sample
+        size_groups(c, geo, natural(cand[k][0], cand[k][1], cand[k][2], fwd, true), kind, pb);
+        if (!(pb.all_fit && pb.fit_frac >= 0.9)) continue;
+      }
+      size_groups(c, geo, natural(cand[k][0], cand[k][1], cand[k][2], fwd, false), kind, pb);
+      if (pb.all_fit && pb.fit_frac >= 0.9) { pick = k; break; }
     }
     if (pick < 0) return fail(c, PVR_ERR_ARG, "no tiling fits the shared-memory budget (extreme transforms?)");
     pl.TU = cand[pick][0];

@@ -89,7 +89,7 @@ struct LatticeArgs {
 
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
 constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
-constexpr int kBpTileBytes = 62 * 1024;   // backprojection (iterations): 8 B/voxel tile budget (3 CTAs/SM)
+constexpr int kBpTileBytes = 96 * 1024;   // backprojection (iterations): 8 B/voxel tile budget
 constexpr int kInitTileBytes = 96 * 1024; // init backprojection: 16 B/voxel hi/lo tile budget
 constexpr int kRBytes = 12 * 1024;         // backprojection: per-pixel (rA, rC) buffer budget
 constexpr int kFwdTileBytes = 56 * 1024;  // forward: 4 B/voxel X tile budget (3 CTAs/SM)

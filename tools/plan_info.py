@@ -13,3 +13,7 @@ ctx.sr_iterate(2, 1.0, 0.02)
 s = ctx.stats()
 print(cfg, {k: s[k] for k in ("fwd_tile", "bp_tile", "fwd_groups", "bp_groups", "fwd_members", "bp_members", "fwd_smem", "bp_smem")})
 print("ms/iter", {k: round(s[k] / 2, 3) for k in ("ms_forward", "ms_backproject", "ms_update", "ms_estep")})
+import time
+for _ in range(3):
+    t0 = time.perf_counter(); ctx.set_transforms(prob["T"]); t1 = time.perf_counter()
+    print("set_transforms %.1f ms" % ((t1 - t0) * 1e3))
