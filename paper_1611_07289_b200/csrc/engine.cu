@@ -434,23 +434,30 @@ void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, 
   while (i < keys.size()) {
     size_t j = i;
     while (j < keys.size() && keys[j].first == keys[i].first) ++j;
-    int64_t rb = 0;
+    int64_t rb = 0, tsum = 0;
     ng.start.push_back((int32_t)ng.mem.size());
     for (size_t k = i; k < j; ++k) {
       const MemberDev& m = mem[keys[k].second];
       const StackPsf& ps = c->stacks[c->patches[c->first + m.patch].stack].psf;
       const int64_t b = r_bytes_of(m, ps);
-      if (!fwd && k > i && rb + b > kRBytes) {  // split by the R buffer budget
+      const int64_t tf = (int64_t)(ps.nu * (m.tu - 1) + 2 * ps.ru + 1) * (ps.nv * (m.tv - 1) + 2 * ps.rv + 1);
+      // split by the R buffer budget (backprojection) / the lattice buffer and member count
+      // (forward: all members' T values are resident at once)
+      const bool full = fwd ? (k > i && (tsum + tf > kFwdTBytes / 4 || (int64_t)ng.mem.size() - ng.start.back() >= kMaxGroupMembers))
+                            : (k > i && (rb + b > kRBytes || (int64_t)ng.mem.size() - ng.start.back() >= kMaxGroupMembers));
+      if (full) {
         ng.max_r_bytes = std::max(ng.max_r_bytes, rb);
+        ng.max_t_floats = std::max(ng.max_t_floats, tsum);
         ng.start.push_back((int32_t)ng.mem.size());
         rb = 0;
+        tsum = 0;
       }
       rb += b;
-      ng.max_t_floats = std::max<int64_t>(ng.max_t_floats, (int64_t)(ps.nu * (m.tu - 1) + 2 * ps.ru + 1) *
-                                                             (ps.nv * (m.tv - 1) + 2 * ps.rv + 1));
+      tsum += tf;
       ng.mem.push_back(m);
     }
     ng.max_r_bytes = std::max(ng.max_r_bytes, rb);
+    ng.max_t_floats = std::max(ng.max_t_floats, tsum);
     i = j;
   }
   ng.start.push_back((int32_t)ng.mem.size());

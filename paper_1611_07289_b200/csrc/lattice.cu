@@ -82,7 +82,18 @@ __device__ __forceinline__ void lattice_origin(const PatchDev& pt, int z, int U0
 // Forward (MODE 0) and coverage (MODE 1).
 //   MODE 0: out = e (residual, 0 if unobserved); stats {sum p e^2, sum p, n_live | max e, -min e}
 //   MODE 1: out = kappa;                         stats {n_obs, n_live, samples | max y, -min y}
-// Dynamic shared memory: [t_floats] lattice values T of one member, then the X tile.
+// One CTA per group: stage the group's X tile, then one balanced pass over the lattice points
+// of all members (T values into shared memory), then one pass over all their pixels.
+// Dynamic shared memory: [t_floats] lattice values T of all members, then the X tile.
+constexpr int kMaxMembers = 16;
+
+struct FwdMember {  // per-member constants in shared memory
+  float of[3], qa[3], qb[3], qc[3];
+  int ob[3];
+  int LU, LV, t0, p0;  // lattice extent, offset into sT, first pixel index in the group order
+  int patch, z, u0, v0, tu, tv;
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_floats,
                                                           const float* __restrict__ X,
@@ -94,6 +105,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
   float* sT = reinterpret_cast<float*>(fsm4);
   float* sX = sT + t_floats;
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
+  __shared__ FwdMember sm[kMaxMembers];
+  __shared__ int s_nt, s_np;  // lattice points / pixels of the group
   double acc_s[3] = {0.0, 0.0, 0.0};
   float acc_m[2] = {-FLT_MAX, -FLT_MAX};
   const int3 n = a.n;
@@ -101,11 +114,12 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = dx * dy;
-    __syncthreads();  // the previous group's readers of sX / sT / tables are done
+    __syncthreads();  // the previous group's readers of sX / sT / tables / sm are done
     // stage X (or the grid indicator) over the group footprint, zero outside the grid: one
     // warp per tile row, lanes along x, asynchronous copies (cp.async, zero-fill out of grid)
+    int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
+    while (ly >= dy) { ly -= dy; ++lz; }
     for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
-      const int ly = row % dy, lz = row / dy;
       const int gy = G.lo[1] + ly, gz = G.lo[2] + lz;
       const bool rin = gy >= 0 && gy < n.y && gz >= 0 && gz < n.z;
       const size_t rowoff = ((size_t)(rin ? gz : 0) * n.y + (rin ? gy : 0)) * n.x;
@@ -122,88 +136,124 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
                        : "memory");
         }
       }
+      ly += kThreads >> 5;
+      while (ly >= dy) { ly -= dy; ++lz; }
+    }
+    // member constants (one thread per member) and the stack's PSF tables
+    if (threadIdx.x < G.nm) {
+      const MemberDev m = a.mem[G.m0 + threadIdx.x];
+      const PatchDev& pt = a.P[m.patch];
+      const StackPsf ps = a.psf[pt.stack];
+      FwdMember& f = sm[threadIdx.x];
+      f.LU = ps.nu * (m.tu - 1) + 2 * ps.ru + 1;
+      f.LV = ps.nv * (m.tv - 1) + 2 * ps.rv + 1;
+      lattice_origin(pt, m.z, ps.nu * m.u0 - ps.ru, ps.nv * m.v0 - ps.rv, -ps.cmax, G.lo, f.ob, f.of);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        f.qa[d] = pt.Qa[d];
+        f.qb[d] = pt.Qb[d];
+        f.qc[d] = pt.Qc[d];
+      }
+      f.patch = m.patch; f.z = m.z; f.u0 = m.u0; f.v0 = m.v0; f.tu = m.tu; f.tv = m.tv;
+    }
+    {
+      const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
+      const int nip = (2 * ps.ru + 1) * (2 * ps.rv + 1);
+      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[ps.ip0 + i];
+      for (int i = threadIdx.x; i < 2 * ps.cmax + 1; i += kThreads) s_tp[i] = a.tab[ps.tp0 + i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0, p = 0;
+      for (int k = 0; k < G.nm; ++k) {
+        sm[k].t0 = t;
+        sm[k].p0 = p;
+        t += sm[k].LU * sm[k].LV;
+        p += sm[k].tu * sm[k].tv;
+      }
+      s_nt = t;
+      s_np = p;
     }
     if (MODE == 0) asm volatile("cp.async.wait_all;" ::: "memory");
-    for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
-      const MemberDev m = a.mem[mi];
-      const PatchDev& pt = a.P[m.patch];
-      const MemberGeom mg = member_geom(a, pt);
-      const int nip = (2 * mg.ru + 1) * (2 * mg.rv + 1);
-      __syncthreads();  // previous member's readers of sT / tables are done
-      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[mg.ip0 + i];
-      for (int i = threadIdx.x; i < mg.ntp; i += kThreads) s_tp[i] = a.tab[mg.tp0 + i];
-      // lattice points needed by the tile's pixels: U in [nu u0 - ru, nu (u0 + tu - 1) + ru]
-      const int LU = mg.nu * (m.tu - 1) + 2 * mg.ru + 1;
-      const int LV = mg.nv * (m.tv - 1) + 2 * mg.rv + 1;
-      const int U0 = mg.nu * m.u0 - mg.ru, V0 = mg.nv * m.v0 - mg.rv;
-      int ob[3];
-      float of[3];
-      lattice_origin(pt, m.z, U0, V0, -mg.cmax, G.lo, ob, of);
-      __syncthreads();
-      for (int i = threadIdx.x; i < LU * LV; i += kThreads) {
-        const float U = (float)(i % LU), V = (float)(i / LU);
-        float rx = of[0] + U * mg.qa[0] + V * mg.qb[0];
-        float ry = of[1] + U * mg.qa[1] + V * mg.qb[1];
-        float rz = of[2] + U * mg.qa[2] + V * mg.qb[2];
-        float acc = 0.0f;
-        for (int c = 0; c < mg.ntp; ++c) {
-          float flx, fly, flz;
-          const int ix = mfloor(rx, flx) + ob[0];
-          const int iy = mfloor(ry, fly) + ob[1];
-          const int iz = mfloor(rz, flz) + ob[2];
-          const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
-          const float* p = sX + iz * dxy + iy * dx + ix;
-          const float x000 = p[0], x100 = p[1], x010 = p[dx], x110 = p[dx + 1];
-          const float x001 = p[dxy], x101 = p[dxy + 1], x011 = p[dxy + dx], x111 = p[dxy + dx + 1];
-          const float c00 = fmaf(fx, x100 - x000, x000), c10 = fmaf(fx, x110 - x010, x010);
-          const float c01 = fmaf(fx, x101 - x001, x001), c11 = fmaf(fx, x111 - x011, x011);
-          const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
-          acc = fmaf(s_tp[c], fmaf(fz, c1 - c0, c0), acc);
-          rx += mg.qc[0];
-          ry += mg.qc[1];
-          rz += mg.qc[2];
-        }
-        sT[i] = acc;
+    __syncthreads();
+    const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
+    const int ntp = 2 * ps.cmax + 1;
+    // lattice points of all members: T(U, V) = sum_c tp(c) trilerp(X, x(U, V, c))
+    for (int i = threadIdx.x; i < s_nt; i += kThreads) {
+      int k = 0;
+      while (k + 1 < G.nm && i >= sm[k + 1].t0) ++k;
+      const FwdMember& f = sm[k];
+      const int li = i - f.t0;
+      const float U = (float)(li % f.LU), V = (float)(li / f.LU);
+      float rx = f.of[0] + U * f.qa[0] + V * f.qb[0];
+      float ry = f.of[1] + U * f.qa[1] + V * f.qb[1];
+      float rz = f.of[2] + U * f.qa[2] + V * f.qb[2];
+      const float qcx = f.qc[0], qcy = f.qc[1], qcz = f.qc[2];
+      const int obx = f.ob[0], oby = f.ob[1], obz = f.ob[2];
+      float acc = 0.0f;
+      for (int c = 0; c < ntp; ++c) {
+        float flx, fly, flz;
+        const int ix = mfloor(rx, flx) + obx;
+        const int iy = mfloor(ry, fly) + oby;
+        const int iz = mfloor(rz, flz) + obz;
+        const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
+        const float* p = sX + iz * dxy + iy * dx + ix;
+        const float x000 = p[0], x100 = p[1], x010 = p[dx], x110 = p[dx + 1];
+        const float x001 = p[dxy], x101 = p[dxy + 1], x011 = p[dxy + dx], x111 = p[dxy + dx + 1];
+        const float c00 = fmaf(fx, x100 - x000, x000), c10 = fmaf(fx, x110 - x010, x010);
+        const float c01 = fmaf(fx, x101 - x001, x001), c11 = fmaf(fx, x111 - x011, x011);
+        const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
+        acc = fmaf(s_tp[c], fmaf(fz, c1 - c0, c0), acc);
+        rx += qcx;
+        ry += qcy;
+        rz += qcz;
       }
-      __syncthreads();
-      if (threadIdx.x < m.tu * m.tv) {
-        const int du = threadIdx.x % m.tu, dv = threadIdx.x / m.tu;
-        const int u = m.u0 + du, v = m.v0 + dv;
-        const int w2 = 2 * mg.ru + 1;
-        float s = 0.0f;
-        for (int b = 0; b <= 2 * mg.rv; ++b) {
-          const float* row = sT + (mg.nv * dv + b) * LU + mg.nu * du;
-          for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
+      sT[i] = acc;
+    }
+    __syncthreads();
+    // pixels of all members: yhat = sum_ab ip(a,b) T(nu u + a, nv v + b) / kappa
+    const int w2 = 2 * ps.ru + 1;
+    for (int i = threadIdx.x; i < s_np; i += kThreads) {
+      int k = 0;
+      while (k + 1 < G.nm && i >= sm[k + 1].p0) ++k;
+      const FwdMember& f = sm[k];
+      const int li = i - f.p0;
+      const int du = li % f.tu, dv = li / f.tu;
+      const int u = f.u0 + du, v = f.v0 + dv;
+      float s = 0.0f;
+      for (int b = 0; b <= 2 * ps.rv; ++b) {
+        const float* row = sT + f.t0 + (ps.nv * dv + b) * f.LU + ps.nu * du;
+        for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
+      }
+      const PatchDev& pt = a.P[f.patch];
+      const int64_t j = pt.pix0 + ((int64_t)f.z * pt.sy + v) * pt.sx + u;
+      const float y = a.ys[pt.y0off + (int64_t)f.z * pt.HW + (int64_t)v * pt.W + u];
+      if (MODE == 1) {
+        out[j] = s;
+        if (s >= a.prm.tau_obs) {
+          acc_s[0] += 1.0;
+          acc_s[2] += (double)pt.S;
         }
-        const int64_t j = pt.pix0 + ((int64_t)m.z * pt.sy + v) * pt.sx + u;
-        const float y = a.ys[pt.y0off + (int64_t)m.z * pt.HW + (int64_t)v * pt.W + u];
-        if (MODE == 1) {
-          out[j] = s;
-          if (s >= a.prm.tau_obs) {
-            acc_s[0] += 1.0;
-            acc_s[2] += (double)pt.S;
-          }
-          if (s >= a.prm.tau_live) {
-            acc_s[1] += 1.0;
-            acc_m[0] = fmaxf(acc_m[0], y);
-            acc_m[1] = fmaxf(acc_m[1], -y);
-          }
-        } else {
-          const float k = kap[j];
-          float ev = 0.0f;
-          if (k >= a.prm.tau_obs) {
-            ev = y - s / k;
-            if (k >= a.prm.tau_live) {
-              const double pp = pprev[j];
-              acc_s[0] += pp * (double)ev * (double)ev;
-              acc_s[1] += pp;
-              acc_s[2] += 1.0;
-              acc_m[0] = fmaxf(acc_m[0], ev);
-              acc_m[1] = fmaxf(acc_m[1], -ev);
-            }
-          }
-          out[j] = ev;
+        if (s >= a.prm.tau_live) {
+          acc_s[1] += 1.0;
+          acc_m[0] = fmaxf(acc_m[0], y);
+          acc_m[1] = fmaxf(acc_m[1], -y);
         }
+      } else {
+        const float kk = kap[j];
+        float ev = 0.0f;
+        if (kk >= a.prm.tau_obs) {
+          ev = y - s / kk;
+          if (kk >= a.prm.tau_live) {
+            const double pp = pprev[j];
+            acc_s[0] += pp * (double)ev * (double)ev;
+            acc_s[1] += pp;
+            acc_s[2] += 1.0;
+            acc_m[0] = fmaxf(acc_m[0], ev);
+            acc_m[1] = fmaxf(acc_m[1], -ev);
+          }
+        }
+        out[j] = ev;
       }
     }
   }
@@ -444,13 +494,21 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
     const double iA = scA > 0.0f ? 1.0 / scA : 0.0, iC = scC > 0.0f ? 1.0 / scC : 0.0;
     const float fA = (float)iA, fC = (float)iC;
     const int hx = (dx + 1) >> 1;
+    // flat pair index i = (zz * dy + yy) * hx + px over all threads, advanced by kThreads
+    // without per-element division
+    const int qs = kThreads / hx, rs = kThreads - qs * hx;
+    int px = threadIdx.x % hx, yy = threadIdx.x / hx, zz = 0;
+    while (yy >= dy) { yy -= dy; ++zz; }
     for (int i = threadIdx.x; i < hx * dy * dz; i += kThreads) {
-      const int px = i % hx, rest = i / hx;
-      const int yy = rest % dy, zz = rest / dy;
-      const int gy = G.lo[1] + yy, gz = G.lo[2] + zz, gx = G.lo[0] + 2 * px;
+      const int pl = px, yl = yy, zl = zz;
+      px += rs;
+      yy += qs;
+      if (px >= hx) { px -= hx; ++yy; }
+      while (yy >= dy) { yy -= dy; ++zz; }
+      const int gy = G.lo[1] + yl, gz = G.lo[2] + zl, gx = G.lo[0] + 2 * pl;
       if (gy < 0 || gy >= n.y || gz < 0 || gz >= n.z || gx < 0 || gx >= a.nxp) continue;
-      const int k = (zz * dy + yy) * dx + 2 * px;
-      const bool two = 2 * px + 1 < dx;  // odd pitch: the last pair has one tile cell
+      const int k = (zl * dy + yl) * dx + 2 * pl;
+      const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
       const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
       int al0 = 0, al1 = 0, cl0 = 0, cl1 = 0;
       if (HILO) {

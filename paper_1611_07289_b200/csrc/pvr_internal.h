@@ -92,7 +92,9 @@ constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics 
 constexpr int kBpTileBytes = 96 * 1024;   // backprojection (iterations): 8 B/voxel tile budget
 constexpr int kInitTileBytes = 96 * 1024; // init backprojection: 16 B/voxel hi/lo tile budget
 constexpr int kRBytes = 12 * 1024;         // backprojection: per-pixel (rA, rC) buffer budget
-constexpr int kFwdTileBytes = 56 * 1024;  // forward: 4 B/voxel X tile budget (3 CTAs/SM)
+constexpr int kFwdTileBytes = 48 * 1024;  // forward: 4 B/voxel X tile budget
+constexpr int kFwdTBytes = 12 * 1024;     // forward: lattice values of a group's members
+constexpr int kMaxGroupMembers = 16;      // members per group (lattice.cu kMaxMembers)
 
 // ---- launchers; all asynchronous on `st` ----
 // lattice.cu
