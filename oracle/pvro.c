@@ -47,6 +47,7 @@ struct pvro_ctx {
   int state;         /* 0 created, 1 stacks, 2 patched, 3 ready */
   /* parameters */
   double delta, tau_patch, c0, tau_live, tau_C, tau_obs, clamp, psf_mode, s2floor, nsigma;
+  double lazy;       /* test-only: set_transforms skips the coverage pass (forward_range use) */
   /* iteration state */
   double* X;         /* [V] */
   double *p, *e, *kappa, *yhat;  /* [P] */
@@ -273,6 +274,7 @@ int pvro_set_param(pvro_ctx* x, int key, double v) {
     case PVRO_PSF_MODE: x->psf_mode = v; break;
     case PVRO_SIGMA2_FLOOR: x->s2floor = v; break;
     case PVRO_PSF_NSIGMA: x->nsigma = v; break;
+    case PVRO_LAZY: x->lazy = v; break;
     default: return -1;
   }
   return 0;
@@ -447,6 +449,7 @@ int pvro_set_transforms(pvro_ctx* x, const double* T, int64_t n) {
   if (n != x->M) return -2;
   memcpy(x->T, T, 12 * n * sizeof(double));
   x->state = 3;
+  if (x->lazy != 0.0) return 0; /* test-only: no coverage / EM reset (forward_range only) */
   /* coverage kappa (step 2) is geometry only: one forward pass on any volume */
   pvro_forward(x, x->X, x->yhat, x->kappa);
   /* EM reset: p_prev = 1, t = 0; live-y range for sigma2_min and the clamp (Q19) */
@@ -488,9 +491,15 @@ int pvro_get_volume(const pvro_ctx* x, double* X) {
  * observed iff kappa_j >= tau_obs; yhat_j = sum_k W_jk X_k,
  * W_jk = kappa_j^-1 sum_q psi_q t_k(x_jq) (each observed row sums to 1).      */
 int pvro_forward(const pvro_ctx* x, const double* X, double* yhat, double* kappa) {
-  if (x->state < 2) return -1;
+  return pvro_forward_range(x, X, 0, x->M, yhat, kappa);
+}
+
+/* Forward of patches [first, first+count) only (yhat, kappa indexed by global pixel). */
+int pvro_forward_range(const pvro_ctx* x, const double* X, int64_t first, int64_t count,
+                       double* yhat, double* kappa) {
+  if (x->state < 2 || first < 0 || first + count > x->M) return -1;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t s = 0; s < x->M; ++s) {
+  for (int64_t s = first; s < first + count; ++s) {
     const int32_t* pt = &x->patch[7 * s];
     const ostack* st = &x->st[pt[0]];
     const double* T = &x->T[12 * s];

@@ -50,6 +50,7 @@ enum {
   PVRO_PSF_MODE = 7,     /* 0: PVR PSF; 1: delta PSF (S = 1, delta_q = 0), test only */
   PVRO_SIGMA2_FLOOR = 9, /* sigma2_min = floor * (ymax - ymin)^2 (1e-6)              */
   PVRO_PSF_NSIGMA = 10,  /* through-plane truncation in sigma_w (3)                  */
+  PVRO_LAZY = 12,        /* test-only: set_transforms skips coverage (forward_range)  */
 };
 
 /* ---- scalar building blocks (pinned individually by tests/test_oracle_*.py) ---- */
@@ -96,6 +97,8 @@ int pvro_set_volume(pvro_ctx*, const double* X);
 int pvro_get_volume(const pvro_ctx*, double* X);
 /* forward operator on an arbitrary volume: yhat[j] (0 if unobserved) and kappa[j] */
 int pvro_forward(const pvro_ctx*, const double* X, double* yhat, double* kappa);
+int pvro_forward_range(const pvro_ctx*, const double* X, int64_t first, int64_t count,
+                       double* yhat, double* kappa);
 /* adjoint operator: out[k] = sum_j W_jk r[j] over observed pixels of patches
    [first, first + count) (out is accumulated into, caller zeroes it) */
 int pvro_adjoint(const pvro_ctx*, const double* r, int64_t first, int64_t count, double* out);

@@ -14,7 +14,7 @@ _SRC = os.path.join(_HERE, "pvro.c")
 
 PARAM = {
     "delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
-    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10,
+    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12,
 }
 
 
@@ -68,6 +68,7 @@ def lib():
         L.pvro_set_volume.argtypes = [vp, vp]
         L.pvro_get_volume.argtypes = [vp, vp]
         L.pvro_forward.argtypes = [vp, vp, vp, vp]
+        L.pvro_forward_range.argtypes = [vp, vp, i64, i64, vp, vp]
         L.pvro_adjoint.argtypes = [vp, vp, i64, i64, vp]
         L.pvro_init_volume.argtypes = [vp]
         L.pvro_sr_iterate.argtypes = [vp, C.c_int, d, d]
@@ -210,6 +211,14 @@ class Oracle:
         yhat = np.zeros(self.P)
         kap = np.zeros(self.P)
         _chk(lib().pvro_forward(self.h, _p(X), _p(yhat), _p(kap)), "forward")
+        return yhat, kap
+
+    def forward_range(self, X, first, count):
+        """yhat, kappa of patches [first, first+count) (global pixel indexing, zeros elsewhere)."""
+        X = np.ascontiguousarray(X, np.float64).reshape(-1)
+        yhat = np.zeros(self.P)
+        kap = np.zeros(self.P)
+        _chk(lib().pvro_forward_range(self.h, _p(X), first, count, _p(yhat), _p(kap)), "forward_range")
         return yhat, kap
 
     def adjoint(self, r, first=0, count=None):

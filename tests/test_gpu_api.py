@@ -1,0 +1,129 @@
+"""C-ABI behaviour on the GPU: state machine, argument errors, empty problems, host vs device
+pointers, caller streams, stats (include/pvr.h conventions)."""
+import numpy as np
+import pytest
+
+import synth
+from helpers import make_gpu
+from paper_1611_07289_b200 import Context, load_problem, pvr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return synth.make_problem("c1")
+
+
+def status_of(fn, *a):
+    try:
+        fn(*a)
+    except pvr.PvrError as e:
+        return e.status
+    return pvr.PVR_OK
+
+
+def test_state_machine_and_argument_errors(c1):
+    ctx = Context(c1["dims"], c1["spacing"], c1["origin"])
+    st = c1["stacks"][0]
+    assert status_of(ctx.extract_patches, 16, 8) == pvr.PVR_ERR_STATE        # no stack yet
+    assert status_of(ctx.set_transforms, c1["T"]) == pvr.PVR_ERR_STATE
+    assert status_of(ctx.sr_iterate, 1, 1.0, 0.0) == pvr.PVR_ERR_STATE
+    assert status_of(ctx.init_volume) == pvr.PVR_ERR_STATE
+    assert status_of(ctx.add_stack, st["slices"], st["G"], -1.0) == pvr.PVR_ERR_ARG  # thickness
+    Gbad = np.zeros((3, 4))
+    assert status_of(ctx.add_stack, st["slices"], Gbad, 2.0) == pvr.PVR_ERR_ARG      # axes
+    assert status_of(ctx.set_param, "nonexistent" if False else 99, 1.0) == pvr.PVR_ERR_ARG
+    for s in c1["stacks"]:
+        ctx.add_stack(s["slices"], s["G"], s["thickness"])
+    assert status_of(ctx.extract_patches, 64, 8) == pvr.PVR_ERR_ARG          # size > W
+    assert status_of(ctx.extract_patches, 16, 17) == pvr.PVR_ERR_ARG         # stride > size
+    assert status_of(ctx.extract_patches, 16, 8, 9, 1) == pvr.PVR_ERR_ARG    # depth > K
+    assert ctx.extract_patches(16, 8) == 216
+    assert status_of(ctx.add_stack, st["slices"], st["G"], 2.0) == pvr.PVR_ERR_STATE
+    assert status_of(ctx.set_param, "psf_mode", 1) == pvr.PVR_ERR_STATE
+    assert status_of(ctx.set_transforms, c1["T"][:10]) == pvr.PVR_ERR_ARG    # n != M
+    ctx.set_transforms(c1["T"])
+    assert status_of(ctx.sr_iterate, 1, -1.0, 0.0) == pvr.PVR_ERR_ARG
+    assert status_of(ctx.sr_iterate, -1, 1.0, 0.0) == pvr.PVR_ERR_ARG
+    ctx.sr_iterate(1, 1.0, 0.1)                                               # alpha*lambda > 3/44
+    assert "maximum principle" in pvr.pvr_last_error(ctx.h)
+    ctx.close()
+    with pytest.raises(pvr.PvrError) as ei:
+        Context((0, 8, 8), 1.0, (0, 0, 0))
+    assert ei.value.status == pvr.PVR_ERR_ARG
+
+
+def test_nothing_to_reconstruct(c1):
+    """Stacks that miss the volume entirely: PVR_ERR_EMPTY (S:336 'nothing to reconstruct')."""
+    ctx = Context(c1["dims"], c1["spacing"], c1["origin"])
+    for s in c1["stacks"]:
+        G = s["G"].copy()
+        G[:, 3] += 1000.0
+        ctx.add_stack(s["slices"], G, s["thickness"])
+    ctx.extract_patches(16, 8)
+    assert status_of(ctx.set_transforms, c1["T"]) == pvr.PVR_ERR_EMPTY
+    ctx.close()
+
+
+def test_device_pointers_and_caller_stream_match_host(c1):
+    import torch
+    ref = make_gpu(c1)
+    ref.init_volume()
+    ref.sr_iterate(2, c1["alpha"], c1["lam"])
+    X_ref = ref.volume()
+    p_ref, _, w_ref = ref.weights()
+    ref.close()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ctx = Context(c1["dims"], c1["spacing"], c1["origin"], 0, stream.cuda_stream)
+        for s in c1["stacks"]:
+            ctx.add_stack(torch.from_numpy(s["slices"]).cuda(), s["G"], s["thickness"])
+        ctx.extract_patches(16, 8)
+        ctx.set_transforms(torch.from_numpy(c1["T"].reshape(-1, 12)).cuda())
+        ctx.init_volume()
+        ctx.sr_iterate(2, c1["alpha"], c1["lam"])
+        Xd = torch.empty(c1["dims"][::-1], dtype=torch.float32, device="cuda")
+        ctx.volume(Xd)
+        pd = torch.empty(ctx.nloc_pix, dtype=torch.float32, device="cuda")
+        wd = torch.empty(ctx.nloc, dtype=torch.float32, device="cuda")
+        pvr.pvr_get_weights(ctx.h, pd, wd, None)
+        stream.synchronize()
+    ctx.close()
+    # same inputs through host vs device pointers; the backprojection's cross-group flush is
+    # a float reduction in arrival order, so equality is to fp32 rounding, not bitwise
+    assert np.abs(Xd.cpu().numpy() - X_ref).max() <= 1e-3
+    assert np.abs(pd.cpu().numpy() - p_ref).max() <= 1e-4
+    assert np.abs(wd.cpu().numpy() - w_ref).max() <= 1e-4
+
+
+def test_forward_is_deterministic_and_stats_count_work(c1):
+    a, b = make_gpu(c1, {"profile": 1}), make_gpu(c1)
+    X = np.random.default_rng(3).uniform(0, 1000, size=c1["dims"][::-1]).astype(np.float32)
+    for ctx in (a, b):
+        ctx.set_volume(X)
+        ctx.sr_iterate(1, c1["alpha"], c1["lam"])
+    ea, _, _, _ = a.taps()
+    eb, _, _, _ = b.taps()
+    assert np.array_equal(ea, eb)                     # forward: fixed summation order
+    s = a.stats()
+    assert s["iterations"] == 1 and s["kernel_launches"] == 6
+    assert s["psf_samples"] > 0 and s["ms_forward"] > 0 and s["ms_backproject"] > 0
+    assert s["fwd_groups"] > 0 and s["bp_groups"] > 0
+    a.close()
+    b.close()
+
+
+def test_set_volume_roundtrip_and_em_state(c1):
+    ctx = make_gpu(c1)
+    rng = np.random.default_rng(1)
+    X = rng.uniform(0, 1000, size=c1["dims"][::-1]).astype(np.float32)
+    ctx.set_volume(X)
+    assert np.array_equal(ctx.volume(), X)
+    em = ctx.em_state()
+    assert em["t"] == 0 and em["hi"] > em["lo"]
+    ctx.sr_iterate(3, 1.0, 0.02)
+    assert ctx.em_state()["t"] == 3
+    ctx.set_transforms(c1["T"])                       # resets the EM state
+    assert ctx.em_state()["t"] == 0
+    ctx.close()
