@@ -536,6 +536,32 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     }
   }
   out.fit_frac = ngrp ? (double)fit / ngrp : 1.0;
+  // Order the CTAs' work along a Morton curve of the groups' bbox centres (16-voxel cells), so
+  // that overlapping footprints of all stacks are processed close in time: the forward's X
+  // reads and the backprojection's (A, C) flushes then hit L2 instead of re-streaming HBM.
+  std::vector<std::pair<uint64_t, int32_t>> order(out.grp.size());
+  for (size_t g = 0; g < out.grp.size(); ++g) {
+    uint64_t key = 0;
+    uint32_t cc[3];
+    for (int d = 0; d < 3; ++d)
+      cc[d] = (uint32_t)std::max(0, (out.grp[g].lo[d] + out.grp[g].dim[d] / 2 + 4096) >> 4) & 0x3FF;
+    for (int b = 9; b >= 0; --b)
+      for (int d = 2; d >= 0; --d) key = (key << 1) | ((cc[d] >> b) & 1u);
+    order[g] = {key, (int32_t)g};
+  }
+  std::stable_sort(order.begin(), order.end());
+  std::vector<GroupDev> grp(out.grp.size());
+  std::vector<MemberDev> mem;
+  mem.reserve(out.mem.size());
+  for (size_t k = 0; k < order.size(); ++k) {
+    GroupDev g = out.grp[order[k].second];
+    const int m0 = g.m0;
+    g.m0 = (int32_t)mem.size();
+    for (int i = 0; i < g.nm; ++i) mem.push_back(out.mem[m0 + i]);
+    grp[k] = g;
+  }
+  out.grp.swap(grp);
+  out.mem.swap(mem);
 }
 
 pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
