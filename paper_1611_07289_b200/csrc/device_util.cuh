@@ -69,6 +69,60 @@ __device__ __forceinline__ int mfloor(float x, float& fl) {
   return __float_as_int(t) - 0x4B400000;
 }
 
+// Packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: two lanes of fp32 math per issue slot).
+// A scalar operand is broadcast by the hardware (R.F32 operand), so pk(s, s) costs nothing.
+struct f2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f2 a) {
+  float l;
+  asm("{.reg .f32 t; mov.b64 {%0, t}, %1;}" : "=f"(l) : "l"(a.v));
+  return l;
+}
+__device__ __forceinline__ float hi2(f2 a) {
+  float h;
+  asm("{.reg .f32 t; mov.b64 {t, %0}, %1;}" : "=f"(h) : "l"(a.v));
+  return h;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 add2_rd(f2 a, f2 b) {
+  f2 r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ f2 mul2s(float s, f2 b) { return mul2(pk(s, s), b); }
+__device__ __forceinline__ f2 fma2s(float s, f2 b, f2 c) { return fma2(pk(s, s), b, c); }
+
+// Shared-memory integer reduction at a 32-bit shared address (+ immediate byte offset).
+template <int OFF>
+__device__ __forceinline__ void sred(unsigned addr, int v) {
+  asm volatile("red.shared.add.s32 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
+}
+
 __device__ __forceinline__ int floor_div(int a, int b) {  // b > 0
   int q = a / b;
   return (a % b != 0 && a < 0) ? q - 1 : q;

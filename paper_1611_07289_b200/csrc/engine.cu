@@ -641,7 +641,7 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
     (fwd ? c->st.fwd_groups : c->st.bp_groups) = pl.ngroups;
     (fwd ? c->st.fwd_members : c->st.bp_members) = (int64_t)pb.mem.size();
     (fwd ? c->st.fwd_smem : c->st.bp_smem) =
-        fwd ? (int64_t)(pl.t_floats + pl.tile_words) * 4 : (int64_t)pl.tile_words * 8 + pl.r_bytes;
+        fwd ? (int64_t)(pl.t_floats + pl.tile_words) * 4 : (int64_t)kBpTileBytes + pl.r_bytes;
   }
   return PVR_OK;
 }

@@ -316,46 +316,161 @@ __device__ __forceinline__ void tile_add(const Tile& T, int idx, float a, float 
   }
 }
 
-// Splat one lattice line (fixed U, V; c over [c0, c1]) into the tile: 8 trilinear corners per
-// sample, each (A, C) term split into exact hi/lo int32 words. Uniform control flow: every
-// lane of a warp issues the same atomics (a register window along c was tried: lanes cross
-// voxel planes at different steps, so the warp serialised the flush branches).
-template <bool HILO>
-__device__ __forceinline__ void splat_line(const Tile& T, const float* s_tp, float rx, float ry,
-                                           float rz, float qcx, float qcy, float qcz, int obx,
-                                           int oby, int obz, int c0, int c1, int cmax, float LA,
-                                           float LC) {
-  rx += c0 * qcx;
-  ry += c0 * qcy;
-  rz += c0 * qcz;
-  const int dx = T.dx, dxy = T.dx * T.dy;
-  for (int c = c0; c <= c1; ++c) {
-    const float t = s_tp[c + cmax];
-    float flx, fly, flz;
-    const int ix = mfloor(rx, flx) + obx;
-    const int iy = mfloor(ry, fly) + oby;
-    const int iz = mfloor(rz, flz) + obz;
-    const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
+// Per-member constants of the backprojection, in the member's window frame: axis 0 (m) is
+// the dominant component of the sample step dir * Qc (so plane floors never decrease along a
+// line), axes 1, 2 (p, q) the transverse ones. Built by warp 0 once per group.
+struct BpMember {
+  float r[3];              // frame position of lattice point (Ulo, Vlo, first sample) - o
+  float du[3], dv[3], dc[3];  // frame steps per U, per V, per sample (dc[0] >= 0)
+  int o[3];                // integer origin in the tile (frame)
+  int s[3];                // tile strides (frame)
+  int ti0, dti, ns;        // tp index of the first sample, its step (+-1), samples per line
+  int Ulo, Vlo, nU;
+  float inv_nU, inv_rw;
+  int lbeg, lend;          // flattened line range of the member in the group
+  int pbeg, pend;          // flattened pixel range (== its R range)
+  int plu, plv, phu, phv, rw;
+  int64_t pixz, yz;        // first pixel of slice z in the local arrays / in the stacks
+  int sx, W;
+  float ws;                // patch weight w (1 in the init pass)
+};
+
+__device__ __forceinline__ float pick3(const float (&v)[3], int ax) {
+  return ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]);
+}
+__device__ __forceinline__ int pick3i(const int (&v)[3], int ax) {
+  return ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]);
+}
+
+// Splat one lattice line into the tile with exact hi/lo words (init pass): 8 trilinear
+// corners per sample, each (A, C) term split into exact hi/lo int32 words.
+__device__ __forceinline__ void splat_line_hilo(const Tile& T, const float* s_tp, const BpMember& M,
+                                                float rm, float rp, float rq, float LA, float LC) {
+  const int s0 = M.s[0], s1 = M.s[1], s2 = M.s[2];
+  int ti = M.ti0;
+  for (int k = 0; k < M.ns; ++k) {
+    const float t = s_tp[ti];
+    float f0, f1, f2_;
+    const int i0 = mfloor(rm, f0) + M.o[0];
+    const int i1 = mfloor(rp, f1) + M.o[1];
+    const int i2 = mfloor(rq, f2_) + M.o[2];
+    const float fm = rm - f0, fp = rp - f1, fq = rq - f2_;
     const float vA = LA * t, vC = LC * t;
-    const int k000 = iz * dxy + iy * dx + ix;
-    const float wy0z0 = (1.0f - fy) * (1.0f - fz), wy1z0 = fy * (1.0f - fz);
-    const float wy0z1 = (1.0f - fy) * fz, wy1z1 = fy * fz;
-    const float a0 = vA * (1.0f - fx), a1 = vA * fx, g0 = vC * (1.0f - fx), g1 = vC * fx;
-    tile_add<HILO>(T, k000, a0, g0, wy0z0);
-    tile_add<HILO>(T, k000 + 1, a1, g1, wy0z0);
-    tile_add<HILO>(T, k000 + dx, a0, g0, wy1z0);
-    tile_add<HILO>(T, k000 + dx + 1, a1, g1, wy1z0);
-    tile_add<HILO>(T, k000 + dxy, a0, g0, wy0z1);
-    tile_add<HILO>(T, k000 + dxy + 1, a1, g1, wy0z1);
-    tile_add<HILO>(T, k000 + dxy + dx, a0, g0, wy1z1);
-    tile_add<HILO>(T, k000 + dxy + dx + 1, a1, g1, wy1z1);
-    rx += qcx;
-    ry += qcy;
-    rz += qcz;
+    const int k0 = i0 * s0 + i1 * s1 + i2 * s2;
+    const float w00 = (1.0f - fp) * (1.0f - fq), w10 = fp * (1.0f - fq);
+    const float w01 = (1.0f - fp) * fq, w11 = fp * fq;
+    const float a0 = vA * (1.0f - fm), a1 = vA * fm, g0 = vC * (1.0f - fm), g1 = vC * fm;
+    tile_add<true>(T, k0, a0, g0, w00);
+    tile_add<true>(T, k0 + s0, a1, g1, w00);
+    tile_add<true>(T, k0 + s1, a0, g0, w10);
+    tile_add<true>(T, k0 + s0 + s1, a1, g1, w10);
+    tile_add<true>(T, k0 + s2, a0, g0, w01);
+    tile_add<true>(T, k0 + s0 + s2, a1, g1, w01);
+    tile_add<true>(T, k0 + s1 + s2, a0, g0, w11);
+    tile_add<true>(T, k0 + s0 + s1 + s2, a1, g1, w11);
+    rm += M.dc[0];
+    rp += M.dc[1];
+    rq += M.dc[2];
+    ti += M.dti;
   }
 }
 
-// Dynamic shared memory: (HILO ? 4 : 2) x tile_words int32 (A, C [, A_lo, C_lo]), then R.
+constexpr int kCOff = kBpTileBytes / 2;  // byte offset of the C plane in the iteration tile
+
+__device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, const f2 (&P)[4], f2 mag) {
+  const f2 t0 = add2(P[0], mag), t1 = add2(P[1], mag), t2 = add2(P[2], mag), t3 = add2(P[3], mag);
+  sred<0>(a, __float_as_int(lo2(t0)) - kMagicBits);
+  sred<kCOff>(a, __float_as_int(hi2(t0)) - kMagicBits);
+  sred<0>(a + sp4, __float_as_int(lo2(t1)) - kMagicBits);
+  sred<kCOff>(a + sp4, __float_as_int(hi2(t1)) - kMagicBits);
+  sred<0>(a + sq4, __float_as_int(lo2(t2)) - kMagicBits);
+  sred<kCOff>(a + sq4, __float_as_int(hi2(t2)) - kMagicBits);
+  sred<0>(a + sp4 + sq4, __float_as_int(lo2(t3)) - kMagicBits);
+  sred<kCOff>(a + sp4 + sq4, __float_as_int(hi2(t3)) - kMagicBits);
+}
+
+// Splat one lattice line with a two-plane register window along the frame's axis 0. A sample
+// at plane floor m adds (1 - f_m) of its 4 in-plane corner terms to plane m (window slot P0)
+// and f_m to plane m + 1 (slot P1). Every step first flushes P0 to the tile (one int32
+// rounding per corner per step instead of one per term and plane), then shifts: a lane whose
+// floor advanced moves P1 into P0; a lane whose floor stayed keeps P1 (its P0 restarts
+// empty); a lane whose transverse floors changed also flushes P1 and restarts. The flush is
+// uniform across the warp (all lanes issue the same 8 shared reductions); only the rarer
+// transverse restart branches. A and C travel as packed fp32 pairs (FFMA2 / FMUL2). Window
+// sums before rounding: < 2 terms of < 2^20 units each (group scale, k_lattice_bp).
+// Tile: A words at shared address tA, C words at tA + kCOff.
+__device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const BpMember& M, float rm,
+                                               float rp, float rq, float LA, float LC) {
+  f2 rpq = pk(rp, rq);
+  const float qm = M.dc[0];
+  const f2 qpq = pk(M.dc[1], M.dc[2]);
+  const f2 mag = pk(kMagic, kMagic);
+  const f2 L = pk(LA, LC);
+  const f2 one0 = pk(1.0f, 0.0f), m1p1 = pk(-1.0f, 1.0f);
+  const int sm4 = 4 * M.s[0], sp4 = 4 * M.s[1], sq4 = 4 * M.s[2];
+  const unsigned org = tA + (unsigned)(M.o[0] * sm4 + M.o[1] * sp4 + M.o[2] * sq4);
+  unsigned ta = s_tp + 4u * M.ti0;
+  const int dta = 4 * M.dti;
+  const int ns = M.ns;
+  float fl;
+  int wm = mfloor(rm, fl);
+  int wp = __float_as_int(lo2(add2_rd(rpq, mag))) - kMagicBits;
+  int wq = __float_as_int(hi2(add2_rd(rpq, mag))) - kMagicBits;
+  f2 P0[4], P1[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) P0[j] = P1[j] = pk(0.0f, 0.0f);
+  for (int k = 0; k < ns; ++k) {
+    const float tm = __fadd_rd(rm, kMagic);
+    const f2 tpq = add2_rd(rpq, mag);
+    const int im = __float_as_int(tm) - kMagicBits;
+    const int ip = __float_as_int(lo2(tpq)) - kMagicBits;
+    const int iq = __float_as_int(hi2(tpq)) - kMagicBits;
+    const bool same = (ip == wp) & (iq == wq);
+    const bool keep = same & (im == wm);
+    const bool adv = same & (im == wm + 1);
+    const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
+    flush4(a0, sp4, sq4, P0, mag);                   // plane wm
+    if (!keep && !adv) flush4(a0 + sm4, sp4, sq4, P1, mag);  // restart: plane wm + 1 too
+    // shift: keep -> (0, P1); advance -> (P1, 0); restart (or a jump) -> (0, 0)
+    const float m0 = adv ? 1.0f : 0.0f, m1 = keep ? 1.0f : 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      P0[j] = mul2s(m0, P1[j]);
+      P1[j] = mul2s(m1, P1[j]);
+    }
+    wm = im;
+    wp = ip;
+    wq = iq;
+    // this sample's terms
+    float t;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(ta));
+    const float flm = __fsub_rn(tm, kMagic);
+    const f2 fpq = sub2(rpq, sub2(tpq, mag));
+    const float fm = rm - flm, fp = lo2(fpq), fq = hi2(fpq);
+    const f2 V = mul2s(t, L);                       // (vA, vC)
+    const f2 WP = fma2s(fp, m1p1, one0);            // (1 - fp, fp)
+    const f2 w01 = mul2s(1.0f - fq, WP), w23 = mul2s(fq, WP);
+    const f2 VL = mul2s(1.0f - fm, V), VH = mul2s(fm, V);
+    P0[0] = fma2s(lo2(w01), VL, P0[0]);
+    P0[1] = fma2s(hi2(w01), VL, P0[1]);
+    P0[2] = fma2s(lo2(w23), VL, P0[2]);
+    P0[3] = fma2s(hi2(w23), VL, P0[3]);
+    P1[0] = fma2s(lo2(w01), VH, P1[0]);
+    P1[1] = fma2s(hi2(w01), VH, P1[1]);
+    P1[2] = fma2s(lo2(w23), VH, P1[2]);
+    P1[3] = fma2s(hi2(w23), VH, P1[3]);
+    rm += qm;
+    rpq = add2(rpq, qpq);
+    ta += dta;
+  }
+  const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
+  flush4(a0, sp4, sq4, P0, mag);
+  flush4(a0 + sm4, sp4, sq4, P1, mag);
+}
+
+// Dynamic shared memory: HILO (init pass): 4 x tile_words int32 (A, C, A_lo, C_lo), then R;
+// iterations: A at 0, C at the fixed byte offset kCOff (an immediate in the splat's shared
+// reductions), R after kBpTileBytes.
 template <bool HILO>
 __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile_words,
                                                          const float* __restrict__ kap,
@@ -366,44 +481,107 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
   extern __shared__ int4 bsm4[];
   int* base = reinterpret_cast<int*>(bsm4);
   constexpr int NW = HILO ? 4 : 2;
-  float2* R = reinterpret_cast<float2*>(base + NW * tile_words);
+  int* cbase = HILO ? base + tile_words : base + kCOff / 4;
+  float2* R = reinterpret_cast<float2*>(HILO ? base + NW * tile_words : base + kBpTileBytes / 4);
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
   __shared__ float s_red[2][32];
   __shared__ float s_scale[2];
+  __shared__ BpMember sbm[kMaxMembers];
+  __shared__ int s_nl, s_np;  // lines / pixels of the group
   const int3 n = a.n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned tA = (unsigned)__cvta_generic_to_shared(base);
+  const unsigned tpA = (unsigned)__cvta_generic_to_shared(s_tp);
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
-    __syncthreads();  // previous group's flush is done with the tile / R / tables
+    __syncthreads();  // previous group's flush is done with the tile / R / tables / sbm
+    // ---- member table (warp 0, one lane per member) with flattened line / pixel ranges
+    if (wid == 0) {
+      int nl = 0, np = 0;
+      BpMember M;
+      if (lane < G.nm) {
+        const MemberDev m = a.mem[G.m0 + lane];
+        const PatchDev& pt = a.P[m.patch];
+        const MemberGeom mg = member_geom(a, pt);
+        const Owned o = owned_range(m, pt, mg);
+        const float aq0 = fabsf(mg.qc[0]), aq1 = fabsf(mg.qc[1]), aq2 = fabsf(mg.qc[2]);
+        const int am = (aq0 >= aq1 && aq0 >= aq2) ? 0 : (aq1 >= aq2 ? 1 : 2);
+        const int ap = am == 0 ? 1 : 0, aq = am == 2 ? 1 : 2;
+        const int dir = pick3(mg.qc, am) >= 0.0f ? 1 : -1;
+        const int cs = dir > 0 ? m.c0 : m.c1;
+        int ob[3];
+        float of[3];
+        lattice_origin(pt, m.z, o.Ulo, o.Vlo, cs, G.lo, ob, of);
+        const int st[3] = {1, dx, dx * dy};
+        const int ax[3] = {am, ap, aq};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          M.r[d] = pick3(of, ax[d]);
+          M.o[d] = pick3i(ob, ax[d]);
+          M.s[d] = pick3i(st, ax[d]);
+          M.du[d] = pick3(mg.qa, ax[d]);
+          M.dv[d] = pick3(mg.qb, ax[d]);
+          M.dc[d] = (float)dir * pick3(mg.qc, ax[d]);
+        }
+        M.ti0 = cs + mg.cmax;
+        M.dti = dir;
+        M.ns = m.c1 - m.c0 + 1;
+        M.Ulo = o.Ulo;
+        M.Vlo = o.Vlo;
+        M.nU = o.Uhi - o.Ulo;
+        M.inv_nU = 1.0f / (float)M.nU;
+        M.plu = o.plu; M.phu = o.phu; M.plv = o.plv; M.phv = o.phv;
+        M.rw = o.phu - o.plu + 1;
+        M.inv_rw = 1.0f / (float)M.rw;
+        M.pixz = pt.pix0 + (int64_t)m.z * pt.sy * pt.sx;
+        M.yz = pt.y0off + (int64_t)m.z * pt.HW;
+        M.sx = pt.sx;
+        M.W = pt.W;
+        M.ws = init ? 1.0f : w[m.patch];
+        nl = M.nU * (o.Vhi - o.Vlo);
+        np = M.rw * (o.phv - o.plv + 1);
+      }
+      int sl = nl, sp = np;  // inclusive scans over the members
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int tl = __shfl_up_sync(0xffffffffu, sl, d), tp = __shfl_up_sync(0xffffffffu, sp, d);
+        if (lane >= d) { sl += tl; sp += tp; }
+      }
+      if (lane < G.nm) {
+        M.lbeg = sl - nl; M.lend = sl;
+        M.pbeg = sp - np; M.pend = sp;
+        sbm[lane] = M;
+      }
+      if (lane == G.nm - 1) { s_nl = sl; s_np = sp; }
+    }
+    __syncthreads();
     // ---- phase A: per-pixel (rA, rC) of every member into R; group maxima for the scale
     float mA = 0.0f, mC = 0.0f;
-    int roff = 0;
-    for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
-      const MemberDev m = a.mem[mi];
-      const PatchDev& pt = a.P[m.patch];
-      const MemberGeom mg = member_geom(a, pt);
-      const Owned o = owned_range(m, pt, mg);
-      const int rw = o.phu - o.plu + 1, rh = o.phv - o.plv + 1;
-      const float ws = init ? 1.0f : w[m.patch];
-      for (int i = threadIdx.x; i < rw * rh; i += kThreads) {
-        const int u = o.plu + i % rw, v = o.plv + i / rw;
-        const int64_t j = pt.pix0 + ((int64_t)m.z * pt.sy + v) * pt.sx + u;
+    {
+      const int np = s_np;
+      int mi = 0;
+      for (int i = threadIdx.x; i < np; i += kThreads) {
+        while (i >= sbm[mi].pend) ++mi;
+        const BpMember& M = sbm[mi];
+        const int li = i - M.pbeg;
+        const int vv = (int)(((float)li + 0.5f) * M.inv_rw);
+        const int u = M.plu + (li - vv * M.rw), v = M.plv + vv;
+        const int64_t j = M.pixz + (int64_t)v * M.sx + u;
         float rA = 0.0f, rC = 0.0f;
         const float k = kap[j];
-        if (ws != 0.0f && k >= a.prm.tau_obs) {
+        if (M.ws != 0.0f && k >= a.prm.tau_obs) {
           const float pv = init ? 1.0f : p[j];
-          const float val = init ? a.ys[pt.y0off + (int64_t)m.z * pt.HW + (int64_t)v * pt.W + u] : e[j];
-          rC = ws * pv / k;
+          const float val = init ? a.ys[M.yz + (int64_t)v * M.W + u] : e[j];
+          rC = M.ws * pv / k;
           rA = rC * val;
         }
-        R[roff + i] = make_float2(rA, rC);
+        R[i] = make_float2(rA, rC);
         mA = fmaxf(mA, fabsf(rA));
         mC = fmaxf(mC, rC);
       }
-      roff += rw * rh;
     }
     mA = warp_max(mA);
     mC = warp_max(mC);
@@ -411,14 +589,14 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
       s_red[0][wid] = mA;
       s_red[1][wid] = mC;
     }
+    const MemberGeom mg = member_geom(a, a.P[a.mem[G.m0].patch]);  // the group's stack
     {  // PSF tables of the group's stack (all members share it) and the tile reset
-      const MemberGeom mg = member_geom(a, a.P[a.mem[G.m0].patch]);
       const int nip = (2 * mg.ru + 1) * (2 * mg.rv + 1);
       for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[mg.ip0 + i];
       for (int i = threadIdx.x; i < mg.ntp; i += kThreads) s_tp[i] = a.tab[mg.tp0 + i];
       for (int i = threadIdx.x; i < nvox; i += kThreads) {
 #pragma unroll
-        for (int q = 0; q < NW; ++q) base[q * tile_words + i] = 0;
+        for (int q = 0; q < NW; ++q) (q == 1 ? cbase : base + q * tile_words)[i] = 0;
       }
     }
     __syncthreads();
@@ -429,50 +607,46 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         xC = fmaxf(xC, s_red[1][i]);
       }
       const float tpmax = a.psf[a.P[a.mem[G.m0].patch].stack].tpmax;
-      // every splat term |L tp w| <= max|r| tpmax  ->  < 2^20 (HILO) / 2^21 units
-      const float tmax = HILO ? kTermMax : 2.0f * kTermMax;
-      s_scale[0] = xA > 0.0f ? tmax / (xA * tpmax) : 0.0f;
-      s_scale[1] = xC > 0.0f ? tmax / (xC * tpmax) : 0.0f;
+      // every splat term |L tp w| <= max|r| tpmax  ->  < 2^20 units; the register window
+      // sums < 4 such terms per corner before rounding (< 2^22)
+      s_scale[0] = xA > 0.0f ? kTermMax / (xA * tpmax) : 0.0f;
+      s_scale[1] = xC > 0.0f ? kTermMax / (xC * tpmax) : 0.0f;
     }
     __syncthreads();
     const float scA = s_scale[0], scC = s_scale[1];
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
-    const Tile T{base, base + tile_words, HILO ? base + 2 * tile_words : nullptr,
+    const Tile T{base, cbase, HILO ? base + 2 * tile_words : nullptr,
                  HILO ? base + 3 * tile_words : nullptr, dx, dy};
 
-    // ---- phase B: splat every owned lattice line of every member
-    roff = 0;
-    for (int mi = G.m0; mi < G.m0 + G.nm; ++mi) {
-      const MemberDev m = a.mem[mi];
-      const PatchDev& pt = a.P[m.patch];
-      const MemberGeom mg = member_geom(a, pt);
-      const Owned o = owned_range(m, pt, mg);
-      const int rw = o.phu - o.plu + 1, rh = o.phv - o.plv + 1;
-      const int nU = o.Uhi - o.Ulo, nV = o.Vhi - o.Vlo;
+    // ---- phase B: splat every owned lattice line of every member, one flattened range
+    // (one tail per group); consecutive lanes take consecutive U lines of a member
+    {
+      const int nl = s_nl;
       const int w2 = 2 * mg.ru + 1;
-      int ob[3];
-      float of[3];
-      lattice_origin(pt, m.z, o.Ulo, o.Vlo, 0, G.lo, ob, of);
-      // consecutive lanes take consecutive lines: their corners fall in consecutive cells of
-      // one tile row (distinct banks), or rows an odd pitch apart (engine.cu: odd dx, dy)
-      for (int i = threadIdx.x; i < nU * nV; i += kThreads) {
-        const int iu = i % nU, iv = i / nU;
-        const int U = o.Ulo + iu, V = o.Vlo + iv;
+      const float inv_nu = 1.0f / (float)mg.nu, inv_nv = 1.0f / (float)mg.nv;
+      int mi = 0;
+      for (int i = threadIdx.x; i < nl; i += kThreads) {
+        while (i >= sbm[mi].lend) ++mi;
+        const BpMember& M = sbm[mi];
+        const int li = i - M.lbeg;
+        const int iv = (int)(((float)li + 0.5f) * M.inv_nU);
+        const int iu = li - iv * M.nU;
+        const int U = M.Ulo + iu, V = M.Vlo + iv;
         // pixels feeding lattice point U: u = (U - a) / nu with a = U mod nu (and a - nu when
-        // that is within [-ru, ru]); same along V
-        const int ub = floor_div(U, mg.nu), ra = U - ub * mg.nu;
-        const int vb = floor_div(V, mg.nv), rb = V - vb * mg.nv;
+        // that is within [-ru, ru]); same along V. U >= -ru > -nu: the float floor is exact.
+        const int ub = __float2int_rd(((float)U + 0.5f) * inv_nu), ra = U - ub * mg.nu;
+        const int vb = __float2int_rd(((float)V + 0.5f) * inv_nv), rb = V - vb * mg.nv;
         float LA = 0.0f, LC = 0.0f;
 #pragma unroll
         for (int jb = 0; jb < 2; ++jb) {
           const int b = jb ? rb - mg.nv : rb, v = vb + jb;
-          if (b < -mg.rv || b > mg.rv || v < o.plv || v > o.phv) continue;
+          if (b < -mg.rv || b > mg.rv || v < M.plv || v > M.phv) continue;
 #pragma unroll
           for (int ja = 0; ja < 2; ++ja) {
             const int aa = ja ? ra - mg.nu : ra, u = ub + ja;
-            if (aa < -mg.ru || aa > mg.ru || u < o.plu || u > o.phu) continue;
+            if (aa < -mg.ru || aa > mg.ru || u < M.plu || u > M.phu) continue;
             const float wt = s_ip[(b + mg.rv) * w2 + (aa + mg.ru)];
-            const float2 rr = R[roff + (v - o.plv) * rw + (u - o.plu)];
+            const float2 rr = R[M.pbeg + (v - M.plv) * M.rw + (u - M.plu)];
             LA += wt * rr.x;
             LC += wt * rr.y;
           }
@@ -481,13 +655,15 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         LA *= scA;
         LC *= scC;
         const float fU = (float)iu, fV = (float)iv;
-        const float r0x = of[0] + fU * mg.qa[0] + fV * mg.qb[0];
-        const float r0y = of[1] + fU * mg.qa[1] + fV * mg.qb[1];
-        const float r0z = of[2] + fU * mg.qa[2] + fV * mg.qb[2];
-        splat_line<HILO>(T, s_tp, r0x, r0y, r0z, mg.qc[0], mg.qc[1], mg.qc[2], ob[0], ob[1], ob[2], m.c0,
-                         m.c1, mg.cmax, LA, LC);
+        const float rm = M.r[0] + fU * M.du[0] + fV * M.dv[0];
+        const float rp = M.r[1] + fU * M.du[1] + fV * M.dv[1];
+        const float rq = M.r[2] + fU * M.du[2] + fV * M.dv[2];
+        if (HILO) {
+          splat_line_hilo(T, s_tp, M, rm, rp, rq, LA, LC);
+        } else {
+          splat_line_win(tA, tpA, M, rm, rp, rq, LA, LC);
+        }
       }
-      roff += rw * rh;
     }
     __syncthreads();
     // ---- phase C: flush the tile, one red.v4 per in-grid (even, odd) voxel pair along x
@@ -568,7 +744,7 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
   if (init) {  // raw intensities: exact hi/lo words
     k_lattice_bp<true><<<grid, kThreads, tile_words * 16 + r_bytes, st>>>(a, tile_words, kap, e, p, w, 1, AC);
   } else {
-    k_lattice_bp<false><<<grid, kThreads, tile_words * 8 + r_bytes, st>>>(a, tile_words, kap, e, p, w, 0, AC);
+    k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, kap, e, p, w, 0, AC);
   }
 }
 
