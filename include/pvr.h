@@ -82,7 +82,8 @@ const char* pvr_version(void);
 
 /* Create a context for one HR volume on cuda_device. cuda_stream: a cudaStream_t to issue
  * all work on (the caller keeps ownership), or NULL for a library-owned stream.
- * Errors: PVR_ERR_ARG (dims < 1, spacing <= 0), PVR_ERR_CUDA, PVR_ERR_OOM. */
+ * Errors: PVR_ERR_ARG (dims < 1, spacing <= 0, (nx + 1) ny nz >= 2^31 voxels: the kernels
+ * index the volume with 32-bit offsets), PVR_ERR_CUDA, PVR_ERR_OOM. */
 pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_stream,
                              pvr_ctx** out);
 pvr_status pvr_destroy(pvr_ctx* ctx);

@@ -689,6 +689,8 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   if (!g || !out) return fail(nullptr, PVR_ERR_ARG, "null argument");
   if (g->dims[0] < 1 || g->dims[1] < 1 || g->dims[2] < 1 || !(g->spacing_mm > 0))
     return fail(nullptr, PVR_ERR_ARG, "invalid geometry (dims >= 1, spacing > 0)");
+  if ((int64_t)(g->dims[0] + 1) * g->dims[1] * g->dims[2] >= (int64_t(1) << 31))
+    return fail(nullptr, PVR_ERR_ARG, "volume too large (kernels index voxels with 32-bit offsets)");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();

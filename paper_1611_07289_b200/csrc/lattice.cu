@@ -117,21 +117,21 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     __syncthreads();  // the previous group's readers of sX / sT / tables / sm are done
     // stage X (or the grid indicator) over the group footprint, zero outside the grid: one
     // warp per tile row, lanes along x, asynchronous copies (cp.async, zero-fill out of grid)
+    // (32-bit offsets: the engine bounds the volume to < 2^31 voxels)
     int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
     while (ly >= dy) { ly -= dy; ++lz; }
+    const unsigned sX0 = (unsigned)__cvta_generic_to_shared(sX);
     for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
       const int gy = G.lo[1] + ly, gz = G.lo[2] + lz;
-      const bool rin = gy >= 0 && gy < n.y && gz >= 0 && gz < n.z;
-      const size_t rowoff = ((size_t)(rin ? gz : 0) * n.y + (rin ? gy : 0)) * n.x;
-      float* dst = sX + row * dx;
+      const bool rin = (unsigned)gy < (unsigned)n.y && (unsigned)gz < (unsigned)n.z;
+      const int rowoff = (gz * n.y + gy) * n.x + G.lo[0];
       for (int lx = threadIdx.x & 31; lx < dx; lx += 32) {
-        const int gx = G.lo[0] + lx;
-        const bool in = rin && gx >= 0 && gx < n.x;
+        const bool in = rin && (unsigned)(G.lo[0] + lx) < (unsigned)n.x;
         if (MODE == 1) {
-          dst[lx] = in ? 1.0f : 0.0f;
+          sX[row * dx + lx] = in ? 1.0f : 0.0f;
         } else {
-          const unsigned s = (unsigned)__cvta_generic_to_shared(dst + lx);
-          const float* src = X + (in ? rowoff + gx : 0);
+          const unsigned s = sX0 + 4u * (unsigned)(row * dx + lx);
+          const float* src = X + (in ? rowoff + lx : 0);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(src), "r"(in ? 4 : 0)
                        : "memory");
         }
@@ -188,24 +188,31 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       float rx = f.of[0] + U * f.qa[0] + V * f.qb[0];
       float ry = f.of[1] + U * f.qa[1] + V * f.qb[1];
       float rz = f.of[2] + U * f.qa[2] + V * f.qb[2];
-      const float qcx = f.qc[0], qcy = f.qc[1], qcz = f.qc[2];
-      const int obx = f.ob[0], oby = f.ob[1], obz = f.ob[2];
+      // (x, y) travel as a packed pair; the lerps run on (z0, z1) pairs (FADD2 / FFMA2)
+      f2 rxy = pk(rx, ry);
+      const f2 qcxy = pk(f.qc[0], f.qc[1]);
+      const float qcz = f.qc[2];
+      const f2 mag = pk(kMagic, kMagic);
+      const float* sXo = sX + f.ob[2] * dxy + f.ob[1] * dx + f.ob[0];
       float acc = 0.0f;
       for (int c = 0; c < ntp; ++c) {
-        float flx, fly, flz;
-        const int ix = mfloor(rx, flx) + obx;
-        const int iy = mfloor(ry, fly) + oby;
-        const int iz = mfloor(rz, flz) + obz;
-        const float fx = rx - flx, fy = ry - fly, fz = rz - flz;
-        const float* p = sX + iz * dxy + iy * dx + ix;
-        const float x000 = p[0], x100 = p[1], x010 = p[dx], x110 = p[dx + 1];
-        const float x001 = p[dxy], x101 = p[dxy + 1], x011 = p[dxy + dx], x111 = p[dxy + dx + 1];
-        const float c00 = fmaf(fx, x100 - x000, x000), c10 = fmaf(fx, x110 - x010, x010);
-        const float c01 = fmaf(fx, x101 - x001, x001), c11 = fmaf(fx, x111 - x011, x011);
-        const float c0 = fmaf(fy, c10 - c00, c00), c1 = fmaf(fy, c11 - c01, c01);
+        const f2 txy = add2_rd(rxy, mag);
+        const float tz = __fadd_rd(rz, kMagic);
+        const int ix = __float_as_int(lo2(txy)) - kMagicBits;
+        const int iy = __float_as_int(hi2(txy)) - kMagicBits;
+        const int iz = __float_as_int(tz) - kMagicBits;
+        const f2 fxy = sub2(rxy, sub2(txy, mag));
+        const float fz = rz - __fsub_rn(tz, kMagic);
+        const float* p = sXo + iz * dxy + iy * dx + ix;
+        const f2 x00 = pk(p[0], p[dxy]), x10 = pk(p[1], p[dxy + 1]);            // (z0, z1) at y0
+        const f2 x01 = pk(p[dx], p[dxy + dx]), x11 = pk(p[dx + 1], p[dxy + dx + 1]);  // at y1
+        const float fx = lo2(fxy), fy = hi2(fxy);
+        const f2 cy0 = fma2s(fx, sub2(x10, x00), x00);   // x-lerp, (z0, z1) at y0
+        const f2 cy1 = fma2s(fx, sub2(x11, x01), x01);   // at y1
+        const f2 cz = fma2s(fy, sub2(cy1, cy0), cy0);    // y-lerp: (z0, z1)
+        const float c0 = lo2(cz), c1 = hi2(cz);
         acc = fmaf(s_tp[c], fmaf(fz, c1 - c0, c0), acc);
-        rx += qcx;
-        ry += qcy;
+        rxy = add2(rxy, qcxy);
         rz += qcz;
       }
       sT[i] = acc;
