@@ -6,6 +6,7 @@
 // plan of the lattice kernels (member tiles grouped by shared stack pixels, each group with
 // its voxel bounding box). The kernels (kernels.cu, lattice.cu) consume fp32 copies. Device
 // work is issued on the context's stream; NCCL is dlopen'd at pvr_comm_init.
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -95,7 +96,7 @@ struct pvr_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int3 dims;
-  int nxp = 0;  // (A, C) row pitch: nx rounded up to even (16-byte aligned voxel pairs)
+  int nxp = 0;  // row pitch of X and (A, C): nx rounded up to a multiple of 4 (TMA: 16-byte rows)
   double s, o[3];
   int64_t V, Vp;  // voxels; padded (A, C) entries
   int state = CREATED;
@@ -123,6 +124,9 @@ struct pvr_ctx {
     size_t mem_cap = 0, grp_cap = 0;
   } fplan, bplan, iplan;  // forward/coverage, backprojection, init backprojection (hi/lo)
   std::vector<std::unique_ptr<NaturalGroups>> ngcache;  // geometry-free group lists
+  std::vector<int> fbox;   // forward TMA box shapes (width, height) of the current plan
+  char* tmaps = nullptr;   // device: CUtensorMap [2 X buffers][box shapes]
+  size_t tmaps_cap = 0;
   // comm
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -343,7 +347,7 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp,
-                  c->partials, c->em};
+                  c->partials, c->em, c->tmaps};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -505,9 +509,24 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
         lo[d] = std::min(lo[d], mlo[3 * i + d]);
         hi[d] = std::max(hi[d], mhi[3 * i + d]);
       }
-    lo[0] -= ((lo[0] % 2) + 2) % 2;  // even x origin: 16-byte aligned flush pairs
     g.m0 = (int32_t)out.mem.size();
     g.nm = b - a;
+    g.tmap = g.pad = 0;
+    if (fwd) {
+      // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
+      // (measured: a box starting at an x not a multiple of 4 floats faults with an illegal
+      // instruction), rows of 4 x odd floats (16-byte TMA rows, 4 (mod 8) banks apart), z
+      // slabs padded to 128 bytes
+      lo[0] -= ((lo[0] % 4) + 4) % 4;
+      int r = (hi[0] - lo[0] + 1 + 3) / 4;
+      if (r % 2 == 0) ++r;
+      for (int d = 0; d < 3; ++d) g.lo[d] = lo[d];
+      g.dim[0] = 4 * r;
+      g.dim[1] = hi[1] - lo[1] + 1;
+      g.dim[2] = hi[2] - lo[2] + 1;
+      return (int64_t)((g.dim[0] * g.dim[1] + 31) & ~31) * g.dim[2];
+    }
+    lo[0] -= ((lo[0] % 2) + 2) % 2;  // even x origin: 16-byte aligned flush pairs
     for (int d = 0; d < 3; ++d) g.lo[d] = lo[d];
     // odd row and plane pitches: lanes stepping along x, y or z hit different banks
     g.dim[0] = (hi[0] - lo[0] + 1) | 1;
@@ -564,6 +583,73 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   out.mem.swap(mem);
 }
 
+// Forward tiles are staged by TMA with one box per group (its own bbox, sized in
+// size_groups): one tensor map per distinct box shape (width, height) and X buffer.
+pvr_status box_forward_groups(pvr_ctx* c, PlanBuild& pb) {
+  std::vector<std::pair<int, int>> shapes;
+  for (GroupDev& g : pb.grp) {
+    if (g.dim[0] > 256 || g.dim[1] > 256)
+      return fail(c, PVR_ERR_ARG, "forward tile %dx%d exceeds the TMA box limit", g.dim[0], g.dim[1]);
+    const std::pair<int, int> sh(g.dim[0], g.dim[1]);
+    size_t k = 0;
+    while (k < shapes.size() && shapes[k] != sh) ++k;  // few distinct shapes per plan
+    if (k == shapes.size()) shapes.push_back(sh);
+    g.tmap = (int32_t)k;
+  }
+  c->fbox.clear();
+  for (auto& sh : shapes) {
+    c->fbox.push_back(sh.first);
+    c->fbox.push_back(sh.second);
+  }
+  return PVR_OK;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+// Tensor maps of both X buffers for every forward box shape: dims (nx, ny, nz), row pitch
+// nxp, box (w, h, 1); out-of-grid elements (negative or >= dims) are zero-filled by TMA.
+// Layout on the device: [X buffer][shape], 128 B each.
+pvr_status encode_tmaps(pvr_ctx* c) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(c, PVR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (EncodeTiledFn)fn;
+  }
+  const size_t nb = c->fbox.size() / 2;
+  std::vector<CUtensorMap> maps(2 * nb);
+  if (nb) memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
+  for (int b = 0; b < 2; ++b)
+    for (size_t k = 0; k < nb; ++k) {
+      const cuuint64_t dim[3] = {(cuuint64_t)c->dims.x, (cuuint64_t)c->dims.y, (cuuint64_t)c->dims.z};
+      const cuuint64_t stride[2] = {(cuuint64_t)c->nxp * 4, (cuuint64_t)c->nxp * c->dims.y * 4};
+      const cuuint32_t box[3] = {(cuuint32_t)c->fbox[2 * k], (cuuint32_t)c->fbox[2 * k + 1], 1};
+      const cuuint32_t es[3] = {1, 1, 1};
+      const CUresult r = encode(&maps[b * nb + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->X[b], dim, stride, box,
+                                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(c, PVR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+  if (maps.size() > c->tmaps_cap) {
+    if (c->tmaps) cudaFree(c->tmaps);
+    c->tmaps = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->tmaps, maps.size() * sizeof(CUtensorMap)));
+    c->tmaps_cap = maps.size();
+  }
+  if (nb) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  return PVR_OK;
+}
+
 pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
   if (pb.mem.size() > pl.mem_cap) {
     if (pl.mem) cudaFree(pl.mem);
@@ -584,7 +670,7 @@ pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
   pl.nsplit = pb.nsplit;
   pl.tile_words = (int)((pb.max_tile_vox + 3) & ~int64_t(3));
   pl.r_bytes = (int)((pb.max_r_bytes + 15) & ~int64_t(15));
-  pl.t_floats = (int)((pb.max_t_floats + 3) & ~int64_t(3));
+  pl.t_floats = (int)((pb.max_t_floats + 31) & ~int64_t(31));  // 128-byte aligned X tile after it
   return PVR_OK;
 }
 
@@ -633,6 +719,10 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
     pl.TU = cand[pick][0];
     pl.TV = cand[pick][1];
     pl.nseg = cand[pick][2];
+    if (fwd) {
+      pvr_status rb = box_forward_groups(c, pb);
+      if (rb != PVR_OK) return rb;
+    }
     pvr_status r = upload_plan(c, pl, pb);
     if (r != PVR_OK) return r;
     if (kind == 2) continue;
@@ -701,7 +791,7 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   memset(&c->st, 0, sizeof(c->st));
   c->device = cuda_device;
   c->dims = make_int3(g->dims[0], g->dims[1], g->dims[2]);
-  c->nxp = g->dims[0] + (g->dims[0] & 1);
+  c->nxp = (g->dims[0] + 3) & ~3;
   c->s = g->spacing_mm;
   for (int d = 0; d < 3; ++d) c->o[d] = g->origin_mm[d];
   c->V = (int64_t)g->dims[0] * g->dims[1] * g->dims[2];
@@ -716,8 +806,8 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
     }
     c->own_stream = true;
   }
-  cudaError_t e1 = cudaMalloc(&c->X[0], c->V * sizeof(float));
-  cudaError_t e2 = cudaMalloc(&c->X[1], c->V * sizeof(float));
+  cudaError_t e1 = cudaMalloc(&c->X[0], c->Vp * sizeof(float));
+  cudaError_t e2 = cudaMalloc(&c->X[1], c->Vp * sizeof(float));
   cudaError_t e3 = cudaMalloc(&c->AC, (c->Vp + 2) * sizeof(float2));
   cudaError_t e4 = cudaMalloc(&c->em, sizeof(EmDev));
   cudaError_t e5 = cudaMalloc(&c->partials, (size_t)kStatBlocks * 5 * sizeof(double));
@@ -728,7 +818,8 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
     delete c;
     return fail(nullptr, PVR_ERR_OOM, "device allocation of the volume buffers failed");
   }
-  cudaMemsetAsync(c->X[0], 0, c->V * sizeof(float), c->stream);
+  cudaMemsetAsync(c->X[0], 0, c->Vp * sizeof(float), c->stream);
+  cudaMemsetAsync(c->X[1], 0, c->Vp * sizeof(float), c->stream);
   cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream);
   cudaMemsetAsync(c->em, 0, sizeof(EmDev), c->stream);
   c->st.voxels = c->V;
@@ -1022,6 +1113,8 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
   pvr_status r = build_plans(c, geo);
   if (r != PVR_OK) return r;
+  r = encode_tmaps(c);
+  if (r != PVR_OK) return r;
   // coverage kappa (geometry only) + live-y range, then the EM reset
   const LatticeArgs la = lattice_args(c, c->fplan);
   launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
@@ -1054,8 +1147,9 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
 pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
   GUARD(c);
   if (!x || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
-  CUDA_TRY(c, cudaMemcpyAsync(c->X[c->cur], x, nvox * sizeof(float),
-                              is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpy2DAsync(c->X[c->cur], c->nxp * sizeof(float), x, c->dims.x * sizeof(float),
+                                c->dims.x * sizeof(float), (size_t)c->dims.y * c->dims.z,
+                                is_device_ptr(x) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
 }
@@ -1088,7 +1182,8 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     float* X2 = c->X[1 - c->cur];
     std::vector<cudaEvent_t>* ev = prof ? prof_slot(c) : nullptr;
     if (prof) cudaEventRecord((*ev)[EV_FWD0], s);
-    launch_forward(s, la, c->fplan.t_floats, c->fplan.tile_words, X0, c->kap, c->p, c->e, c->partials);
+    launch_forward(s, la, c->fplan.t_floats, c->fplan.tile_words, c->tmaps + c->cur * (c->fbox.size() / 2) * 128,
+                   c->kap, c->p, c->e, c->partials);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_FWD1], s);
     launch_em_reduce(s, c->partials, kStatBlocks, c->em);
@@ -1128,8 +1223,9 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
 pvr_status pvr_get_volume(pvr_ctx* c, float* out, size_t nvox) {
   GUARD(c);
   if (!out || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
-  CUDA_TRY(c, cudaMemcpyAsync(out, c->X[c->cur], nvox * sizeof(float),
-                              is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpy2DAsync(out, c->dims.x * sizeof(float), c->X[c->cur], c->nxp * sizeof(float),
+                                c->dims.x * sizeof(float), (size_t)c->dims.y * c->dims.z,
+                                is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
 }

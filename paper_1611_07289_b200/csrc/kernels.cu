@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
     const int i = bx + hx, j = by + hy, l = bz + hz;
     float x0 = 0.0f, x1 = __int_as_float(0x7fc00000);
     if (i >= 0 && i < n.x && j >= 0 && j < n.y && l >= 0 && l < n.z) {
-      x0 = X0[((size_t)l * n.y + j) * n.x + i];
+      x0 = X0[((size_t)l * n.y + j) * nxp + i];
       const float2 ac = AC[((size_t)l * n.y + j) * nxp + i];
       if (ac.y > prm.tau_C) {
         float x = x0 + alpha * ac.x / ac.y;   // a6: X1 = clip(X0 + alpha A / C)
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
           }
       out = x1 + al * sum;
     }
-    X2[((size_t)l * n.y + j) * n.x + i] = out;
+    X2[((size_t)l * n.y + j) * nxp + i] = out;
   }
 }
 
@@ -205,8 +205,9 @@ __global__ void __launch_bounds__(256) k_init_fill(const float2* __restrict__ AC
     const int j = (int)((k / n.x) % n.y);
     const int l = (int)(k / ((int64_t)n.x * n.y));
     const float2 ac = AC[((int64_t)l * n.y + j) * nxp + i];
+    float* xo = X + ((int64_t)l * n.y + j) * nxp + i;
     if (ac.y > prm.tau_C) {
-      X[k] = ac.x / ac.y;
+      *xo = ac.x / ac.y;
       continue;
     }
     float sum = 0.0f;
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(256) k_init_fill(const float2* __restrict__ AC
             ++cnt;
           }
         }
-    X[k] = cnt ? sum / (float)cnt : 0.0f;
+    *xo = cnt ? sum / (float)cnt : 0.0f;
   }
 }
 

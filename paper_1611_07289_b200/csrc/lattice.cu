@@ -96,48 +96,63 @@ struct FwdMember {  // per-member constants in shared memory
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_floats,
-                                                          const float* __restrict__ X,
+                                                          const char* __restrict__ tmaps,
                                                           const float* __restrict__ kap,
                                                           const float* __restrict__ pprev,
                                                           float* __restrict__ out,
                                                           double* __restrict__ partials) {
-  extern __shared__ float4 fsm4[];
+  extern __shared__ __align__(128) float4 fsm4[];
   float* sT = reinterpret_cast<float*>(fsm4);
-  float* sX = sT + t_floats;
+  float* sX = sT + t_floats;  // t_floats is a multiple of 32: 128-byte aligned TMA slabs
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
   __shared__ FwdMember sm[kMaxMembers];
   __shared__ int s_nt, s_np;  // lattice points / pixels of the group
+  __shared__ __align__(8) uint64_t s_bar;  // TMA completion barrier (MODE 0)
   double acc_s[3] = {0.0, 0.0, 0.0};
   float acc_m[2] = {-FLT_MAX, -FLT_MAX};
   const int3 n = a.n;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+  const unsigned sX0 = (unsigned)__cvta_generic_to_shared(sX);
+  if (MODE == 0 && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned phase = 0;
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
-    const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = dx * dy;
+    // tile: rows of pitch dx (the group's TMA box width), z slabs of dxy floats (128-byte
+    // aligned); the box covers the group footprint (engine.cu: size_groups)
+    const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = (dx * dy + 31) & ~31;
     __syncthreads();  // the previous group's readers of sX / sT / tables / sm are done
-    // stage X (or the grid indicator) over the group footprint, zero outside the grid: one
-    // warp per tile row, lanes along x, asynchronous copies (cp.async, zero-fill out of grid)
-    // (32-bit offsets: the engine bounds the volume to < 2^31 voxels)
-    int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
-    while (ly >= dy) { ly -= dy; ++lz; }
-    const unsigned sX0 = (unsigned)__cvta_generic_to_shared(sX);
-    for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
-      const int gy = G.lo[1] + ly, gz = G.lo[2] + lz;
-      const bool rin = (unsigned)gy < (unsigned)n.y && (unsigned)gz < (unsigned)n.z;
-      const int rowoff = (gz * n.y + gy) * n.x + G.lo[0];
-      for (int lx = threadIdx.x & 31; lx < dx; lx += 32) {
-        const bool in = rin && (unsigned)(G.lo[0] + lx) < (unsigned)n.x;
-        if (MODE == 1) {
-          sX[row * dx + lx] = in ? 1.0f : 0.0f;
-        } else {
-          const unsigned s = sX0 + 4u * (unsigned)(row * dx + lx);
-          const float* src = X + (in ? rowoff + lx : 0);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(src), "r"(in ? 4 : 0)
-                       : "memory");
-        }
+    if (MODE == 0) {
+      // X footprint by TMA: one 3D tensor copy (box dx x dy x 1) per z slab, zero fill
+      // outside the grid, completion on an mbarrier
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // sX reads -> async writes
+        const char* tm = tmaps + 128 * G.tmap;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(dz * dx * dy * 4)
+                     : "memory");
+        for (int z = 0; z < dz; ++z)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sX0 + 4u * (unsigned)(z * dxy)),
+              "l"(tm), "r"(G.lo[0]), "r"(G.lo[1]), "r"(G.lo[2] + z), "r"(bar)
+              : "memory");
       }
-      ly += kThreads >> 5;
+    } else {
+      // the grid indicator over the same layout
+      int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
       while (ly >= dy) { ly -= dy; ++lz; }
+      for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
+        const int gy = G.lo[1] + ly, gz = G.lo[2] + lz;
+        const bool rin = (unsigned)gy < (unsigned)n.y && (unsigned)gz < (unsigned)n.z;
+        for (int lx = threadIdx.x & 31; lx < dx; lx += 32)
+          sX[lz * dxy + ly * dx + lx] = (rin && (unsigned)(G.lo[0] + lx) < (unsigned)n.x) ? 1.0f : 0.0f;
+        ly += kThreads >> 5;
+        while (ly >= dy) { ly -= dy; ++lz; }
+      }
     }
     // member constants (one thread per member) and the stack's PSF tables
     if (threadIdx.x < G.nm) {
@@ -174,7 +189,16 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       s_nt = t;
       s_np = p;
     }
-    if (MODE == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (MODE == 0) {  // the X tile has landed
+      unsigned done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+      phase ^= 1u;
+    }
     __syncthreads();
     const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
     const int ntp = 2 * ps.cmax + 1;
@@ -735,11 +759,12 @@ void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_
                                                         partials);
 }
 
-void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, const float* X,
+void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, const void* tmaps,
                     const float* kap, const float* p, float* e, double* partials) {
   configure();
   const int smem = (t_floats + x_floats) * 4;
-  k_lattice_fwd<0><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, X, kap, p, e, partials);
+  k_lattice_fwd<0><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, (const char*)tmaps, kap, p, e,
+                                                        partials);
 }
 
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,

@@ -50,8 +50,11 @@ struct MemberDev {
 };
 struct GroupDev {
   int32_t m0, nm;           // members [m0, m0 + nm)
-  int32_t lo[3];            // voxel bbox origin (not clipped to the grid; lo[0] even)
-  int32_t dim[3];           // voxel bbox size (dim[0] even)
+  int32_t lo[3];            // voxel bbox origin (not clipped to the grid; lo[0] even, forward:
+                            // a multiple of 4)
+  int32_t dim[3];           // voxel bbox size (row / plane pitches of the shared tile: odd;
+                            // forward: dim[0] = 4 x odd, the TMA box width)
+  int32_t tmap, pad;        // forward: index of the group's TMA box tensor map
 };
 
 // EM state on the device (written by k_em_params / k_range_finish, read by later kernels).
@@ -82,7 +85,7 @@ struct LatticeArgs {
   const GroupDev* grp;
   int32_t ngroups;
   int3 n;                  // volume dims
-  int32_t nxp;             // row pitch of the (A, C) volume (nx rounded up to even)
+  int32_t nxp;             // row pitch of X and (A, C) (nx rounded up to a multiple of 4)
   const float* ys;         // concatenated stacks
   Params prm;
 };
@@ -100,8 +103,10 @@ constexpr int kMaxGroupMembers = 16;      // members per group (lattice.cu kMaxM
 // lattice.cu
 void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
                      float* kap, double* partials);
+// tmaps: device array of CUtensorMap (128 B each), one per box shape (GroupDev::tmap), over
+// the X buffer to read
 void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
-                    const float* X, const float* kap, const float* p, float* e,
+                    const void* tmaps, const float* kap, const float* p, float* e,
                     double* partials);
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         const float* kap, const float* e, const float* p, const float* w,
