@@ -11,6 +11,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <memory>
 #include <cmath>
 #include <cstdarg>
@@ -89,6 +91,18 @@ struct Nccl {
 };
 Nccl g_nccl;
 
+// PVR_TRACE=1: host-side phase timings of pvr_set_transforms on stderr (diagnostics only)
+struct Trace {
+  bool on = getenv("PVR_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pvr] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 }  // namespace
 
 struct pvr_ctx {
@@ -123,6 +137,8 @@ struct pvr_ctx {
     GroupDev* grp = nullptr;
     size_t mem_cap = 0, grp_cap = 0;
   } fplan, bplan, iplan;  // forward/coverage, backprojection, init backprojection (hi/lo)
+  bool iplan_valid = false;     // the init plan is built lazily by pvr_init_volume
+  std::vector<PatchGeo> geo;    // composed geometry of the local patches (last set_transforms)
   std::vector<std::unique_ptr<NaturalGroups>> ngcache;  // geometry-free group lists
   std::vector<int> fbox;   // forward TMA box shapes (width, height) of the current plan
   char* tmaps = nullptr;   // device: CUtensorMap [2 X buffers][box shapes]
@@ -511,7 +527,10 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
       }
     g.m0 = (int32_t)out.mem.size();
     g.nm = b - a;
-    g.tmap = g.pad = 0;
+    g.tmap = 0;
+    g.interior = 1;
+    for (int d = 0; d < 3; ++d)
+      if (lo[d] < 0 || hi[d] > (d == 0 ? c->dims.x : d == 1 ? c->dims.y : c->dims.z) - 1) g.interior = 0;
     if (fwd) {
       // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
       // (measured: a box starting at an x not a multiple of 4 floats faults with an illegal
@@ -678,7 +697,7 @@ pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
 // natural groups fit whole and every single member fits; large tiles amortise the flush, the
 // staging and the lattice halo. Candidates are first screened on a sample of patches; the last
 // choice is tried first, so repeated set_transforms with similar motion only resize bboxes.
-pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
+pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo, int kind_hi) {
   std::vector<int64_t> sample, all(c->nloc);
   for (int64_t s = 0; s < c->nloc; ++s) all[s] = s;
   const int64_t step = std::max<int64_t>(1, c->nloc / 128);
@@ -695,7 +714,8 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
     ng.sample = smp;
     return ng;
   };
-  for (int kind = 0; kind < 3; ++kind) {
+  Trace tr;
+  for (int kind = kind_lo; kind < kind_hi; ++kind) {
     const bool fwd = kind == 0;
     pvr_ctx::Plan& pl = kind == 0 ? c->fplan : kind == 1 ? c->bplan : c->iplan;
     const int(*cand)[3] = fwd ? fcand : bcand;
@@ -723,8 +743,10 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo) {
       pvr_status rb = box_forward_groups(c, pb);
       if (rb != PVR_OK) return rb;
     }
+    tr.mark(kind == 0 ? "  plan forward" : kind == 1 ? "  plan backprojection" : "  plan init");
     pvr_status r = upload_plan(c, pl, pb);
     if (r != PVR_OK) return r;
+    tr.mark("  upload");
     if (kind == 2) continue;
     int32_t* tile = fwd ? c->st.fwd_tile : c->st.bp_tile;
     tile[0] = pl.TU; tile[1] = pl.TV; tile[2] = pl.nseg;
@@ -1048,6 +1070,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   GUARD(c);
   if (c->state < PATCHED) return fail(c, PVR_ERR_STATE, "set_transforms needs extract_patches");
   if (!T || n != c->M) return fail(c, PVR_ERR_ARG, "expected %lld transforms, got %lld", (long long)c->M, (long long)n);
+  Trace tr;
   std::vector<double> Th((size_t)12 * c->nloc);
   const double* Tl = T + 12 * c->first;
   if (is_device_ptr(T)) {
@@ -1111,10 +1134,15 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
     }
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
-  pvr_status r = build_plans(c, geo);
+  tr.mark("compose patches");
+  pvr_status r = build_plans(c, geo, 0, 2);  // forward + backprojection; init plan: lazily
   if (r != PVR_OK) return r;
+  c->iplan_valid = false;
+  c->geo.swap(geo);
+  tr.mark("build plans");
   r = encode_tmaps(c);
   if (r != PVR_OK) return r;
+  tr.mark("tensor maps");
   // coverage kappa (geometry only) + live-y range, then the EM reset
   const LatticeArgs la = lattice_args(c, c->fplan);
   launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
@@ -1132,6 +1160,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   EmDev h;
   CUDA_TRY(c, cudaMemcpyAsync(&h, c->em, sizeof(EmDev), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  tr.mark("coverage + EM reset (GPU)");
   if (!(h.stats[0] > 0)) return fail(c, PVR_ERR_EMPTY, "no observed pixel: nothing to reconstruct");
   // PSF samples visited per iteration (observed pixels x S, all ranks after the allreduce)
   c->samples_obs = (int64_t)h.stats[2];
@@ -1157,6 +1186,11 @@ pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
 pvr_status pvr_init_volume(pvr_ctx* c) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
+  if (!c->iplan_valid) {
+    pvr_status rp = build_plans(c, c->geo, 2, 3);
+    if (rp != PVR_OK) return rp;
+    c->iplan_valid = true;
+  }
   const LatticeArgs lb = lattice_args(c, c->iplan);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
   launch_backproject(c->stream, lb, c->iplan.tile_words, c->iplan.r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);

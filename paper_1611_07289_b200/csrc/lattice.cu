@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
               "l"(tm), "r"(G.lo[0]), "r"(G.lo[1]), "r"(G.lo[2] + z), "r"(bar)
               : "memory");
       }
-    } else {
-      // the grid indicator over the same layout
+    } else if (!G.interior) {
+      // the grid indicator over the same layout (interior groups: kappa = 1, no lattice pass)
       int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
       while (ly >= dy) { ly -= dy; ++lz; }
       for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
     const int ntp = 2 * ps.cmax + 1;
     // lattice points of all members: T(U, V) = sum_c tp(c) trilerp(X, x(U, V, c))
-    for (int i = threadIdx.x; i < s_nt; i += kThreads) {
+    const bool skip = MODE == 1 && G.interior;
+    for (int i = skip ? s_nt : threadIdx.x; i < s_nt; i += kThreads) {
       int k = 0;
       while (k + 1 < G.nm && i >= sm[k + 1].t0) ++k;
       const FwdMember& f = sm[k];
@@ -252,9 +253,13 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       const int du = li % f.tu, dv = li / f.tu;
       const int u = f.u0 + du, v = f.v0 + dv;
       float s = 0.0f;
-      for (int b = 0; b <= 2 * ps.rv; ++b) {
-        const float* row = sT + f.t0 + (ps.nv * dv + b) * f.LU + ps.nu * du;
-        for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
+      if (skip) {
+        s = 1.0f;  // every sample fully in the grid: kappa = sum psi = 1 (reading Q27)
+      } else {
+        for (int b = 0; b <= 2 * ps.rv; ++b) {
+          const float* row = sT + f.t0 + (ps.nv * dv + b) * f.LU + ps.nu * du;
+          for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
+        }
       }
       const PatchDev& pt = a.P[f.patch];
       const int64_t j = pt.pix0 + ((int64_t)f.z * pt.sy + v) * pt.sx + u;

@@ -54,7 +54,9 @@ struct GroupDev {
                             // a multiple of 4)
   int32_t dim[3];           // voxel bbox size (row / plane pitches of the shared tile: odd;
                             // forward: dim[0] = 4 x odd, the TMA box width)
-  int32_t tmap, pad;        // forward: index of the group's TMA box tensor map
+  int32_t tmap;             // forward: index of the group's TMA box tensor map
+  int32_t interior;         // forward: 1 if every PSF sample's 8 trilinear corners are in the
+                            // grid (kappa = sum psi = 1 exactly; coverage skips the lattice)
 };
 
 // EM state on the device (written by k_em_params / k_range_finish, read by later kernels).
