@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <parallel/algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <memory>
@@ -495,29 +496,24 @@ struct PlanBuild {
 // Bounding boxes for the current transforms and the final group list of one plan.
 // kind 0: forward / coverage (4 B per voxel of staged X), 1: backprojection in the iterations
 // (8 B: one int32 per quantity), 2: init backprojection (16 B: hi/lo pairs).
+// All per-member and per-group passes run in parallel (OpenMP); the output is deterministic.
 void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const NaturalGroups& ng, int kind,
                  PlanBuild& out) {
   const bool fwd = kind == 0;
+  Trace tr;
   const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 : kInitTileBytes / 16;
-  const size_t nm = ng.mem.size();
+  const int64_t nm = (int64_t)ng.mem.size();
   std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < (int64_t)nm; ++i) {
+  for (int64_t i = 0; i < nm; ++i) {
     const MemberDev& m = ng.mem[i];
     const HostPatch& hp = c->patches[c->first + m.patch];
     int lo[3], hi[3];
     member_bbox(m, hp, c->stacks[hp.stack].psf, geo[m.patch], fwd, lo, hi);
     for (int d = 0; d < 3; ++d) { mlo[3 * i + d] = lo[d]; mhi[3 * i + d] = hi[d]; }
   }
-  out.mem.clear();
-  out.grp.clear();
-  out.max_tile_vox = 0;
-  out.max_r_bytes = ng.max_r_bytes;
-  out.max_t_floats = ng.max_t_floats;
-  out.nsplit = 0;
-  out.all_fit = true;
-  int fit = 0;
-  const int ngrp = (int)ng.start.size() - 1;
+  tr.mark("    member bboxes");
+  const int n3[3] = {c->dims.x, c->dims.y, c->dims.z};
   auto group = [&](int a, int b, GroupDev& g) {  // union bbox of members [a, b)
     int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
     for (int i = a; i < b; ++i)
@@ -525,12 +521,12 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
         lo[d] = std::min(lo[d], mlo[3 * i + d]);
         hi[d] = std::max(hi[d], mhi[3 * i + d]);
       }
-    g.m0 = (int32_t)out.mem.size();
+    g.m0 = a;  // natural member index; renumbered below
     g.nm = b - a;
     g.tmap = 0;
     g.interior = 1;
     for (int d = 0; d < 3; ++d)
-      if (lo[d] < 0 || hi[d] > (d == 0 ? c->dims.x : d == 1 ? c->dims.y : c->dims.z) - 1) g.interior = 0;
+      if (lo[d] < 0 || hi[d] > n3[d] - 1) g.interior = 0;
     if (fwd) {
       // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
       // (measured: a box starting at an x not a multiple of 4 floats faults with an illegal
@@ -553,32 +549,47 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     g.dim[2] = hi[2] - lo[2] + 1;
     return (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
   };
+  // natural groups (parallel); a group over the tile budget is split into single members
+  const int ngrp = (int)ng.start.size() - 1;
+  std::vector<GroupDev> nat(ngrp);
+  std::vector<int64_t> nvox(ngrp);
+#pragma omp parallel for schedule(static)
+  for (int gi = 0; gi < ngrp; ++gi) nvox[gi] = group(ng.start[gi], ng.start[gi + 1], nat[gi]);
+  out.grp.clear();
+  out.grp.reserve(ngrp);
+  out.max_tile_vox = 0;
+  out.max_r_bytes = ng.max_r_bytes;
+  out.max_t_floats = ng.max_t_floats;
+  out.nsplit = 0;
+  out.all_fit = true;
+  int fit = 0;
   for (int gi = 0; gi < ngrp; ++gi) {
     const int a = ng.start[gi], b = ng.start[gi + 1];
-    GroupDev g;
-    int64_t vox = group(a, b, g);
-    if (vox <= vox_budget) {
+    if (nvox[gi] <= vox_budget) {
       ++fit;
-      for (int i = a; i < b; ++i) out.mem.push_back(ng.mem[i]);
-      out.grp.push_back(g);
-      out.max_tile_vox = std::max(out.max_tile_vox, vox);
+      out.grp.push_back(nat[gi]);
+      out.max_tile_vox = std::max(out.max_tile_vox, nvox[gi]);
       continue;
     }
     if (b - a > 1) ++out.nsplit;
     for (int i = a; i < b; ++i) {
-      vox = group(i, i + 1, g);
+      GroupDev g;
+      const int64_t vox = group(i, i + 1, g);
       if (vox > vox_budget) out.all_fit = false;
-      out.mem.push_back(ng.mem[i]);
       out.grp.push_back(g);
       out.max_tile_vox = std::max(out.max_tile_vox, vox);
     }
   }
   out.fit_frac = ngrp ? (double)fit / ngrp : 1.0;
+  tr.mark("    group boxes");
   // Order the CTAs' work along a Morton curve of the groups' bbox centres (16-voxel cells), so
   // that overlapping footprints of all stacks are processed close in time: the forward's X
   // reads and the backprojection's (A, C) flushes then hit L2 instead of re-streaming HBM.
-  std::vector<std::pair<uint64_t, int32_t>> order(out.grp.size());
-  for (size_t g = 0; g < out.grp.size(); ++g) {
+  // Keys carry the group index as tie-break: the order is unique (deterministic).
+  const int64_t ng2 = (int64_t)out.grp.size();
+  std::vector<std::pair<uint64_t, int32_t>> order(ng2);
+#pragma omp parallel for schedule(static)
+  for (int64_t g = 0; g < ng2; ++g) {
     uint64_t key = 0;
     uint32_t cc[3];
     for (int d = 0; d < 3; ++d)
@@ -587,33 +598,38 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
       for (int d = 2; d >= 0; --d) key = (key << 1) | ((cc[d] >> b) & 1u);
     order[g] = {key, (int32_t)g};
   }
-  std::stable_sort(order.begin(), order.end());
-  std::vector<GroupDev> grp(out.grp.size());
-  std::vector<MemberDev> mem;
-  mem.reserve(out.mem.size());
-  for (size_t k = 0; k < order.size(); ++k) {
+  tr.mark("    morton keys");
+  __gnu_parallel::sort(order.begin(), order.end());
+  tr.mark("    morton sort");
+  std::vector<GroupDev> grp(ng2);
+  std::vector<int32_t> m0(ng2 + 1, 0);
+  for (int64_t k = 0; k < ng2; ++k) m0[k + 1] = m0[k] + out.grp[order[k].second].nm;
+  out.mem.resize(m0[ng2]);
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < ng2; ++k) {
     GroupDev g = out.grp[order[k].second];
-    const int m0 = g.m0;
-    g.m0 = (int32_t)mem.size();
-    for (int i = 0; i < g.nm; ++i) mem.push_back(out.mem[m0 + i]);
+    for (int i = 0; i < g.nm; ++i) out.mem[m0[k] + i] = ng.mem[g.m0 + i];
+    g.m0 = m0[k];
     grp[k] = g;
   }
   out.grp.swap(grp);
-  out.mem.swap(mem);
+  tr.mark("    reorder");
 }
 
 // Forward tiles are staged by TMA with one box per group (its own bbox, sized in
 // size_groups): one tensor map per distinct box shape (width, height) and X buffer.
 pvr_status box_forward_groups(pvr_ctx* c, PlanBuild& pb) {
   std::vector<std::pair<int, int>> shapes;
+  std::vector<int32_t> index(257 * 257, -1);  // (width, height) -> shape number
   for (GroupDev& g : pb.grp) {
     if (g.dim[0] > 256 || g.dim[1] > 256)
       return fail(c, PVR_ERR_ARG, "forward tile %dx%d exceeds the TMA box limit", g.dim[0], g.dim[1]);
-    const std::pair<int, int> sh(g.dim[0], g.dim[1]);
-    size_t k = 0;
-    while (k < shapes.size() && shapes[k] != sh) ++k;  // few distinct shapes per plan
-    if (k == shapes.size()) shapes.push_back(sh);
-    g.tmap = (int32_t)k;
+    int32_t& k = index[g.dim[0] * 257 + g.dim[1]];
+    if (k < 0) {
+      k = (int32_t)shapes.size();
+      shapes.emplace_back(g.dim[0], g.dim[1]);
+    }
+    g.tmap = k;
   }
   c->fbox.clear();
   for (auto& sh : shapes) {
