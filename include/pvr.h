@@ -162,6 +162,18 @@ pvr_status pvr_sr_iterate(pvr_ctx* ctx, int n, float alpha, float lambda);
 
 /* Copy X out (float32 [nz][ny][nx]; host or device pointer). Errors: PVR_ERR_ARG. */
 pvr_status pvr_get_volume(pvr_ctx* ctx, float* out, size_t nvox);
+/* Rigidity map ("Integrating p and pbar into a 3D volume using the
+ * same PSF as for the reconstruction identifies candidate regions, solely containing rigid
+ * motion components"; reading Q28 in DESIGN.md):
+ *   out_k = [W^T (p pbar_s)]_k / [W^T 1]_k  where [W^T 1]_k > tau_C, else 0,
+ * W^T over the observed pixels (kappa >= tau_obs) of ALL patches (excluded ones included:
+ * their low pbar marks non-rigid regions) with the reconstruction's PSF and 1/kappa row
+ * normalisation; p, pbar of the last E-step (all 1 right after set_transforms). Values lie in
+ * [0, 1]. out: float32 [nz][ny][nx], host or device pointer; one backprojection pass on the
+ * device (exact hi/lo tiles, as pvr_init_volume). Overwrites the addon / confidence returned
+ * by pvr_get_taps. Errors: PVR_ERR_ARG (nvox != V), PVR_ERR_STATE (before set_transforms).
+ * Collective when nranks > 1. */
+pvr_status pvr_rigidity_map(pvr_ctx* ctx, float* out, size_t nvox);
 /* Weights of this rank's shard after the last iteration: pixel posteriors p
  * [n_local_pixels], patch weights w and patch scores pbar [n_local]; any may be NULL. */
 pvr_status pvr_get_weights(pvr_ctx* ctx, float* pixel_p, float* patch_w, float* patch_pbar);

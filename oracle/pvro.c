@@ -597,6 +597,33 @@ int pvro_init_volume(pvro_ctx* x) {
   return 0;
 }
 
+/* Rigidity map (reading Q28): W^T (p pbar) / W^T 1 where W^T 1 > tau_C, else 0. */
+int pvro_rigidity_map(const pvro_ctx* x, double* out) {
+  if (x->state < 3) return -1;
+  const int64_t V = (int64_t)x->n[0] * x->n[1] * x->n[2];
+  double* r = (double*)malloc(x->P * sizeof(double));
+  double* ones = (double*)malloc(x->P * sizeof(double));
+  double* num = (double*)calloc(V, sizeof(double));
+  double* den = (double*)calloc(V, sizeof(double));
+  for (int64_t s = 0; s < x->M; ++s) {
+    const int32_t* pt = &x->patch[7 * s];
+    const int64_t n = (int64_t)pt[4] * pt[5] * pt[6];
+    for (int64_t j = x->pix0[s]; j < x->pix0[s] + n; ++j) { r[j] = x->p[j] * x->pbar[s]; ones[j] = 1.0; }
+  }
+  pvro_adjoint(x, r, 0, x->M, num);
+  pvro_adjoint(x, ones, 0, x->M, den);
+  for (int64_t k = 0; k < V; ++k) out[k] = den[k] > x->tau_C ? num[k] / den[k] : 0.0;
+  free(r); free(ones); free(num); free(den);
+  return 0;
+}
+
+int pvro_set_weights(pvro_ctx* x, const double* p, const double* pbar) {
+  if (x->state < 3) return -1;
+  if (p) memcpy(x->p, p, x->P * sizeof(double));
+  if (pbar) memcpy(x->pbar, pbar, x->M * sizeof(double));
+  return 0;
+}
+
 /* One SR iteration = SURVEY §8(c) steps 1-11, in order. */
 static int sr_step(pvro_ctx* x, double alpha, double lambda) {
   int64_t V = (int64_t)x->n[0] * x->n[1] * x->n[2];

@@ -103,6 +103,13 @@ int pvro_forward_range(const pvro_ctx*, const double* X, int64_t first, int64_t 
    [first, first + count) (out is accumulated into, caller zeroes it) */
 int pvro_adjoint(const pvro_ctx*, const double* r, int64_t first, int64_t count, double* out);
 int pvro_init_volume(pvro_ctx*);
+/* Rigidity map ("Integrating p and pbar into a 3D volume using the same PSF as for
+ * the reconstruction"; reading Q28): out_k = [W^T (p pbar_s)]_k /
+ * [W^T 1]_k where [W^T 1]_k > tau_C, else 0; W^T over the observed pixels of all patches with
+ * the reconstruction's row normalisation 1/kappa; p, pbar of the last E-step (1 before any). */
+int pvro_rigidity_map(const pvro_ctx*, double* out);
+/* Test hook: overwrite the E-step state p [P] and pbar [M] (either may be NULL). */
+int pvro_set_weights(pvro_ctx*, const double* p, const double* pbar);
 int pvro_sr_iterate(pvro_ctx*, int n, double alpha, double lambda);
 /* state after the last iteration: per-pixel p and e, per-patch pbar and w */
 int pvro_get_weights(const pvro_ctx*, double* p, double* pbar, double* w);

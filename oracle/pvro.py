@@ -71,6 +71,8 @@ def lib():
         L.pvro_forward_range.argtypes = [vp, vp, i64, i64, vp, vp]
         L.pvro_adjoint.argtypes = [vp, vp, i64, i64, vp]
         L.pvro_init_volume.argtypes = [vp]
+        L.pvro_rigidity_map.argtypes = [vp, vp]
+        L.pvro_set_weights.argtypes = [vp, vp, vp]
         L.pvro_sr_iterate.argtypes = [vp, C.c_int, d, d]
         L.pvro_get_weights.argtypes = [vp, vp, vp, vp]
         L.pvro_get_taps.argtypes = [vp, vp, vp, vp, vp]
@@ -233,6 +235,18 @@ class Oracle:
 
     def sr_iterate(self, n, alpha, lam):
         _chk(lib().pvro_sr_iterate(self.h, n, float(alpha), float(lam)), "sr_iterate")
+
+    def set_weights(self, p=None, pbar=None):
+        """Test hook: overwrite the E-step state (p [P], pbar [M])."""
+        pa = None if p is None else np.ascontiguousarray(p, np.float64)
+        pb = None if pbar is None else np.ascontiguousarray(pbar, np.float64)
+        _chk(lib().pvro_set_weights(self.h, _p(pa), _p(pb)), "set_weights")
+
+    def rigidity_map(self):
+        """W^T(p pbar) / W^T 1 where W^T 1 > tau_C, else 0 (reading Q28)."""
+        R = np.zeros(self.V, np.float64)
+        _chk(lib().pvro_rigidity_map(self.h, _p(R)), "rigidity_map")
+        return R.reshape(self.dims[::-1])
 
     def weights(self):
         p = np.zeros(self.P)

@@ -1219,6 +1219,32 @@ pvr_status pvr_init_volume(pvr_ctx* c) {
   return PVR_OK;
 }
 
+pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "rigidity_map needs set_transforms");
+  if (!out || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
+  if (!c->iplan_valid) {
+    pvr_status rp = build_plans(c, c->geo, 2, 3);
+    if (rp != PVR_OK) return rp;
+    c->iplan_valid = true;
+  }
+  const LatticeArgs lb = lattice_args(c, c->iplan);
+  CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
+  // W^T (p pbar) and W^T 1 with the exact hi/lo tiles of the init pass (pbar rides in w)
+  launch_backproject(c->stream, lb, c->iplan.tile_words, c->iplan.r_bytes, c->kap, c->e, c->p, c->pbar, 2, c->AC);
+  CHECK_LAUNCH(c);
+  pvr_status r = allreduce_ac(c);
+  if (r != PVR_OK) return r;
+  float* tmp = c->X[1 - c->cur];  // scratch between iterations
+  launch_ratio(c->stream, c->AC, c->dims, c->nxp, (float)c->tau_C, tmp);
+  CHECK_LAUNCH(c);
+  CUDA_TRY(c, cudaMemcpy2DAsync(out, c->dims.x * sizeof(float), tmp, c->nxp * sizeof(float),
+                                c->dims.x * sizeof(float), (size_t)c->dims.y * c->dims.z,
+                                is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
 pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "sr_iterate needs set_transforms");

@@ -228,6 +228,16 @@ __global__ void __launch_bounds__(256) k_init_fill(const float2* __restrict__ AC
   }
 }
 
+// f2 rigidity map (reading Q28): out = A / C where C > tau_C, else 0 (pitch nxp).
+__global__ void __launch_bounds__(256) k_ratio(const float2* __restrict__ AC, int3 n, int nxp, float tau_C,
+                                               float* __restrict__ out) {
+  const int64_t V = (int64_t)nxp * n.y * n.z;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < V; k += (int64_t)gridDim.x * blockDim.x) {
+    const float2 ac = AC[k];
+    out[k] = ac.y > tau_C ? ac.x / ac.y : 0.0f;
+  }
+}
+
 __global__ void k_fill(float* __restrict__ x, int64_t n, float v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = v;
@@ -262,6 +272,10 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2) {
   const dim3 grid((dims.x + kUX - 1) / kUX, (dims.y + kUY - 1) / kUY, (dims.z + kUZ - 1) / kUZ);
   k_update<<<grid, 256, 0, st>>>(X0, AC, dims, nxp, prm, em, alpha, lambda, X2);
+}
+
+void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out) {
+  k_ratio<<<148 * 8, 256, 0, st>>>(AC, dims, nxp, tau_C, out);
 }
 
 void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, int nxp, Params prm, float* X) {

@@ -368,7 +368,8 @@ struct BpMember {
   int plu, plv, phu, phv, rw;
   int64_t pixz, yz;        // first pixel of slice z in the local arrays / in the stacks
   int sx, W;
-  float ws;                // patch weight w (1 in the init pass)
+  float ws;                // patch weight w (1 in the init and rigidity passes)
+  float vs;                // rigidity pass: the patch score pbar
 };
 
 __device__ __forceinline__ float pick3(const float (&v)[3], int ax) {
@@ -577,6 +578,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         M.sx = pt.sx;
         M.W = pt.W;
         M.ws = init ? 1.0f : w[m.patch];
+        M.vs = init == 2 ? w[m.patch] : 1.0f;
         nl = M.nU * (o.Vhi - o.Vlo);
         np = M.rw * (o.phv - o.plv + 1);
       }
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         const float k = kap[j];
         if (M.ws != 0.0f && k >= a.prm.tau_obs) {
           const float pv = init ? 1.0f : p[j];
-          const float val = init ? a.ys[M.yz + (int64_t)v * M.W + u] : e[j];
+          const float val = init == 1 ? a.ys[M.yz + (int64_t)v * M.W + u] : init == 2 ? p[j] * M.vs : e[j];
           rC = M.ws * pv / k;
           rA = rC * val;
         }
@@ -778,8 +780,8 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
   if (a.ngroups <= 0) return;
   configure();
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
-  if (init) {  // raw intensities: exact hi/lo words
-    k_lattice_bp<true><<<grid, kThreads, tile_words * 16 + r_bytes, st>>>(a, tile_words, kap, e, p, w, 1, AC);
+  if (init) {  // init (raw intensities) / rigidity pass: exact hi/lo words
+    k_lattice_bp<true><<<grid, kThreads, tile_words * 16 + r_bytes, st>>>(a, tile_words, kap, e, p, w, init, AC);
   } else {
     k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, kap, e, p, w, 0, AC);
   }

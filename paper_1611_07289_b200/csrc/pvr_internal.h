@@ -110,6 +110,8 @@ void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_
 void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
                     const void* tmaps, const float* kap, const float* p, float* e,
                     double* partials);
+// init: 0 iteration (w p e / kappa, w p / kappa), 1 init pass (y / kappa, 1 / kappa),
+// 2 rigidity pass (p pbar / kappa, 1 / kappa; w carries pbar)
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         const float* kap, const float* e, const float* p, const float* w,
                         int init, float2* AC);
@@ -122,6 +124,7 @@ void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm
                   const float* kap, const float* e, float* p, float* pbar, float* w);
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2);
+void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);
 void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, int nxp, Params prm,
                       float* X);
 

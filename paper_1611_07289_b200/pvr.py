@@ -25,7 +25,7 @@ PARAM = {"delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_ob
 EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", "pvr_comm_init",
            "pvr_comm_unique_id", "pvr_add_stack", "pvr_extract_patches", "pvr_plan_shards",
            "pvr_get_shard", "pvr_get_patches", "pvr_set_transforms", "pvr_set_volume",
-           "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume",
+           "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume", "pvr_rigidity_map",
            "pvr_get_weights", "pvr_get_taps", "pvr_get_em_state", "pvr_get_stats",
            "pvr_reset_stats"]
 
@@ -91,6 +91,7 @@ def lib():
             "pvr_set_param": (i32, [vp, i32, d]),
             "pvr_sr_iterate": (i32, [vp, i32, f, f]),
             "pvr_get_volume": (i32, [vp, vp, C.c_size_t]),
+            "pvr_rigidity_map": (i32, [vp, vp, C.c_size_t]),
             "pvr_get_weights": (i32, [vp, vp, vp, vp]),
             "pvr_get_taps": (i32, [vp, vp, vp, vp, vp]),
             "pvr_get_em_state": (i32, [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i64),
@@ -216,6 +217,11 @@ def pvr_get_volume(ctx, out):
     return out
 
 
+def pvr_rigidity_map(ctx, out):
+    _check(ctx, lib().pvr_rigidity_map(ctx, _ptr(out), int(np.prod(out.shape))))
+    return out
+
+
 def pvr_get_weights(ctx, pixel_p=None, patch_w=None, patch_pbar=None):
     _check(ctx, lib().pvr_get_weights(ctx, _ptr(pixel_p), _ptr(patch_w), _ptr(patch_pbar)))
 
@@ -295,6 +301,11 @@ class Context:
     def volume(self, out=None):
         out = np.zeros(self.dims[::-1], np.float32) if out is None else out
         return pvr_get_volume(self.h, out)
+
+    def rigidity_map(self, out=None):
+        """W^T(p pbar) / W^T 1 (f2; float32 [nz][ny][nx], host or device out)."""
+        out = np.zeros(self.dims[::-1], np.float32) if out is None else out
+        return pvr_rigidity_map(self.h, out)
 
     def weights(self):
         p = np.zeros(self.nloc_pix, np.float32)

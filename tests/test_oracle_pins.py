@@ -453,3 +453,80 @@ def test_zero_weights_leave_volume_unchanged():
     X0 = orc.volume()
     orc.sr_iterate(1, 1.0, 0.02)
     assert np.array_equal(orc.volume(), X0)
+
+
+# ------------------------------------------------- f2 rigidity map (reading Q28)
+@pytest.fixture(scope="module")
+def c1_oracle():
+    import helpers
+    prob = synth.make_problem("c1")
+    return prob, helpers.make_oracle(prob)
+
+
+def test_rigidity_map_all_posteriors_one_is_one_on_observed_voxels(c1_oracle):
+    """SPEC rigidity_map example 'all posteriors 1 -> map = 1 on observed voxels': right after
+    set_transforms p = pbar = 1, so W^T(p pbar) = W^T 1 and the ratio is exactly 1 wherever
+    W^T 1 > tau_C (0 elsewhere)."""
+    _, orc = c1_oracle
+    orc.set_weights(np.ones(orc.P), np.ones(orc.M))
+    R = orc.rigidity_map()
+    on = R != 0.0
+    assert on.mean() > 0.5                      # c1: most of the grid is observed
+    assert np.abs(R[on] - 1.0).max() <= 1e-12
+
+
+def test_rigidity_map_zero_and_uniform_posteriors(c1_oracle):
+    """SPEC example 'all posteriors 0 -> map = 0'; and p = 0.3 everywhere, pbar = sqrt(mean
+    p^2) = 0.3 (Eq. P:206) gives the closed form p pbar = 0.09 on every observed voxel."""
+    _, orc = c1_oracle
+    orc.set_weights(np.zeros(orc.P), np.zeros(orc.M))
+    assert np.abs(orc.rigidity_map()).max() == 0.0
+    orc.set_weights(np.full(orc.P, 0.3), np.full(orc.M, 0.3))
+    R = orc.rigidity_map()
+    on = R != 0.0
+    assert on.mean() > 0.5 and np.abs(R[on] - 0.09).max() <= 1e-12
+
+
+def test_rigidity_map_single_contributor_patch_scaling(c1_oracle):
+    """Linearity in pbar: scaling one patch's pbar by k scales its numerator share; a voxel
+    seen by that patch alone takes p pbar of that patch (weighted mean of one term)."""
+    _, orc = c1_oracle
+    rng = np.random.default_rng(7)
+    p = rng.uniform(0.2, 1.0, orc.P)
+    pb = rng.uniform(0.2, 1.0, orc.M)
+    orc.set_weights(p, pb)
+    R1 = orc.rigidity_map()
+    orc.set_weights(p, 2.0 * pb)
+    R2 = orc.rigidity_map()
+    on = R1 != 0.0
+    assert np.abs(R2[on] - 2.0 * R1[on]).max() <= 1e-12 * max(1.0, np.abs(R2).max())
+    assert (R1 >= 0).all() and (R1 <= 1.0 + 1e-12).all()
+
+
+def test_rigidity_map_marks_corrupted_patches():
+    """SPEC rigidity_map example (region-mean comparison): in a c4-structured problem with 10%
+    gross transform errors, after EM the map is lower where corrupted patches dominate the
+    coverage than where only consistent patches contribute (pbar of corrupted patches ~0.55
+    vs ~0.98 here)."""
+    import helpers
+    prob = synth.make_problem("c4", scale=(48, 48, 12), size=16, stride=8)
+    orc = helpers.make_oracle(prob)
+    orc.init_volume()
+    orc.sr_iterate(2, prob["alpha"], prob["lam"])
+    R = orc.rigidity_map().ravel()
+    assert (R >= 0).all() and (R <= 1.0 + 1e-12).all()
+    bad = np.asarray(prob["corrupted"], bool)
+    assert bad.any() and not bad.all()
+    pix0 = np.concatenate([[0], np.cumsum([np.prod(p[4:7]) for p in orc.patches()])]).astype(np.int64)
+    ind = np.zeros(orc.P)
+    for s in np.flatnonzero(bad):
+        ind[pix0[s]:pix0[s + 1]] = 1.0
+    den_bad = orc.adjoint(ind).ravel()
+    den_all = orc.adjoint(np.ones(orc.P)).ravel()
+    obs = den_all > 1e-3
+    # corrupted patches are 10% of an overlapping set: voxels where they carry > 15% of the
+    # coverage vs voxels they never reach
+    B = obs & (den_bad > 0.15 * den_all)
+    G = obs & (den_bad == 0.0)
+    assert B.sum() > 10 and G.sum() > 10
+    assert R[B].mean() < R[G].mean() - 0.03
