@@ -295,6 +295,22 @@ def run_ours(args):
     e2e = {"value": samples / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": int(T_host.numel() * 8), "d2h_bytes_per_step": int(X_host.numel() * 4),
            "calls": "pvr_set_transforms(host T) + pvr_sr_iterate(1) + pvr_get_volume(host X)"}
+
+    # ---- f2 rigidity map: one pvr_rigidity_map call into a device buffer,
+    # timed on the library's stream (one exact hi/lo backprojection + ratio + copy)
+    R_dev = torch.empty(prob["dims"][::-1], dtype=torch.float32, device="cuda")
+    ctx.rigidity_map(R_dev)  # builds the init plan once
+    r0 = torch.cuda.Event(enable_timing=True)
+    r1 = torch.cuda.Event(enable_timing=True)
+    reps = 3
+    r0.record(stream)
+    for _ in range(reps):
+        ctx.rigidity_map(R_dev)
+    r1.record(stream)
+    r1.synchronize()
+    rig_ms = r0.elapsed_time(r1) / reps
+    rigidity = {"ms_per_map": rig_ms, "psf_samples_per_s": samples / (rig_ms * 1e-3),
+                "call": "pvr_rigidity_map(device out) after the timed iterations"}
     ctx.close()
 
     line = None
@@ -312,7 +328,8 @@ def run_ours(args):
                     "psf_samples_per_iteration": samples, "parallelism": f"patch-shard x{ws}"}),
                 "roofline": roof, "iteration_hbm_frac_alg": hbm_iter / pk["hbm_gbs"],
                 "kernels": breakdown, "clocks": clk.summary(), "e2e": e2e,
-                "gpu_launches": int(st["kernel_launches"]), "cpu_baseline": cpu}
+                "gpu_launches": int(st["kernel_launches"]), "cpu_baseline": cpu,
+                "extras": {"f2_rigidity_map": rigidity}}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -105,3 +105,23 @@ def test_c3_init_is_a_weighted_mean(c3):
     y = patch_pixels_y(c3, pts)[kap >= 0.5]
     assert X.min() >= y.min() - 1e-3 * abs(y.min()) - 1e-3
     assert X.max() <= y.max() * (1 + 1e-6) + 1e-3
+
+
+def test_c3_rigidity_map_closed_forms(c3):
+    """f2 at full size, in the launch configuration of bench.py's extras: right after
+    set_transforms (p = pbar = 1) the map is exactly 1 on every observed voxel (SPEC 'all
+    posteriors 1'); after iterations it stays a weighted mean of p pbar in [0, 1]."""
+    ctx = make_gpu(c3)
+    try:
+        R = ctx.rigidity_map()
+        on = R != 0
+        assert on.mean() > 0.3
+        assert np.abs(R[on] - 1.0).max() <= 1e-5
+        ctx.init_volume()
+        ctx.sr_iterate(1, c3["alpha"], c3["lam"])
+        R = ctx.rigidity_map()
+        assert (R >= 0).all() and (R <= 1.0 + 1e-5).all()
+        _, pb, _ = ctx.weights()
+        assert R[R != 0].mean() <= 1.0 and R[R != 0].mean() >= 0.5 * pb.mean() ** 2
+    finally:
+        ctx.close()
