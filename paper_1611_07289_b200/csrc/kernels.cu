@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
       x0 = X0[((size_t)l * n.y + j) * nxp + i];
       const float2 ac = AC[((size_t)l * n.y + j) * nxp + i];
       if (ac.y > prm.tau_C) {
-        float x = x0 + alpha * ac.x / ac.y;   // a6: X1 = clip(X0 + alpha A / C)
+        float x = x0 + alpha * __fdividef(ac.x, ac.y);  // a6: X1 = clip(X0 + alpha A / C)
         if (prm.clamp) x = fminf(fmaxf(x, lo), hi);
         x1 = x;
       }
@@ -162,7 +162,10 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
     s1[hz][hy][hx] = x1;
   }
   __syncthreads();
-  const float inv_delta = 1.0f / prm.delta, al = alpha * lambda;
+  const float al = alpha * lambda;
+  // b_d = phi / sqrt(1 + phi g^2), g = dX0 / delta  ==  rsqrt(1/phi^2 + (1/phi) g^2): one
+  // FFMA + MUFU per neighbour with g in units of delta; two neighbours per packed pair
+  const float id = 1.0f / prm.delta;
   for (int t = threadIdx.x; t < kUX * kUY * kUZ; t += blockDim.x) {
     const int tx = t % kUX, ty = (t / kUX) % kUY, tz = t / (kUX * kUY);
     const int i = bx + 1 + tx, j = by + 1 + ty, l = bz + 1 + tz;
@@ -175,7 +178,11 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
     } else {
       // a7 (reading Q17): sum over the 26 neighbours d of b_d (X1_{k+d} - X1_k),
       // b_d = phi_d / sqrt(1 + phi_d ((X0_{k+d} - X0_k) / delta)^2), phi_d = 1/|d|_1
-      float sum = 0.0f;
+      f2 sum2 = pk(0.0f, 0.0f);
+      const f2 X0p = pk(x0, x0), X1p = pk(x1, x1), idp = pk(id, id);
+      float pend_x0 = 0.0f, pend_x1 = 0.0f;
+      int pend_w = 0;
+      bool have = false;
 #pragma unroll
       for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
@@ -183,13 +190,23 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
 #pragma unroll
           for (int dx = -1; dx <= 1; ++dx) {
             if (!dx && !dy && !dz) continue;
-            const float phi = 1.0f / (float)((dx != 0) + (dy != 0) + (dz != 0));
-            const float xn1 = s1[hz + dz][hy + dy][hx + dx];
-            if (xn1 != xn1) continue;  // neighbour uncovered or off-grid
-            const float g = (s0[hz + dz][hy + dy][hx + dx] - x0) * inv_delta;
-            sum += phi * rsqrtf(1.0f + phi * g * g) * (xn1 - x1);
+            const int w = (dx != 0) + (dy != 0) + (dz != 0);  // |d|_1 = 1 / phi
+            const float xn0 = s0[hz + dz][hy + dy][hx + dx], xn1 = s1[hz + dz][hy + dy][hx + dx];
+            if (!have) {
+              pend_x0 = xn0; pend_x1 = xn1; pend_w = w; have = true;
+              continue;
+            }
+            // the pair (pending neighbour, this neighbour)
+            const f2 g = mul2(sub2(pk(pend_x0, xn0), X0p), idp);
+            const f2 c = pk((float)pend_w, (float)w), a = pk((float)(pend_w * pend_w), (float)(w * w));
+            const f2 q = fma2(mul2(c, g), g, a);  // 1/phi^2 + (1/phi) g^2
+            const f2 dv = sub2(pk(pend_x1, xn1), X1p);
+            const float d0 = lo2(dv) == lo2(dv) ? lo2(dv) : 0.0f;  // neighbour uncovered / off-grid
+            const float d1 = hi2(dv) == hi2(dv) ? hi2(dv) : 0.0f;
+            sum2 = fma2(pk(rsqrtf(lo2(q)), rsqrtf(hi2(q))), pk(d0, d1), sum2);
+            have = false;
           }
-      out = x1 + al * sum;
+      out = x1 + al * (lo2(sum2) + hi2(sum2));
     }
     X2[((size_t)l * n.y + j) * nxp + i] = out;
   }
