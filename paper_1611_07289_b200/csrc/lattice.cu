@@ -331,27 +331,6 @@ struct Tile {  // planar int32 accumulators of the group bbox: A, C (+ lo words 
   int dx, dy;
 };
 
-// Add one (A, C) term to tile cell idx. HILO: exact hi/lo words (init pass: raw intensities,
-// the widest dynamic range); otherwise one int32 word per quantity, round-to-nearest on the
-// group's 2^-21 grid (iterations: residual-weighted terms; bounded dynamic range).
-// Term (a w, c w) for corner weight w: one FFMA per quantity forms round(a w) in the magic's
-// mantissa (|a w| < 2^22).
-template <bool HILO>
-__device__ __forceinline__ void tile_add(const Tile& T, int idx, float a, float c, float w) {
-  if (HILO) {
-    int h, l;
-    split_hilo(a * w, h, l);
-    atomicAdd(T.ah + idx, h);
-    atomicAdd(T.al + idx, l);
-    split_hilo(c * w, h, l);
-    atomicAdd(T.ch + idx, h);
-    atomicAdd(T.cl + idx, l);
-  } else {
-    atomicAdd(T.ah + idx, __float_as_int(__fmaf_rn(a, w, kMagic)) - kMagicBits);
-    atomicAdd(T.ch + idx, __float_as_int(__fmaf_rn(c, w, kMagic)) - kMagicBits);
-  }
-}
-
 // Per-member constants of the backprojection, in the member's window frame: axis 0 (m) is
 // the dominant component of the sample step dir * Qc (so plane floors never decrease along a
 // line), axes 1, 2 (p, q) the transverse ones. Built by warp 0 once per group.
@@ -379,51 +358,45 @@ __device__ __forceinline__ int pick3i(const int (&v)[3], int ax) {
   return ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]);
 }
 
-// Splat one lattice line into the tile with exact hi/lo words (init pass): 8 trilinear
-// corners per sample, each (A, C) term split into exact hi/lo int32 words.
-__device__ __forceinline__ void splat_line_hilo(const Tile& T, const float* s_tp, const BpMember& M,
-                                                float rm, float rp, float rq, float LA, float LC) {
-  const int s0 = M.s[0], s1 = M.s[1], s2 = M.s[2];
-  int ti = M.ti0;
-  for (int k = 0; k < M.ns; ++k) {
-    const float t = s_tp[ti];
-    float f0, f1, f2_;
-    const int i0 = mfloor(rm, f0) + M.o[0];
-    const int i1 = mfloor(rp, f1) + M.o[1];
-    const int i2 = mfloor(rq, f2_) + M.o[2];
-    const float fm = rm - f0, fp = rp - f1, fq = rq - f2_;
-    const float vA = LA * t, vC = LC * t;
-    const int k0 = i0 * s0 + i1 * s1 + i2 * s2;
-    const float w00 = (1.0f - fp) * (1.0f - fq), w10 = fp * (1.0f - fq);
-    const float w01 = (1.0f - fp) * fq, w11 = fp * fq;
-    const float a0 = vA * (1.0f - fm), a1 = vA * fm, g0 = vC * (1.0f - fm), g1 = vC * fm;
-    tile_add<true>(T, k0, a0, g0, w00);
-    tile_add<true>(T, k0 + s0, a1, g1, w00);
-    tile_add<true>(T, k0 + s1, a0, g0, w10);
-    tile_add<true>(T, k0 + s0 + s1, a1, g1, w10);
-    tile_add<true>(T, k0 + s2, a0, g0, w01);
-    tile_add<true>(T, k0 + s0 + s2, a1, g1, w01);
-    tile_add<true>(T, k0 + s1 + s2, a0, g0, w11);
-    tile_add<true>(T, k0 + s0 + s1 + s2, a1, g1, w11);
-    rm += M.dc[0];
-    rp += M.dc[1];
-    rq += M.dc[2];
-    ti += M.dti;
+constexpr int kCOff = kBpTileBytes / 2;  // byte offset of the C plane in the iteration tile
+// init / rigidity tile (HILO): A_hi, C_hi, A_lo, C_lo planes at fixed byte offsets
+constexpr int kHQ = kInitTileBytes / 4;
+static_assert(kInitTileBytes == kBpTileBytes, "both tiles put R at the same offset");
+
+template <bool HILO>
+__device__ __forceinline__ void flush_word(unsigned a, float v, bool is_c) {
+  if (HILO) {
+    int h, l;
+    split_hilo(v, h, l);
+    if (is_c) { sred<kHQ>(a, h); sred<3 * kHQ>(a, l); }
+    else      { sred<0>(a, h);   sred<2 * kHQ>(a, l); }
+  } else {
+    const int q = __float_as_int(__fadd_rn(v, kMagic)) - kMagicBits;
+    if (is_c) sred<kCOff>(a, q);
+    else      sred<0>(a, q);
   }
 }
 
-constexpr int kCOff = kBpTileBytes / 2;  // byte offset of the C plane in the iteration tile
-
+template <bool HILO>
 __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, const f2 (&P)[4], f2 mag) {
-  const f2 t0 = add2(P[0], mag), t1 = add2(P[1], mag), t2 = add2(P[2], mag), t3 = add2(P[3], mag);
-  sred<0>(a, __float_as_int(lo2(t0)) - kMagicBits);
-  sred<kCOff>(a, __float_as_int(hi2(t0)) - kMagicBits);
-  sred<0>(a + sp4, __float_as_int(lo2(t1)) - kMagicBits);
-  sred<kCOff>(a + sp4, __float_as_int(hi2(t1)) - kMagicBits);
-  sred<0>(a + sq4, __float_as_int(lo2(t2)) - kMagicBits);
-  sred<kCOff>(a + sq4, __float_as_int(hi2(t2)) - kMagicBits);
-  sred<0>(a + sp4 + sq4, __float_as_int(lo2(t3)) - kMagicBits);
-  sred<kCOff>(a + sp4 + sq4, __float_as_int(hi2(t3)) - kMagicBits);
+  if (!HILO) {
+    const f2 t0 = add2(P[0], mag), t1 = add2(P[1], mag), t2 = add2(P[2], mag), t3 = add2(P[3], mag);
+    sred<0>(a, __float_as_int(lo2(t0)) - kMagicBits);
+    sred<kCOff>(a, __float_as_int(hi2(t0)) - kMagicBits);
+    sred<0>(a + sp4, __float_as_int(lo2(t1)) - kMagicBits);
+    sred<kCOff>(a + sp4, __float_as_int(hi2(t1)) - kMagicBits);
+    sred<0>(a + sq4, __float_as_int(lo2(t2)) - kMagicBits);
+    sred<kCOff>(a + sq4, __float_as_int(hi2(t2)) - kMagicBits);
+    sred<0>(a + sp4 + sq4, __float_as_int(lo2(t3)) - kMagicBits);
+    sred<kCOff>(a + sp4 + sq4, __float_as_int(hi2(t3)) - kMagicBits);
+  } else {
+    const unsigned ac[4] = {a, a + sp4, a + sq4, a + sp4 + sq4};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      flush_word<true>(ac[j], lo2(P[j]), false);
+      flush_word<true>(ac[j], hi2(P[j]), true);
+    }
+  }
 }
 
 // Splat one lattice line with a two-plane register window along the frame's axis 0. A sample
@@ -434,8 +407,10 @@ __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, const f2 (&
 // empty); a lane whose transverse floors changed also flushes P1 and restarts. The flush is
 // uniform across the warp (all lanes issue the same 8 shared reductions); only the rarer
 // transverse restart branches. A and C travel as packed fp32 pairs (FFMA2 / FMUL2). Window
-// sums before rounding: < 2 terms of < 2^20 units each (group scale, k_lattice_bp).
-// Tile: A words at shared address tA, C words at tA + kCOff.
+// sums before rounding: < 4 terms of < 2^20 units each (group scale, k_lattice_bp).
+// Tile: A words at shared address tA, C words at tA + kCOff; HILO (init / rigidity passes):
+// every window sum split into exact hi / lo words (A_hi, C_hi, A_lo, C_lo planes, kHQ apart).
+template <bool HILO>
 __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const BpMember& M, float rm,
                                                float rp, float rq, float LA, float LC) {
   f2 rpq = pk(rp, rq);
@@ -466,8 +441,8 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
     const bool keep = same & (im == wm);
     const bool adv = same & (im == wm + 1);
     const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-    flush4(a0, sp4, sq4, P0, mag);                   // plane wm
-    if (!keep && !adv) flush4(a0 + sm4, sp4, sq4, P1, mag);  // restart: plane wm + 1 too
+    flush4<HILO>(a0, sp4, sq4, P0, mag);                   // plane wm
+    if (!keep && !adv) flush4<HILO>(a0 + sm4, sp4, sq4, P1, mag);  // restart: plane wm + 1 too
     // shift: keep -> (0, P1); advance -> (P1, 0); restart (or a jump) -> (0, 0)
     const float m0 = adv ? 1.0f : 0.0f, m1 = keep ? 1.0f : 0.0f;
 #pragma unroll
@@ -501,8 +476,8 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
     ta += dta;
   }
   const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-  flush4(a0, sp4, sq4, P0, mag);
-  flush4(a0 + sm4, sp4, sq4, P1, mag);
+  flush4<HILO>(a0, sp4, sq4, P0, mag);
+  flush4<HILO>(a0 + sm4, sp4, sq4, P1, mag);
 }
 
 // Dynamic shared memory: HILO (init pass): 4 x tile_words int32 (A, C, A_lo, C_lo), then R;
@@ -518,8 +493,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
   extern __shared__ int4 bsm4[];
   int* base = reinterpret_cast<int*>(bsm4);
   constexpr int NW = HILO ? 4 : 2;
-  int* cbase = HILO ? base + tile_words : base + kCOff / 4;
-  float2* R = reinterpret_cast<float2*>(HILO ? base + NW * tile_words : base + kBpTileBytes / 4);
+  int* cbase = HILO ? base + kHQ / 4 : base + kCOff / 4;
+  float2* R = reinterpret_cast<float2*>(base + kBpTileBytes / 4);
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
   __shared__ float s_red[2][32];
   __shared__ float s_scale[2];
@@ -634,7 +609,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
       for (int i = threadIdx.x; i < mg.ntp; i += kThreads) s_tp[i] = a.tab[mg.tp0 + i];
       for (int i = threadIdx.x; i < nvox; i += kThreads) {
 #pragma unroll
-        for (int q = 0; q < NW; ++q) (q == 1 ? cbase : base + q * tile_words)[i] = 0;
+        for (int q = 0; q < NW; ++q) (HILO ? base + q * (kHQ / 4) : (q == 1 ? cbase : base))[i] = 0;
       }
     }
     __syncthreads();
@@ -653,8 +628,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
     __syncthreads();
     const float scA = s_scale[0], scC = s_scale[1];
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
-    const Tile T{base, cbase, HILO ? base + 2 * tile_words : nullptr,
-                 HILO ? base + 3 * tile_words : nullptr, dx, dy};
+    const Tile T{base, cbase, HILO ? base + 2 * (kHQ / 4) : nullptr,
+                 HILO ? base + 3 * (kHQ / 4) : nullptr, dx, dy};
 
     // ---- phase B: splat every owned lattice line of every member, one flattened range
     // (one tail per group); consecutive lanes take consecutive U lines of a member
@@ -696,11 +671,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         const float rm = M.r[0] + fU * M.du[0] + fV * M.dv[0];
         const float rp = M.r[1] + fU * M.du[1] + fV * M.dv[1];
         const float rq = M.r[2] + fU * M.du[2] + fV * M.dv[2];
-        if (HILO) {
-          splat_line_hilo(T, s_tp, M, rm, rp, rq, LA, LC);
-        } else {
-          splat_line_win(tA, tpA, M, rm, rp, rq, LA, LC);
-        }
+        splat_line_win<HILO>(tA, tpA, M, rm, rp, rq, LA, LC);
       }
     }
     __syncthreads();
@@ -781,7 +752,7 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
   configure();
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
   if (init) {  // init (raw intensities) / rigidity pass: exact hi/lo words
-    k_lattice_bp<true><<<grid, kThreads, tile_words * 16 + r_bytes, st>>>(a, tile_words, kap, e, p, w, init, AC);
+    k_lattice_bp<true><<<grid, kThreads, kInitTileBytes + r_bytes, st>>>(a, tile_words, kap, e, p, w, init, AC);
   } else {
     k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, kap, e, p, w, 0, AC);
   }
