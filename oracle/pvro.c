@@ -624,6 +624,167 @@ int pvro_set_weights(pvro_ctx* x, const double* p, const double* pbar) {
   return 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* f1: rigid patch-to-volume registration (reading Q29).   */
+
+double pvro_cc(int64_t n, const double* a, const double* b) {
+  if (n < 2) return NAN;
+  double ma = 0.0, mb = 0.0;
+  for (int64_t i = 0; i < n; ++i) { ma += a[i]; mb += b[i]; }
+  ma /= n;
+  mb /= n;
+  double sab = 0.0, saa = 0.0, sbb = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    sab += (a[i] - ma) * (b[i] - mb);
+    saa += (a[i] - ma) * (a[i] - ma);
+    sbb += (b[i] - mb) * (b[i] - mb);
+  }
+  if (!(saa > 0.0) || !(sbb > 0.0)) return NAN;
+  return sab / sqrt(saa * sbb);
+}
+
+/* Rotation R = Rz(rz) Ry(ry) Rx(rx), angles in degrees (row-major 3x3). */
+static void pose_rotation(const double* pose, double R[9]) {
+  const double k = M_PI / 180.0;
+  const double cx = cos(k * pose[3]), sx = sin(k * pose[3]);
+  const double cy = cos(k * pose[4]), sy = sin(k * pose[4]);
+  const double cz = cos(k * pose[5]), sz = sin(k * pose[5]);
+  const double Rx[9] = {1, 0, 0, 0, cx, -sx, 0, sx, cx};
+  const double Ry[9] = {cy, 0, sy, 0, 1, 0, -sy, 0, cy};
+  const double Rz[9] = {cz, -sz, 0, sz, cz, 0, 0, 0, 1};
+  double Ryx[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      Ryx[3 * i + j] = 0.0;
+      for (int t = 0; t < 3; ++t) Ryx[3 * i + j] += Ry[3 * i + t] * Rx[3 * t + j];
+    }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      R[3 * i + j] = 0.0;
+      for (int t = 0; t < 3; ++t) R[3 * i + j] += Rz[3 * i + t] * Ryx[3 * t + j];
+    }
+}
+
+/* World position of pixel (u, v, z) of patch s under T_s. */
+static void patch_world(const pvro_ctx* x, int64_t s, double u, double v, double z, double out[3]) {
+  const int32_t* pt = &x->patch[7 * s];
+  const ostack* st = &x->st[pt[0]];
+  const double* T = &x->T[12 * s];
+  double c[3];
+  for (int d = 0; d < 3; ++d)
+    c[d] = st->G[4 * d] * (pt[1] + u) + st->G[4 * d + 1] * (pt[2] + v) + st->G[4 * d + 2] * (pt[3] + z) +
+           st->G[4 * d + 3];
+  for (int d = 0; d < 3; ++d) out[d] = T[4 * d] * c[0] + T[4 * d + 1] * c[1] + T[4 * d + 2] * c[2] + T[4 * d + 3];
+}
+
+/* Q29: the pose acts after T_s, rotating about the transformed patch centre. */
+static void patch_centre(const pvro_ctx* x, int64_t s, double c[3]) {
+  const int32_t* pt = &x->patch[7 * s];
+  patch_world(x, s, 0.5 * (pt[4] - 1), 0.5 * (pt[5] - 1), 0.5 * (pt[6] - 1), c);
+}
+
+int pvro_compose_pose(const pvro_ctx* x, int64_t s, const double* pose, double* Tn) {
+  if (x->state < 3 || s < 0 || s >= x->M) return -1;
+  double R[9], c[3];
+  pose_rotation(pose, R);
+  patch_centre(x, s, c);
+  const double* T = &x->T[12 * s];
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) {
+      Tn[4 * i + j] = 0.0;
+      for (int t = 0; t < 3; ++t) Tn[4 * i + j] += R[3 * i + t] * T[4 * t + j];
+    }
+    double b = 0.0;
+    for (int t = 0; t < 3; ++t) b += R[3 * i + t] * (T[4 * t + 3] - c[t]);
+    Tn[4 * i + 3] = b + c[i] + pose[i];
+  }
+  return 0;
+}
+
+int pvro_patch_cc(const pvro_ctx* x, const double* Xl, int64_t s, const double* pose, int min_valid,
+                  double* cc, int64_t* nvalid) {
+  if (x->state < 3 || s < 0 || s >= x->M) return -1;
+  const int32_t* pt = &x->patch[7 * s];
+  const int64_t np = (int64_t)pt[4] * pt[5] * pt[6];
+  double* ys = (double*)malloc(np * sizeof(double));
+  double* xs = (double*)malloc(np * sizeof(double));
+  double R[9], c[3];
+  pose_rotation(pose, R);
+  patch_centre(x, s, c);
+  int64_t n = 0;
+  for (int z = 0; z < pt[6]; ++z)
+    for (int v = 0; v < pt[5]; ++v)
+      for (int u = 0; u < pt[4]; ++u) {
+        double w[3], m[3], g[3];
+        patch_world(x, s, u, v, z, w);
+        for (int i = 0; i < 3; ++i) {
+          m[i] = R[3 * i] * (w[0] - c[0]) + R[3 * i + 1] * (w[1] - c[1]) + R[3 * i + 2] * (w[2] - c[2]) + c[i] +
+                 pose[i];
+          g[i] = (m[i] - x->o[i]) / x->s;
+        }
+        int64_t idx[8];
+        double wt[8];
+        const int nc = trilinear(x, g, idx, wt);
+        double val = 0.0;
+        for (int k = 0; k < nc; ++k) val += wt[k] * Xl[idx[k]];
+        ys[n] = pixel_y(x, pt, u, v, z);
+        xs[n] = val;
+        ++n;
+      }
+  *nvalid = n;
+  *cc = n >= min_valid ? pvro_cc(n, ys, xs) : NAN;
+  free(ys);
+  free(xs);
+  return 0;
+}
+
+/* level L moves by 2^-L x (2 mm, 4 degrees) */
+
+int pvro_register(const pvro_ctx* x, int levels, int iters, int min_valid, double* T_out, int32_t* status,
+                  double* pose_out) {
+  if (x->state < 3) return -1;
+  const double* Xl = x->X;  /* Q29: levels are step sizes on the unblurred reconstruction */
+  double* pose = (double*)calloc(6 * x->M, sizeof(double));
+  for (int64_t s = 0; s < x->M; ++s) status[s] = 1;
+  for (int L = 0; L < levels; ++L) {
+    const double step_t = ldexp(2.0, -L), step_r = ldexp(4.0, -L);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t s = 0; s < x->M; ++s) {
+      if (!status[s]) continue;
+      double* p = &pose[6 * s];
+      double cur;
+      int64_t nv;
+      pvro_patch_cc(x, Xl, s, p, min_valid, &cur, &nv);
+      if (isnan(cur)) {
+        if (L == 0) status[s] = 0;  /* unregistrable: transform left unchanged */
+        continue;
+      }
+      for (int it = 0; it < iters; ++it) {
+        double best = cur, q[6], qb[6];
+        int bk = -1;
+        for (int k = 0; k < 12; ++k) {
+          memcpy(q, p, sizeof(q));
+          const double step = (k / 2) < 3 ? step_t : step_r;
+          q[k / 2] += (k % 2) ? -step : step;
+          double cc;
+          pvro_patch_cc(x, Xl, s, q, min_valid, &cc, &nv);
+          if (!isnan(cc) && cc > best) { best = cc; bk = k; memcpy(qb, q, sizeof(qb)); }
+        }
+        if (bk < 0) break;
+        memcpy(p, qb, sizeof(qb));
+        cur = best;
+      }
+    }
+  }
+  for (int64_t s = 0; s < x->M; ++s) {
+    if (status[s]) pvro_compose_pose(x, s, &pose[6 * s], &T_out[12 * s]);
+    else memcpy(&T_out[12 * s], &x->T[12 * s], 12 * sizeof(double));
+    if (pose_out) memcpy(&pose_out[6 * s], &pose[6 * s], 6 * sizeof(double));
+  }
+  free(pose);
+  return 0;
+}
+
 /* One SR iteration = SURVEY §8(c) steps 1-11, in order. */
 static int sr_step(pvro_ctx* x, double alpha, double lambda) {
   int64_t V = (int64_t)x->n[0] * x->n[1] * x->n[2];

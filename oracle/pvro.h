@@ -108,6 +108,27 @@ int pvro_init_volume(pvro_ctx*);
  * [W^T 1]_k where [W^T 1]_k > tau_C, else 0; W^T over the observed pixels of all patches with
  * the reconstruction's row normalisation 1/kappa; p, pbar of the last E-step (1 before any). */
 int pvro_rigidity_map(const pvro_ctx*, double* out);
+/* ---- f1: rigid patch-to-volume registration by cross correlation (
+ * P:185-186 "individual 2D patches are continuously rigidly registered to the current 3D
+ * reconstruction"; CC as the similarity; reading Q29). ---------------- */
+/* Pearson correlation of n pairs (two-pass); NaN if n < 2 or either side is constant. */
+double pvro_cc(int64_t n, const double* a, const double* b);
+/* CC of patch s against volume Xl under pose (tx, ty, tz [mm], rx, ry, rz [deg]) applied
+ * after the patch's transform T_s, about the transformed patch centre (Q29): over all the
+ * patch's pixels, y_j against the trilinear sample of Xl at the pixel's mapped centre
+ * (corners outside the grid dropped, i.e. zero, as in the forward model, Q6). *cc = NaN if
+ * the patch has fewer than min_valid pixels or either side is constant; *nvalid = pixels. */
+int pvro_patch_cc(const pvro_ctx*, const double* Xl, int64_t s, const double* pose, int min_valid,
+                  double* cc, int64_t* nvalid);
+/* Compose T_new = T_pose o T_s (3x4 row-major) for patch s. */
+int pvro_compose_pose(const pvro_ctx*, int64_t s, const double* pose, double* T_new);
+/* Register every patch against the current X: `levels` levels of step size 2^-L (2 mm,
+ * 4 deg), L = 0 .. levels-1, on the unblurred X, compass search of at most `iters` moves per level over
+ * the 12 coordinate moves +-step (best strict improvement, first index on ties), starting
+ * from the identity pose. T_out [M][12]: the composed transforms; status [M]: 1 registered, 0
+ * unregistrable (undefined CC at the start: transform left unchanged); pose_out [M][6]. */
+int pvro_register(const pvro_ctx*, int levels, int iters, int min_valid, double* T_out, int32_t* status,
+                  double* pose_out);
 /* Test hook: overwrite the E-step state p [P] and pbar [M] (either may be NULL). */
 int pvro_set_weights(pvro_ctx*, const double* p, const double* pbar);
 int pvro_sr_iterate(pvro_ctx*, int n, double alpha, double lambda);

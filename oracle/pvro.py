@@ -73,6 +73,11 @@ def lib():
         L.pvro_init_volume.argtypes = [vp]
         L.pvro_rigidity_map.argtypes = [vp, vp]
         L.pvro_set_weights.argtypes = [vp, vp, vp]
+        L.pvro_cc.restype = d
+        L.pvro_cc.argtypes = [i64, vp, vp]
+        L.pvro_patch_cc.argtypes = [vp, vp, i64, vp, C.c_int, vp, vp]
+        L.pvro_compose_pose.argtypes = [vp, i64, vp, vp]
+        L.pvro_register.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]
         L.pvro_sr_iterate.argtypes = [vp, C.c_int, d, d]
         L.pvro_get_weights.argtypes = [vp, vp, vp, vp]
         L.pvro_get_taps.argtypes = [vp, vp, vp, vp, vp]
@@ -92,6 +97,13 @@ def _chk(rc, what):
 
 
 # ---- scalar building blocks ----
+def cc(a, b):
+    """Pearson correlation (oracle/pvro.c pvro_cc); NaN if degenerate."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    return lib().pvro_cc(len(a), _p(a), _p(b))
+
+
 def sinc_taylor(x):
     return lib().pvro_sinc_taylor(float(x))
 
@@ -241,6 +253,29 @@ class Oracle:
         pa = None if p is None else np.ascontiguousarray(p, np.float64)
         pb = None if pbar is None else np.ascontiguousarray(pbar, np.float64)
         _chk(lib().pvro_set_weights(self.h, _p(pa), _p(pb)), "set_weights")
+
+    # ---- f1 registration (reading Q29)
+    def patch_cc(self, Xl, s, pose, min_valid=32):
+        Xl = np.ascontiguousarray(Xl, np.float64).reshape(-1)
+        pose = np.ascontiguousarray(pose, np.float64)
+        cc = np.zeros(1)
+        nv = np.zeros(1, np.int64)
+        _chk(lib().pvro_patch_cc(self.h, _p(Xl), int(s), _p(pose), int(min_valid), _p(cc), _p(nv)), "patch_cc")
+        return float(cc[0]), int(nv[0])
+
+    def compose_pose(self, s, pose):
+        out = np.zeros(12)
+        _chk(lib().pvro_compose_pose(self.h, int(s), _p(np.ascontiguousarray(pose, np.float64)), _p(out)),
+             "compose_pose")
+        return out.reshape(3, 4)
+
+    def register(self, levels=4, iters=20, min_valid=32):
+        T = np.zeros((self.M, 12))
+        st = np.zeros(self.M, np.int32)
+        poses = np.zeros((self.M, 6))
+        _chk(lib().pvro_register(self.h, int(levels), int(iters), int(min_valid), _p(T), _p(st), _p(poses)),
+             "register")
+        return T.reshape(self.M, 3, 4), st, poses
 
     def rigidity_map(self):
         """W^T(p pbar) / W^T 1 where W^T 1 > tau_C, else 0 (reading Q28)."""
