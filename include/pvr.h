@@ -174,6 +174,34 @@ pvr_status pvr_get_volume(pvr_ctx* ctx, float* out, size_t nvox);
  * by pvr_get_taps. Errors: PVR_ERR_ARG (nvox != V), PVR_ERR_STATE (before set_transforms).
  * Collective when nranks > 1. */
 pvr_status pvr_rigidity_map(pvr_ctx* ctx, float* out, size_t nvox);
+
+/* f1 rigid patch-to-volume registration ("individual 2D patches
+ * are continuously rigidly registered to the current 3D reconstruction", with cross
+ * correlation as the similarity; reading Q29 in DESIGN.md). For every patch of this
+ * rank, a rigid pose p = (tx, ty, tz [mm], rx, ry, rz [deg]) applied AFTER its current
+ * transform T_s (the last pvr_set_transforms), rotating about the transformed patch centre c:
+ *   x -> R (x - c) + c + t,  R = Rz(rz) Ry(ry) Rx(rx),
+ * maximising CC(y_s, X(p)) over all the patch's pixels, X(p)_j = trilinear sample of the
+ * current X at pixel j's mapped centre (corners outside the grid read 0). Optimiser: levels
+ * L = 0 .. levels-1 with steps 2^-L x (2 mm, 4 deg); per level at most `iters` compass moves
+ * (the 12 coordinate moves +-step are evaluated; the best strict CC improvement is taken,
+ * first index on ties; the level ends when none improves). Recommended: levels 4, iters 20.
+ * Outputs (host or device pointers, any may be NULL), written for this rank's patches only
+ * (rows first .. first + n_local - 1 of the global arrays):
+ *   T_out  double [M][12]: T_pose o T_s (row-major 3x4), = T_s when unregistrable;
+ *   status int32 [M]: 1 registered, 0 unregistrable (fewer than 32 pixels, or an undefined
+ *          CC at the start: constant patch or constant samples);
+ *   poses  float [M][6]: the pose parameters.
+ * The reconstruction state is unchanged; pass T_out to pvr_set_transforms to use it.
+ * Errors: PVR_ERR_STATE (before set_transforms), PVR_ERR_ARG (levels outside [1, 16],
+ * iters < 0, a patch over 190 KB of pixels), PVR_ERR_CUDA. Not collective. */
+pvr_status pvr_register_patches(pvr_ctx* ctx, int levels, int iters, double* T_out, int32_t* status,
+                                float* poses);
+/* The registration's similarity at given poses (tap for tests and diagnostics): cc[i] = CC
+ * of global patch patch[i] (must be on this rank) under pose poses[i][0..5] (as above);
+ * NaN when undefined. patch int64 [n], poses float [n][6], cc double [n]: host or device.
+ * Errors: PVR_ERR_STATE, PVR_ERR_ARG (n < 0, NULL arrays, a patch not on this rank). */
+pvr_status pvr_patch_cc(pvr_ctx* ctx, int64_t n, const int64_t* patch, const float* poses, double* cc);
 /* Weights of this rank's shard after the last iteration: pixel posteriors p
  * [n_local_pixels], patch weights w and patch scores pbar [n_local]; any may be NULL. */
 pvr_status pvr_get_weights(pvr_ctx* ctx, float* pixel_p, float* patch_w, float* patch_pbar);

@@ -140,6 +140,9 @@ struct pvr_ctx {
   } fplan, bplan, iplan;  // forward/coverage, backprojection, init backprojection (hi/lo)
   bool iplan_valid = false;     // the init plan is built lazily by pvr_init_volume
   std::vector<PatchGeo> geo;    // composed geometry of the local patches (last set_transforms)
+  std::vector<double> Tloc;     // the local patches' transforms (last set_transforms), [nloc][12]
+  RegPatch* regP = nullptr;     // f1: device per-patch registration geometry
+  size_t regP_cap = 0;
   std::vector<std::unique_ptr<NaturalGroups>> ngcache;  // geometry-free group lists
   std::vector<int> fbox;   // forward TMA box shapes (width, height) of the current plan
   char* tmaps = nullptr;   // device: CUtensorMap [2 X buffers][box shapes]
@@ -364,7 +367,7 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp,
-                  c->partials, c->em, c->tmaps};
+                  c->partials, c->em, c->tmaps, c->regP};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -1155,6 +1158,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   if (r != PVR_OK) return r;
   c->iplan_valid = false;
   c->geo.swap(geo);
+  c->Tloc = Th;
   tr.mark("build plans");
   r = encode_tmaps(c);
   if (r != PVR_OK) return r;
@@ -1243,6 +1247,186 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
                                 is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
+}
+
+// host src -> caller dst (host or device)
+static pvr_status host_out(pvr_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!dst || bytes == 0) return PVR_OK;
+  if (is_device_ptr(dst)) CUDA_TRY(c, cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  else memcpy(dst, src, bytes);
+  return PVR_OK;
+}
+
+// ---- f1: rigid patch-to-volume registration (registration.cu; reading Q29) ----------
+static void pose_rotation_host(const double* p, double R[9]) {
+  const double k = M_PI / 180.0;
+  const double cx = cos(k * p[3]), sx = sin(k * p[3]), cy = cos(k * p[4]), sy = sin(k * p[4]);
+  const double cz = cos(k * p[5]), sz = sin(k * p[5]);
+  const double Ryx[9] = {cy, sy * sx, sy * cx, 0.0, cx, -sx, -sy, cy * sx, cy * cx};
+  const double Rz[9] = {cz, -sz, 0.0, sz, cz, 0.0, 0.0, 0.0, 1.0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      R[3 * i + j] = Rz[3 * i] * Ryx[j] + Rz[3 * i + 1] * Ryx[3 + j] + Rz[3 * i + 2] * Ryx[6 + j];
+}
+
+// Per-patch geometry for the registration kernels (fp64, from the last set_transforms).
+static pvr_status upload_reg_patches(pvr_ctx* c, int& max_pix) {
+  std::vector<RegPatch> rp(c->nloc);
+  max_pix = 1;
+  for (int64_t s = 0; s < c->nloc; ++s) {
+    const HostPatch& hp = c->patches[c->first + s];
+    const HostStack& st = c->stacks[hp.stack];
+    const double* A = &c->Tloc[12 * s];
+    auto world = [&](double u, double v, double z, double out[3]) {
+      double w[3];
+      for (int d = 0; d < 3; ++d)
+        w[d] = st.G[4 * d] * (hp.x0 + u) + st.G[4 * d + 1] * (hp.y0 + v) + st.G[4 * d + 2] * (hp.z0 + z) + st.G[4 * d + 3];
+      for (int d = 0; d < 3; ++d) out[d] = A[4 * d] * w[0] + A[4 * d + 1] * w[1] + A[4 * d + 2] * w[2] + A[4 * d + 3];
+    };
+    RegPatch& q = rp[s];
+    memset(&q, 0, sizeof(q));
+    world(0, 0, 0, q.m0);
+    double t[3];
+    world(1, 0, 0, t);
+    for (int d = 0; d < 3; ++d) q.mu[d] = t[d] - q.m0[d];
+    world(0, 1, 0, t);
+    for (int d = 0; d < 3; ++d) q.mv[d] = t[d] - q.m0[d];
+    world(0, 0, 1, t);
+    for (int d = 0; d < 3; ++d) q.mz[d] = t[d] - q.m0[d];
+    world(0.5 * (hp.sx - 1), 0.5 * (hp.sy - 1), 0.5 * (hp.sz - 1), q.c);
+    q.y0off = st.y_off + ((int64_t)hp.z0 * st.H + hp.y0) * st.W + hp.x0;
+    q.W = st.W;
+    q.HW = st.W * st.H;
+    q.sx = hp.sx; q.sy = hp.sy; q.sz = hp.sz;
+    max_pix = std::max(max_pix, hp.sx * hp.sy * hp.sz);
+  }
+  if ((size_t)c->nloc > c->regP_cap) {
+    if (c->regP) cudaFree(c->regP);
+    c->regP = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->regP, std::max<int64_t>(c->nloc, 1) * sizeof(RegPatch)));
+    c->regP_cap = c->nloc;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->regP, rp.data(), rp.size() * sizeof(RegPatch), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if ((int64_t)max_pix * 4 > 190 * 1024) return fail(c, PVR_ERR_ARG, "patch of %d pixels too large to register", max_pix);
+  return PVR_OK;
+}
+
+static RegArgs reg_args(const pvr_ctx* c, int levels, int iters) {
+  RegArgs a;
+  memset(&a, 0, sizeof(a));
+  a.P = c->regP;
+  a.X = c->X[c->cur];
+  a.ys = c->ys;
+  a.n = c->dims;
+  a.nxp = c->nxp;
+  for (int d = 0; d < 3; ++d) a.o[d] = c->o[d];
+  a.s = c->s;
+  a.levels = levels;
+  a.iters = iters;
+  a.min_valid = 32;
+  return a;
+}
+
+pvr_status pvr_register_patches(pvr_ctx* c, int levels, int iters, double* T_out, int32_t* status, float* poses) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "register_patches needs set_transforms");
+  if (levels < 1 || levels > 16 || iters < 0) return fail(c, PVR_ERR_ARG, "levels in [1, 16], iters >= 0");
+  int max_pix = 1;
+  pvr_status r = upload_reg_patches(c, max_pix);
+  if (r != PVR_OK) return r;
+  float* dpose = nullptr;
+  int32_t* dst = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dpose, std::max<int64_t>(c->nloc, 1) * 6 * sizeof(float)));
+  cudaError_t e2 = cudaMalloc(&dst, std::max<int64_t>(c->nloc, 1) * sizeof(int32_t));
+  if (e2 != cudaSuccess) { cudaFree(dpose); return fail(c, PVR_ERR_OOM, "register buffers"); }
+  cudaMemsetAsync(dpose, 0, c->nloc * 6 * sizeof(float), c->stream);
+  launch_register(c->stream, reg_args(c, levels, iters), (int)c->nloc, max_pix, dpose, dst);
+  cudaError_t le = cudaGetLastError();
+  std::vector<float> hp(6 * c->nloc);
+  std::vector<int32_t> hs(c->nloc);
+  cudaMemcpyAsync(hp.data(), dpose, hp.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream);
+  cudaMemcpyAsync(hs.data(), dst, hs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t se = cudaStreamSynchronize(c->stream);
+  cudaFree(dpose);
+  cudaFree(dst);
+  if (le != cudaSuccess || se != cudaSuccess)
+    return fail(c, PVR_ERR_CUDA, "register kernel: %s", cudaGetErrorString(le != cudaSuccess ? le : se));
+  // T_new = T_pose o T_s in fp64 (the kernel returns the pose parameters)
+  std::vector<double> Tn(12 * c->nloc);
+  for (int64_t s = 0; s < c->nloc; ++s) {
+    const double* T = &c->Tloc[12 * s];
+    double* o = &Tn[12 * s];
+    if (!hs[s]) { memcpy(o, T, 12 * sizeof(double)); continue; }
+    double p[6], R[9], ctr[3];
+    for (int k = 0; k < 6; ++k) p[k] = hp[6 * s + k];
+    pose_rotation_host(p, R);
+    const HostPatch& h = c->patches[c->first + s];
+    const HostStack& st = c->stacks[h.stack];
+    double w[3];
+    const double uu = h.x0 + 0.5 * (h.sx - 1), vv = h.y0 + 0.5 * (h.sy - 1), zz = h.z0 + 0.5 * (h.sz - 1);
+    for (int d = 0; d < 3; ++d) w[d] = st.G[4 * d] * uu + st.G[4 * d + 1] * vv + st.G[4 * d + 2] * zz + st.G[4 * d + 3];
+    for (int d = 0; d < 3; ++d) ctr[d] = T[4 * d] * w[0] + T[4 * d + 1] * w[1] + T[4 * d + 2] * w[2] + T[4 * d + 3];
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) o[4 * i + j] = R[3 * i] * T[j] + R[3 * i + 1] * T[4 + j] + R[3 * i + 2] * T[8 + j];
+      o[4 * i + 3] = R[3 * i] * (T[3] - ctr[0]) + R[3 * i + 1] * (T[7] - ctr[1]) + R[3 * i + 2] * (T[11] - ctr[2]) +
+                     ctr[i] + p[i];
+    }
+  }
+  if (T_out) {
+    r = host_out(c, T_out + 12 * c->first, Tn.data(), Tn.size() * sizeof(double));
+    if (r != PVR_OK) return r;
+  }
+  if (status) {
+    r = host_out(c, status + c->first, hs.data(), hs.size() * sizeof(int32_t));
+    if (r != PVR_OK) return r;
+  }
+  if (poses) {
+    r = host_out(c, poses + 6 * c->first, hp.data(), hp.size() * sizeof(float));
+    if (r != PVR_OK) return r;
+  }
+  return PVR_OK;
+}
+
+pvr_status pvr_patch_cc(pvr_ctx* c, int64_t n, const int64_t* patch, const float* poses, double* cc) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "patch_cc needs set_transforms");
+  if (n < 0 || (n > 0 && (!patch || !poses || !cc))) return fail(c, PVR_ERR_ARG, "patch_cc arguments");
+  if (n == 0) return PVR_OK;
+  std::vector<int64_t> ph(n);
+  std::vector<float> qh(6 * n);
+  if (is_device_ptr(patch)) CUDA_TRY(c, cudaMemcpy(ph.data(), patch, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  else memcpy(ph.data(), patch, n * sizeof(int64_t));
+  if (is_device_ptr(poses)) CUDA_TRY(c, cudaMemcpy(qh.data(), poses, 6 * n * sizeof(float), cudaMemcpyDeviceToHost));
+  else memcpy(qh.data(), poses, 6 * n * sizeof(float));
+  std::vector<int32_t> wh(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (ph[i] < c->first || ph[i] >= c->first + c->nloc) return fail(c, PVR_ERR_ARG, "patch %lld not on this rank", (long long)ph[i]);
+    wh[i] = (int32_t)(ph[i] - c->first);
+  }
+  int max_pix = 1;
+  pvr_status r = upload_reg_patches(c, max_pix);
+  if (r != PVR_OK) return r;
+  int32_t* dw = nullptr;
+  float* dq = nullptr;
+  double* dc = nullptr;
+  cudaError_t e = cudaMalloc(&dw, n * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&dq, 6 * n * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&dc, n * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dw, wh.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dq, qh.data(), 6 * n * sizeof(float), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    launch_patch_cc(c->stream, reg_args(c, 1, 0), (int)n, max_pix, dw, dq, dc);
+    e = cudaGetLastError();
+  }
+  std::vector<double> hc(n);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), dc, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dw);
+  cudaFree(dq);
+  cudaFree(dc);
+  if (e != cudaSuccess) return fail(c, PVR_ERR_CUDA, "patch_cc: %s", cudaGetErrorString(e));
+  return host_out(c, cc, hc.data(), n * sizeof(double));
 }
 
 pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {

@@ -101,6 +101,23 @@ constexpr int kFwdTileBytes = 48 * 1024;  // forward: 4 B/voxel X tile budget
 constexpr int kFwdTBytes = 12 * 1024;     // forward: lattice values of a group's members
 constexpr int kMaxGroupMembers = 16;      // members per group (lattice.cu kMaxMembers)
 
+// f1 registration (registration.cu): per local patch, pixel (u, v, z) sits at world position
+// m0 + u mu + v mv + z mz under its current transform T_s; c = the transformed patch centre.
+struct RegPatch {
+  double m0[3], mu[3], mv[3], mz[3], c[3];
+  int64_t y0off;             // offset of pixel (0, 0, 0) in the concatenated stacks
+  int32_t W, HW, sx, sy, sz, pad;
+};
+struct RegArgs {
+  const RegPatch* P;
+  const float* X;            // current reconstruction, row pitch nxp
+  const float* ys;
+  int3 n;
+  int32_t nxp;
+  double o[3], s;            // voxel (0,0,0) world position and spacing
+  int32_t levels, iters, min_valid, pad;
+};
+
 // ---- launchers; all asynchronous on `st` ----
 // lattice.cu
 void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
@@ -115,6 +132,10 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         const float* kap, const float* e, const float* p, const float* w,
                         int init, float2* AC);
+// registration.cu (f1)
+void launch_register(cudaStream_t st, const RegArgs& a, int nloc, int max_pix, float* pose, int32_t* status);
+void launch_patch_cc(cudaStream_t st, const RegArgs& a, int n, int max_pix, const int32_t* which,
+                     const float* poses, double* out);
 // kernels.cu
 void launch_range_finish(cudaStream_t st, double s2floor, EmDev* em);
 void launch_fill(cudaStream_t st, float* x, int64_t n, float v);

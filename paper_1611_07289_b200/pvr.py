@@ -26,6 +26,7 @@ EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", 
            "pvr_comm_unique_id", "pvr_add_stack", "pvr_extract_patches", "pvr_plan_shards",
            "pvr_get_shard", "pvr_get_patches", "pvr_set_transforms", "pvr_set_volume",
            "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume", "pvr_rigidity_map",
+           "pvr_register_patches", "pvr_patch_cc",
            "pvr_get_weights", "pvr_get_taps", "pvr_get_em_state", "pvr_get_stats",
            "pvr_reset_stats"]
 
@@ -92,6 +93,8 @@ def lib():
             "pvr_sr_iterate": (i32, [vp, i32, f, f]),
             "pvr_get_volume": (i32, [vp, vp, C.c_size_t]),
             "pvr_rigidity_map": (i32, [vp, vp, C.c_size_t]),
+            "pvr_register_patches": (i32, [vp, C.c_int, C.c_int, vp, vp, vp]),
+            "pvr_patch_cc": (i32, [vp, C.c_int64, vp, vp, vp]),
             "pvr_get_weights": (i32, [vp, vp, vp, vp]),
             "pvr_get_taps": (i32, [vp, vp, vp, vp, vp]),
             "pvr_get_em_state": (i32, [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i64),
@@ -222,6 +225,15 @@ def pvr_rigidity_map(ctx, out):
     return out
 
 
+def pvr_register_patches(ctx, levels, iters, T_out=None, status=None, poses=None):
+    _check(ctx, lib().pvr_register_patches(ctx, int(levels), int(iters), _ptr(T_out), _ptr(status), _ptr(poses)))
+
+
+def pvr_patch_cc(ctx, patch, poses, cc):
+    _check(ctx, lib().pvr_patch_cc(ctx, int(len(patch)), _ptr(patch), _ptr(poses), _ptr(cc)))
+    return cc
+
+
 def pvr_get_weights(ctx, pixel_p=None, patch_w=None, patch_pbar=None):
     _check(ctx, lib().pvr_get_weights(ctx, _ptr(pixel_p), _ptr(patch_w), _ptr(patch_pbar)))
 
@@ -301,6 +313,21 @@ class Context:
     def volume(self, out=None):
         out = np.zeros(self.dims[::-1], np.float32) if out is None else out
         return pvr_get_volume(self.h, out)
+
+    def register(self, levels=4, iters=20):
+        """f1: rigid patch-to-volume registration by CC (pvr_register_patches). Returns
+        (T [M][3][4] float64, status [M] int32, poses [M][6] float32); rows of other ranks are 0."""
+        T = np.zeros((self.M, 12), np.float64)
+        st = np.zeros(self.M, np.int32)
+        poses = np.zeros((self.M, 6), np.float32)
+        pvr_register_patches(self.h, levels, iters, T, st, poses)
+        return T.reshape(self.M, 3, 4), st, poses
+
+    def patch_cc(self, patch, poses):
+        patch = np.ascontiguousarray(patch, np.int64)
+        poses = np.ascontiguousarray(poses, np.float32).reshape(-1, 6)
+        cc = np.zeros(len(patch), np.float64)
+        return pvr_patch_cc(self.h, patch, poses, cc)
 
     def rigidity_map(self, out=None):
         """W^T(p pbar) / W^T 1 (f2; float32 [nz][ny][nx], host or device out)."""
