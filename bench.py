@@ -311,6 +311,16 @@ def run_ours(args):
     rig_ms = r0.elapsed_time(r1) / reps
     rigidity = {"ms_per_map": rig_ms, "psf_samples_per_s": samples / (rig_ms * 1e-3),
                 "call": "pvr_rigidity_map(device out) after the timed iterations"}
+
+    # ---- f1 rigid patch-to-volume registration: one pvr_register_patches
+    # call (4 levels, <= 20 compass moves per level) of every patch against the current X
+    torch.cuda.synchronize()
+    t0r = time.perf_counter()
+    _, reg_st, _ = ctx.register(levels=4, iters=20)
+    reg_ms = (time.perf_counter() - t0r) * 1e3
+    registration = {"ms_per_call": reg_ms, "patches": int(ctx.M), "patches_per_s": ctx.M / (reg_ms * 1e-3),
+                    "registered": int((reg_st == 1).sum()),
+                    "call": "pvr_register_patches(levels=4, iters=20), host outputs, wall clock"}
     ctx.close()
 
     line = None
@@ -329,7 +339,7 @@ def run_ours(args):
                 "roofline": roof, "iteration_hbm_frac_alg": hbm_iter / pk["hbm_gbs"],
                 "kernels": breakdown, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(st["kernel_launches"]), "cpu_baseline": cpu,
-                "extras": {"f2_rigidity_map": rigidity}}
+                "extras": {"f2_rigidity_map": rigidity, "f1_registration": registration}}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
