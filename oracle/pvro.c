@@ -48,6 +48,7 @@ struct pvro_ctx {
   /* parameters */
   double delta, tau_patch, c0, tau_live, tau_C, tau_obs, clamp, psf_mode, s2floor, nsigma;
   double lazy;       /* test-only: set_transforms skips the coverage pass (forward_range use) */
+  double quality;    /* PSF lattice density factor q (1; 2 = f4 quality mode) */
   /* iteration state */
   double* X;         /* [V] */
   double *p, *e, *kappa, *yhat;  /* [P] */
@@ -72,9 +73,10 @@ double pvro_sinc_taylor(double x) {
   return sum;
 }
 
-static int lattice_count(double pitch, double s) {
-  /* Reading Q5: lattice step <= the HR voxel size, at least 2 steps per pitch. */
-  int n = (int)ceil(pitch / s - 1e-9);
+static int lattice_count(double pitch, double s, double q) {
+  /* Reading Q5: lattice step <= the HR voxel size / q, at least 2 steps per pitch
+   * (q = 1 default; q = 2 the f4 quality mode). */
+  int n = (int)ceil(q * pitch / s - 1e-9);
   return n < 2 ? 2 : n;
 }
 
@@ -84,8 +86,13 @@ static int lattice_count(double pitch, double s) {
  * Q5 (lattice discretisation). psi is normalised to sum 1.                     */
 int pvro_psf_table(double dx, double dy, double theta, double s, double nsigma, int cap,
                    int32_t* abc, double* psi, double* hw_out) {
-  if (!(dx > 0) || !(dy > 0) || !(theta > 0) || !(s > 0)) return -1;
-  int nu = lattice_count(dx, s), nv = lattice_count(dy, s), nw = lattice_count(theta, s);
+  return pvro_psf_table_q(dx, dy, theta, s, nsigma, 1.0, cap, abc, psi, hw_out);
+}
+
+int pvro_psf_table_q(double dx, double dy, double theta, double s, double nsigma, double q, int cap,
+                     int32_t* abc, double* psi, double* hw_out) {
+  if (!(dx > 0) || !(dy > 0) || !(theta > 0) || !(s > 0) || !(q >= 1)) return -1;
+  int nu = lattice_count(dx, s, q), nv = lattice_count(dy, s, q), nw = lattice_count(theta, s, q);
   double hu = dx / nu, hv = dy / nv, hw = theta / nw;
   double sigw = theta / (2.0 * sqrt(2.0 * log(2.0)));
   int S = 0;
@@ -246,7 +253,7 @@ pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin
   for (int d = 0; d < 3; ++d) { x->n[d] = dims[d]; x->o[d] = origin[d]; }
   x->s = spacing;
   x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-3;
-  x->tau_obs = 0.5; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0;
+  x->tau_obs = 0.5; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0; x->quality = 1.0;
   int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
   x->X = (double*)calloc(V, sizeof(double));
   x->A = (double*)calloc(V, sizeof(double));
@@ -275,6 +282,7 @@ int pvro_set_param(pvro_ctx* x, int key, double v) {
     case PVRO_SIGMA2_FLOOR: x->s2floor = v; break;
     case PVRO_PSF_NSIGMA: x->nsigma = v; break;
     case PVRO_LAZY: x->lazy = v; break;
+    case PVRO_PSF_QUALITY: x->quality = v; break;
     default: return -1;
   }
   return 0;
@@ -330,7 +338,7 @@ static int build_psf(pvro_ctx* x, ostack* st) {
     return 0;
   }
   double hw[7];
-  st->S = pvro_psf_table(dx, dy, st->theta, x->s, x->nsigma, PVRO_MAX_PSF, st->abc, st->psi, hw);
+  st->S = pvro_psf_table_q(dx, dy, st->theta, x->s, x->nsigma, x->quality, PVRO_MAX_PSF, st->abc, st->psi, hw);
   st->h[0] = hw[3]; st->h[1] = hw[4]; st->h[2] = hw[5];
   return st->S > 0 ? 0 : -1;
 }

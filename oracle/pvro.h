@@ -51,6 +51,7 @@ enum {
   PVRO_SIGMA2_FLOOR = 9, /* sigma2_min = floor * (ymax - ymin)^2 (1e-6)              */
   PVRO_PSF_NSIGMA = 10,  /* through-plane truncation in sigma_w (3)                  */
   PVRO_LAZY = 12,        /* test-only: set_transforms skips coverage (forward_range)  */
+  PVRO_PSF_QUALITY = 13, /* PSF lattice density q: n = max(2, ceil(q pitch / s)) (1)   */
 };
 
 /* ---- scalar building blocks (pinned individually by tests/test_oracle_*.py) ---- */
@@ -59,6 +60,9 @@ double pvro_sinc_taylor(double x);                       /* sin(x)/x by its Tayl
    Returns S (number of samples) or <0. hw_out (nullable) = {n_u,n_v,n_w,h_u,h_v,h_w,sigma_w}. */
 int pvro_psf_table(double dx, double dy, double theta, double s, double nsigma,
                    int cap, int32_t* abc, double* psi, double* hw_out);
+/* Same with the lattice density factor q >= 1 (SURVEY 8(f) f4 "q = 2 PSF quality mode"). */
+int pvro_psf_table_q(double dx, double dy, double theta, double s, double nsigma, double q, int cap,
+                     int32_t* abc, double* psi, double* hw_out);
 /* Square-window extraction along one axis (clamp-last reading Q22).
    Returns the number of windows, writes starts to out (cap entries). */
 int pvro_windows(int dim, int size, int stride, int cap, int32_t* out);

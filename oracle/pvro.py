@@ -14,7 +14,7 @@ _SRC = os.path.join(_HERE, "pvro.c")
 
 PARAM = {
     "delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
-    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12,
+    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12, "psf_quality": 13,
 }
 
 
@@ -41,6 +41,8 @@ def lib():
         L.pvro_sinc_taylor.argtypes = [d]
         L.pvro_psf_table.restype = C.c_int
         L.pvro_psf_table.argtypes = [d, d, d, d, d, C.c_int, vp, vp, vp]
+        L.pvro_psf_table_q.restype = C.c_int
+        L.pvro_psf_table_q.argtypes = [d, d, d, d, d, d, C.c_int, vp, vp, vp]
         L.pvro_windows.restype = C.c_int
         L.pvro_windows.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.pvro_posterior.restype = d
@@ -108,12 +110,12 @@ def sinc_taylor(x):
     return lib().pvro_sinc_taylor(float(x))
 
 
-def psf_table(dx, dy, theta, s, nsigma=3.0):
+def psf_table(dx, dy, theta, s, nsigma=3.0, q=1.0):
     cap = 20000
     abc = np.zeros((cap, 3), np.int32)
     psi = np.zeros(cap, np.float64)
     hw = np.zeros(7, np.float64)
-    S = _chk(lib().pvro_psf_table(dx, dy, theta, s, nsigma, cap, _p(abc), _p(psi), _p(hw)), "psf")
+    S = _chk(lib().pvro_psf_table_q(dx, dy, theta, s, nsigma, float(q), cap, _p(abc), _p(psi), _p(hw)), "psf")
     return abc[:S].copy(), psi[:S].copy(), hw
 
 

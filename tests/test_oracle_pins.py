@@ -139,11 +139,13 @@ def test_constant_field_rows_sum_to_one():
     assert np.abs(yhat[obs] - 437.25).max() <= 1e-10
 
 
-def test_linear_field_is_reproduced_at_pixel_centre():
+@pytest.mark.parametrize("q", [1.0, 2.0])
+def test_linear_field_is_reproduced_at_pixel_centre(q):
     """trilinear is exact for linear fields; the PSF is symmetric (zero mean offset),
-    so a fully-covered pixel sees the linear field at its transformed centre."""
+    so a fully-covered pixel sees the linear field at its transformed centre (default and the
+    f4 q = 2 lattice)."""
     prob = synth.make_problem("c2", scale=(48, 24, 4))
-    orc = _problem_oracle(prob)
+    orc = _problem_oracle(prob, {"psf_quality": q})
     nx, ny, nz = prob["dims"]
     l, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
     a, b, c, d = 0.7, -1.3, 2.1, 5.0
@@ -530,3 +532,23 @@ def test_rigidity_map_marks_corrupted_patches():
     G = obs & (den_bad == 0.0)
     assert B.sum() > 10 and G.sum() > 10
     assert R[B].mean() < R[G].mean() - 0.03
+
+
+# ------------------------------------------------------ f4 q = 2 PSF quality mode (Q5)
+@pytest.mark.parametrize("cfg,S", [("c1", 99), ("c2", 189), ("c3", 1305), ("c4", 1305), ("c5", 2829)])
+def test_psf_quality_two_lattice(cfg, S):
+    """n_u = max(2, ceil(2 pitch / s)), n_w = max(2, ceil(2 theta / s)); c3:
+    S = 45 x 29 = 1305 (SURVEY calc). The table stays normalised, positive and symmetric, and
+    q = 1 reproduces the default table exactly."""
+    c = synth.CONFIGS[cfg]
+    abc, psi, hw = O.psf_table(c["pitch"], c["pitch"], c["theta"], c["s"], q=2.0)
+    assert len(psi) == S
+    assert list(hw[:3]) == [max(2, math.ceil(2 * c["pitch"] / c["s"] - 1e-9))] * 2 + \
+        [max(2, math.ceil(2 * c["theta"] / c["s"] - 1e-9))]
+    assert abs(psi.sum() - 1.0) <= 1e-14 and (psi > 0).all()
+    table = {tuple(a): v for a, v in zip(abc.tolist(), psi)}
+    for a, v in table.items():
+        assert abs(table[(-a[0], -a[1], -a[2])] - v) <= 1e-15
+    a1, p1, h1 = O.psf_table(c["pitch"], c["pitch"], c["theta"], c["s"])
+    a2, p2, h2 = O.psf_table(c["pitch"], c["pitch"], c["theta"], c["s"], q=1.0)
+    assert np.array_equal(a1, a2) and np.array_equal(p1, p2)
