@@ -199,7 +199,7 @@ def run_ours(args):
         uid = [pvr.pvr_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.comm_init(ws, rank, uid[0])
-    load_problem(ctx, prob)
+    load_problem(ctx, prob, {"psf_quality": args.psf_quality} if args.psf_quality != 1 else None)
     ctx.init_volume()
     for _ in range(args.warmup):
         ctx.sr_iterate(1, prob["alpha"], prob["lam"])
@@ -335,7 +335,8 @@ def run_ours(args):
                 "data": "synthetic (seeded analytic phantom acquisition; synth/)",
                 "config": config_block(args.config, extra={
                     "M": int(ctx.M), "P": int(st["pixels"]) if ws == 1 else None,
-                    "psf_samples_per_iteration": samples, "parallelism": f"patch-shard x{ws}"}),
+                    "psf_samples_per_iteration": samples, "parallelism": f"patch-shard x{ws}",
+                    "psf_quality": args.psf_quality}),
                 "roofline": roof, "iteration_hbm_frac_alg": hbm_iter / pk["hbm_gbs"],
                 "kernels": breakdown, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(st["kernel_launches"]), "cpu_baseline": cpu,
@@ -357,6 +358,8 @@ def main():
                     help="slices per stack of the oracle's bounded sample")
     ap.add_argument("--one-call", action="store_true", help="time one pvr_sr_iterate(K) call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--psf-quality", type=float, default=1.0,
+                    help="f4 PSF lattice density q (2 = the q = 2 quality mode); default 1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -74,7 +74,10 @@ enum {
   PVR_PARAM_PSF_MODE = 7,     /* (extract) 0: PVR PSF; 1: delta PSF (tests only) [0]       */
   PVR_PARAM_SIGMA2_FLOOR = 9, /* sigma2 >= floor * (ymax - ymin)^2 [1e-6] (Q10)            */
   PVR_PARAM_PSF_NSIGMA = 10,  /* (extract) slice profile cut at nsigma * sigma_w [3] (Q3)  */
-  PVR_PARAM_PROFILE = 11      /* 1: time every kernel with CUDA events (pvr_get_stats) [0] */
+  PVR_PARAM_PROFILE = 11,     /* 1: time every kernel with CUDA events (pvr_get_stats) [0] */
+  PVR_PARAM_PSF_QUALITY = 12  /* (extract) PSF lattice density q in [1, 4]: n_u = max(2,
+                                 ceil(q pitch / s)), n_w = max(2, ceil(q theta / s)) (Q5);
+                                 2 = the f4 "q = 2 quality mode" [1]        */
 };
 
 /* Version string of the library build. */

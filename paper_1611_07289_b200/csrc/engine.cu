@@ -120,7 +120,7 @@ struct pvr_ctx {
   // parameters
   double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-3, tau_obs = 0.5;
   int clamp = 1, psf_mode = 0, profile = 0;
-  double s2floor = 1e-6, nsigma = 3.0;
+  double s2floor = 1e-6, nsigma = 3.0, quality = 1.0;
   // stacks / patches
   std::vector<HostStack> stacks;
   std::vector<float> psf_tab;        // separable PSF factors of all stacks
@@ -228,8 +228,8 @@ double taylor_sinc(double x) {
   return sum;
 }
 
-int psf_steps(double pitch, double s) {  // reading Q5: n = max(2, ceil(pitch / s))
-  int n = (int)std::ceil(pitch / s - 1e-9);
+int psf_steps(double pitch, double s, double q) {  // reading Q5: n = max(2, ceil(q pitch / s))
+  int n = (int)std::ceil(q * pitch / s - 1e-9);
   return std::max(2, n);
 }
 
@@ -251,7 +251,8 @@ pvr_status build_psf(pvr_ctx* c, HostStack& st) {
   }
   const double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
   const double px = norm3(c0), py = norm3(c1);
-  const int nu = psf_steps(px, c->s), nv = psf_steps(py, c->s), nw = psf_steps(st.theta, c->s);
+  const int nu = psf_steps(px, c->s, c->quality), nv = psf_steps(py, c->s, c->quality),
+            nw = psf_steps(st.theta, c->s, c->quality);
   st.h[0] = px / nu;
   st.h[1] = py / nv;
   st.h[2] = st.theta / nw;
@@ -910,7 +911,7 @@ pvr_status pvr_comm_init(pvr_ctx* c, int nranks, int rank, const void* uid) {
 
 pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
   GUARD(c);
-  const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA;
+  const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA || key == PVR_PARAM_PSF_QUALITY;
   if (extract_key && c->state >= PATCHED)
     return fail(c, PVR_ERR_STATE, "parameter %d must be set before extract_patches", key);
   switch (key) {
@@ -924,6 +925,7 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
     case PVR_PARAM_PSF_MODE: if (v != 0 && v != 1) goto bad; c->psf_mode = (int)v; break;
     case PVR_PARAM_SIGMA2_FLOOR: if (!(v >= 0)) goto bad; c->s2floor = v; break;
     case PVR_PARAM_PSF_NSIGMA: if (!(v > 0)) goto bad; c->nsigma = v; break;
+    case PVR_PARAM_PSF_QUALITY: if (!(v >= 1 && v <= 4)) goto bad; c->quality = v; break;
     case PVR_PARAM_PROFILE: c->profile = v != 0; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }

@@ -90,3 +90,12 @@ def test_oblique_stacks_small():
     """c5's oblique stacks (30 deg about x, 45 deg about y) and dense 75% overlap."""
     prob = synth.make_problem("c5", scale=(64, 64, 12), size=16, stride=4)
     run_pair(prob, 1)
+
+
+@pytest.mark.parametrize("cfg,kw,iters", [("c1", {}, 2),
+                                          ("c3", dict(scale=(96, 96, 12), size=32, stride=16), 2)])
+def test_psf_quality_two(cfg, kw, iters):
+    """f4 q = 2 PSF quality mode: denser PSF lattice (c3: S = 1305), same
+    parity bar."""
+    prob = synth.make_problem(cfg, **kw)
+    run_pair(prob, iters, params={"psf_quality": 2})
