@@ -15,7 +15,7 @@
 constexpr int WORDS = 8192;  // 32 KB tile
 constexpr int ITERS = 512;
 
-template <int MODE>  // 0 LDS, 1 ATOMS int, 2 f32 atomicAdd (CAS)
+template <int MODE>  // 0 LDS, 1 ATOMS int, 2 f32 atomicAdd (CAS), 3 ATOMS u64 (packed A|C pair)
 __global__ void k_smem(float* out, int pattern) {
   __shared__ float s[WORDS];
   for (int i = threadIdx.x; i < WORDS; i += blockDim.x) s[i] = 0.f;
@@ -31,6 +31,7 @@ __global__ void k_smem(float* out, int pattern) {
       int a = b + off + (c & 1) + ((c >> 1) & 1) * 32 + (c >> 2) * 1024;
       if (MODE == 0) acc += s[a];
       else if (MODE == 1) atomicAdd(reinterpret_cast<int*>(&s[a]), it);
+      else if (MODE == 3) atomicAdd(reinterpret_cast<unsigned long long*>(&s[2 * (a & (WORDS / 2 - 1))]), (unsigned long long)it);
       else atomicAdd(&s[a], 1.0f);
     }
   }
@@ -101,6 +102,8 @@ int main() {
       cudaEventElapsedTime(&ms, a, b); snprintf(nm, 64, "LDS gather (%s)", pn); rep(nm, ms, smem_ops);
       cudaEventRecord(a); k_smem<1><<<blocks, threads>>>(out, pat); cudaEventRecord(b); CK(cudaEventSynchronize(b));
       cudaEventElapsedTime(&ms, a, b); snprintf(nm, 64, "ATOMS.ADD int32 (%s)", pn); rep(nm, ms, smem_ops);
+      cudaEventRecord(a); k_smem<3><<<blocks, threads>>>(out, pat); cudaEventRecord(b); CK(cudaEventSynchronize(b));
+      cudaEventElapsedTime(&ms, a, b); snprintf(nm, 64, "ATOMS.ADD u64 (%s)", pn); rep(nm, ms, smem_ops);
       cudaEventRecord(a); k_smem<2><<<blocks, threads>>>(out, pat); cudaEventRecord(b); CK(cudaEventSynchronize(b));
       cudaEventElapsedTime(&ms, a, b); snprintf(nm, 64, "atomicAdd f32 smem CAS (%s)", pn); rep(nm, ms, smem_ops);
       cudaEventRecord(a); k_gred_v2<<<blocks, threads>>>(g2, (1 << 24) - 1, pat); cudaEventRecord(b); CK(cudaEventSynchronize(b));
