@@ -267,6 +267,7 @@ class Context:
         self.dims = tuple(int(d) for d in dims)
         self.h = pvr_create_volume(self.dims, spacing_mm, origin_mm, cuda_device, cuda_stream)
         self.V = int(np.prod(self.dims))
+        self.M = 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -320,7 +321,10 @@ class Context:
         T = np.zeros((self.M, 12), np.float64)
         st = np.zeros(self.M, np.int32)
         poses = np.zeros((self.M, 6), np.float32)
-        pvr_register_patches(self.h, levels, iters, T, st, poses)
+        if self.M == 0:
+            pvr_register_patches(self.h, levels, iters)
+        else:
+            pvr_register_patches(self.h, levels, iters, T, st, poses)
         return T.reshape(self.M, 3, 4), st, poses
 
     def patch_cc(self, patch, poses):

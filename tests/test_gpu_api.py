@@ -127,3 +127,23 @@ def test_set_volume_roundtrip_and_em_state(c1):
     ctx.set_transforms(c1["T"])                       # resets the EM state
     assert ctx.em_state()["t"] == 0
     ctx.close()
+
+
+def test_next_row_calls_state_and_arguments(c1):
+    """f1 / f2 calls: state machine and argument errors (include/pvr.h)."""
+    ctx = Context(c1["dims"], c1["spacing"], c1["origin"])
+    out = np.zeros(c1["dims"][::-1], np.float32)
+    assert status_of(ctx.rigidity_map, out) == pvr.PVR_ERR_STATE
+    assert status_of(ctx.register) == pvr.PVR_ERR_STATE
+    for s in c1["stacks"]:
+        ctx.add_stack(s["slices"], s["G"], s["thickness"])
+    ctx.extract_patches(16, 8)
+    ctx.set_transforms(c1["T"])
+    assert status_of(ctx.rigidity_map, np.zeros(10, np.float32)) == pvr.PVR_ERR_ARG
+    assert status_of(ctx.register, 0, 5) == pvr.PVR_ERR_ARG          # levels < 1
+    assert status_of(ctx.register, 2, -1) == pvr.PVR_ERR_ARG         # iters < 0
+    assert status_of(ctx.patch_cc, [9999], np.zeros((1, 6))) == pvr.PVR_ERR_ARG
+    T, st, poses = ctx.register(1, 0)                                 # no moves: identity
+    assert np.array_equal(T, np.asarray(c1["T"]).reshape(-1, 3, 4)) and np.abs(poses).max() == 0
+    assert len(ctx.patch_cc(np.array([], np.int64), np.zeros((0, 6)))) == 0
+    ctx.close()
