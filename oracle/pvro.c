@@ -49,6 +49,7 @@ struct pvro_ctx {
   double delta, tau_patch, c0, tau_live, tau_C, tau_obs, clamp, psf_mode, s2floor, nsigma;
   double lazy;       /* test-only: set_transforms skips the coverage pass (forward_range use) */
   double quality;    /* PSF lattice density factor q (1; 2 = f4 quality mode) */
+  double em_rounds, em_tol;  /* f4 multi-round EM (1 round; 1e-6) */
   /* iteration state */
   double* X;         /* [V] */
   double *p, *e, *kappa, *yhat;  /* [P] */
@@ -176,6 +177,49 @@ int pvro_em_round(int64_t n, const double* e, const uint8_t* live, const double*
   return degenerate;
 }
 
+double pvro_em_loglik(int64_t n, const double* e, const uint8_t* live, double sigma2, double c, double m) {
+  double ll = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (!live[j]) continue;
+    const double G = exp(-e[j] * e[j] / (2.0 * sigma2)) / sqrt(2.0 * M_PI * sigma2);
+    ll += log(c * G + (1.0 - c) * m);
+  }
+  return ll;
+}
+
+int pvro_em_rounds(int64_t n, const double* e, const uint8_t* live, const double* p_prev, int64_t t,
+                   double c0, double sigma2_min, int rounds, double tol, double* p_out,
+                   double* sigma2_out, double* c_out, double* m_out, double* ll_out) {
+  double sigma2, c, m;
+  const int degenerate = pvro_em_round(n, e, live, p_prev, t, c0, sigma2_min, p_out, &sigma2, &c, &m);
+  double ll = degenerate ? NAN : pvro_em_loglik(n, e, live, sigma2, c, m), ll_prev = NAN;
+  if (ll_out) ll_out[0] = ll;
+  int r = 1;
+  int64_t nl = 0;
+  for (int64_t j = 0; j < n; ++j) nl += live[j] != 0;
+  while (!degenerate && r < rounds && nl > 0) {
+    if (r >= 2 && ll - ll_prev < tol * fabs(ll_prev)) break;
+    double s_pe2 = 0.0, s_p = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (!live[j]) continue;
+      s_pe2 += p_out[j] * e[j] * e[j];
+      s_p += p_out[j];
+    }
+    sigma2 = s_p > 0.0 ? s_pe2 / s_p : 0.0;
+    if (sigma2 < sigma2_min) sigma2 = sigma2_min;
+    c = s_p / (double)nl;
+    for (int64_t j = 0; j < n; ++j) p_out[j] = pvro_posterior(e[j], sigma2, c, m);
+    ll_prev = ll;
+    ll = pvro_em_loglik(n, e, live, sigma2, c, m);
+    if (ll_out) ll_out[r] = ll;
+    ++r;
+  }
+  if (sigma2_out) *sigma2_out = sigma2;
+  if (c_out) *c_out = c;
+  if (m_out) *m_out = m;
+  return r;
+}
+
 /* P:207 pbar = sqrt((sum p^2) / N), N = number of (live) pixels of the patch. */
 double pvro_patch_score(int64_t n, const double* p, const uint8_t* live) {
   double s = 0.0;
@@ -254,6 +298,7 @@ pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin
   x->s = spacing;
   x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-3;
   x->tau_obs = 0.5; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0; x->quality = 1.0;
+  x->em_rounds = 1.0; x->em_tol = 1e-6;
   int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
   x->X = (double*)calloc(V, sizeof(double));
   x->A = (double*)calloc(V, sizeof(double));
@@ -283,6 +328,8 @@ int pvro_set_param(pvro_ctx* x, int key, double v) {
     case PVRO_PSF_NSIGMA: x->nsigma = v; break;
     case PVRO_LAZY: x->lazy = v; break;
     case PVRO_PSF_QUALITY: x->quality = v; break;
+    case PVRO_EM_ROUNDS: x->em_rounds = v; break;
+    case PVRO_EM_TOL: x->em_tol = v; break;
     default: return -1;
   }
   return 0;
@@ -813,7 +860,8 @@ static int sr_step(pvro_ctx* x, double alpha, double lambda) {
   }
   /* steps 5-6: M-step (p_prev = p of the previous E-step) then E-step */
   double* pnew = (double*)malloc(x->P * sizeof(double));
-  pvro_em_round(x->P, x->e, live, x->p, x->t, x->c0, x->s2min, pnew, &x->sigma2, &x->c, &x->m);
+  pvro_em_rounds(x->P, x->e, live, x->p, x->t, x->c0, x->s2min, (int)x->em_rounds, x->em_tol, pnew, &x->sigma2,
+                 &x->c, &x->m, NULL);
   for (int64_t j = 0; j < x->P; ++j) x->p[j] = (x->kappa[j] >= x->tau_obs) ? pnew[j] : 0.0;
   free(pnew);
   /* step 7: patch score and weight (reading Q13) */

@@ -52,6 +52,8 @@ enum {
   PVRO_PSF_NSIGMA = 10,  /* through-plane truncation in sigma_w (3)                  */
   PVRO_LAZY = 12,        /* test-only: set_transforms skips coverage (forward_range)  */
   PVRO_PSF_QUALITY = 13, /* PSF lattice density q: n = max(2, ceil(q pitch / s)) (1)   */
+  PVRO_EM_ROUNDS = 14,   /* EM rounds per SR iteration, f4 multi-round EM (1)          */
+  PVRO_EM_TOL = 15,      /* stop rounds when the log-likelihood gains < tol |LL| (1e-6) */
 };
 
 /* ---- scalar building blocks (pinned individually by tests/test_oracle_*.py) ---- */
@@ -74,6 +76,18 @@ double pvro_posterior(double e, double sigma2, double c, double m);
 int pvro_em_round(int64_t n, const double* e, const uint8_t* live, const double* p_prev,
                   int64_t t, double c0, double sigma2_min, double* p_out,
                   double* sigma2_out, double* c_out, double* m_out);
+/* f4 multi-round EM ("alternates (E) ... with (M) ... until
+ * log-likelihood sum log P(e | sigma, c) increases by < 1e-6 or 20 EM rounds"; reading Q30).
+ * Round 1 is pvro_em_round. Round r >= 2 (only while not degenerate, and not when round r-1
+ * gained less than tol |LL_{r-2}| over round r-2): M-step sigma^2 = max(sum p e^2 / sum p,
+ * sigma2_min), c = sum p / N over live pixels from the previous round's p (m = 1 / spread is
+ * fixed by e), E-step p = posterior on every pixel. LL_r = sum_live log(c G(e) + (1-c) m).
+ * ll_out [rounds] (may be NULL) receives LL_1 .. LL_R' ; returns R' (>= 1), the rounds run. */
+int pvro_em_rounds(int64_t n, const double* e, const uint8_t* live, const double* p_prev, int64_t t,
+                   double c0, double sigma2_min, int rounds, double tol, double* p_out,
+                   double* sigma2_out, double* c_out, double* m_out, double* ll_out);
+/* log-likelihood sum_live log(c G_sigma(e) + (1-c) m) of the mixture. */
+double pvro_em_loglik(int64_t n, const double* e, const uint8_t* live, double sigma2, double c, double m);
 /* pbar = sqrt(sum_{live} p^2 / N_live); 0 if N_live = 0. */
 double pvro_patch_score(int64_t n, const double* p, const uint8_t* live);
 /* SR update (step 9) + regulariser (step 10) on a bare grid, for the closed-form pins. */

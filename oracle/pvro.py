@@ -14,7 +14,7 @@ _SRC = os.path.join(_HERE, "pvro.c")
 
 PARAM = {
     "delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
-    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12, "psf_quality": 13,
+    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12, "psf_quality": 13, "em_rounds": 14, "em_tol": 15,
 }
 
 
@@ -49,6 +49,10 @@ def lib():
         L.pvro_posterior.argtypes = [d, d, d, d]
         L.pvro_em_round.restype = C.c_int
         L.pvro_em_round.argtypes = [i64, vp, vp, vp, i64, d, d, vp, vp, vp, vp]
+        L.pvro_em_rounds.restype = C.c_int
+        L.pvro_em_rounds.argtypes = [i64, vp, vp, vp, i64, d, d, C.c_int, d, vp, vp, vp, vp, vp]
+        L.pvro_em_loglik.restype = d
+        L.pvro_em_loglik.argtypes = [i64, vp, vp, d, d, d]
         L.pvro_patch_score.restype = d
         L.pvro_patch_score.argtypes = [i64, vp, vp]
         L.pvro_update_regularise.restype = C.c_int
@@ -138,6 +142,25 @@ def em_round(e, live, p_prev, t, c0=0.9, sigma2_min=0.0):
     deg = lib().pvro_em_round(len(e), _p(e), _p(live), _p(p_prev), int(t), c0, sigma2_min, _p(p),
                               C.byref(s2), C.byref(c), C.byref(m))
     return p, s2.value, c.value, m.value, bool(deg)
+
+
+def em_rounds(e, live, p_prev, t, rounds, tol=1e-6, c0=0.9, sigma2_min=0.0):
+    """f4 multi-round EM (reading Q30): (p, sigma2, c, m, LL per round)."""
+    e = np.ascontiguousarray(e, np.float64)
+    live = np.ascontiguousarray(live, np.uint8)
+    p_prev = np.ascontiguousarray(p_prev, np.float64)
+    p = np.zeros_like(e)
+    ll = np.zeros(max(1, rounds))
+    s2, c, m = C.c_double(), C.c_double(), C.c_double()
+    r = lib().pvro_em_rounds(len(e), _p(e), _p(live), _p(p_prev), int(t), c0, sigma2_min, int(rounds),
+                             float(tol), _p(p), C.byref(s2), C.byref(c), C.byref(m), _p(ll))
+    return p, s2.value, c.value, m.value, ll[:r].copy()
+
+
+def em_loglik(e, live, sigma2, c, m):
+    e = np.ascontiguousarray(e, np.float64)
+    live = np.ascontiguousarray(live, np.uint8)
+    return lib().pvro_em_loglik(len(e), _p(e), _p(live), float(sigma2), float(c), float(m))
 
 
 def patch_score(p, live=None):

@@ -552,3 +552,36 @@ def test_psf_quality_two_lattice(cfg, S):
     a1, p1, h1 = O.psf_table(c["pitch"], c["pitch"], c["theta"], c["s"])
     a2, p2, h2 = O.psf_table(c["pitch"], c["pitch"], c["theta"], c["s"], q=1.0)
     assert np.array_equal(a1, a2) and np.array_equal(p1, p2)
+
+
+# ------------------------------------------------------ f4 multi-round EM (Q30)
+def test_em_loglik_is_the_mixture_density():
+    """LL = sum_live log(c N(e; 0, sigma^2) + (1 - c) m) == scipy.stats.norm."""
+    from scipy.stats import norm
+    rng = np.random.default_rng(2)
+    e = rng.normal(0, 4, 500)
+    live = rng.uniform(size=500) > 0.2
+    want = np.log(0.8 * norm.pdf(e[live], 0, 3.0) + 0.2 * 0.01).sum()
+    assert abs(O.em_loglik(e, live, 9.0, 0.8, 0.01) - want) <= 1e-9 * abs(want)
+
+
+def test_em_rounds_monotone_consistent_and_spec_examples():
+    """S:420 invariant: the EM log-likelihood never decreases across rounds; S:404 example:
+    pure zero-mean Gaussian residuals -> c >= 0.95; a 90/10 Gaussian/uniform mixture recovers
+    c and sigma^2 (consistency of the mixture MLE); rounds = 1 is exactly pvro_em_round."""
+    rng = np.random.default_rng(0)
+    e = rng.normal(0, 3, 20000)
+    e[:2000] = rng.uniform(-60, 60, 2000)
+    one = np.ones(len(e))
+    p, s2, c, m, ll = O.em_rounds(e, one, one, 1, 20)
+    assert len(ll) >= 3 and (np.diff(ll) >= -1e-9 * np.abs(ll[:-1])).all()
+    assert abs(c - 0.9) <= 0.01 and abs(s2 - 9.0) <= 0.3
+    p1, s21, c1, m1, _ = O.em_round(e, one, one, 1)
+    pr, s2r, cr, mr, llr = O.em_rounds(e, one, one, 1, 1)
+    assert np.array_equal(pr, p1) and (s2r, cr, mr) == (s21, c1, m1) and len(llr) == 1
+    g = rng.normal(0, 3, 20000)
+    _, _, cg, _, _ = O.em_rounds(g, one, one, 1, 20)
+    assert cg >= 0.95
+    # degenerate (zero spread): a single round, p = 1
+    pd, _, _, _, lld = O.em_rounds(np.full(100, 2.0), np.ones(100), np.ones(100), 1, 20)
+    assert len(lld) == 1 and (pd == 1.0).all()
