@@ -75,9 +75,14 @@ enum {
   PVR_PARAM_SIGMA2_FLOOR = 9, /* sigma2 >= floor * (ymax - ymin)^2 [1e-6] (Q10)            */
   PVR_PARAM_PSF_NSIGMA = 10,  /* (extract) slice profile cut at nsigma * sigma_w [3] (Q3)  */
   PVR_PARAM_PROFILE = 11,     /* 1: time every kernel with CUDA events (pvr_get_stats) [0] */
-  PVR_PARAM_PSF_QUALITY = 12  /* (extract) PSF lattice density q in [1, 4]: n_u = max(2,
+  PVR_PARAM_PSF_QUALITY = 12, /* (extract) PSF lattice density q in [1, 4]: n_u = max(2,
                                  ceil(q pitch / s)), n_w = max(2, ceil(q theta / s)) (Q5);
                                  2 = the f4 "q = 2 quality mode" [1]        */
+  PVR_PARAM_EM_ROUNDS = 13,   /* EM rounds per SR iteration in [1, 100] (f4 multi-round EM,
+                                 S:399-402, reading Q30): rounds 2.. re-run the M- and E-step
+                                 on the iteration's residuals until the log-likelihood gain
+                                 is below tol |LL| [1]                                      */
+  PVR_PARAM_EM_TOL = 14       /* that relative tolerance [1e-6]                              */
 };
 
 /* Version string of the library build. */

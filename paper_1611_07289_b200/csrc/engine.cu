@@ -160,6 +160,9 @@ struct pvr_ctx {
   StackPsf* psf = nullptr;
   PatchDev* pdev = nullptr;
   double* partials = nullptr;
+  double* rpart = nullptr;      // f4 multi-round EM: per-patch E-step partials [nloc][3]
+  int em_rounds = 1;
+  double em_tol = 1e-6;
   EmDev* em = nullptr;
   // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of the
   // pool, drained (synchronised) only by pvr_get_stats or when the pool is large
@@ -354,6 +357,14 @@ pvr_status allreduce_stats(pvr_ctx* c) {
                     "ncclAllReduce(stats max)");
 }
 
+// f4 multi-round EM: SUM of the E-step partials {sum p e^2, sum p, LL} before each M-step.
+pvr_status allreduce_stats2(pvr_ctx* c) {
+  if (c->nranks <= 1) return PVR_OK;
+  double* s = c->em->stats2;
+  return nccl_check(c, g_nccl.AllReduce(s, s, 3, ncclFloat64, ncclSum, c->comm, c->stream),
+                    "ncclAllReduce(E-step stats)");
+}
+
 // Addon / confidence allreduce (C2): SUM over the interleaved, row-padded (A, C) volume.
 pvr_status allreduce_ac(pvr_ctx* c) {
   if (c->nranks <= 1) return PVR_OK;
@@ -368,7 +379,7 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp,
-                  c->partials, c->em, c->tmaps, c->regP};
+                  c->partials, c->em, c->tmaps, c->regP, c->rpart};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -926,6 +937,11 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
     case PVR_PARAM_SIGMA2_FLOOR: if (!(v >= 0)) goto bad; c->s2floor = v; break;
     case PVR_PARAM_PSF_NSIGMA: if (!(v > 0)) goto bad; c->nsigma = v; break;
     case PVR_PARAM_PSF_QUALITY: if (!(v >= 1 && v <= 4)) goto bad; c->quality = v; break;
+    case PVR_PARAM_EM_ROUNDS:
+      if (!(v >= 1 && v <= 100) || v != std::floor(v)) goto bad;
+      c->em_rounds = (int)v;
+      break;
+    case PVR_PARAM_EM_TOL: if (!(v >= 0)) goto bad; c->em_tol = v; break;
     case PVR_PARAM_PROFILE: c->profile = v != 0; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }
@@ -1438,6 +1454,8 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   const LatticeArgs la = lattice_args(c, c->fplan), lb = lattice_args(c, c->bplan);
   const Params prm = la.prm;
   const bool prof = c->profile != 0;
+  if (c->em_rounds > 1 && !c->rpart)
+    CUDA_TRY(c, cudaMalloc(&c->rpart, (size_t)std::max<int64_t>(c->nloc, 1) * 3 * sizeof(double)));
   cudaStream_t s = c->stream;
   for (int it = 0; it < n; ++it) {
     float* X0 = c->X[c->cur];
@@ -1455,8 +1473,21 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     launch_em_params(s, prm, c->em);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_EM1], s);
-    launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w);
+    launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w, 1,
+                 c->em_rounds > 1 ? c->rpart : nullptr);
     CHECK_LAUNCH(c);
+    // f4 multi-round EM (reading Q30): rounds 2..R re-run M and E on the same residuals until
+    // the log-likelihood gain falls below tol |LL| (decided on the device: later launches
+    // of a converged iteration are no-ops)
+    for (int round = 2; round <= c->em_rounds; ++round) {
+      launch_em_reduce3(s, c->rpart, c->nloc, c->em);
+      pvr_status r2 = allreduce_stats2(c);
+      if (r2 != PVR_OK) return r2;
+      launch_em_round(s, prm, c->em, round, c->em_tol);
+      launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w, round, c->rpart);
+      CHECK_LAUNCH(c);
+      c->st.kernel_launches += 3;
+    }
     if (prof) cudaEventRecord((*ev)[EV_EST1], s);
     CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
     launch_backproject(s, lb, c->bplan.tile_words, c->bplan.r_bytes, c->kap, c->e, c->p, c->w, 0, c->AC);

@@ -56,6 +56,22 @@ __global__ void k_em_reduce(const double* partials, int nblk, EmDev* em) {
   }
 }
 
+// E-step constants of (sigma^2, c, m): mode, logistic offset, uniform log term.
+__device__ void set_mode(EmDev* em, bool degenerate) {
+  const double sigma2 = em->sigma2, c = em->c, m = em->m;
+  if (degenerate || c >= 1.0) {
+    em->mode = 1;
+  } else if (c <= 0.0) {
+    em->mode = 2;
+  } else {
+    em->mode = 0;
+    // P:202 in logistic form: p = 1 / (1 + exp(ln(m (1-c) / c) + e^2/(2 s2) + ln(2 pi s2)/2))
+    em->logk = (float)(log(m * (1.0 - c) / c) + 0.5 * log(2.0 * M_PI * sigma2));
+    em->inv2s2 = (float)(1.0 / (2.0 * sigma2));
+    em->lnbm = (float)log((1.0 - c) * m);
+  }
+}
+
 // a3 (reading Q10): sigma^2 = max(sum p e^2 / sum p, s2min),
 // c = c0 at t = 1 else sum p / N, m = 1 / (max e - min e). Degenerate (no live pixel or
 // spread <= sqrt(s2min)): p = 1 for every observed pixel.
@@ -73,57 +89,98 @@ __global__ void k_em_params(Params prm, EmDev* em) {
   em->sigma2 = sigma2;
   em->c = c;
   em->m = m;
-  if (degenerate || c >= 1.0) {
-    em->mode = 1;
-  } else if (c <= 0.0) {
-    em->mode = 2;
-  } else {
-    em->mode = 0;
-    // P:202 in logistic form: p = 1 / (1 + exp(ln(m (1-c) / c) + e^2/(2 s2) + ln(2 pi s2)/2))
-    em->logk = (float)(log(m * (1.0 - c) / c) + 0.5 * log(2.0 * M_PI * sigma2));
-    em->inv2s2 = (float)(1.0 / (2.0 * sigma2));
+  set_mode(em, degenerate);
+  em->degenerate = degenerate;
+  em->done = degenerate;  // f4 rounds: nothing to iterate on the degenerate path
+  em->ll_prev = NAN;
+  em->rounds = 1;
+}
+
+// f4 multi-round EM, round >= 2 (reading Q30): stop when the last round gained
+// less than tol |LL| over the round before (round >= 3); else the M-step from the last
+// E-step's partials: sigma^2 = max(sum p e^2 / sum p, s2min), c = sum p / N (m fixed by e).
+__global__ void k_em_round(Params prm, EmDev* em, int round, double tol) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || em->done) return;
+  const double ll = em->stats2[2];
+  if (round >= 3 && !(ll - em->ll_prev >= tol * fabs(em->ll_prev))) {
+    em->done = 1;
+    return;
   }
+  em->ll_prev = ll;
+  const double spe2 = em->stats2[0], sp = em->stats2[1], nl = em->stats[2];
+  double sigma2 = sp > 0.0 ? spe2 / sp : 0.0;
+  if (sigma2 < em->s2min) sigma2 = em->s2min;
+  em->sigma2 = sigma2;
+  em->c = nl > 0.0 ? sp / nl : em->c;
+  set_mode(em, false);
+  em->rounds = round;
 }
 
 // --------------------------------------------------------------------------------------
 // a4: p_j (observed pixels; 0 elsewhere), pbar_s = sqrt(sum_live p^2 / N_live),
 // w_s = pbar_s if pbar_s >= tau_patch else 0 (reading Q13). One CTA per patch.
 __global__ void __launch_bounds__(256) k_estep(const PatchDev* __restrict__ P, Params prm,
-                                               const EmDev* __restrict__ em,
+                                               EmDev* __restrict__ em,
                                                const float* __restrict__ kap,
                                                const float* __restrict__ e, float* __restrict__ p,
-                                               float* __restrict__ pbar, float* __restrict__ w) {
+                                               float* __restrict__ pbar, float* __restrict__ w,
+                                               int round, double* __restrict__ rpart) {
+  if (round >= 2 && em->done) return;  // f4 rounds converged: keep the last p, pbar, w
   const PatchDev& pt = P[blockIdx.x];
   const int npix = pt.sx * pt.sy * pt.sz;
   const int mode = em->mode;
-  const float logk = em->logk, inv2s2 = em->inv2s2;
-  double s[2] = {0.0, 0.0};
+  const float logk = em->logk, inv2s2 = em->inv2s2, lnbm = em->lnbm;
+  // live-pixel sums: {sum p^2, N} for pbar, and {sum p e^2, sum p, LL} for the next M-step
+  double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   float mx[1] = {0.0f};
   for (int q = threadIdx.x; q < npix; q += blockDim.x) {
     const int64_t j = pt.pix0 + q;
     const float k = kap[j];
-    float pv = 0.0f;
+    float pv = 0.0f, ll = 0.0f;
+    const float ev = e[j];
     if (k >= prm.tau_obs) {
       if (mode == 1) {
         pv = 1.0f;
       } else if (mode == 0) {
-        const float ev = e[j];
-        pv = 1.0f / (1.0f + expf(logk + ev * ev * inv2s2));
+        const float z = logk + ev * ev * inv2s2;
+        pv = 1.0f / (1.0f + expf(z));
+        ll = lnbm + log1pf(expf(-z));  // ln(c G + (1 - c) m) = ln((1-c) m) + ln(1 + e^-z)
       }
     }
     p[j] = pv;
     if (k >= prm.tau_live) {
       s[0] += (double)pv * (double)pv;
       s[1] += 1.0;
+      s[2] += (double)pv * (double)ev * (double)ev;
+      s[3] += (double)pv;
+      s[4] += (double)ll;
     }
   }
-  __shared__ double res[3];
-  block_reduce_store<2, 1>(s, mx, res);
+  __shared__ double res[6];
+  block_reduce_store<5, 1>(s, mx, res);
   if (threadIdx.x == 0) {
     const float pb = res[1] > 0.0 ? (float)sqrt(res[0] / res[1]) : 0.0f;
     pbar[blockIdx.x] = pb;
     w[blockIdx.x] = pb >= prm.tau_patch ? pb : 0.0f;
+    if (rpart) {
+      rpart[3 * blockIdx.x] = res[2];
+      rpart[3 * blockIdx.x + 1] = res[3];
+      rpart[3 * blockIdx.x + 2] = res[4];
+    }
   }
+}
+
+// Deterministic reduction of the E-step partials into em->stats2 (one CTA).
+__global__ void k_em_reduce3(const double* __restrict__ rpart, int64_t npatch, EmDev* em) {
+  if (em->done) return;
+  double a[3] = {0.0, 0.0, 0.0};
+  for (int64_t b = threadIdx.x; b < npatch; b += blockDim.x)
+    for (int i = 0; i < 3; ++i) a[i] += rpart[3 * b + i];
+  float mx[1] = {0.0f};
+  __shared__ double res[4];
+  block_reduce_store<3, 1>(a, mx, res);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 3; ++i) em->stats2[i] = res[i];
 }
 
 // --------------------------------------------------------------------------------------
@@ -279,10 +336,19 @@ void launch_em_params(cudaStream_t st, Params prm, EmDev* em) {
   k_em_params<<<1, 32, 0, st>>>(prm, em);
 }
 
-void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, const EmDev* em,
-                  const float* kap, const float* e, float* p, float* pbar, float* w) {
+void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, EmDev* em,
+                  const float* kap, const float* e, float* p, float* pbar, float* w, int round,
+                  double* rpart) {
   if (npatch <= 0) return;
-  k_estep<<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w);
+  k_estep<<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w, round, rpart);
+}
+
+void launch_em_reduce3(cudaStream_t st, const double* rpart, int64_t npatch, EmDev* em) {
+  k_em_reduce3<<<1, 1024, 0, st>>>(rpart, npatch, em);
+}
+
+void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double tol) {
+  k_em_round<<<1, 32, 0, st>>>(prm, em, round, tol);
 }
 
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,

@@ -70,6 +70,13 @@ struct EmDev {
   int64_t t;                   // iterations since set_transforms
   double stats[5];             // reduced {sum p e^2, sum p, n_live, max e, -min e}
                                // (after coverage: {n_obs, n_live, samples_obs, max y, -min y})
+  // f4 multi-round EM (reading Q30)
+  double stats2[3];            // reduced E-step partials {sum p e^2, sum p, LL} over live pixels
+  double ll_prev;              // LL of the round before the last
+  float lnbm;                  // ln((1 - c) m): the uniform term of the log-likelihood
+  int32_t done;                // rounds converged (or degenerate): later rounds are no-ops
+  int32_t degenerate;          // round 1 took the degenerate path
+  int32_t rounds;              // E-step rounds run in the last iteration
 };
 
 struct Params {
@@ -141,8 +148,13 @@ void launch_range_finish(cudaStream_t st, double s2floor, EmDev* em);
 void launch_fill(cudaStream_t st, float* x, int64_t n, float v);
 void launch_em_reduce(cudaStream_t st, const double* partials, int nblk, EmDev* em);
 void launch_em_params(cudaStream_t st, Params prm, EmDev* em);
-void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, const EmDev* em,
-                  const float* kap, const float* e, float* p, float* pbar, float* w);
+// round 1: always runs; round >= 2: a no-op once em->done. rpart [npatch][3] (may be NULL):
+// per-patch {sum p e^2, sum p, LL} over live pixels for the next M-step.
+void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, EmDev* em,
+                  const float* kap, const float* e, float* p, float* pbar, float* w, int round,
+                  double* rpart);
+void launch_em_reduce3(cudaStream_t st, const double* rpart, int64_t npatch, EmDev* em);
+void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double tol);
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2);
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);

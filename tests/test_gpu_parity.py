@@ -99,3 +99,35 @@ def test_psf_quality_two(cfg, kw, iters):
     parity bar."""
     prob = synth.make_problem(cfg, **kw)
     run_pair(prob, iters, params={"psf_quality": 2})
+
+
+@pytest.mark.parametrize("cfg,kw,iters", [("c1", {}, 3),
+                                          ("c4", dict(scale=(96, 96, 16), size=32, stride=16), 2)])
+def test_multi_round_em(cfg, kw, iters):
+    """f4 multi-round EM (reading Q30): up to 8 M/E rounds per iteration until the
+    log-likelihood gain is below 1e-6 |LL|; same parity bar (the convergence decision is taken
+    in each side's precision; p and w agree within the bar either way)."""
+    prob = synth.make_problem(cfg, **kw)
+    run_pair(prob, iters, params={"em_rounds": 8})
+
+
+def test_multi_round_em_changes_the_estimates():
+    """The extra rounds run: sigma^2 and c after one iteration differ from the single-round
+    values and match the oracle's multi-round values."""
+    prob = synth.make_problem("c4", scale=(96, 96, 16), size=32, stride=16)
+    out = {}
+    for R in (1, 8):
+        orc = make_oracle(prob, {"em_rounds": R})
+        ctx = make_gpu(prob, {"em_rounds": R})
+        try:
+            orc.init_volume()
+            ctx.init_volume()
+            for _ in range(2):
+                orc.sr_iterate(1, prob["alpha"], prob["lam"])
+                ctx.sr_iterate(1, prob["alpha"], prob["lam"])
+            out[R] = (ctx.em_state(), orc.em_state())
+        finally:
+            ctx.close()
+    for key in ("sigma2", "c"):
+        assert abs(out[8][0][key] - out[8][1][key]) <= 1e-4 * abs(out[8][1][key])
+        assert abs(out[8][0][key] - out[1][0][key]) > 1e-3 * abs(out[1][0][key])
