@@ -161,6 +161,8 @@ struct pvr_ctx {
   PatchDev* pdev = nullptr;
   double* partials = nullptr;
   double* rpart = nullptr;      // f4 multi-round EM: per-patch E-step partials [nloc][3]
+  int* replan_buf = nullptr;    // device replan results {fwd max vox, fail, bp max vox, fail}
+  int* fbox_dev = nullptr;      // the forward box shapes (width, height) for k_replan
   int em_rounds = 1;
   double em_tol = 1e-6;
   EmDev* em = nullptr;
@@ -379,7 +381,7 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp,
-                  c->partials, c->em, c->tmaps, c->regP, c->rpart};
+                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -516,7 +518,9 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
                  PlanBuild& out) {
   const bool fwd = kind == 0;
   Trace tr;
-  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 : kInitTileBytes / 16;
+  // the iteration backprojection plans to 90% of its tile budget: the device re-plan of a
+  // later set_transforms (k_replan) accepts growth up to 100% before falling back here
+  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 * 9 / 10 : kInitTileBytes / 16;
   const int64_t nm = (int64_t)ng.mem.size();
   std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
 #pragma omp parallel for schedule(static)
@@ -646,6 +650,16 @@ pvr_status box_forward_groups(pvr_ctx* c, PlanBuild& pb) {
     }
     g.tmap = k;
   }
+  // spare shapes for the device re-plan of later set_transforms: each shape grown by 8 in x
+  // (keeps 4 x odd) and 2 in y, so a group whose footprint grew a little still finds a box
+  const size_t base = shapes.size();
+  for (size_t k = 0; k < base; ++k) {
+    const int w = shapes[k].first + 8, h = shapes[k].second + 2;
+    if (w > 256 || h > 256 || index[w * 257 + h] >= 0) continue;
+    index[w * 257 + h] = (int32_t)shapes.size();
+    shapes.emplace_back(w, h);
+  }
+  if ((int)shapes.size() > kMaxBoxShapes) shapes.resize(std::max<size_t>(base, kMaxBoxShapes));
   c->fbox.clear();
   for (auto& sh : shapes) {
     c->fbox.push_back(sh.first);
@@ -1103,6 +1117,8 @@ pvr_status pvr_get_patches(const pvr_ctx* c, int32_t* out) {
   return PVR_OK;
 }
 
+static pvr_status replan_on_device(pvr_ctx* c);
+
 pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   GUARD(c);
   if (c->state < PATCHED) return fail(c, PVR_ERR_STATE, "set_transforms needs extract_patches");
@@ -1172,7 +1188,13 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
   tr.mark("compose patches");
-  pvr_status r = build_plans(c, geo, 0, 2);  // forward + backprojection; init plan: lazily
+  pvr_status r = PVR_ERR_STATE;
+  if (c->fplan.ngroups > 0 && c->bplan.ngroups > 0) r = replan_on_device(c);
+  if (r != PVR_OK) {
+    tr.mark("device replan (failed)");
+    r = build_plans(c, geo, 0, 2);  // forward + backprojection; init plan: lazily
+    ++c->st.host_replans;
+  }
   if (r != PVR_OK) return r;
   c->iplan_valid = false;
   c->geo.swap(geo);
@@ -1264,6 +1286,37 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
                                 c->dims.x * sizeof(float), (size_t)c->dims.y * c->dims.z,
                                 is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+// set_transforms fast path: keep both plans' groups (membership, order, forward TMA boxes) and
+// recompute their boxes for the new geometry on the device (k_replan). Falls back to the host
+// planner (returns non-OK) when a forward footprint outgrew its box or a group its budget.
+static pvr_status replan_on_device(pvr_ctx* c) {
+  if (!c->replan_buf) CUDA_TRY(c, cudaMalloc(&c->replan_buf, 4 * sizeof(int)));
+  CUDA_TRY(c, cudaMemsetAsync(c->replan_buf, 0, 4 * sizeof(int), c->stream));
+  const int nshape = (int)(c->fbox.size() / 2);
+  if (nshape <= 0 || nshape > kMaxBoxShapes) return PVR_ERR_ARG;
+  if (!c->fbox_dev) CUDA_TRY(c, cudaMalloc(&c->fbox_dev, 2 * kMaxBoxShapes * sizeof(int)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->fbox_dev, c->fbox.data(), 2 * nshape * sizeof(int), cudaMemcpyHostToDevice,
+                              c->stream));
+  // forward: the planning budget + 50% (more X staged per CTA, 2-3 CTAs / SM until the next
+  // host plan); backprojection: the hard tile budget (the host planned to 90% of it)
+  launch_replan(c->stream, c->fplan.mem, c->fplan.grp, c->fplan.ngroups, c->pdev, c->psf, 1, c->dims,
+                kFwdTileBytes / 4 * 3 / 2, c->fbox_dev, nshape, c->replan_buf, c->replan_buf + 1);
+  launch_replan(c->stream, c->bplan.mem, c->bplan.grp, c->bplan.ngroups, c->pdev, c->psf, 0, c->dims,
+                kBpTileBytes / 8, nullptr, 0, c->replan_buf + 2, c->replan_buf + 3);
+  CHECK_LAUNCH(c);
+  int h[4];
+  CUDA_TRY(c, cudaMemcpyAsync(h, c->replan_buf, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (getenv("PVR_TRACE"))
+    fprintf(stderr, "[pvr] device replan: fwd max vox %d fail %d, bp max vox %d fail %d\n", h[0], h[1], h[2], h[3]);
+  if (h[1] || h[3]) return PVR_ERR_ARG;
+  c->fplan.tile_words = (h[0] + 3) & ~3;
+  c->bplan.tile_words = (h[2] + 3) & ~3;
+  c->st.fwd_smem = (int64_t)(c->fplan.t_floats + c->fplan.tile_words) * 4;
+  ++c->st.device_replans;
   return PVR_OK;
 }
 

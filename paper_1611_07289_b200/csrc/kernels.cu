@@ -312,6 +312,87 @@ __global__ void __launch_bounds__(256) k_ratio(const float2* __restrict__ AC, in
   }
 }
 
+// set_transforms fast path (engine.cu: replan_on_device): recompute every group's voxel
+// bounding box of an existing plan for the new geometry, with the host planner's rules
+// (member_bbox / size_groups in engine.cu): fp64 member boxes over the lattice range's 8
+// corners with a 1e-3 voxel margin; a forward group takes the smallest-area TMA box shape of
+// the plan (shapes: the tensor maps already encoded) that holds its new footprint (x origin
+// aligned to 4); backprojection groups get fresh odd pitches. A group without a shape or over
+// the tile budget sets *fail (the host then replans from scratch).
+__global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict__ grp, int ngroups,
+                         const PatchDev* __restrict__ P, const StackPsf* __restrict__ psf, int fwd, int3 n,
+                         int64_t vox_budget, const int* __restrict__ shapes, int nshape,
+                         int* __restrict__ maxvox, int* __restrict__ fail) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  GroupDev G = grp[g];
+  int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+  for (int i = G.m0; i < G.m0 + G.nm; ++i) {
+    const MemberDev m = mem[i];
+    const PatchDev& pt = P[m.patch];
+    const StackPsf ps = psf[pt.stack];
+    int Ulo, Uhi, Vlo, Vhi;
+    if (fwd) {
+      Ulo = ps.nu * m.u0 - ps.ru;
+      Uhi = ps.nu * (m.u0 + m.tu - 1) + ps.ru + 1;
+      Vlo = ps.nv * m.v0 - ps.rv;
+      Vhi = ps.nv * (m.v0 + m.tv - 1) + ps.rv + 1;
+    } else {
+      Ulo = ps.nu * m.u0 - ps.ru;
+      Uhi = (m.u0 + m.tu >= pt.sx) ? ps.nu * (pt.sx - 1) + ps.ru + 1 : ps.nu * (m.u0 + m.tu) - ps.ru;
+      Vlo = ps.nv * m.v0 - ps.rv;
+      Vhi = (m.v0 + m.tv >= pt.sy) ? ps.nv * (pt.sy - 1) + ps.rv + 1 : ps.nv * (m.v0 + m.tv) - ps.rv;
+    }
+    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+    for (int c8 = 0; c8 < 8; ++c8) {
+      const double U = (c8 & 1) ? Uhi - 1 : Ulo, V = (c8 & 2) ? Vhi - 1 : Vlo, C = (c8 & 4) ? m.c1 : m.c0;
+      for (int d = 0; d < 3; ++d) {
+        const double x = pt.t0d[d] + m.z * pt.Mzd[d] + U * pt.Qad[d] + V * pt.Qbd[d] + C * pt.Qcd[d];
+        mn[d] = fmin(mn[d], x);
+        mx[d] = fmax(mx[d], x);
+      }
+    }
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = min(lo[d], (int)floor(mn[d] - 1e-3));
+      hi[d] = max(hi[d], (int)floor(mx[d] + 1e-3) + 1);
+    }
+  }
+  const int nn[3] = {n.x, n.y, n.z};
+  G.interior = 1;
+  for (int d = 0; d < 3; ++d)
+    if (lo[d] < 0 || hi[d] > nn[d] - 1) G.interior = 0;
+  int64_t vox;
+  if (fwd) {
+    lo[0] -= ((lo[0] % 4) + 4) % 4;
+    const int w = hi[0] - lo[0] + 1, h = hi[1] - lo[1] + 1;
+    int best = -1, barea = 1 << 30;
+    for (int k = 0; k < nshape; ++k) {
+      const int sw = shapes[2 * k], sh = shapes[2 * k + 1];
+      if (sw >= w && sh >= h && sw * sh < barea) { barea = sw * sh; best = k; }
+    }
+    if (best < 0) {
+      atomicExch(fail, 1);
+      best = G.tmap;
+    }
+    G.tmap = best;
+    G.dim[0] = shapes[2 * best];
+    G.dim[1] = shapes[2 * best + 1];
+    for (int d = 0; d < 3; ++d) G.lo[d] = lo[d];
+    G.dim[2] = hi[2] - lo[2] + 1;
+    vox = (int64_t)((G.dim[0] * G.dim[1] + 31) & ~31) * G.dim[2];
+  } else {
+    lo[0] -= ((lo[0] % 2) + 2) % 2;
+    for (int d = 0; d < 3; ++d) G.lo[d] = lo[d];
+    G.dim[0] = (hi[0] - lo[0] + 1) | 1;
+    G.dim[1] = (hi[1] - lo[1] + 1) | 1;
+    G.dim[2] = hi[2] - lo[2] + 1;
+    vox = (int64_t)G.dim[0] * G.dim[1] * G.dim[2];
+  }
+  if (vox > vox_budget) atomicExch(fail, 1);
+  atomicMax(maxvox, (int)(vox < (1 << 30) ? vox : (1 << 30)));
+  grp[g] = G;
+}
+
 __global__ void k_fill(float* __restrict__ x, int64_t n, float v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = v;
@@ -355,6 +436,14 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2) {
   const dim3 grid((dims.x + kUX - 1) / kUX, (dims.y + kUY - 1) / kUY, (dims.z + kUZ - 1) / kUZ);
   k_update<<<grid, 256, 0, st>>>(X0, AC, dims, nxp, prm, em, alpha, lambda, X2);
+}
+
+void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, const PatchDev* P,
+                   const StackPsf* psf, int fwd, int3 n, int64_t vox_budget, const int* shapes, int nshape,
+                   int* maxvox, int* fail) {
+  if (ngroups > 0)
+    k_replan<<<(ngroups + 255) / 256, 256, 0, st>>>(mem, grp, ngroups, P, psf, fwd, n, vox_budget, shapes, nshape,
+                                                     maxvox, fail);
 }
 
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out) {

@@ -158,6 +158,10 @@ void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double t
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2);
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);
+constexpr int kMaxBoxShapes = 4096;  // forward TMA box shapes the device re-plan may pick from
+void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, const PatchDev* P,
+                   const StackPsf* psf, int fwd, int3 n, int64_t vox_budget, const int* shapes, int nshape,
+                   int* maxvox, int* fail);
 void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, int nxp, Params prm,
                       float* X);
 

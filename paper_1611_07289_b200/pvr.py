@@ -53,7 +53,8 @@ class pvr_stats(C.Structure):
                                           "bytes_alg_update")] + \
                [("fwd_tile", C.c_int32 * 3), ("bp_tile", C.c_int32 * 3)] + \
                [(n, C.c_int64) for n in ("fwd_groups", "bp_groups", "fwd_members", "bp_members",
-                                          "fwd_smem", "bp_smem")]
+                                          "fwd_smem", "bp_smem",
+                                          "device_replans", "host_replans")]
 
     def as_dict(self):
         d = {}

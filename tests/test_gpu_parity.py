@@ -131,3 +131,44 @@ def test_multi_round_em_changes_the_estimates():
     for key in ("sigma2", "c"):
         assert abs(out[8][0][key] - out[8][1][key]) <= 1e-4 * abs(out[8][1][key])
         assert abs(out[8][0][key] - out[1][0][key]) > 1e-3 * abs(out[1][0][key])
+
+
+@pytest.mark.parametrize("deg,mm,device", [(0.1, 0.1, True), (3.0, 2.0, False)])
+def test_new_transforms_replan(deg, mm, device):
+    """set_transforms with patches moved about their centres: a small registration-like
+    update (0.1 deg / 0.1 mm rms) re-plans on the device (k_replan: same groups, new boxes);
+    a large one (3 deg / 2 mm) falls back to the host planner. Either way the iterations stay
+    within the parity bar against the oracle given the same new transforms."""
+    from regprob import patch_centre_world, rigid_about
+    prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
+    orc = make_oracle(prob)
+    ctx = make_gpu(prob)
+    try:
+        rng = np.random.default_rng(9)
+        pts = ctx.patches()
+        T2 = np.asarray(prob["T"], np.float64).reshape(-1, 3, 4).copy()
+        for s in range(len(T2)):
+            a = np.radians(rng.normal(0, deg, 3))
+            cx, sx, cy, sy, cz, sz = np.cos(a[0]), np.sin(a[0]), np.cos(a[1]), np.sin(a[1]), np.cos(a[2]), np.sin(a[2])
+            R = np.array([[cz, -sz, 0], [sz, cz, 0], [0, 0, 1]]) @ np.array([[cy, 0, sy], [0, 1, 0], [-sy, 0, cy]]) @ \
+                np.array([[1, 0, 0], [0, cx, -sx], [0, sx, cx]])
+            D = rigid_about(R, patch_centre_world(prob, pts[s], T2[s]), rng.normal(0, mm, 3))
+            T2[s] = np.hstack([D[:, :3] @ T2[s][:, :3], (D[:, :3] @ T2[s][:, 3] + D[:, 3])[:, None]])
+        before = ctx.stats()
+        orc.set_transforms(T2)
+        ctx.set_transforms(T2)
+        after = ctx.stats()
+        assert after["device_replans"] == before["device_replans"] + int(device)
+        assert after["host_replans"] == before["host_replans"] + int(not device)
+        orc.init_volume()
+        ctx.init_volume()
+        for it in range(2):
+            orc.sr_iterate(1, prob["alpha"], prob["lam"])
+            ctx.sr_iterate(1, prob["alpha"], prob["lam"])
+            assert rel_l2(ctx.volume(), orc.volume()) <= 1e-4
+            po, pbo, wo = orc.weights()
+            pg, pbg, wg = ctx.weights()
+            dp, dw, _ = weight_mismatch(pg, po, pbg, pbo, wg, wo)
+            assert dp <= 1e-3 and dw <= 1e-3
+    finally:
+        ctx.close()
