@@ -50,6 +50,7 @@ struct pvro_ctx {
   double lazy;       /* test-only: set_transforms skips the coverage pass (forward_range use) */
   double quality;    /* PSF lattice density factor q (1; 2 = f4 quality mode) */
   double em_rounds, em_tol;  /* f4 multi-round EM (1 round; 1e-6) */
+  double patch_mixture;      /* f4 two-Gaussian patch classification (0) */
   /* iteration state */
   double* X;         /* [V] */
   double *p, *e, *kappa, *yhat;  /* [P] */
@@ -220,6 +221,56 @@ int pvro_em_rounds(int64_t n, const double* e, const uint8_t* live, const double
   return r;
 }
 
+static double gauss_pdf(double x, double mu, double s2) {
+  return exp(-(x - mu) * (x - mu) / (2.0 * s2)) / sqrt(2.0 * M_PI * s2);
+}
+
+int pvro_patch_mixture(int64_t M, const double* pbar, const uint8_t* valid, int rounds, double tol,
+                       double* r_out) {
+  double n = 0.0, s1 = 0.0, s2 = 0.0, mx = -INFINITY, mn = INFINITY;
+  for (int64_t s = 0; s < M; ++s) {
+    r_out[s] = 0.0;
+    if (!valid[s]) continue;
+    n += 1.0;
+    s1 += pbar[s];
+    s2 += pbar[s] * pbar[s];
+    if (pbar[s] > mx) mx = pbar[s];
+    if (pbar[s] < mn) mn = pbar[s];
+  }
+  if (n <= 0.0) return 0;
+  if (!(mx - mn > 1e-6)) {
+    for (int64_t s = 0; s < M; ++s) r_out[s] = valid[s] ? 1.0 : 0.0;
+    return 0;
+  }
+  double var = s2 / n - (s1 / n) * (s1 / n);
+  if (var < 1e-6) var = 1e-6;
+  double mu_in = mx, mu_out = mn, v_in = var, v_out = var, pi = 0.5, ll_prev = NAN;
+  int r = 0;
+  for (; r < rounds; ++r) {
+    /* E-step with the current parameters, and the log-likelihood of those parameters */
+    double sr = 0.0, srp = 0.0, srp2 = 0.0, so = 0.0, sop = 0.0, sop2 = 0.0, ll = 0.0;
+    for (int64_t s = 0; s < M; ++s) {
+      if (!valid[s]) continue;
+      const double a = pi * gauss_pdf(pbar[s], mu_in, v_in), b = (1.0 - pi) * gauss_pdf(pbar[s], mu_out, v_out);
+      const double rs = (a + b > 0.0) ? a / (a + b) : (pbar[s] >= 0.5 * (mu_in + mu_out) ? 1.0 : 0.0);
+      r_out[s] = rs;
+      ll += log(a + b > 0.0 ? a + b : 1e-300);
+      sr += rs; srp += rs * pbar[s]; srp2 += rs * pbar[s] * pbar[s];
+      so += 1.0 - rs; sop += (1.0 - rs) * pbar[s]; sop2 += (1.0 - rs) * pbar[s] * pbar[s];
+    }
+    if (r >= 1 && ll - ll_prev < tol * fabs(ll_prev)) { ++r; break; }
+    ll_prev = ll;
+    /* M-step */
+    pi = sr / n;
+    if (sr > 0.0) { mu_in = srp / sr; v_in = srp2 / sr - mu_in * mu_in; }
+    if (so > 0.0) { mu_out = sop / so; v_out = sop2 / so - mu_out * mu_out; }
+    if (v_in < 1e-6) v_in = 1e-6;
+    if (v_out < 1e-6) v_out = 1e-6;
+    if (pi <= 0.0 || pi >= 1.0) { ++r; break; }
+  }
+  return r;
+}
+
 /* P:207 pbar = sqrt((sum p^2) / N), N = number of (live) pixels of the patch. */
 double pvro_patch_score(int64_t n, const double* p, const uint8_t* live) {
   double s = 0.0;
@@ -298,7 +349,7 @@ pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin
   x->s = spacing;
   x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-3;
   x->tau_obs = 0.5; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0; x->quality = 1.0;
-  x->em_rounds = 1.0; x->em_tol = 1e-6;
+  x->em_rounds = 1.0; x->em_tol = 1e-6; x->patch_mixture = 0.0;
   int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
   x->X = (double*)calloc(V, sizeof(double));
   x->A = (double*)calloc(V, sizeof(double));
@@ -330,6 +381,7 @@ int pvro_set_param(pvro_ctx* x, int key, double v) {
     case PVRO_PSF_QUALITY: x->quality = v; break;
     case PVRO_EM_ROUNDS: x->em_rounds = v; break;
     case PVRO_EM_TOL: x->em_tol = v; break;
+    case PVRO_PATCH_MIXTURE: x->patch_mixture = v; break;
     default: return -1;
   }
   return 0;
@@ -864,12 +916,22 @@ static int sr_step(pvro_ctx* x, double alpha, double lambda) {
                  &x->c, &x->m, NULL);
   for (int64_t j = 0; j < x->P; ++j) x->p[j] = (x->kappa[j] >= x->tau_obs) ? pnew[j] : 0.0;
   free(pnew);
-  /* step 7: patch score and weight (reading Q13) */
+  /* step 7: patch score and weight (reading Q13; Q31 with the mixture) */
+  uint8_t* pvalid = (uint8_t*)malloc(x->M);
   for (int64_t s = 0; s < x->M; ++s) {
-    int64_t j0 = x->pix0[s], n = x->pix0[s + 1] - j0;
+    int64_t j0 = x->pix0[s], n = x->pix0[s + 1] - j0, nl = 0;
+    for (int64_t j = j0; j < j0 + n; ++j) nl += live[j] != 0;
     x->pbar[s] = pvro_patch_score(n, &x->p[j0], &live[j0]);
     x->wpatch[s] = x->pbar[s] >= x->tau_patch ? x->pbar[s] : 0.0;
+    pvalid[s] = nl > 0;
   }
+  if (x->patch_mixture != 0.0) {
+    double* r = (double*)malloc(x->M * sizeof(double));
+    pvro_patch_mixture(x->M, x->pbar, pvalid, 50, 1e-6, r);
+    for (int64_t s = 0; s < x->M; ++s) x->wpatch[s] = r[s] >= 0.5 ? r[s] : 0.0;
+    free(r);
+  }
+  free(pvalid);
   free(live);
   /* step 8: A = W^T (w p e), C = W^T (w p) */
   double* rA = (double*)malloc(x->P * sizeof(double));

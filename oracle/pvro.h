@@ -54,6 +54,7 @@ enum {
   PVRO_PSF_QUALITY = 13, /* PSF lattice density q: n = max(2, ceil(q pitch / s)) (1)   */
   PVRO_EM_ROUNDS = 14,   /* EM rounds per SR iteration, f4 multi-round EM (1)          */
   PVRO_EM_TOL = 15,      /* stop rounds when the log-likelihood gains < tol |LL| (1e-6) */
+  PVRO_PATCH_MIXTURE = 16, /* 1: patch weights from a two-Gaussian mixture on pbar (0)    */
 };
 
 /* ---- scalar building blocks (pinned individually by tests/test_oracle_*.py) ---- */
@@ -86,6 +87,16 @@ int pvro_em_round(int64_t n, const double* e, const uint8_t* live, const double*
 int pvro_em_rounds(int64_t n, const double* e, const uint8_t* live, const double* p_prev, int64_t t,
                    double c0, double sigma2_min, int rounds, double tol, double* p_out,
                    double* sigma2_out, double* c_out, double* m_out, double* ll_out);
+/* f4 two-Gaussian patch classification ("an inlier and outlier probability for each
+ * y_s ... exclude it ... if classified as an outlier"; reading Q31): a 1D mixture
+ * pi N(mu_in, s_in^2) + (1 - pi) N(mu_out, s_out^2) over the patch scores pbar of the valid
+ * patches (valid[s] != 0: at least one live pixel), fitted by EM from mu_in = max, mu_out = min,
+ * s_in^2 = s_out^2 = the scores' variance, pi = 1/2; rounds until the mixture log-likelihood
+ * gains < tol |LL| (at most `rounds`); variances floored at 1e-6. r_out [M]: the inlier
+ * posterior (0 for invalid patches; 1 for all valid ones when the scores are all equal to
+ * 1e-6). Returns the rounds run. */
+int pvro_patch_mixture(int64_t M, const double* pbar, const uint8_t* valid, int rounds, double tol,
+                       double* r_out);
 /* log-likelihood sum_live log(c G_sigma(e) + (1-c) m) of the mixture. */
 double pvro_em_loglik(int64_t n, const double* e, const uint8_t* live, double sigma2, double c, double m);
 /* pbar = sqrt(sum_{live} p^2 / N_live); 0 if N_live = 0. */

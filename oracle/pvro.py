@@ -14,7 +14,7 @@ _SRC = os.path.join(_HERE, "pvro.c")
 
 PARAM = {
     "delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
-    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12, "psf_quality": 13, "em_rounds": 14, "em_tol": 15,
+    "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "lazy": 12, "psf_quality": 13, "em_rounds": 14, "em_tol": 15, "patch_mixture": 16,
 }
 
 
@@ -51,6 +51,8 @@ def lib():
         L.pvro_em_round.argtypes = [i64, vp, vp, vp, i64, d, d, vp, vp, vp, vp]
         L.pvro_em_rounds.restype = C.c_int
         L.pvro_em_rounds.argtypes = [i64, vp, vp, vp, i64, d, d, C.c_int, d, vp, vp, vp, vp, vp]
+        L.pvro_patch_mixture.restype = C.c_int
+        L.pvro_patch_mixture.argtypes = [i64, vp, vp, C.c_int, d, vp]
         L.pvro_em_loglik.restype = d
         L.pvro_em_loglik.argtypes = [i64, vp, vp, d, d, d]
         L.pvro_patch_score.restype = d
@@ -155,6 +157,15 @@ def em_rounds(e, live, p_prev, t, rounds, tol=1e-6, c0=0.9, sigma2_min=0.0):
     r = lib().pvro_em_rounds(len(e), _p(e), _p(live), _p(p_prev), int(t), c0, sigma2_min, int(rounds),
                              float(tol), _p(p), C.byref(s2), C.byref(c), C.byref(m), _p(ll))
     return p, s2.value, c.value, m.value, ll[:r].copy()
+
+
+def patch_mixture(pbar, valid=None, rounds=50, tol=1e-6):
+    """f4 two-Gaussian patch classification (reading Q31): inlier posterior per patch."""
+    pbar = np.ascontiguousarray(pbar, np.float64)
+    valid = np.ones(len(pbar), np.uint8) if valid is None else np.ascontiguousarray(valid, np.uint8)
+    r = np.zeros(len(pbar))
+    n = lib().pvro_patch_mixture(len(pbar), _p(pbar), _p(valid), int(rounds), float(tol), _p(r))
+    return r, n
 
 
 def em_loglik(e, live, sigma2, c, m):

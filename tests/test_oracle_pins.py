@@ -585,3 +585,50 @@ def test_em_rounds_monotone_consistent_and_spec_examples():
     # degenerate (zero spread): a single round, p = 1
     pd, _, _, _, lld = O.em_rounds(np.full(100, 2.0), np.ones(100), np.ones(100), 1, 20)
     assert len(lld) == 1 and (pd == 1.0).all()
+
+
+# ------------------------------------------- f4 two-Gaussian patch classification (Q31)
+def test_patch_mixture_matches_sklearn_and_separates():
+    """P:209 'an inlier and outlier probability for each y_s': the two-Gaussian mixture on
+    pbar fitted by EM equals scikit-learn's GaussianMixture (library routine) started from the
+    same parameters, and separates a 90/10 mixture of good / corrupted patch scores."""
+    from sklearn.mixture import GaussianMixture
+    rng = np.random.default_rng(0)
+    pb = np.r_[rng.normal(0.95, 0.02, 900), rng.normal(0.4, 0.08, 100)].clip(0, 1)
+    r, n = O.patch_mixture(pb, rounds=500, tol=1e-12)
+    assert (r[:900] >= 0.5).mean() >= 0.99 and (r[900:] < 0.5).mean() >= 0.99
+    var = pb.var()
+    gm = GaussianMixture(2, covariance_type="full", tol=1e-12, max_iter=2000, reg_covar=0.0,
+                         weights_init=[0.5, 0.5], means_init=[[pb.max()], [pb.min()]],
+                         precisions_init=[[[1 / var]], [[1 / var]]]).fit(pb[:, None])
+    assert np.abs(gm.predict_proba(pb[:, None])[:, 0] - r).max() <= 1e-4
+
+
+def test_patch_mixture_degenerate_and_invalid():
+    """Equal scores: every valid patch is an inlier (r = 1); invalid patches (no live pixel)
+    get r = 0 and do not enter the fit."""
+    r, _ = O.patch_mixture(np.full(10, 0.8), np.r_[np.ones(8), np.zeros(2)])
+    assert (r[:8] == 1.0).all() and (r[8:] == 0.0).all()
+    rng = np.random.default_rng(1)
+    pb = np.r_[rng.normal(0.9, 0.03, 50), rng.normal(0.3, 0.05, 10), [0.99, 0.01]]
+    valid = np.r_[np.ones(60), [0, 0]]
+    r1, _ = O.patch_mixture(pb, valid)
+    r2, _ = O.patch_mixture(pb[:60])
+    assert np.array_equal(r1[:60], r2) and (r1[60:] == 0).all()
+
+
+def test_patch_mixture_excludes_corrupted_patches():
+    """S:401 example (10% of patches under gross transform errors, c4 structure, two SR
+    iterations): the mixture labels most corrupted patches outliers (w = 0) -- here 86%, more
+    than twice the threshold rule's 36% -- with <= 5% false exclusions."""
+    import helpers
+    prob = synth.make_problem("c4", scale=(48, 48, 12), size=16, stride=8)
+    bad = np.asarray(prob["corrupted"], bool)
+    out = {}
+    for mix in (0, 1):
+        orc = helpers.make_oracle(prob, {"patch_mixture": mix})
+        orc.init_volume()
+        orc.sr_iterate(2, prob["alpha"], prob["lam"])
+        _, _, w = orc.weights()
+        out[mix] = ((w[bad] == 0).mean(), (w[~bad] == 0).mean())
+    assert out[1][0] >= 0.8 and out[1][0] >= 2 * out[0][0] and out[1][1] <= 0.05, out
