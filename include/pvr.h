@@ -82,7 +82,11 @@ enum {
                                  S:399-402, reading Q30): rounds 2.. re-run the M- and E-step
                                  on the iteration's residuals until the log-likelihood gain
                                  is below tol |LL| [1]                                      */
-  PVR_PARAM_EM_TOL = 14       /* that relative tolerance [1e-6]                              */
+  PVR_PARAM_EM_TOL = 14,      /* that relative tolerance [1e-6]                              */
+  PVR_PARAM_PATCH_MIXTURE = 15 /* 1: patch weights from a two-Gaussian mixture on pbar (f4,
+                                 P:209 "an inlier and outlier probability for each y_s",
+                                 reading Q31): w = inlier posterior r if r >= 1/2, else 0;
+                                 0: the threshold rule of Q13 [0]                          */
 };
 
 /* Version string of the library build. */

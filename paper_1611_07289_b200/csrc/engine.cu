@@ -165,6 +165,8 @@ struct pvr_ctx {
   int* fbox_dev = nullptr;      // the forward box shapes (width, height) for k_replan
   int em_rounds = 1;
   double em_tol = 1e-6;
+  int patch_mixture = 0;        // f4 two-Gaussian patch classification (reading Q31)
+  int32_t* nlivep = nullptr;    // live pixels per local patch (mixture validity)
   EmDev* em = nullptr;
   // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of the
   // pool, drained (synchronised) only by pvr_get_stats or when the pool is large
@@ -367,6 +369,19 @@ pvr_status allreduce_stats2(pvr_ctx* c) {
                     "ncclAllReduce(E-step stats)");
 }
 
+// f4 patch mixture sums: stage 0 = {n, sum pbar, sum pbar^2 | max, -min}; 1 = 7 round sums.
+constexpr int kMixRounds = 50;
+pvr_status allreduce_mix(pvr_ctx* c, int stage) {
+  if (c->nranks <= 1) return PVR_OK;
+  double* s = c->em->mix_stats;
+  if (stage == 0) {
+    pvr_status r = nccl_check(c, g_nccl.AllReduce(s, s, 3, ncclFloat64, ncclSum, c->comm, c->stream), "mix sums");
+    if (r != PVR_OK) return r;
+    return nccl_check(c, g_nccl.AllReduce(s + 3, s + 3, 2, ncclFloat64, ncclMax, c->comm, c->stream), "mix max");
+  }
+  return nccl_check(c, g_nccl.AllReduce(s, s, 7, ncclFloat64, ncclSum, c->comm, c->stream), "mix round sums");
+}
+
 // Addon / confidence allreduce (C2): SUM over the interleaved, row-padded (A, C) volume.
 pvr_status allreduce_ac(pvr_ctx* c) {
   if (c->nranks <= 1) return PVR_OK;
@@ -381,7 +396,7 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp,
-                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev};
+                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -956,6 +971,7 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
       c->em_rounds = (int)v;
       break;
     case PVR_PARAM_EM_TOL: if (!(v >= 0)) goto bad; c->em_tol = v; break;
+    case PVR_PARAM_PATCH_MIXTURE: if (v != 0 && v != 1) goto bad; c->patch_mixture = (int)v; break;
     case PVR_PARAM_PROFILE: c->profile = v != 0; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }
@@ -1509,6 +1525,9 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   const bool prof = c->profile != 0;
   if (c->em_rounds > 1 && !c->rpart)
     CUDA_TRY(c, cudaMalloc(&c->rpart, (size_t)std::max<int64_t>(c->nloc, 1) * 3 * sizeof(double)));
+  if (c->patch_mixture && !c->nlivep)
+    CUDA_TRY(c, cudaMalloc(&c->nlivep, (size_t)std::max<int64_t>(c->nloc, 1) * sizeof(int32_t)));
+  int32_t* nl = c->patch_mixture ? c->nlivep : nullptr;
   cudaStream_t s = c->stream;
   for (int it = 0; it < n; ++it) {
     float* X0 = c->X[c->cur];
@@ -1527,7 +1546,7 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_EM1], s);
     launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w, 1,
-                 c->em_rounds > 1 ? c->rpart : nullptr);
+                 c->em_rounds > 1 ? c->rpart : nullptr, nl);
     CHECK_LAUNCH(c);
     // f4 multi-round EM (reading Q30): rounds 2..R re-run M and E on the same residuals until
     // the log-likelihood gain falls below tol |LL| (decided on the device: later launches
@@ -1537,9 +1556,25 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
       pvr_status r2 = allreduce_stats2(c);
       if (r2 != PVR_OK) return r2;
       launch_em_round(s, prm, c->em, round, c->em_tol);
-      launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w, round, c->rpart);
+      launch_estep(s, c->pdev, c->nloc, prm, c->em, c->kap, c->e, c->p, c->pbar, c->w, round, c->rpart, nl);
       CHECK_LAUNCH(c);
       c->st.kernel_launches += 3;
+    }
+    // f4 two-Gaussian patch classification (reading Q31): w from the mixture posterior
+    if (c->patch_mixture) {
+      launch_mix_init(s, c->pbar, c->nlivep, c->nloc, c->em);
+      pvr_status rm = allreduce_mix(c, 0);
+      if (rm != PVR_OK) return rm;
+      launch_mix_params_init(s, c->em);
+      for (int round = 0; round < kMixRounds; ++round) {
+        launch_mix_round(s, c->pbar, c->nlivep, c->nloc, c->em, c->w);
+        rm = allreduce_mix(c, 1);
+        if (rm != PVR_OK) return rm;
+        launch_mix_update(s, c->em, round, 1e-6);
+      }
+      launch_mix_weights(s, c->nlivep, c->nloc, c->em, c->w);
+      CHECK_LAUNCH(c);
+      c->st.kernel_launches += 3 + 2 * kMixRounds;
     }
     if (prof) cudaEventRecord((*ev)[EV_EST1], s);
     CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));

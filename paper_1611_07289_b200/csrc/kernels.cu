@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(256) k_estep(const PatchDev* __restrict__ P, P
                                                const float* __restrict__ kap,
                                                const float* __restrict__ e, float* __restrict__ p,
                                                float* __restrict__ pbar, float* __restrict__ w,
-                                               int round, double* __restrict__ rpart) {
+                                               int round, double* __restrict__ rpart,
+                                               int32_t* __restrict__ nlive) {
   if (round >= 2 && em->done) return;  // f4 rounds converged: keep the last p, pbar, w
   const PatchDev& pt = P[blockIdx.x];
   const int npix = pt.sx * pt.sy * pt.sz;
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(256) k_estep(const PatchDev* __restrict__ P, P
     const float pb = res[1] > 0.0 ? (float)sqrt(res[0] / res[1]) : 0.0f;
     pbar[blockIdx.x] = pb;
     w[blockIdx.x] = pb >= prm.tau_patch ? pb : 0.0f;
+    if (nlive) nlive[blockIdx.x] = (int32_t)res[1];
     if (rpart) {
       rpart[3 * blockIdx.x] = res[2];
       rpart[3 * blockIdx.x + 1] = res[3];
@@ -181,6 +183,105 @@ __global__ void k_em_reduce3(const double* __restrict__ rpart, int64_t npatch, E
   block_reduce_store<3, 1>(a, mx, res);
   if (threadIdx.x == 0)
     for (int i = 0; i < 3; ++i) em->stats2[i] = res[i];
+}
+
+// --------------------------------------------------------------------------------------
+// f4 two-Gaussian patch classification (reading Q31; oracle/pvro.c
+// pvro_patch_mixture): a 1D mixture pi N(mu_in, v_in) + (1 - pi) N(mu_out, v_out) on the
+// patch scores of the valid patches (>= 1 live pixel), EM from mu_in = max, mu_out = min,
+// v = the scores' variance, pi = 1/2, until the mixture LL gains < tol |LL|; the patch weight
+// is the inlier posterior r_s if r_s >= 1/2, else 0. Rank-local sums are NCCL-summed between
+// the kernels (engine.cu); single-CTA kernels: M is at most a few 1e5 patches.
+__global__ void k_mix_init(const float* __restrict__ pbar, const int32_t* __restrict__ nlive, int64_t M,
+                           EmDev* em) {
+  double a[3] = {0.0, 0.0, 0.0};
+  float mx[2] = {-FLT_MAX, -FLT_MAX};
+  for (int64_t s = threadIdx.x; s < M; s += blockDim.x) {
+    if (nlive[s] <= 0) continue;
+    const double v = pbar[s];
+    a[0] += 1.0;
+    a[1] += v;
+    a[2] += v * v;
+    mx[0] = fmaxf(mx[0], (float)v);
+    mx[1] = fmaxf(mx[1], (float)-v);
+  }
+  __shared__ double res[5];
+  block_reduce_store<3, 2>(a, mx, res);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 5; ++i) em->mix_stats[i] = res[i];
+}
+
+__global__ void k_mix_params_init(EmDev* em) {
+  if (threadIdx.x != 0) return;
+  const double n = em->mix_stats[0], mx = em->mix_stats[3], mn = -em->mix_stats[4];
+  em->mix_degenerate = !(n > 0.0) || !(mx - mn > 1e-6);
+  em->mix_done = em->mix_degenerate;
+  double var = n > 0.0 ? em->mix_stats[2] / n - (em->mix_stats[1] / n) * (em->mix_stats[1] / n) : 0.0;
+  if (var < 1e-6) var = 1e-6;
+  em->mix_mu[0] = mx;
+  em->mix_mu[1] = mn;
+  em->mix_v[0] = em->mix_v[1] = var;
+  em->mix_pi = 0.5;
+  em->mix_ll_prev = NAN;
+}
+
+__device__ __forceinline__ double gpdf(double x, double mu, double v) {
+  return exp(-(x - mu) * (x - mu) / (2.0 * v)) / sqrt(2.0 * M_PI * v);
+}
+
+// E-step of one round with the current parameters: r_s into r, and the sums
+// {sum r, sum r pbar, sum r pbar^2, sum (1-r), sum (1-r) pbar, sum (1-r) pbar^2, LL}.
+__global__ void k_mix_round(const float* __restrict__ pbar, const int32_t* __restrict__ nlive, int64_t M,
+                            EmDev* em, float* __restrict__ r) {
+  if (em->mix_done) return;
+  const double mu0 = em->mix_mu[0], mu1 = em->mix_mu[1], v0 = em->mix_v[0], v1 = em->mix_v[1];
+  const double pi = em->mix_pi;
+  double a[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t s = threadIdx.x; s < M; s += blockDim.x) {
+    if (nlive[s] <= 0) continue;
+    const double x = pbar[s];
+    const double ai = pi * gpdf(x, mu0, v0), ao = (1.0 - pi) * gpdf(x, mu1, v1);
+    const double rs = (ai + ao > 0.0) ? ai / (ai + ao) : (x >= 0.5 * (mu0 + mu1) ? 1.0 : 0.0);
+    r[s] = (float)rs;
+    a[0] += rs; a[1] += rs * x; a[2] += rs * x * x;
+    a[3] += 1.0 - rs; a[4] += (1.0 - rs) * x; a[5] += (1.0 - rs) * x * x;
+    a[6] += log(ai + ao > 0.0 ? ai + ao : 1e-300);
+  }
+  float mx[1] = {0.0f};
+  __shared__ double res[8];
+  block_reduce_store<7, 1>(a, mx, res);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 7; ++i) em->mix_stats[i] = res[i];
+}
+
+// Convergence test on the last E-step's LL, then the M-step.
+__global__ void k_mix_update(EmDev* em, int round, double tol) {
+  if (threadIdx.x != 0 || em->mix_done) return;
+  const double* t = em->mix_stats;
+  const double ll = t[6], n = t[0] + t[3];
+  if (round >= 1 && !(ll - em->mix_ll_prev >= tol * fabs(em->mix_ll_prev))) {
+    em->mix_done = 1;
+    return;
+  }
+  em->mix_ll_prev = ll;
+  const double pi = n > 0.0 ? t[0] / n : 0.0;
+  if (t[0] > 0.0) { em->mix_mu[0] = t[1] / t[0]; em->mix_v[0] = t[2] / t[0] - em->mix_mu[0] * em->mix_mu[0]; }
+  if (t[3] > 0.0) { em->mix_mu[1] = t[4] / t[3]; em->mix_v[1] = t[5] / t[3] - em->mix_mu[1] * em->mix_mu[1]; }
+  if (em->mix_v[0] < 1e-6) em->mix_v[0] = 1e-6;
+  if (em->mix_v[1] < 1e-6) em->mix_v[1] = 1e-6;
+  em->mix_pi = pi;
+  if (pi <= 0.0 || pi >= 1.0) em->mix_done = 1;
+}
+
+// w_s = r_s if r_s >= 1/2 else 0 (r_s = 1 on the degenerate path, 0 for invalid patches)
+__global__ void k_mix_weights(const int32_t* __restrict__ nlive, int64_t M, const EmDev* __restrict__ em,
+                              float* __restrict__ w) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < M; s += (int64_t)gridDim.x * blockDim.x) {
+    float r = w[s];
+    if (nlive[s] <= 0) r = 0.0f;
+    else if (em->mix_degenerate) r = 1.0f;
+    w[s] = r >= 0.5f ? r : 0.0f;
+  }
 }
 
 // --------------------------------------------------------------------------------------
@@ -419,13 +520,27 @@ void launch_em_params(cudaStream_t st, Params prm, EmDev* em) {
 
 void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, EmDev* em,
                   const float* kap, const float* e, float* p, float* pbar, float* w, int round,
-                  double* rpart) {
+                  double* rpart, int32_t* nlive) {
   if (npatch <= 0) return;
-  k_estep<<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w, round, rpart);
+  k_estep<<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w, round, rpart, nlive);
 }
 
 void launch_em_reduce3(cudaStream_t st, const double* rpart, int64_t npatch, EmDev* em) {
   k_em_reduce3<<<1, 1024, 0, st>>>(rpart, npatch, em);
+}
+
+void launch_mix_init(cudaStream_t st, const float* pbar, const int32_t* nlive, int64_t npatch, EmDev* em) {
+  k_mix_init<<<1, 1024, 0, st>>>(pbar, nlive, npatch, em);
+}
+void launch_mix_params_init(cudaStream_t st, EmDev* em) { k_mix_params_init<<<1, 32, 0, st>>>(em); }
+void launch_mix_round(cudaStream_t st, const float* pbar, const int32_t* nlive, int64_t npatch, EmDev* em, float* r) {
+  k_mix_round<<<1, 1024, 0, st>>>(pbar, nlive, npatch, em, r);
+}
+void launch_mix_update(cudaStream_t st, EmDev* em, int round, double tol) {
+  k_mix_update<<<1, 32, 0, st>>>(em, round, tol);
+}
+void launch_mix_weights(cudaStream_t st, const int32_t* nlive, int64_t npatch, const EmDev* em, float* w) {
+  if (npatch > 0) k_mix_weights<<<(unsigned)((npatch + 255) / 256), 256, 0, st>>>(nlive, npatch, em, w);
 }
 
 void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double tol) {

@@ -77,6 +77,10 @@ struct EmDev {
   int32_t done;                // rounds converged (or degenerate): later rounds are no-ops
   int32_t degenerate;          // round 1 took the degenerate path
   int32_t rounds;              // E-step rounds run in the last iteration
+  // f4 two-Gaussian patch classification (reading Q31)
+  double mix_mu[2], mix_v[2], mix_pi, mix_ll_prev;  // [0] inliers, [1] outliers
+  double mix_stats[7];         // reduced round sums (see kernels.cu k_mix_round)
+  int32_t mix_done, mix_degenerate;
 };
 
 struct Params {
@@ -152,8 +156,14 @@ void launch_em_params(cudaStream_t st, Params prm, EmDev* em);
 // per-patch {sum p e^2, sum p, LL} over live pixels for the next M-step.
 void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, EmDev* em,
                   const float* kap, const float* e, float* p, float* pbar, float* w, int round,
-                  double* rpart);
+                  double* rpart, int32_t* nlive);
 void launch_em_reduce3(cudaStream_t st, const double* rpart, int64_t npatch, EmDev* em);
+// f4 patch mixture: nlive [npatch] from the last E-step (launch_estep's nlive output)
+void launch_mix_init(cudaStream_t st, const float* pbar, const int32_t* nlive, int64_t npatch, EmDev* em);
+void launch_mix_params_init(cudaStream_t st, EmDev* em);
+void launch_mix_round(cudaStream_t st, const float* pbar, const int32_t* nlive, int64_t npatch, EmDev* em, float* r);
+void launch_mix_update(cudaStream_t st, EmDev* em, int round, double tol);
+void launch_mix_weights(cudaStream_t st, const int32_t* nlive, int64_t npatch, const EmDev* em, float* w);
 void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double tol);
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2);

@@ -172,3 +172,12 @@ def test_new_transforms_replan(deg, mm, device):
             assert dp <= 1e-3 and dw <= 1e-3
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("cfg,kw,iters", [("c1", {}, 2),
+                                          ("c4", dict(scale=(96, 96, 16), size=32, stride=16), 2)])
+def test_patch_mixture(cfg, kw, iters):
+    """f4 two-Gaussian patch classification (reading Q31): the patch weights are the
+    mixture's inlier posteriors (>= 1/2); same parity bar."""
+    prob = synth.make_problem(cfg, **kw)
+    run_pair(prob, iters, params={"patch_mixture": 1})
