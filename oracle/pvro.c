@@ -51,6 +51,7 @@ struct pvro_ctx {
   double quality;    /* PSF lattice density factor q (1; 2 = f4 quality mode) */
   double em_rounds, em_tol;  /* f4 multi-round EM (1 round; 1e-6) */
   double patch_mixture;      /* f4 two-Gaussian patch classification (0) */
+  uint8_t* mask;             /* f3: per-pixel patch mask [P] (NULL = all pixels) */
   /* iteration state */
   double* X;         /* [V] */
   double *p, *e, *kappa, *yhat;  /* [P] */
@@ -361,7 +362,7 @@ void pvro_destroy(pvro_ctx* x) {
   if (!x) return;
   for (int i = 0; i < x->n_stacks; ++i) { free(x->st[i].y); free(x->st[i].abc); free(x->st[i].psi); }
   free(x->patch); free(x->pix0); free(x->T); free(x->X); free(x->A); free(x->C);
-  free(x->p); free(x->e); free(x->kappa); free(x->yhat); free(x->pbar); free(x->wpatch);
+  free(x->p); free(x->e); free(x->kappa); free(x->yhat); free(x->pbar); free(x->wpatch); free(x->mask);
   free(x);
 }
 
@@ -442,6 +443,34 @@ static int build_psf(pvro_ctx* x, ostack* st) {
   return st->S > 0 ? 0 : -1;
 }
 
+static int64_t install_patches(pvro_ctx* x, int64_t M);
+
+/* f3 (Eq. 3; reading Q32): an explicit patch table instead of
+ * the square windows: rects [n][7] = (stack, x0, y0, z0, sx, sy, sz) inside their stacks, and
+ * an optional per-pixel mask [sum sx sy sz] (patch-major; NULL = all pixels). Masked-out
+ * pixels are never observations: their coverage kappa is 0 (so e = 0, p = 0, no splat). */
+int64_t pvro_set_patches(pvro_ctx* x, int64_t n, const int32_t* rects, const uint8_t* mask) {
+  if (x->state != 1 || n <= 0) return -1;
+  for (int64_t s = 0; s < n; ++s) {
+    const int32_t* r = &rects[7 * s];
+    if (r[0] < 0 || r[0] >= x->n_stacks) return -1;
+    const ostack* st = &x->st[r[0]];
+    if (r[4] < 1 || r[5] < 1 || r[6] < 1 || r[1] < 0 || r[2] < 0 || r[3] < 0 || r[1] + r[4] > st->W ||
+        r[2] + r[5] > st->H || r[3] + r[6] > st->K)
+      return -1;
+  }
+  for (int i = 0; i < x->n_stacks; ++i)
+    if (build_psf(x, &x->st[i]) != 0) return -1;
+  x->patch = (int32_t*)malloc(7 * n * sizeof(int32_t));
+  memcpy(x->patch, rects, 7 * n * sizeof(int32_t));
+  const int64_t M = install_patches(x, n);
+  if (mask) {
+    x->mask = (uint8_t*)malloc(x->P);
+    memcpy(x->mask, mask, x->P);
+  }
+  return M;
+}
+
 int64_t pvro_extract_patches(pvro_ctx* x, int size, int stride, int depth, int stride_z) {
   if (x->state != 1) return -1;
   for (int i = 0; i < x->n_stacks; ++i)
@@ -471,6 +500,11 @@ int64_t pvro_extract_patches(pvro_ctx* x, int size, int stride, int depth, int s
     if (pass == 0) x->patch = (int32_t*)malloc(7 * (M > 0 ? M : 1) * sizeof(int32_t));
   }
   free(xs); free(ys); free(zs);
+  return install_patches(x, M);
+}
+
+/* Patch table installed (x->patch holds M rows): pixel offsets and the per-pixel state. */
+static int64_t install_patches(pvro_ctx* x, int64_t M) {
   x->M = M;
   x->pix0 = (int64_t*)malloc((M + 1) * sizeof(int64_t));
   x->pix0[0] = 0;
@@ -625,6 +659,7 @@ int pvro_forward_range(const pvro_ctx* x, const double* X, int64_t first, int64_
               acc += st->psi[q] * wt[c] * X[idx[c]];
             }
           }
+          if (x->mask && !x->mask[j]) kap = 0.0;  /* f3: masked-out pixel (Q32) */
           kappa[j] = kap;
           yhat[j] = (kap >= x->tau_obs) ? acc / kap : 0.0;
         }

@@ -117,6 +117,10 @@ int pvro_add_stack(pvro_ctx*, const float* slices, int W, int H, int K,
 int pvro_add_stack_f64(pvro_ctx*, const double* slices, int W, int H, int K,
                        const double G[12], double thickness);
 int64_t pvro_extract_patches(pvro_ctx*, int size, int stride, int depth, int stride_z);
+/* f3 (reading Q32): explicit patch table rects [n][7] = (stack, x0, y0, z0,
+ * sx, sy, sz) and an optional per-pixel mask (patch-major, NULL = all): masked-out pixels are
+ * never observations (kappa = 0). Instead of pvro_extract_patches. Returns M or < 0. */
+int64_t pvro_set_patches(pvro_ctx*, int64_t n, const int32_t* rects, const uint8_t* mask);
 int64_t pvro_num_pixels(const pvro_ctx*);
 /* patch table: 7 int32 per patch {stack, x0, y0, z0, sx, sy, sz} */
 int pvro_get_patches(const pvro_ctx*, int32_t* out);

@@ -68,6 +68,8 @@ def lib():
         L.pvro_add_stack_f64.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp, d]
         L.pvro_extract_patches.restype = i64
         L.pvro_extract_patches.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.pvro_set_patches.restype = i64
+        L.pvro_set_patches.argtypes = [vp, i64, vp, vp]
         L.pvro_num_pixels.restype = i64
         L.pvro_num_pixels.argtypes = [vp]
         L.pvro_get_patches.argtypes = [vp, vp]
@@ -228,6 +230,14 @@ class Oracle:
 
     def extract_patches(self, size, stride, depth=1, stride_z=1):
         self.M = _chk(lib().pvro_extract_patches(self.h, size, stride, depth, stride_z), "extract")
+        self.P = lib().pvro_num_pixels(self.h)
+        return self.M
+
+    def set_patches(self, rects, mask=None):
+        """f3: explicit patch rectangles [n][7] and optional per-pixel mask (reading Q32)."""
+        rects = np.ascontiguousarray(rects, np.int32).reshape(-1, 7)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        self.M = _chk(lib().pvro_set_patches(self.h, len(rects), _p(rects), _p(m)), "set_patches")
         self.P = lib().pvro_num_pixels(self.h)
         return self.M
 

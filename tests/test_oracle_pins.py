@@ -632,3 +632,64 @@ def test_patch_mixture_excludes_corrupted_patches():
         _, _, w = orc.weights()
         out[mix] = ((w[bad] == 0).mean(), (w[~bad] == 0).mean())
     assert out[1][0] >= 0.8 and out[1][0] >= 2 * out[0][0] and out[1][1] <= 0.05, out
+
+
+# ------------------------------------------------------- f3 explicit / masked patches (Q32)
+def _c1_with(rects=None, mask=None, **kw):
+    prob = synth.make_problem("c1")
+    orc = Oracle(prob["dims"], prob["spacing"], prob["origin"])
+    for st in prob["stacks"]:
+        orc.add_stack(st["slices"], st["G"], st["thickness"])
+    return prob, orc
+
+
+def test_set_patches_without_mask_equals_extract():
+    """Explicit rectangles equal to the square windows reproduce extract_patches exactly."""
+    prob, a = _c1_with()
+    a.extract_patches(16, 8)
+    a.set_transforms(prob["T"])
+    rects = a.patches()
+    _, b = _c1_with()
+    b.set_patches(rects)
+    b.set_transforms(prob["T"])
+    for o in (a, b):
+        o.init_volume()
+        o.sr_iterate(1, prob["alpha"], prob["lam"])
+    # equal up to the order of the oracle's OpenMP atomic fp64 sums
+    assert np.abs(a.volume() - b.volume()).max() <= 1e-12 * np.abs(a.volume()).max()
+
+
+def test_masked_pixels_are_not_observations_and_adjoint_is_additive():
+    """Masked-out pixels get kappa = 0 (never observed); the rest keep their coverage; and the
+    backprojection of a masked patch equals that of its kept pixels as 1x1 patches (W^T is a
+    sum over observations)."""
+    prob, a = _c1_with()
+    rects = np.array([[0, 4, 6, 3, 12, 10, 1], [1, 0, 0, 2, 16, 16, 1]], np.int32)
+    rng = np.random.default_rng(4)
+    mask = (rng.uniform(size=12 * 10 + 256) > 0.4).astype(np.uint8)
+    a.set_patches(rects, mask)
+    T = np.tile(np.hstack([np.eye(3), np.zeros((3, 1))]), (2, 1, 1))
+    a.set_transforms(T)
+    _, b = _c1_with()
+    b.set_patches(rects)
+    b.set_transforms(T)
+    _, ka, _, _ = a.taps()
+    _, kb, _, _ = b.taps()
+    assert (ka[mask == 0] == 0).all() and np.array_equal(ka[mask == 1], kb[mask == 1])
+    # single-pixel patches of the kept pixels
+    singles = []
+    j = 0
+    for r in rects:
+        for z in range(r[6]):
+            for v in range(r[5]):
+                for u in range(r[4]):
+                    if mask[j]:
+                        singles.append([r[0], r[1] + u, r[2] + v, r[3] + z, 1, 1, 1])
+                    j += 1
+    _, c = _c1_with()
+    c.set_patches(np.array(singles, np.int32))
+    c.set_transforms(np.tile(np.hstack([np.eye(3), np.zeros((3, 1))]), (len(singles), 1, 1)))
+    y = rng.uniform(0, 10, len(mask))
+    Aa = a.adjoint(y)
+    Ac = c.adjoint(y[mask == 1])
+    assert np.abs(Aa - Ac).max() <= 1e-12 * max(1.0, np.abs(Aa).max())
