@@ -131,6 +131,16 @@ pvr_status pvr_add_stack(pvr_ctx* ctx, const float* slices, int W, int H, int K,
  * stride_z < 1 or > depth), PVR_ERR_STATE, PVR_ERR_EMPTY (M = 0). */
 pvr_status pvr_extract_patches(pvr_ctx* ctx, int size, int stride, int depth, int stride_z,
                                int64_t* n_patches_out);
+/* f3 arbitrary-shape patches (Eq. 3: patches y_s need not be
+ * squares; superpixels dilated by gamma pixels; reading Q32), instead of
+ * pvr_extract_patches: n explicit rectangles rects int32 [n][7] = (stack, x0, y0, z0, sx, sy,
+ * sz), each inside its stack, and an optional per-pixel mask uint8 (patch-major, sum of
+ * sx sy sz bytes; NULL = every pixel): a masked-out pixel is never an observation (its
+ * coverage kappa is 0, so it has no residual, posterior or splat). Host or device pointers.
+ * Errors: PVR_ERR_STATE (not right after the stacks), PVR_ERR_ARG (n < 1, a rectangle
+ * outside its stack). */
+pvr_status pvr_set_patches(pvr_ctx* ctx, int64_t n, const int32_t* rects, const uint8_t* mask,
+                           int64_t* n_patches);
 /* Host-only helper (no GPU needed): contiguous shard plan of M patches over nranks,
  * balanced by cost[s] (pixels x PSF samples of patch s): rank r owns patches
  * [bounds[r], bounds[r+1]); bounds has nranks + 1 entries, bounds[0] = 0, bounds[nranks] = M.

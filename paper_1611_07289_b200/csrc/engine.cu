@@ -167,6 +167,7 @@ struct pvr_ctx {
   double em_tol = 1e-6;
   int patch_mixture = 0;        // f4 two-Gaussian patch classification (reading Q31)
   int32_t* nlivep = nullptr;    // live pixels per local patch (mixture validity)
+  uint8_t* mask = nullptr;      // f3: per-pixel patch mask of the local shard (NULL = all)
   EmDev* em = nullptr;
   // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of the
   // pool, drained (synchronised) only by pvr_get_stats or when the pool is large
@@ -341,6 +342,7 @@ LatticeArgs lattice_args(const pvr_ctx* c, const pvr_ctx::Plan& pl) {
   a.n = c->dims;
   a.nxp = c->nxp;
   a.ys = c->ys;
+  a.mask = c->mask;
   a.prm = make_params(c);
   return a;
 }
@@ -396,7 +398,7 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp,
-                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep};
+                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep, c->mask};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -1036,6 +1038,8 @@ pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* 
   return PVR_OK;
 }
 
+static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_out);
+
 pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int stride_z, int64_t* n_out) {
   GUARD(c);
   if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "extract_patches needs stacks and runs once");
@@ -1045,12 +1049,6 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
     if (size > st.W || size > st.H || depth > st.K)
       return fail(c, PVR_ERR_ARG, "patch %dx%dx%d larger than a %dx%dx%d stack", size, size, depth,
                   st.W, st.H, st.K);
-  // PSF tables (host fp64 -> device fp32 factors)
-  c->psf_tab.clear();
-  for (auto& st : c->stacks) {
-    pvr_status r = build_psf(c, st);
-    if (r != PVR_OK) return r;
-  }
   // patch list, order stack, z0, y0, x0
   c->patches.clear();
   for (int si = 0; si < (int)c->stacks.size(); ++si) {
@@ -1059,6 +1057,39 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
       for (int y0 : windows(st.H, size, stride))
         for (int x0 : windows(st.W, size, stride))
           c->patches.push_back(HostPatch{si, x0, y0, z0, size, size, depth});
+  }
+  return install_patches(c, nullptr, n_out);
+}
+
+// f3 (reading Q32): explicit patch rectangles [n][7] with an optional per-pixel mask.
+pvr_status pvr_set_patches(pvr_ctx* c, int64_t n, const int32_t* rects, const uint8_t* mask, int64_t* n_out) {
+  GUARD(c);
+  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "set_patches needs stacks and runs once");
+  if (n <= 0 || !rects) return fail(c, PVR_ERR_ARG, "set_patches needs n >= 1 rectangles");
+  std::vector<int32_t> rh(7 * n);
+  if (is_device_ptr(rects)) CUDA_TRY(c, cudaMemcpy(rh.data(), rects, rh.size() * 4, cudaMemcpyDeviceToHost));
+  else memcpy(rh.data(), rects, rh.size() * 4);
+  c->patches.clear();
+  for (int64_t s = 0; s < n; ++s) {
+    const int32_t* r = &rh[7 * s];
+    if (r[0] < 0 || r[0] >= (int)c->stacks.size()) return fail(c, PVR_ERR_ARG, "patch %lld: bad stack", (long long)s);
+    const HostStack& st = c->stacks[r[0]];
+    if (r[4] < 1 || r[5] < 1 || r[6] < 1 || r[1] < 0 || r[2] < 0 || r[3] < 0 || r[1] + r[4] > st.W ||
+        r[2] + r[5] > st.H || r[3] + r[6] > st.K)
+      return fail(c, PVR_ERR_ARG, "patch %lld outside its %dx%dx%d stack", (long long)s, st.W, st.H, st.K);
+    c->patches.push_back(HostPatch{r[0], r[1], r[2], r[3], r[4], r[5], r[6]});
+  }
+  return install_patches(c, mask, n_out);
+}
+
+// Common tail of pvr_extract_patches / pvr_set_patches: PSF tables, pixel offsets, shards,
+// the concatenated stacks and the per-pixel / per-patch device arrays.
+static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_out) {
+  // PSF tables (host fp64 -> device fp32 factors)
+  c->psf_tab.clear();
+  for (auto& st : c->stacks) {
+    pvr_status r = build_psf(c, st);
+    if (r != PVR_OK) return r;
   }
   c->M = (int64_t)c->patches.size();
   if (c->M == 0) return fail(c, PVR_ERR_EMPTY, "no patches");
@@ -1104,6 +1135,11 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
   CUDA_TRY(c, cudaMemsetAsync(c->e, 0, np * sizeof(float), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->p, 0, np * sizeof(float), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->kap, 0, np * sizeof(float), c->stream));
+  if (mask) {  // f3: this rank's slice of the per-pixel mask (masked pixels: kappa = 0)
+    CUDA_TRY(c, cudaMalloc(&c->mask, np));
+    CUDA_TRY(c, cudaMemcpyAsync(c->mask, mask + c->first_pix, c->nloc_pix,
+                                is_device_ptr(mask) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->st.pixels = c->nloc_pix;
   c->st.patches = c->nloc;

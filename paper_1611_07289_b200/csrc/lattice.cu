@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       const int64_t j = pt.pix0 + ((int64_t)f.z * pt.sy + v) * pt.sx + u;
       const float y = a.ys[pt.y0off + (int64_t)f.z * pt.HW + (int64_t)v * pt.W + u];
       if (MODE == 1) {
+        if (a.mask && !a.mask[j]) s = 0.0f;  // f3: masked-out pixel is never observed (Q32)
         out[j] = s;
         if (s >= a.prm.tau_obs) {
           acc_s[0] += 1.0;

@@ -100,6 +100,7 @@ struct LatticeArgs {
   int3 n;                  // volume dims
   int32_t nxp;             // row pitch of X and (A, C) (nx rounded up to a multiple of 4)
   const float* ys;         // concatenated stacks
+  const uint8_t* mask;     // f3: per-pixel patch mask (local shard; NULL = all pixels)
   Params prm;
 };
 

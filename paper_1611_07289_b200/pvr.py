@@ -27,7 +27,7 @@ EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", 
            "pvr_comm_unique_id", "pvr_add_stack", "pvr_extract_patches", "pvr_plan_shards",
            "pvr_get_shard", "pvr_get_patches", "pvr_set_transforms", "pvr_set_volume",
            "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume", "pvr_rigidity_map",
-           "pvr_register_patches", "pvr_patch_cc",
+           "pvr_register_patches", "pvr_patch_cc", "pvr_set_patches",
            "pvr_get_weights", "pvr_get_taps", "pvr_get_em_state", "pvr_get_stats",
            "pvr_reset_stats"]
 
@@ -97,6 +97,7 @@ def lib():
             "pvr_rigidity_map": (i32, [vp, vp, C.c_size_t]),
             "pvr_register_patches": (i32, [vp, C.c_int, C.c_int, vp, vp, vp]),
             "pvr_patch_cc": (i32, [vp, C.c_int64, vp, vp, vp]),
+            "pvr_set_patches": (i32, [vp, C.c_int64, vp, vp, vp]),
             "pvr_get_weights": (i32, [vp, vp, vp, vp]),
             "pvr_get_taps": (i32, [vp, vp, vp, vp, vp]),
             "pvr_get_em_state": (i32, [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i64),
@@ -334,6 +335,16 @@ class Context:
         poses = np.ascontiguousarray(poses, np.float32).reshape(-1, 6)
         cc = np.zeros(len(patch), np.float64)
         return pvr_patch_cc(self.h, patch, poses, cc)
+
+    def set_patches(self, rects, mask=None):
+        """f3: explicit patch rectangles [n][7] and optional per-pixel mask (pvr_set_patches)."""
+        rects = np.ascontiguousarray(rects, np.int32).reshape(-1, 7)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        n = C.c_int64()
+        _check(self.h, lib().pvr_set_patches(self.h, len(rects), _ptr(rects), _ptr(m), C.byref(n)))
+        self.M = n.value
+        self.first, self.nloc, self.first_pix, self.nloc_pix = pvr_get_shard(self.h)
+        return self.M
 
     def rigidity_map(self, out=None):
         """W^T(p pbar) / W^T 1 (f2; float32 [nz][ny][nx], host or device out)."""
