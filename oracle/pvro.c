@@ -471,6 +471,143 @@ int64_t pvro_set_patches(pvro_ctx* x, int64_t n, const int32_t* rects, const uin
   return M;
 }
 
+/* ---- f3 superpixels (reading Q33) ---- */
+static int slic_quant(float y, float ymin, float ymax) {
+  if (!(ymax > ymin)) return 0;
+  const double t = ((double)y - (double)ymin) * 1023.0 / ((double)ymax - (double)ymin);
+  return (int)floor(t + 0.5);
+}
+
+int pvro_slic(int W, int H, const float* img, float ymin, float ymax, int S, int m, int iters, int32_t* labels) {
+  if (W < 1 || H < 1 || S < 2 || m < 1 || iters < 0) return -1;
+  const int nxc = (W + S - 1) / S, nyc = (H + S - 1) / S, nc = nxc * nyc;
+  int64_t* cx = (int64_t*)malloc(nc * sizeof(int64_t));
+  int64_t* cy = (int64_t*)malloc(nc * sizeof(int64_t));
+  int64_t* cI = (int64_t*)malloc(nc * sizeof(int64_t));
+  int64_t* acc = (int64_t*)malloc(4 * nc * sizeof(int64_t));
+  for (int j = 0; j < nyc; ++j)
+    for (int i = 0; i < nxc; ++i) {
+      const int k = j * nxc + i;
+      const int px = i * S + S / 2 < W - 1 ? i * S + S / 2 : W - 1;
+      const int py = j * S + S / 2 < H - 1 ? j * S + S / 2 : H - 1;
+      cx[k] = 16 * (int64_t)px;
+      cy[k] = 16 * (int64_t)py;
+      cI[k] = 16 * (int64_t)slic_quant(img[(int64_t)py * W + px], ymin, ymax);
+    }
+  const int64_t S2 = (int64_t)S * S, m2 = (int64_t)m * m;
+  for (int round = 0; round <= iters; ++round) {
+    /* assignment */
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        const int64_t I16 = 16 * (int64_t)slic_quant(img[(int64_t)y * W + x], ymin, ymax);
+        const int ci = x / S, cj = y / S;
+        int64_t best = INT64_MAX;
+        int bk = -1;
+        for (int dj = -1; dj <= 1; ++dj)
+          for (int di = -1; di <= 1; ++di) {
+            const int i = ci + di, j = cj + dj;
+            if (i < 0 || i >= nxc || j < 0 || j >= nyc) continue;
+            const int k = j * nxc + i;
+            const int64_t dI = I16 - cI[k], dx = 16 * (int64_t)x - cx[k], dy = 16 * (int64_t)y - cy[k];
+            const int64_t D = S2 * dI * dI + m2 * (dx * dx + dy * dy);
+            if (D < best) { best = D; bk = k; }
+          }
+        labels[(int64_t)y * W + x] = bk;
+      }
+    if (round == iters) break;
+    /* update */
+    memset(acc, 0, 4 * nc * sizeof(int64_t));
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        const int k = labels[(int64_t)y * W + x];
+        acc[4 * k] += 1;
+        acc[4 * k + 1] += x;
+        acc[4 * k + 2] += y;
+        acc[4 * k + 3] += slic_quant(img[(int64_t)y * W + x], ymin, ymax);
+      }
+    for (int k = 0; k < nc; ++k) {
+      const int64_t n = acc[4 * k];
+      if (n == 0) continue;
+      cx[k] = (16 * acc[4 * k + 1] + n / 2) / n;
+      cy[k] = (16 * acc[4 * k + 2] + n / 2) / n;
+      cI[k] = (16 * acc[4 * k + 3] + n / 2) / n;
+    }
+  }
+  free(cx); free(cy); free(cI); free(acc);
+  return nc;
+}
+
+int64_t pvro_superpixel_patches(pvro_ctx* x, int S, int m, int iters, int gamma) {
+  if (x->state != 1 || S < 2 || m < 1 || iters < 0 || gamma < 0) return -1;
+  /* pass 0 counts (rects, pixels); pass 1 fills */
+  int64_t nrect = 0, npix = 0;
+  int32_t* rects = NULL;
+  uint8_t* mask = NULL;
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t r = 0, q = 0;
+    for (int si = 0; si < x->n_stacks; ++si) {
+      const ostack* st = &x->st[si];
+      const int64_t HW = (int64_t)st->W * st->H;
+      float ymin = INFINITY, ymax = -INFINITY;
+      for (int64_t t = 0; t < HW * st->K; ++t) {
+        const float v = (float)st->y[t];
+        if (v < ymin) ymin = v;
+        if (v > ymax) ymax = v;
+      }
+      float* img = (float*)malloc(HW * sizeof(float));
+      int32_t* lab = (int32_t*)malloc(HW * sizeof(int32_t));
+      for (int z = 0; z < st->K; ++z) {
+        for (int64_t t = 0; t < HW; ++t) img[t] = (float)st->y[z * HW + t];
+        const int nc = pvro_slic(st->W, st->H, img, ymin, ymax, S, m, iters, lab);
+        for (int k = 0; k < nc; ++k) {
+          int xmin = st->W, xmax = -1, ymn = st->H, ymx = -1;
+          for (int yy = 0; yy < st->H; ++yy)
+            for (int xx = 0; xx < st->W; ++xx)
+              if (lab[(int64_t)yy * st->W + xx] == k) {
+                if (xx < xmin) xmin = xx;
+                if (xx > xmax) xmax = xx;
+                if (yy < ymn) ymn = yy;
+                if (yy > ymx) ymx = yy;
+              }
+          if (xmax < 0) continue;
+          const int x0 = xmin - gamma > 0 ? xmin - gamma : 0, x1 = xmax + gamma < st->W - 1 ? xmax + gamma : st->W - 1;
+          const int y0 = ymn - gamma > 0 ? ymn - gamma : 0, y1 = ymx + gamma < st->H - 1 ? ymx + gamma : st->H - 1;
+          const int sx = x1 - x0 + 1, sy = y1 - y0 + 1;
+          if (pass == 1) {
+            int32_t* rr = &rects[7 * r];
+            rr[0] = si; rr[1] = x0; rr[2] = y0; rr[3] = z; rr[4] = sx; rr[5] = sy; rr[6] = 1;
+            for (int v = 0; v < sy; ++v)
+              for (int u = 0; u < sx; ++u) {
+                int hit = 0;
+                for (int dv = -gamma; dv <= gamma && !hit; ++dv)
+                  for (int du = -gamma; du <= gamma && !hit; ++du) {
+                    const int xx = x0 + u + du, yy = y0 + v + dv;
+                    if (xx >= 0 && xx < st->W && yy >= 0 && yy < st->H && lab[(int64_t)yy * st->W + xx] == k) hit = 1;
+                  }
+                mask[q + (int64_t)v * sx + u] = (uint8_t)hit;
+              }
+          }
+          ++r;
+          q += (int64_t)sx * sy;
+        }
+      }
+      free(img);
+      free(lab);
+    }
+    if (pass == 0) {
+      nrect = r;
+      npix = q;
+      if (nrect == 0) return -1;
+      rects = (int32_t*)malloc(7 * nrect * sizeof(int32_t));
+      mask = (uint8_t*)malloc(npix);
+    }
+  }
+  const int64_t M = pvro_set_patches(x, nrect, rects, mask);
+  free(rects);
+  free(mask);
+  return M;
+}
+
 int64_t pvro_extract_patches(pvro_ctx* x, int size, int stride, int depth, int stride_z) {
   if (x->state != 1) return -1;
   for (int i = 0; i < x->n_stacks; ++i)
@@ -523,6 +660,13 @@ static int64_t install_patches(pvro_ctx* x, int64_t M) {
 }
 
 int64_t pvro_num_pixels(const pvro_ctx* x) { return x->P; }
+
+int pvro_get_mask(const pvro_ctx* x, uint8_t* out) {
+  if (x->state < 2) return -1;
+  if (x->mask) memcpy(out, x->mask, x->P);
+  else memset(out, 1, x->P);
+  return 0;
+}
 
 int pvro_get_patches(const pvro_ctx* x, int32_t* out) {
   if (x->state < 2) return -1;

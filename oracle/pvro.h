@@ -117,6 +117,24 @@ int pvro_add_stack(pvro_ctx*, const float* slices, int W, int H, int K,
 int pvro_add_stack_f64(pvro_ctx*, const double* slices, int W, int H, int K,
                        const double G[12], double thickness);
 int64_t pvro_extract_patches(pvro_ctx*, int size, int stride, int depth, int stride_z);
+/* f3 superpixels (Eq. 3 P:140-145 "superpixels ... SLIC"; reading Q33): integer
+ * SLIC on one slice (W x H floats, row-major) so that every decision is exact on any machine:
+ * intensities quantised I = floor(1023 (y - ymin) / (ymax - ymin) + 0.5) (fp64; I = 0 if
+ * ymax = ymin); cluster centres on the S-grid (cell (i, j) at min(i S + S/2, W-1),
+ * min(j S + S/2, H-1)) in 1/16 units; each pixel picks, among the centres of its own and the 8
+ * neighbouring grid cells, the smallest D = S^2 (16 I - cI)^2 + m^2 ((16 x - cx)^2 + (16 y - cy)^2)
+ * (int64; ties to the lowest cluster index k = j ceil(W/S) + i); centres move to the rounded
+ * means (c = (16 sum + n/2) / n; empty clusters stay); `iters` assign+update rounds, then a final
+ * assignment. labels [H][W] = k. Returns the number of clusters ceil(W/S) ceil(H/S). */
+int pvro_slic(int W, int H, const float* img, float ymin, float ymax, int S, int m, int iters, int32_t* labels);
+/* Superpixel patches of all stacks (reading Q32, Q33): SLIC on every slice (the stack's own
+ * intensity range), then per non-empty cluster (stack, slice, k order) the bounding box dilated
+ * by gamma pixels (clipped to the slice) and the mask of pixels within Chebyshev distance
+ * gamma of the cluster (dilation by a flat structuring element). Installs them as
+ * pvro_set_patches does. Returns M or < 0. */
+int64_t pvro_superpixel_patches(pvro_ctx*, int S, int m, int iters, int gamma);
+/* The per-pixel patch mask [P] (1 everywhere when none was given). */
+int pvro_get_mask(const pvro_ctx*, uint8_t* out);
 /* f3 (reading Q32): explicit patch table rects [n][7] = (stack, x0, y0, z0,
  * sx, sy, sz) and an optional per-pixel mask (patch-major, NULL = all): masked-out pixels are
  * never observations (kappa = 0). Instead of pvro_extract_patches. Returns M or < 0. */

@@ -70,6 +70,11 @@ def lib():
         L.pvro_extract_patches.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
         L.pvro_set_patches.restype = i64
         L.pvro_set_patches.argtypes = [vp, i64, vp, vp]
+        L.pvro_slic.restype = C.c_int
+        L.pvro_slic.argtypes = [C.c_int, C.c_int, vp, C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, vp]
+        L.pvro_superpixel_patches.restype = i64
+        L.pvro_superpixel_patches.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.pvro_get_mask.argtypes = [vp, vp]
         L.pvro_num_pixels.restype = i64
         L.pvro_num_pixels.argtypes = [vp]
         L.pvro_get_patches.argtypes = [vp, vp]
@@ -170,6 +175,17 @@ def patch_mixture(pbar, valid=None, rounds=50, tol=1e-6):
     return r, n
 
 
+def slic(img, S, m, iters=10, ymin=None, ymax=None):
+    """f3: integer SLIC labels of one slice (reading Q33)."""
+    img = np.ascontiguousarray(img, np.float32)
+    H, W = img.shape
+    lab = np.zeros((H, W), np.int32)
+    lo = float(img.min()) if ymin is None else ymin
+    hi = float(img.max()) if ymax is None else ymax
+    n = _chk(lib().pvro_slic(W, H, _p(img), lo, hi, int(S), int(m), int(iters), _p(lab)), "slic")
+    return lab, n
+
+
 def em_loglik(e, live, sigma2, c, m):
     e = np.ascontiguousarray(e, np.float64)
     live = np.ascontiguousarray(live, np.uint8)
@@ -240,6 +256,17 @@ class Oracle:
         self.M = _chk(lib().pvro_set_patches(self.h, len(rects), _p(rects), _p(m)), "set_patches")
         self.P = lib().pvro_num_pixels(self.h)
         return self.M
+
+    def superpixel_patches(self, S, m, iters=10, gamma=2):
+        """f3: SLIC superpixel patches of every slice, dilated by gamma (reading Q33)."""
+        self.M = _chk(lib().pvro_superpixel_patches(self.h, int(S), int(m), int(iters), int(gamma)), "superpixels")
+        self.P = lib().pvro_num_pixels(self.h)
+        return self.M
+
+    def mask(self):
+        out = np.zeros(self.P, np.uint8)
+        _chk(lib().pvro_get_mask(self.h, _p(out)), "get_mask")
+        return out
 
     def patches(self):
         out = np.zeros((self.M, 7), np.int32)

@@ -693,3 +693,59 @@ def test_masked_pixels_are_not_observations_and_adjoint_is_additive():
     Aa = a.adjoint(y)
     Ac = c.adjoint(y[mask == 1])
     assert np.abs(Aa - Ac).max() <= 1e-12 * max(1.0, np.abs(Aa).max())
+
+
+# ------------------------------------------------------------ f3 superpixels (SLIC, Q33)
+def test_slic_partition_locality_and_boundary_adherence():
+    """SLIC (Eq. 3): labels partition the slice; every pixel's cluster is one of the
+    3x3 grid cells around it (SLIC's 2S x 2S search window); on a two-region image with a
+    small compactness m no superpixel straddles the intensity edge (boundary adherence)."""
+    rng = np.random.default_rng(3)
+    img = rng.normal(500, 30, (48, 64)).astype(np.float32)
+    lab, nc = O.slic(img, 8, 10, 10)
+    assert nc == 6 * 8 and lab.min() >= 0 and lab.max() < nc
+    yy, xx = np.mgrid[0:48, 0:64]
+    ci, cj = lab % 8, lab // 8
+    assert (np.abs(ci - xx // 8) <= 1).all() and (np.abs(cj - yy // 8) <= 1).all()
+    two = np.where(xx < 29, 100.0, 900.0).astype(np.float32) + rng.normal(0, 5, (48, 64)).astype(np.float32)
+    lab2, _ = O.slic(two, 8, 1, 10)
+    for k in np.unique(lab2):
+        side = xx[lab2 == k] < 29
+        assert side.all() or (~side).all(), k
+
+
+def test_superpixel_patch_masks_are_dilated_superpixels():
+    """Superpixel patches: with gamma = 0 the masks partition every slice (each pixel
+    in exactly one patch) and each rectangle is its superpixel's bounding box; with gamma > 0
+    each mask is exactly the superpixel dilated by a (2 gamma + 1)^2 square, clipped to the
+    slice (scipy.ndimage.binary_dilation, a library routine)."""
+    from scipy import ndimage
+    prob = synth.make_problem("c1")
+    S, m, it = 8, 10, 5
+    for gamma in (0, 2):
+        orc = Oracle(prob["dims"], prob["spacing"], prob["origin"])
+        for st in prob["stacks"]:
+            orc.add_stack(st["slices"], st["G"], st["thickness"])
+        orc.superpixel_patches(S, m, it, gamma)
+        rects, mask = orc.patches(), orc.mask()
+        offs = np.concatenate([[0], np.cumsum(rects[:, 4] * rects[:, 5] * rects[:, 6])])
+        for si, st in enumerate(prob["stacks"]):
+            vol = st["slices"]
+            K, H, W = vol.shape
+            lo, hi = float(vol.min()), float(vol.max())
+            count = np.zeros((K, H, W), np.int32)
+            for z in range(K):
+                lab, nc = O.slic(vol[z], S, m, it, lo, hi)
+                mine = np.flatnonzero((rects[:, 0] == si) & (rects[:, 3] == z))
+                ks = [k for k in range(nc) if (lab == k).any()]
+                assert len(mine) == len(ks)
+                for s_, k in zip(mine, ks):
+                    r = rects[s_]
+                    got = mask[offs[s_]:offs[s_ + 1]].reshape(r[5], r[4]).astype(bool)
+                    want = ndimage.binary_dilation(lab == k, np.ones((2 * gamma + 1,) * 2, bool)) if gamma else lab == k
+                    ys, xs = np.nonzero(want)
+                    assert (r[1], r[2], r[4], r[5]) == (xs.min(), ys.min(), xs.max() - xs.min() + 1, ys.max() - ys.min() + 1)
+                    assert np.array_equal(got, want[r[2]:r[2] + r[5], r[1]:r[1] + r[4]])
+                    count[z, r[2]:r[2] + r[5], r[1]:r[1] + r[4]] += got
+            if gamma == 0:
+                assert (count == 1).all()
