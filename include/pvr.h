@@ -141,6 +141,22 @@ pvr_status pvr_extract_patches(pvr_ctx* ctx, int size, int stride, int depth, in
  * outside its stack). */
 pvr_status pvr_set_patches(pvr_ctx* ctx, int64_t n, const int32_t* rects, const uint8_t* mask,
                            int64_t* n_patches);
+/* f3 superpixels (Eq. 3; reading Q33): SLIC labels of every slice
+ * of one stack, int32 [K][H][W] (host or device): integer SLIC (exact, reproducible) with grid
+ * step S >= 2 pixels, compactness m >= 1 and `iters` >= 0 update rounds; label = the cluster
+ * index on the slice's ceil(W/S) x ceil(H/S) grid. Needs the stacks, before the patches
+ * (PVR_ERR_STATE otherwise). */
+pvr_status pvr_superpixels(pvr_ctx* ctx, int stack, int S, int m, int iters, int32_t* labels);
+/* f3 superpixel patches ("dilate each superpixel y_s by gamma pixels using a flat
+ * structuring element"; readings Q32, Q33), instead of pvr_extract_patches: SLIC on every
+ * slice of every stack, then one patch per non-empty superpixel (order: stack, slice,
+ * cluster): its bounding box dilated by gamma pixels (clipped to the slice) with the mask of
+ * the superpixel dilated by a (2 gamma + 1)^2 square. Errors as pvr_superpixels, plus
+ * PVR_ERR_EMPTY (no superpixel). */
+pvr_status pvr_superpixel_patches(pvr_ctx* ctx, int S, int m, int iters, int gamma, int64_t* n_patches);
+/* The per-pixel patch mask of this rank's pixels, uint8 [n_local_pixels] (1 everywhere unless
+ * the patches came with masks). Host or device. */
+pvr_status pvr_get_mask(pvr_ctx* ctx, uint8_t* out);
 /* Host-only helper (no GPU needed): contiguous shard plan of M patches over nranks,
  * balanced by cost[s] (pixels x PSF samples of patch s): rank r owns patches
  * [bounds[r], bounds[r+1]); bounds has nranks + 1 entries, bounds[0] = 0, bounds[nranks] = M.

@@ -1082,6 +1082,88 @@ pvr_status pvr_set_patches(pvr_ctx* c, int64_t n, const int32_t* rects, const ui
   return install_patches(c, mask, n_out);
 }
 
+// ---- f3 superpixels (superpixels.cu; readings Q32, Q33) -------------------------------
+pvr_status pvr_superpixels(pvr_ctx* c, int stack, int S, int m, int iters, int32_t* labels) {
+  GUARD(c);
+  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "superpixels need the stacks before patch extraction");
+  if (stack < 0 || stack >= (int)c->stacks.size() || S < 2 || m < 1 || iters < 0 || !labels)
+    return fail(c, PVR_ERR_ARG, "superpixels: stack, S >= 2, m >= 1, iters >= 0, labels");
+  const HostStack& st = c->stacks[stack];
+  const size_t n = (size_t)st.W * st.H * st.K;
+  int32_t* lab = nullptr;
+  if (is_device_ptr(labels)) lab = labels;
+  else CUDA_TRY(c, cudaMalloc(&lab, n * sizeof(int32_t)));
+  cudaError_t e = slic_stack(c->stream, st.y_dev, st.W, st.H, st.K, S, m, iters, lab);
+  if (e == cudaSuccess && lab != labels) e = cudaMemcpy(labels, lab, n * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (lab != labels) cudaFree(lab);
+  if (e != cudaSuccess) return fail(c, PVR_ERR_CUDA, "superpixels: %s", cudaGetErrorString(e));
+  return PVR_OK;
+}
+
+// Superpixel patches: per stack, slice and non-empty cluster (in that order) the cluster's
+// bounding box dilated by gamma (clipped to the slice) and its mask = the cluster dilated by a
+// (2 gamma + 1)^2 square (separable running max over rows, then columns).
+pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma, int64_t* n_out) {
+  GUARD(c);
+  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "superpixel patches need stacks and run once");
+  if (S < 2 || m < 1 || iters < 0 || gamma < 0) return fail(c, PVR_ERR_ARG, "S >= 2, m >= 1, iters >= 0, gamma >= 0");
+  std::vector<uint8_t> mask;
+  c->patches.clear();
+  for (int si = 0; si < (int)c->stacks.size(); ++si) {
+    const HostStack& st = c->stacks[si];
+    const int W = st.W, H = st.H;
+    std::vector<int32_t> lab((size_t)W * H * st.K);
+    pvr_status r = pvr_superpixels(c, si, S, m, iters, lab.data());
+    if (r != PVR_OK) return r;
+    const int nc = ((W + S - 1) / S) * ((H + S - 1) / S);
+    std::vector<int> bx0(nc), bx1(nc), by0(nc), by1(nc);
+    std::vector<uint8_t> rowd;
+    for (int z = 0; z < st.K; ++z) {
+      const int32_t* L = lab.data() + (size_t)z * W * H;
+      std::fill(bx0.begin(), bx0.end(), W);
+      std::fill(bx1.begin(), bx1.end(), -1);
+      std::fill(by0.begin(), by0.end(), H);
+      std::fill(by1.begin(), by1.end(), -1);
+      for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+          const int k = L[(size_t)y * W + x];
+          bx0[k] = std::min(bx0[k], x); bx1[k] = std::max(bx1[k], x);
+          by0[k] = std::min(by0[k], y); by1[k] = std::max(by1[k], y);
+        }
+      for (int k = 0; k < nc; ++k) {
+        if (bx1[k] < 0) continue;
+        const int x0 = std::max(0, bx0[k] - gamma), x1 = std::min(W - 1, bx1[k] + gamma);
+        const int y0 = std::max(0, by0[k] - gamma), y1 = std::min(H - 1, by1[k] + gamma);
+        const int sx = x1 - x0 + 1, sy = y1 - y0 + 1;
+        c->patches.push_back(HostPatch{si, x0, y0, z, sx, sy, 1});
+        // rows y0..y1: horizontal dilation of (L == k) over columns x0..x1
+        rowd.assign((size_t)sx * sy, 0);
+        for (int v = 0; v < sy; ++v) {
+          const int32_t* row = L + (size_t)(y0 + v) * W;
+          for (int u = 0; u < sx; ++u) {
+            const int xa = std::max(0, x0 + u - gamma), xb = std::min(W - 1, x0 + u + gamma);
+            uint8_t hit = 0;
+            for (int xx = xa; xx <= xb && !hit; ++xx) hit = row[xx] == k;
+            rowd[(size_t)v * sx + u] = hit;
+          }
+        }
+        // vertical dilation: rows outside y0..y1 cannot hold the cluster (the box is dilated)
+        const size_t base = mask.size();
+        mask.resize(base + (size_t)sx * sy);
+        for (int v = 0; v < sy; ++v)
+          for (int u = 0; u < sx; ++u) {
+            uint8_t hit = 0;
+            for (int vv = std::max(0, v - gamma); vv <= std::min(sy - 1, v + gamma) && !hit; ++vv)
+              hit = rowd[(size_t)vv * sx + u];
+            mask[base + (size_t)v * sx + u] = hit;
+          }
+      }
+    }
+  }
+  if (c->patches.empty()) return fail(c, PVR_ERR_EMPTY, "no superpixels");
+  return install_patches(c, mask.data(), n_out);
+}
+
 // Common tail of pvr_extract_patches / pvr_set_patches: PSF tables, pixel offsets, shards,
 // the concatenated stacks and the per-pixel / per-patch device arrays.
 static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_out) {
@@ -1145,6 +1227,19 @@ static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_ou
   c->st.patches = c->nloc;
   c->state = PATCHED;
   if (n_out) *n_out = c->M;
+  return PVR_OK;
+}
+
+pvr_status pvr_get_mask(pvr_ctx* c, uint8_t* out) {
+  GUARD(c);
+  if (c->state < PATCHED) return fail(c, PVR_ERR_STATE, "no patches yet");
+  if (!out) return fail(c, PVR_ERR_ARG, "null output");
+  if (!c->mask) {
+    if (is_device_ptr(out)) CUDA_TRY(c, cudaMemset(out, 1, c->nloc_pix));
+    else memset(out, 1, c->nloc_pix);
+    return PVR_OK;
+  }
+  CUDA_TRY(c, cudaMemcpy(out, c->mask, c->nloc_pix, is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
   return PVR_OK;
 }
 

@@ -144,6 +144,9 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         const float* kap, const float* e, const float* p, const float* w,
                         int init, float2* AC);
+// superpixels.cu (f3): SLIC labels [K][H][W] (device) of one stack (device), synchronous
+cudaError_t slic_stack(cudaStream_t st, const float* y, int W, int H, int K, int S, int m, int iters,
+                       int32_t* lab);
 // registration.cu (f1)
 void launch_register(cudaStream_t st, const RegArgs& a, int nloc, int max_pix, float* pose, int32_t* status);
 void launch_patch_cc(cudaStream_t st, const RegArgs& a, int n, int max_pix, const int32_t* which,

@@ -27,7 +27,8 @@ EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", 
            "pvr_comm_unique_id", "pvr_add_stack", "pvr_extract_patches", "pvr_plan_shards",
            "pvr_get_shard", "pvr_get_patches", "pvr_set_transforms", "pvr_set_volume",
            "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume", "pvr_rigidity_map",
-           "pvr_register_patches", "pvr_patch_cc", "pvr_set_patches",
+           "pvr_register_patches", "pvr_patch_cc", "pvr_set_patches", "pvr_superpixels",
+           "pvr_superpixel_patches", "pvr_get_mask",
            "pvr_get_weights", "pvr_get_taps", "pvr_get_em_state", "pvr_get_stats",
            "pvr_reset_stats"]
 
@@ -98,6 +99,9 @@ def lib():
             "pvr_register_patches": (i32, [vp, C.c_int, C.c_int, vp, vp, vp]),
             "pvr_patch_cc": (i32, [vp, C.c_int64, vp, vp, vp]),
             "pvr_set_patches": (i32, [vp, C.c_int64, vp, vp, vp]),
+            "pvr_superpixels": (i32, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+            "pvr_superpixel_patches": (i32, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+            "pvr_get_mask": (i32, [vp, vp]),
             "pvr_get_weights": (i32, [vp, vp, vp, vp]),
             "pvr_get_taps": (i32, [vp, vp, vp, vp, vp]),
             "pvr_get_em_state": (i32, [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i64),
@@ -345,6 +349,25 @@ class Context:
         self.M = n.value
         self.first, self.nloc, self.first_pix, self.nloc_pix = pvr_get_shard(self.h)
         return self.M
+
+    def superpixels(self, stack, S, m, iters=10, shape=None):
+        """f3: SLIC labels [K][H][W] of one stack (pvr_superpixels); shape = (K, H, W)."""
+        lab = np.zeros(shape, np.int32)
+        _check(self.h, lib().pvr_superpixels(self.h, int(stack), int(S), int(m), int(iters), _ptr(lab)))
+        return lab
+
+    def superpixel_patches(self, S, m, iters=10, gamma=2):
+        """f3: dilated SLIC superpixel patches of every slice (pvr_superpixel_patches)."""
+        n = C.c_int64()
+        _check(self.h, lib().pvr_superpixel_patches(self.h, int(S), int(m), int(iters), int(gamma), C.byref(n)))
+        self.M = n.value
+        self.first, self.nloc, self.first_pix, self.nloc_pix = pvr_get_shard(self.h)
+        return self.M
+
+    def mask(self):
+        out = np.zeros(self.nloc_pix, np.uint8)
+        _check(self.h, lib().pvr_get_mask(self.h, _ptr(out)))
+        return out
 
     def rigidity_map(self, out=None):
         """W^T(p pbar) / W^T 1 (f2; float32 [nz][ny][nx], host or device out)."""
