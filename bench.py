@@ -338,6 +338,36 @@ def run_ours(args):
     registration = {"ms_per_call": reg_ms, "patches": int(ctx.M), "patches_per_s": ctx.M / (reg_ms * 1e-3),
                     "registered": int((reg_st == 1).sum()),
                     "call": "pvr_register_patches(levels=4, iters=20), host outputs, wall clock"}
+
+    # ---- f3 superpixel patches: SLIC on every slice of the same stacks
+    # (S = 32 px, m = 20, 10 rounds, dilation 4 px), then one SR iteration on those patches
+    superpixels = None
+    if ws == 1 and not args.no_extras:
+        sp = Context(prob["dims"], prob["spacing"], prob["origin"], local, stream.cuda_stream)
+        for stk in prob["stacks"]:
+            sp.add_stack(stk["slices"], stk["G"], stk["thickness"])
+        torch.cuda.synchronize()
+        t0s = time.perf_counter()
+        Msp = sp.superpixel_patches(32, 20, 10, 4)
+        sp_ms = (time.perf_counter() - t0s) * 1e3
+        Tsp = np.tile(np.hstack([np.eye(3), np.zeros((3, 1))]), (Msp, 1, 1))
+        sp.set_transforms(Tsp)
+        sp.init_volume()
+        sp.sr_iterate(1, prob["alpha"], prob["lam"])
+        sp.reset_stats()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        sp.sr_iterate(3, prob["alpha"], prob["lam"])
+        s1.record(stream)
+        s1.synchronize()
+        sst = sp.stats()
+        it_ms = s0.elapsed_time(s1) / 3
+        superpixels = {"ms_extract": sp_ms, "patches": int(Msp), "ms_per_iteration": it_ms,
+                       "psf_samples_per_s": sst["psf_samples"] / 3 / (it_ms * 1e-3),
+                       "call": "pvr_superpixel_patches(S=32, m=20, iters=10, gamma=4) (wall clock), "
+                               "then pvr_sr_iterate on those patches (CUDA events)"}
+        sp.close()
     ctx.close()
 
     line = None
@@ -357,7 +387,8 @@ def run_ours(args):
                 "roofline": roof, "iteration_hbm_frac_alg": hbm_iter / pk["hbm_gbs"],
                 "kernels": breakdown, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(st["kernel_launches"]), "cpu_baseline": cpu,
-                "extras": {"f2_rigidity_map": rigidity, "f1_registration": registration}}
+                "extras": {"f2_rigidity_map": rigidity, "f1_registration": registration,
+                           "f3_superpixels": superpixels}}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -375,6 +406,7 @@ def main():
                     help="slices per stack of the oracle's bounded sample")
     ap.add_argument("--one-call", action="store_true", help="time one pvr_sr_iterate(K) call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the f3 superpixel measurement")
     ap.add_argument("--psf-quality", type=float, default=1.0,
                     help="f4 PSF lattice density q (2 = the q = 2 quality mode); default 1")
     args = ap.parse_args()
