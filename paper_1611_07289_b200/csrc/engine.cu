@@ -1107,6 +1107,7 @@ pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma
   GUARD(c);
   if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "superpixel patches need stacks and run once");
   if (S < 2 || m < 1 || iters < 0 || gamma < 0) return fail(c, PVR_ERR_ARG, "S >= 2, m >= 1, iters >= 0, gamma >= 0");
+  Trace tr;
   std::vector<uint8_t> mask;
   c->patches.clear();
   for (int si = 0; si < (int)c->stacks.size(); ++si) {
@@ -1115,15 +1116,16 @@ pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma
     std::vector<int32_t> lab((size_t)W * H * st.K);
     pvr_status r = pvr_superpixels(c, si, S, m, iters, lab.data());
     if (r != PVR_OK) return r;
+    tr.mark("  SLIC (GPU) + labels D2H");
     const int nc = ((W + S - 1) / S) * ((H + S - 1) / S);
-    std::vector<int> bx0(nc), bx1(nc), by0(nc), by1(nc);
-    std::vector<uint8_t> rowd;
+    // slices are independent: build their patches and masks in parallel, concatenate in order
+    std::vector<std::vector<HostPatch>> sp(st.K);
+    std::vector<std::vector<uint8_t>> sm(st.K);
+#pragma omp parallel for schedule(dynamic, 1)
     for (int z = 0; z < st.K; ++z) {
       const int32_t* L = lab.data() + (size_t)z * W * H;
-      std::fill(bx0.begin(), bx0.end(), W);
-      std::fill(bx1.begin(), bx1.end(), -1);
-      std::fill(by0.begin(), by0.end(), H);
-      std::fill(by1.begin(), by1.end(), -1);
+      std::vector<int> bx0(nc, W), bx1(nc, -1), by0(nc, H), by1(nc, -1);
+      std::vector<uint8_t> rowd;
       for (int y = 0; y < H; ++y)
         for (int x = 0; x < W; ++x) {
           const int k = L[(size_t)y * W + x];
@@ -1135,30 +1137,41 @@ pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma
         const int x0 = std::max(0, bx0[k] - gamma), x1 = std::min(W - 1, bx1[k] + gamma);
         const int y0 = std::max(0, by0[k] - gamma), y1 = std::min(H - 1, by1[k] + gamma);
         const int sx = x1 - x0 + 1, sy = y1 - y0 + 1;
-        c->patches.push_back(HostPatch{si, x0, y0, z, sx, sy, 1});
-        // rows y0..y1: horizontal dilation of (L == k) over columns x0..x1
+        sp[z].push_back(HostPatch{si, x0, y0, z, sx, sy, 1});
+        // horizontal dilation of (L == k) over the rectangle's rows (running count of hits in
+        // the window [u - gamma, u + gamma] of the row)
         rowd.assign((size_t)sx * sy, 0);
         for (int v = 0; v < sy; ++v) {
           const int32_t* row = L + (size_t)(y0 + v) * W;
+          int cnt = 0;
+          for (int xx = std::max(0, x0 - gamma); xx <= std::min(W - 1, x0 + gamma - 1); ++xx) cnt += row[xx] == k;
           for (int u = 0; u < sx; ++u) {
-            const int xa = std::max(0, x0 + u - gamma), xb = std::min(W - 1, x0 + u + gamma);
-            uint8_t hit = 0;
-            for (int xx = xa; xx <= xb && !hit; ++xx) hit = row[xx] == k;
-            rowd[(size_t)v * sx + u] = hit;
+            const int add = x0 + u + gamma, drop = x0 + u - gamma - 1;
+            if (add < W) cnt += row[add] == k;
+            if (drop >= 0) cnt -= row[drop] == k;
+            rowd[(size_t)v * sx + u] = cnt > 0;
           }
         }
-        // vertical dilation: rows outside y0..y1 cannot hold the cluster (the box is dilated)
-        const size_t base = mask.size();
-        mask.resize(base + (size_t)sx * sy);
-        for (int v = 0; v < sy; ++v)
-          for (int u = 0; u < sx; ++u) {
-            uint8_t hit = 0;
-            for (int vv = std::max(0, v - gamma); vv <= std::min(sy - 1, v + gamma) && !hit; ++vv)
-              hit = rowd[(size_t)vv * sx + u];
-            mask[base + (size_t)v * sx + u] = hit;
+        // vertical dilation (rows outside the dilated box cannot hold the cluster)
+        const size_t base = sm[z].size();
+        sm[z].resize(base + (size_t)sx * sy);
+        for (int u = 0; u < sx; ++u) {
+          int cnt = 0;
+          for (int vv = 0; vv <= std::min(sy - 1, gamma - 1); ++vv) cnt += rowd[(size_t)vv * sx + u];
+          for (int v = 0; v < sy; ++v) {
+            const int add = v + gamma, drop = v - gamma - 1;
+            if (add < sy) cnt += rowd[(size_t)add * sx + u];
+            if (drop >= 0) cnt -= rowd[(size_t)drop * sx + u];
+            sm[z][base + (size_t)v * sx + u] = cnt > 0;
           }
+        }
       }
     }
+    for (int z = 0; z < st.K; ++z) {
+      c->patches.insert(c->patches.end(), sp[z].begin(), sp[z].end());
+      mask.insert(mask.end(), sm[z].begin(), sm[z].end());
+    }
+    tr.mark("  superpixel boxes + masks");
   }
   if (c->patches.empty()) return fail(c, PVR_ERR_EMPTY, "no superpixels");
   return install_patches(c, mask.data(), n_out);
