@@ -244,10 +244,12 @@ def run_ours(args):
     }
     name = max(kern, key=lambda k: kern[k][0])
     kms, bound, flops, bytes_alg = kern[name]
-    traffic = None
+    traffic, counters = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(args.config, {}).get(name)
+            tj = json.load(f)
+        traffic = tj.get(args.config, {}).get(name)
+        counters = tj.get(args.config + "_counters", {}).get(name)
     except Exception:
         pass
     if bound == "alu":
@@ -256,6 +258,16 @@ def run_ours(args):
                 "unit": "TFLOP/s", "frac": ach / pk["fp32_tflops"], "traffic": traffic,
                 "peak_source": "FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)",
                 "ms_per_launch": kms, "flop_per_launch": flops}
+        if counters:  # the limiters the kernel actually hits (ncu counts per launch / live time)
+            fclk = pk["sm_max_mhz"] * 1e6
+            roof["secondary"] = {
+                "shared_lsu": {"achieved": counters["shared_wavefronts"] / (kms * 1e-3) / 1e9,
+                               "peak": 148 * fclk / 1e9, "unit": "G wavefronts/s",
+                               "frac": counters["shared_wavefronts"] / (kms * 1e-3) / (148 * fclk)},
+                "issue": {"achieved": counters["warp_instructions"] / (kms * 1e-3) / 1e9,
+                          "peak": 148 * 4 * fclk / 1e9, "unit": "G warp-instr/s",
+                          "frac": counters["warp_instructions"] / (kms * 1e-3) / (148 * 4 * fclk)},
+                "source": "ncu counts of one launch (profiles/ncu_traffic.json) over the live launch time"}
     else:
         ach = bytes_alg / (kms * 1e-3) / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"],
