@@ -131,6 +131,11 @@ pvr_status pvr_add_stack(pvr_ctx* ctx, const float* slices, int W, int H, int K,
  * stride_z < 1 or > depth), PVR_ERR_STATE, PVR_ERR_EMPTY (M = 0). */
 pvr_status pvr_extract_patches(pvr_ctx* ctx, int size, int stride, int depth, int stride_z,
                                int64_t* n_patches_out);
+/* Patch extraction (pvr_extract_patches, pvr_set_patches, pvr_superpixel_patches) may be
+ * repeated in a context that already has patches: the f3 multi-scale schedule (P:147-153,
+ * "different scales Y_i ... for each iteration i"). The previous patches, their weights and
+ * plans are dropped; the stacks and the reconstruction X stay; pvr_set_transforms (for the new
+ * patch count) is required before the next iteration. */
 /* f3 arbitrary-shape patches (Eq. 3: patches y_s need not be
  * squares; superpixels dilated by gamma pixels; reading Q32), instead of
  * pvr_extract_patches: n explicit rectangles rects int32 [n][7] = (stack, x0, y0, z0, sx, sy,

@@ -445,12 +445,25 @@ static int build_psf(pvro_ctx* x, ostack* st) {
 
 static int64_t install_patches(pvro_ctx* x, int64_t M);
 
+/* f3 multi-scale schedule: a context that has patches may extract new ones; the
+ * patch table and per-pixel state are dropped, the stacks and X stay (set_transforms again). */
+static void drop_patches(pvro_ctx* x) {
+  if (x->state < 2) return;
+  free(x->patch); free(x->pix0); free(x->T);
+  free(x->p); free(x->e); free(x->kappa); free(x->yhat); free(x->pbar); free(x->wpatch); free(x->mask);
+  x->patch = NULL; x->pix0 = NULL; x->T = NULL; x->p = x->e = x->kappa = x->yhat = NULL;
+  x->pbar = x->wpatch = NULL; x->mask = NULL;
+  for (int i = 0; i < x->n_stacks; ++i) { free(x->st[i].abc); free(x->st[i].psi); x->st[i].abc = NULL; x->st[i].psi = NULL; }
+  x->M = x->P = 0;
+  x->state = 1;
+}
+
 /* f3 (Eq. 3; reading Q32): an explicit patch table instead of
  * the square windows: rects [n][7] = (stack, x0, y0, z0, sx, sy, sz) inside their stacks, and
  * an optional per-pixel mask [sum sx sy sz] (patch-major; NULL = all pixels). Masked-out
  * pixels are never observations: their coverage kappa is 0 (so e = 0, p = 0, no splat). */
 int64_t pvro_set_patches(pvro_ctx* x, int64_t n, const int32_t* rects, const uint8_t* mask) {
-  if (x->state != 1 || n <= 0) return -1;
+  if (x->state < 1 || n <= 0) return -1;
   for (int64_t s = 0; s < n; ++s) {
     const int32_t* r = &rects[7 * s];
     if (r[0] < 0 || r[0] >= x->n_stacks) return -1;
@@ -459,6 +472,7 @@ int64_t pvro_set_patches(pvro_ctx* x, int64_t n, const int32_t* rects, const uin
         r[2] + r[5] > st->H || r[3] + r[6] > st->K)
       return -1;
   }
+  drop_patches(x);
   for (int i = 0; i < x->n_stacks; ++i)
     if (build_psf(x, &x->st[i]) != 0) return -1;
   x->patch = (int32_t*)malloc(7 * n * sizeof(int32_t));
@@ -538,7 +552,7 @@ int pvro_slic(int W, int H, const float* img, float ymin, float ymax, int S, int
 }
 
 int64_t pvro_superpixel_patches(pvro_ctx* x, int S, int m, int iters, int gamma) {
-  if (x->state != 1 || S < 2 || m < 1 || iters < 0 || gamma < 0) return -1;
+  if (x->state < 1 || S < 2 || m < 1 || iters < 0 || gamma < 0) return -1;
   /* pass 0 counts (rects, pixels); pass 1 fills */
   int64_t nrect = 0, npix = 0;
   int32_t* rects = NULL;
@@ -609,7 +623,8 @@ int64_t pvro_superpixel_patches(pvro_ctx* x, int S, int m, int iters, int gamma)
 }
 
 int64_t pvro_extract_patches(pvro_ctx* x, int size, int stride, int depth, int stride_z) {
-  if (x->state != 1) return -1;
+  if (x->state < 1) return -1;
+  drop_patches(x);
   for (int i = 0; i < x->n_stacks; ++i)
     if (build_psf(x, &x->st[i]) != 0) return -1;
   int64_t M = 0;

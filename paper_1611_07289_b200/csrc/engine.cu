@@ -1040,15 +1040,52 @@ pvr_status pvr_plan_shards(const int64_t* cost, int64_t M, int nranks, int64_t* 
 
 static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_out);
 
+// f3 multi-scale schedule ("different scales Y_i ... for each iteration i"):
+// patches may be re-extracted in a context that already has patches. Every per-patch and
+// per-pixel structure is dropped (plans, caches, weights, EM / registration scratch); the
+// stacks and the reconstruction X stay; pvr_set_transforms is required again.
+static pvr_status begin_extraction(pvr_ctx* c) {
+  if (c->state == STACKS) return PVR_OK;
+  if (c->state < STACKS) return fail(c, PVR_ERR_STATE, "patches need stacks");
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  void* ptrs[] = {c->e, c->p, c->kap, c->pbar, c->w, c->tab, c->psf, c->pdev, c->fplan.mem, c->fplan.grp,
+                  c->bplan.mem, c->bplan.grp, c->iplan.mem, c->iplan.grp, c->regP, c->rpart, c->nlivep, c->mask};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  c->e = c->p = c->kap = c->pbar = c->w = c->tab = nullptr;
+  c->psf = nullptr;
+  c->pdev = nullptr;
+  c->regP = nullptr;
+  c->regP_cap = 0;
+  c->rpart = nullptr;
+  c->nlivep = nullptr;
+  c->mask = nullptr;
+  for (pvr_ctx::Plan* pl : {&c->fplan, &c->bplan, &c->iplan}) {
+    pl->mem = nullptr;
+    pl->grp = nullptr;
+    pl->mem_cap = pl->grp_cap = 0;
+    pl->ngroups = 0;
+  }
+  c->iplan_valid = false;
+  c->ngcache.clear();
+  c->geo.clear();
+  c->Tloc.clear();
+  c->patches.clear();
+  c->state = STACKS;
+  return PVR_OK;
+}
+
 pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int stride_z, int64_t* n_out) {
   GUARD(c);
-  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "extract_patches needs stacks and runs once");
+  if (c->state < STACKS) return fail(c, PVR_ERR_STATE, "extract_patches needs stacks");
   if (size < 1 || stride < 1 || stride > size || depth < 1 || stride_z < 1 || stride_z > depth)
     return fail(c, PVR_ERR_ARG, "invalid patch size/stride (1 <= stride <= size, 1 <= stride_z <= depth)");
   for (auto& st : c->stacks)
     if (size > st.W || size > st.H || depth > st.K)
       return fail(c, PVR_ERR_ARG, "patch %dx%dx%d larger than a %dx%dx%d stack", size, size, depth,
                   st.W, st.H, st.K);
+  pvr_status rb = begin_extraction(c);
+  if (rb != PVR_OK) return rb;
   // patch list, order stack, z0, y0, x0
   c->patches.clear();
   for (int si = 0; si < (int)c->stacks.size(); ++si) {
@@ -1064,12 +1101,12 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
 // f3 (reading Q32): explicit patch rectangles [n][7] with an optional per-pixel mask.
 pvr_status pvr_set_patches(pvr_ctx* c, int64_t n, const int32_t* rects, const uint8_t* mask, int64_t* n_out) {
   GUARD(c);
-  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "set_patches needs stacks and runs once");
+  if (c->state < STACKS) return fail(c, PVR_ERR_STATE, "set_patches needs stacks");
   if (n <= 0 || !rects) return fail(c, PVR_ERR_ARG, "set_patches needs n >= 1 rectangles");
   std::vector<int32_t> rh(7 * n);
   if (is_device_ptr(rects)) CUDA_TRY(c, cudaMemcpy(rh.data(), rects, rh.size() * 4, cudaMemcpyDeviceToHost));
   else memcpy(rh.data(), rects, rh.size() * 4);
-  c->patches.clear();
+  std::vector<HostPatch> list;
   for (int64_t s = 0; s < n; ++s) {
     const int32_t* r = &rh[7 * s];
     if (r[0] < 0 || r[0] >= (int)c->stacks.size()) return fail(c, PVR_ERR_ARG, "patch %lld: bad stack", (long long)s);
@@ -1077,15 +1114,18 @@ pvr_status pvr_set_patches(pvr_ctx* c, int64_t n, const int32_t* rects, const ui
     if (r[4] < 1 || r[5] < 1 || r[6] < 1 || r[1] < 0 || r[2] < 0 || r[3] < 0 || r[1] + r[4] > st.W ||
         r[2] + r[5] > st.H || r[3] + r[6] > st.K)
       return fail(c, PVR_ERR_ARG, "patch %lld outside its %dx%dx%d stack", (long long)s, st.W, st.H, st.K);
-    c->patches.push_back(HostPatch{r[0], r[1], r[2], r[3], r[4], r[5], r[6]});
+    list.push_back(HostPatch{r[0], r[1], r[2], r[3], r[4], r[5], r[6]});
   }
+  pvr_status rb = begin_extraction(c);
+  if (rb != PVR_OK) return rb;
+  c->patches.swap(list);
   return install_patches(c, mask, n_out);
 }
 
 // ---- f3 superpixels (superpixels.cu; readings Q32, Q33) -------------------------------
 pvr_status pvr_superpixels(pvr_ctx* c, int stack, int S, int m, int iters, int32_t* labels) {
   GUARD(c);
-  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "superpixels need the stacks before patch extraction");
+  if (c->state < STACKS) return fail(c, PVR_ERR_STATE, "superpixels need the stacks");
   if (stack < 0 || stack >= (int)c->stacks.size() || S < 2 || m < 1 || iters < 0 || !labels)
     return fail(c, PVR_ERR_ARG, "superpixels: stack, S >= 2, m >= 1, iters >= 0, labels");
   const HostStack& st = c->stacks[stack];
@@ -1093,7 +1133,8 @@ pvr_status pvr_superpixels(pvr_ctx* c, int stack, int S, int m, int iters, int32
   int32_t* lab = nullptr;
   if (is_device_ptr(labels)) lab = labels;
   else CUDA_TRY(c, cudaMalloc(&lab, n * sizeof(int32_t)));
-  cudaError_t e = slic_stack(c->stream, st.y_dev, st.W, st.H, st.K, S, m, iters, lab);
+  const float* yd = st.y_dev ? st.y_dev : c->ys + st.y_off;  // before / after the first extraction
+  cudaError_t e = slic_stack(c->stream, yd, st.W, st.H, st.K, S, m, iters, lab);
   if (e == cudaSuccess && lab != labels) e = cudaMemcpy(labels, lab, n * sizeof(int32_t), cudaMemcpyDeviceToHost);
   if (lab != labels) cudaFree(lab);
   if (e != cudaSuccess) return fail(c, PVR_ERR_CUDA, "superpixels: %s", cudaGetErrorString(e));
@@ -1105,11 +1146,11 @@ pvr_status pvr_superpixels(pvr_ctx* c, int stack, int S, int m, int iters, int32
 // (2 gamma + 1)^2 square (separable running max over rows, then columns).
 pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma, int64_t* n_out) {
   GUARD(c);
-  if (c->state != STACKS) return fail(c, PVR_ERR_STATE, "superpixel patches need stacks and run once");
+  if (c->state < STACKS) return fail(c, PVR_ERR_STATE, "superpixel patches need stacks");
   if (S < 2 || m < 1 || iters < 0 || gamma < 0) return fail(c, PVR_ERR_ARG, "S >= 2, m >= 1, iters >= 0, gamma >= 0");
   Trace tr;
   std::vector<uint8_t> mask;
-  c->patches.clear();
+  std::vector<HostPatch> list;
   for (int si = 0; si < (int)c->stacks.size(); ++si) {
     const HostStack& st = c->stacks[si];
     const int W = st.W, H = st.H;
@@ -1168,12 +1209,15 @@ pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma
       }
     }
     for (int z = 0; z < st.K; ++z) {
-      c->patches.insert(c->patches.end(), sp[z].begin(), sp[z].end());
+      list.insert(list.end(), sp[z].begin(), sp[z].end());
       mask.insert(mask.end(), sm[z].begin(), sm[z].end());
     }
     tr.mark("  superpixel boxes + masks");
   }
-  if (c->patches.empty()) return fail(c, PVR_ERR_EMPTY, "no superpixels");
+  if (list.empty()) return fail(c, PVR_ERR_EMPTY, "no superpixels");
+  pvr_status rb = begin_extraction(c);
+  if (rb != PVR_OK) return rb;
+  c->patches.swap(list);
   return install_patches(c, mask.data(), n_out);
 }
 
@@ -1203,15 +1247,17 @@ static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_ou
   c->nloc = bounds[c->rank + 1] - bounds[c->rank];
   c->first_pix = c->pix0_global[c->first];
   c->nloc_pix = c->pix0_global[c->first + c->nloc] - c->first_pix;
-  // concatenated stacks
-  int64_t L = 0;
-  for (auto& st : c->stacks) { st.y_off = L; L += (int64_t)st.W * st.H * st.K; }
-  CUDA_TRY(c, cudaMalloc(&c->ys, std::max<int64_t>(L, 1) * sizeof(float)));
-  for (auto& st : c->stacks)
-    CUDA_TRY(c, cudaMemcpyAsync(c->ys + st.y_off, st.y_dev, (size_t)st.W * st.H * st.K * sizeof(float),
-                                cudaMemcpyDeviceToDevice, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  for (auto& st : c->stacks) { cudaFree(st.y_dev); st.y_dev = nullptr; }
+  // concatenated stacks (once: a re-extraction keeps them)
+  if (!c->ys) {
+    int64_t L = 0;
+    for (auto& st : c->stacks) { st.y_off = L; L += (int64_t)st.W * st.H * st.K; }
+    CUDA_TRY(c, cudaMalloc(&c->ys, std::max<int64_t>(L, 1) * sizeof(float)));
+    for (auto& st : c->stacks)
+      CUDA_TRY(c, cudaMemcpyAsync(c->ys + st.y_off, st.y_dev, (size_t)st.W * st.H * st.K * sizeof(float),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (auto& st : c->stacks) { cudaFree(st.y_dev); st.y_dev = nullptr; }
+  }
   // per-pixel / per-patch arrays of the local shard
   const size_t np = (size_t)std::max<int64_t>(c->nloc_pix, 1), mp = (size_t)std::max<int64_t>(c->nloc, 1);
   CUDA_TRY(c, cudaMalloc(&c->e, np * sizeof(float)));

@@ -66,3 +66,27 @@ def test_superpixel_patches_identical_and_sr_parity():
             assert dp <= 1e-3 and dw <= 1e-3
     finally:
         ctx.close()
+
+
+def test_multiscale_reextraction():
+    """f3 multi-scale schedule (different patch scales per iteration): one context
+    re-extracts superpixel patches at a finer scale between iterations, keeping X; both sides
+    follow the same schedule within the parity bar."""
+    prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
+    orc, ctx = both(prob)
+    try:
+        for i, (S, gamma) in enumerate([(24, 4), (12, 2)]):
+            Mo = orc.superpixel_patches(S, 20, 10, gamma)
+            Mg = ctx.superpixel_patches(S, 20, 10, gamma)
+            assert Mo == Mg and np.array_equal(ctx.patches(), orc.patches())
+            T = np.tile(np.hstack([np.eye(3), np.zeros((3, 1))]), (Mo, 1, 1))
+            orc.set_transforms(T)
+            ctx.set_transforms(T)
+            if i == 0:
+                orc.init_volume()
+                ctx.init_volume()
+            orc.sr_iterate(1, prob["alpha"], prob["lam"])
+            ctx.sr_iterate(1, prob["alpha"], prob["lam"])
+            assert rel_l2(ctx.volume(), orc.volume()) <= 1e-4, (S, rel_l2(ctx.volume(), orc.volume()))
+    finally:
+        ctx.close()
