@@ -247,3 +247,27 @@ def test_explicit_masked_patches():
             assert dp <= 1e-3 and dw <= 1e-3
     finally:
         ctx.close()
+
+
+def test_odd_volume_dims_small_patches():
+    """Edge shapes: a 37^3 volume (rows padded to 40 floats for the TMA pitch), 29x29 stacks
+    of 5 slices, 8x8 patches at stride 4 (ragged last windows)."""
+    prob = synth.make_problem("c3", scale=(37, 29, 5), size=8, stride=4)
+    run_pair(prob, 2)
+
+
+def test_delta_psf_mode():
+    """psf_mode = 1 (test-only delta PSF: one sample at the pixel centre, S:64 trilinear
+    sampling) through the same kernels."""
+    prob = synth.make_problem("c1")
+    run_pair(prob, 2, params={"psf_mode": 1})
+
+
+def test_patches_partly_outside_the_volume():
+    """Transforms that move a quarter of the patches 14 mm out along x: their pixels are
+    partly unobserved (kappa < tau_obs) or graze the grid border."""
+    prob = synth.make_problem("c2", scale=(64, 64, 12))
+    T = np.asarray(prob["T"], np.float64).reshape(-1, 3, 4).copy()
+    T[::4, 0, 3] += 14.0
+    prob["T"] = T
+    run_pair(prob, 2)
