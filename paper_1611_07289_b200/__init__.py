@@ -6,3 +6,4 @@ ctypes binding (pvr.py) with the same names as the C calls.
 """
 from .pvr import (Context, PvrError, load_problem, pvr_plan_shards, pvr_version,  # noqa: F401
                   lib, SO_PATH)
+from .pipeline import reconstruct  # noqa: F401
