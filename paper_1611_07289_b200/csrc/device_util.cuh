@@ -52,9 +52,6 @@ __device__ __forceinline__ void block_reduce_store(double (&s)[NS], float (&mx)[
   __syncthreads();
 }
 
-__device__ __forceinline__ void red_v2(float2* addr, float a, float c) {
-  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(c) : "memory");
-}
 __device__ __forceinline__ void red_v4(float2* addr, float a0, float c0, float a1, float c1) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a0), "f"(c0),
                "f"(a1), "f"(c1)
