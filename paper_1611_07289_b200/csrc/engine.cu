@@ -137,7 +137,12 @@ struct pvr_ctx {
     MemberDev* mem = nullptr;
     GroupDev* grp = nullptr;
     size_t mem_cap = 0, grp_cap = 0;
-  } fplan, bplan, iplan;  // forward/coverage, backprojection, init backprojection (hi/lo)
+    int64_t nmem = 0;
+    void* btab = nullptr;          // backprojection member / group tables (geometry only)
+    size_t btab_cap = 0, btab_goff = 0;
+    uint64_t btab_epoch = 0;       // geo_epoch the tables were built for (0: never)
+  } fplan, bplan, iplan;
+  uint64_t geo_epoch = 1;          // bumped whenever patch geometry or a plan changes  // forward/coverage, backprojection, init backprojection (hi/lo)
   bool iplan_valid = false;     // the init plan is built lazily by pvr_init_volume
   std::vector<PatchGeo> geo;    // composed geometry of the local patches (last set_transforms)
   std::vector<double> Tloc;     // the local patches' transforms (last set_transforms), [nloc][12]
@@ -397,7 +402,7 @@ void free_dev(pvr_ctx* c) {
     if (s.y_dev) cudaFree(s.y_dev), s.y_dev = nullptr;
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
-                  c->iplan.mem, c->iplan.grp,
+                  c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
                   c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep, c->mask};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -748,6 +753,8 @@ pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
   CUDA_TRY(c, cudaMemcpyAsync(pl.grp, pb.grp.data(), pb.grp.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // the host vectors go out of scope
   pl.ngroups = (int)pb.grp.size();
+  pl.nmem = (int64_t)pb.mem.size();
+  ++c->geo_epoch;
   pl.nsplit = pb.nsplit;
   pl.tile_words = (int)((pb.max_tile_vox + 3) & ~int64_t(3));
   pl.r_bytes = (int)((pb.max_r_bytes + 15) & ~int64_t(15));
@@ -1049,7 +1056,8 @@ static pvr_status begin_extraction(pvr_ctx* c) {
   if (c->state < STACKS) return fail(c, PVR_ERR_STATE, "patches need stacks");
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   void* ptrs[] = {c->e, c->p, c->kap, c->pbar, c->w, c->tab, c->psf, c->pdev, c->fplan.mem, c->fplan.grp,
-                  c->bplan.mem, c->bplan.grp, c->iplan.mem, c->iplan.grp, c->regP, c->rpart, c->nlivep, c->mask};
+                  c->bplan.mem, c->bplan.grp, c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
+                  c->regP, c->rpart, c->nlivep, c->mask};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   c->e = c->p = c->kap = c->pbar = c->w = c->tab = nullptr;
@@ -1065,7 +1073,12 @@ static pvr_status begin_extraction(pvr_ctx* c) {
     pl->grp = nullptr;
     pl->mem_cap = pl->grp_cap = 0;
     pl->ngroups = 0;
+    pl->nmem = 0;
+    pl->btab = nullptr;
+    pl->btab_cap = 0;
+    pl->btab_epoch = 0;
   }
+  ++c->geo_epoch;
   c->iplan_valid = false;
   c->ngcache.clear();
   c->geo.clear();
@@ -1393,6 +1406,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
     }
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
+  ++c->geo_epoch;  // the backprojection tables are rebuilt by the next backprojection
   tr.mark("compose patches");
   pvr_status r = PVR_ERR_STATE;
   if (c->fplan.ngroups > 0 && c->bplan.ngroups > 0) r = replan_on_device(c);
@@ -1449,6 +1463,31 @@ pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
   return PVR_OK;
 }
 
+// Backprojection with the plan's member tables, rebuilt first when the geometry changed.
+pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const LatticeArgs& lb, const float* w,
+                       int init) {
+  size_t goff = 0;
+  const size_t bytes = bp_table_bytes(pl.nmem, pl.ngroups, &goff);
+  if (bytes > pl.btab_cap) {
+    if (pl.btab) cudaFree(pl.btab);
+    pl.btab = nullptr;
+    pl.btab_cap = 0;
+    CUDA_TRY(c, cudaMalloc(&pl.btab, bytes));
+    pl.btab_cap = bytes;
+    pl.btab_epoch = 0;
+  }
+  if (pl.btab_goff != goff) pl.btab_epoch = 0;
+  pl.btab_goff = goff;
+  const bool build = pl.btab_epoch != c->geo_epoch;
+  launch_backproject(s, lb, pl.tile_words, pl.r_bytes, pl.btab, goff, build, c->kap, c->e, c->p, w, init, c->AC);
+  CHECK_LAUNCH(c);
+  if (build) {
+    pl.btab_epoch = c->geo_epoch;
+    c->st.kernel_launches += 1;
+  }
+  return PVR_OK;
+}
+
 pvr_status pvr_init_volume(pvr_ctx* c) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
@@ -1459,8 +1498,8 @@ pvr_status pvr_init_volume(pvr_ctx* c) {
   }
   const LatticeArgs lb = lattice_args(c, c->iplan);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
-  launch_backproject(c->stream, lb, c->iplan.tile_words, c->iplan.r_bytes, c->kap, c->e, c->p, c->w, 1, c->AC);
-  CHECK_LAUNCH(c);
+  pvr_status rb = backproject(c, c->stream, c->iplan, lb, c->w, 1);
+  if (rb != PVR_OK) return rb;
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;
   launch_init_fill(c->stream, c->AC, c->dims, c->nxp, lb.prm, c->X[c->cur]);
@@ -1481,8 +1520,8 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
   const LatticeArgs lb = lattice_args(c, c->iplan);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
   // W^T (p pbar) and W^T 1 with the exact hi/lo tiles of the init pass (pbar rides in w)
-  launch_backproject(c->stream, lb, c->iplan.tile_words, c->iplan.r_bytes, c->kap, c->e, c->p, c->pbar, 2, c->AC);
-  CHECK_LAUNCH(c);
+  pvr_status rb = backproject(c, c->stream, c->iplan, lb, c->pbar, 2);
+  if (rb != PVR_OK) return rb;
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;
   float* tmp = c->X[1 - c->cur];  // scratch between iterations
@@ -1768,8 +1807,8 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     }
     if (prof) cudaEventRecord((*ev)[EV_EST1], s);
     CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
-    launch_backproject(s, lb, c->bplan.tile_words, c->bplan.r_bytes, c->kap, c->e, c->p, c->w, 0, c->AC);
-    CHECK_LAUNCH(c);
+    r = backproject(c, s, c->bplan, lb, c->w, 0);
+    if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_BP1], s);
     r = allreduce_ac(c);
     if (r != PVR_OK) return r;

@@ -334,8 +334,10 @@ struct Tile {  // planar int32 accumulators of the group bbox: A, C (+ lo words 
 
 // Per-member constants of the backprojection, in the member's window frame: axis 0 (m) is
 // the dominant component of the sample step dir * Qc (so plane floors never decrease along a
-// line), axes 1, 2 (p, q) the transverse ones. Built by warp 0 once per group.
-struct BpMember {
+// line), axes 1, 2 (p, q) the transverse ones. Geometry only: built once per geometry by
+// k_bp_table (a warp per group, a lane per member) into global memory, indexed like the plan's
+// members, and copied into shared memory by each group's CTA.
+struct __align__(16) BpMember {
   float r[3];              // frame position of lattice point (Ulo, Vlo, first sample) - o
   float du[3], dv[3], dc[3];  // frame steps per U, per V, per sample (dc[0] >= 0)
   int o[3];                // integer origin in the tile (frame)
@@ -348,8 +350,15 @@ struct BpMember {
   int plu, plv, phu, phv, rw;
   int64_t pixz, yz;        // first pixel of slice z in the local arrays / in the stacks
   int sx, W;
-  float ws;                // patch weight w (1 in the init and rigidity passes)
-  float vs;                // rigidity pass: the patch score pbar
+  int patch;               // local patch index (its weight w is read per iteration)
+};
+static_assert(sizeof(BpMember) % 16 == 0, "BpMember is copied as int4");
+
+struct __align__(16) BpGroupHdr {  // per-group totals and the group's stack PSF constants
+  int nl, np;              // lattice lines / pixels of all members
+  int nu, nv, ru, rv, ip0, tp0, ntp;
+  float tpmax;
+  int pad[2];
 };
 
 __device__ __forceinline__ float pick3(const float (&v)[3], int ax) {
@@ -362,7 +371,6 @@ __device__ __forceinline__ int pick3i(const int (&v)[3], int ax) {
 constexpr int kCOff = kBpTileBytes / 2;  // byte offset of the C plane in the iteration tile
 // init / rigidity tile (HILO): A_hi, C_hi, A_lo, C_lo planes at fixed byte offsets
 constexpr int kHQ = kInitTileBytes / 4;
-static_assert(kInitTileBytes == kBpTileBytes, "both tiles put R at the same offset");
 
 template <bool HILO>
 __device__ __forceinline__ void flush_word(unsigned a, float v, bool is_c) {
@@ -481,11 +489,91 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
   flush4<HILO>(a0 + sm4, sp4, sq4, P1, mag);
 }
 
+// Member tables of all groups of a backprojection plan (geometry only: rebuilt after every
+// set_transforms / re-plan, reused by every iteration). One warp per group, one lane per
+// member; the flattened line / pixel ranges by warp scans.
+__global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* __restrict__ tm,
+                                                      BpGroupHdr* __restrict__ th) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (kThreads >> 5) + (threadIdx.x >> 5);
+  if (g >= a.ngroups) return;  // uniform per warp
+  const GroupDev G = a.grp[g];
+  const int dx = G.dim[0], dy = G.dim[1];
+  int nl = 0, np = 0;
+  BpMember M;
+  MemberGeom mg;
+  if (lane < G.nm) {
+    const MemberDev m = a.mem[G.m0 + lane];
+    const PatchDev& pt = a.P[m.patch];
+    mg = member_geom(a, pt);
+    const Owned o = owned_range(m, pt, mg);
+    const float aq0 = fabsf(mg.qc[0]), aq1 = fabsf(mg.qc[1]), aq2 = fabsf(mg.qc[2]);
+    const int am = (aq0 >= aq1 && aq0 >= aq2) ? 0 : (aq1 >= aq2 ? 1 : 2);
+    const int ap = am == 0 ? 1 : 0, aq = am == 2 ? 1 : 2;
+    const int dir = pick3(mg.qc, am) >= 0.0f ? 1 : -1;
+    const int cs = dir > 0 ? m.c0 : m.c1;
+    int ob[3];
+    float of[3];
+    lattice_origin(pt, m.z, o.Ulo, o.Vlo, cs, G.lo, ob, of);
+    const int st[3] = {1, dx, dx * dy};
+    const int ax[3] = {am, ap, aq};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      M.r[d] = pick3(of, ax[d]);
+      M.o[d] = pick3i(ob, ax[d]);
+      M.s[d] = pick3i(st, ax[d]);
+      M.du[d] = pick3(mg.qa, ax[d]);
+      M.dv[d] = pick3(mg.qb, ax[d]);
+      M.dc[d] = (float)dir * pick3(mg.qc, ax[d]);
+    }
+    M.ti0 = cs + mg.cmax;
+    M.dti = dir;
+    M.ns = m.c1 - m.c0 + 1;
+    M.Ulo = o.Ulo;
+    M.Vlo = o.Vlo;
+    M.nU = o.Uhi - o.Ulo;
+    M.inv_nU = 1.0f / (float)M.nU;
+    M.plu = o.plu; M.phu = o.phu; M.plv = o.plv; M.phv = o.phv;
+    M.rw = o.phu - o.plu + 1;
+    M.inv_rw = 1.0f / (float)M.rw;
+    M.pixz = pt.pix0 + (int64_t)m.z * pt.sy * pt.sx;
+    M.yz = pt.y0off + (int64_t)m.z * pt.HW;
+    M.sx = pt.sx;
+    M.W = pt.W;
+    M.patch = m.patch;
+    nl = M.nU * (o.Vhi - o.Vlo);
+    np = M.rw * (o.phv - o.plv + 1);
+  }
+  int sl = nl, sp = np;  // inclusive scans over the members
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int tl = __shfl_up_sync(0xffffffffu, sl, d), tp = __shfl_up_sync(0xffffffffu, sp, d);
+    if (lane >= d) { sl += tl; sp += tp; }
+  }
+  const int tl = __shfl_sync(0xffffffffu, sl, G.nm - 1), tpx = __shfl_sync(0xffffffffu, sp, G.nm - 1);
+  if (lane < G.nm) {
+    M.lbeg = sl - nl; M.lend = sl;
+    M.pbeg = sp - np; M.pend = sp;
+    tm[G.m0 + lane] = M;
+  }
+  if (lane == 0) {  // all members of a group share the stack (and its PSF)
+    BpGroupHdr h;
+    h.nl = tl; h.np = tpx;
+    h.nu = mg.nu; h.nv = mg.nv; h.ru = mg.ru; h.rv = mg.rv;
+    h.ip0 = mg.ip0; h.tp0 = mg.tp0; h.ntp = mg.ntp;
+    h.tpmax = a.psf[a.P[a.mem[G.m0].patch].stack].tpmax;
+    h.pad[0] = h.pad[1] = 0;
+    th[g] = h;
+  }
+}
+
 // Dynamic shared memory: HILO (init pass): 4 x tile_words int32 (A, C, A_lo, C_lo), then R;
 // iterations: A at 0, C at the fixed byte offset kCOff (an immediate in the splat's shared
-// reductions), R after kBpTileBytes.
+// reductions), R after kBpTileBytes (init: after kInitTileBytes).
 template <bool HILO>
 __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile_words,
+                                                         const BpMember* __restrict__ tm,
+                                                         const BpGroupHdr* __restrict__ th,
                                                          const float* __restrict__ kap,
                                                          const float* __restrict__ e,
                                                          const float* __restrict__ p,
@@ -495,12 +583,10 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
   int* base = reinterpret_cast<int*>(bsm4);
   constexpr int NW = HILO ? 4 : 2;
   int* cbase = HILO ? base + kHQ / 4 : base + kCOff / 4;
-  float2* R = reinterpret_cast<float2*>(base + kBpTileBytes / 4);
+  float2* R = reinterpret_cast<float2*>(base + (HILO ? kInitTileBytes : kBpTileBytes) / 4);
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
-  __shared__ float s_red[2][32];
-  __shared__ float s_scale[2];
+  __shared__ float s_red[2][kThreads >> 5];
   __shared__ BpMember sbm[kMaxMembers];
-  __shared__ int s_nl, s_np;  // lines / pixels of the group
   const int3 n = a.n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned tA = (unsigned)__cvta_generic_to_shared(base);
@@ -508,88 +594,52 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
+    const BpGroupHdr H = th[g];
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
     __syncthreads();  // previous group's flush is done with the tile / R / tables / sbm
-    // ---- member table (warp 0, one lane per member) with flattened line / pixel ranges
-    if (wid == 0) {
-      int nl = 0, np = 0;
-      BpMember M;
-      if (lane < G.nm) {
-        const MemberDev m = a.mem[G.m0 + lane];
-        const PatchDev& pt = a.P[m.patch];
-        const MemberGeom mg = member_geom(a, pt);
-        const Owned o = owned_range(m, pt, mg);
-        const float aq0 = fabsf(mg.qc[0]), aq1 = fabsf(mg.qc[1]), aq2 = fabsf(mg.qc[2]);
-        const int am = (aq0 >= aq1 && aq0 >= aq2) ? 0 : (aq1 >= aq2 ? 1 : 2);
-        const int ap = am == 0 ? 1 : 0, aq = am == 2 ? 1 : 2;
-        const int dir = pick3(mg.qc, am) >= 0.0f ? 1 : -1;
-        const int cs = dir > 0 ? m.c0 : m.c1;
-        int ob[3];
-        float of[3];
-        lattice_origin(pt, m.z, o.Ulo, o.Vlo, cs, G.lo, ob, of);
-        const int st[3] = {1, dx, dx * dy};
-        const int ax[3] = {am, ap, aq};
+    {  // member table, the stack's PSF factors, the tile reset
+      const int4* src = reinterpret_cast<const int4*>(tm + G.m0);
+      int4* dst = reinterpret_cast<int4*>(sbm);
+      const int nq = G.nm * (int)(sizeof(BpMember) / 16);
+      for (int i = threadIdx.x; i < nq; i += kThreads) dst[i] = __ldg(src + i);
+      const int nip = (2 * H.ru + 1) * (2 * H.rv + 1);
+      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[H.ip0 + i];
+      for (int i = threadIdx.x; i < H.ntp; i += kThreads) s_tp[i] = a.tab[H.tp0 + i];
+      const int4 z4 = make_int4(0, 0, 0, 0);
+      const int nv4 = (nvox + 3) >> 2;  // tile_words is a multiple of 4
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          M.r[d] = pick3(of, ax[d]);
-          M.o[d] = pick3i(ob, ax[d]);
-          M.s[d] = pick3i(st, ax[d]);
-          M.du[d] = pick3(mg.qa, ax[d]);
-          M.dv[d] = pick3(mg.qb, ax[d]);
-          M.dc[d] = (float)dir * pick3(mg.qc, ax[d]);
-        }
-        M.ti0 = cs + mg.cmax;
-        M.dti = dir;
-        M.ns = m.c1 - m.c0 + 1;
-        M.Ulo = o.Ulo;
-        M.Vlo = o.Vlo;
-        M.nU = o.Uhi - o.Ulo;
-        M.inv_nU = 1.0f / (float)M.nU;
-        M.plu = o.plu; M.phu = o.phu; M.plv = o.plv; M.phv = o.phv;
-        M.rw = o.phu - o.plu + 1;
-        M.inv_rw = 1.0f / (float)M.rw;
-        M.pixz = pt.pix0 + (int64_t)m.z * pt.sy * pt.sx;
-        M.yz = pt.y0off + (int64_t)m.z * pt.HW;
-        M.sx = pt.sx;
-        M.W = pt.W;
-        M.ws = init ? 1.0f : w[m.patch];
-        M.vs = init == 2 ? w[m.patch] : 1.0f;
-        nl = M.nU * (o.Vhi - o.Vlo);
-        np = M.rw * (o.phv - o.plv + 1);
+      for (int q = 0; q < NW; ++q) {
+        int4* t4 = reinterpret_cast<int4*>(HILO ? base + q * (kHQ / 4) : (q == 1 ? cbase : base));
+        for (int i = threadIdx.x; i < nv4; i += kThreads) t4[i] = z4;
       }
-      int sl = nl, sp = np;  // inclusive scans over the members
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int tl = __shfl_up_sync(0xffffffffu, sl, d), tp = __shfl_up_sync(0xffffffffu, sp, d);
-        if (lane >= d) { sl += tl; sp += tp; }
-      }
-      if (lane < G.nm) {
-        M.lbeg = sl - nl; M.lend = sl;
-        M.pbeg = sp - np; M.pend = sp;
-        sbm[lane] = M;
-      }
-      if (lane == G.nm - 1) { s_nl = sl; s_np = sp; }
     }
     __syncthreads();
     // ---- phase A: per-pixel (rA, rC) of every member into R; group maxima for the scale
     float mA = 0.0f, mC = 0.0f;
     {
-      const int np = s_np;
-      int mi = 0;
+      const int np = H.np;
+      int mi = 0, wmi = -1;
+      float ws = 0.0f, vs = 1.0f;  // the member's patch weight (1 in the init / rigidity
+                                   // passes), and the rigidity pass's patch score pbar
       for (int i = threadIdx.x; i < np; i += kThreads) {
         while (i >= sbm[mi].pend) ++mi;
         const BpMember& M = sbm[mi];
+        if (mi != wmi) {
+          wmi = mi;
+          ws = init ? 1.0f : w[M.patch];
+          vs = init == 2 ? w[M.patch] : 1.0f;
+        }
         const int li = i - M.pbeg;
         const int vv = (int)(((float)li + 0.5f) * M.inv_rw);
         const int u = M.plu + (li - vv * M.rw), v = M.plv + vv;
         const int64_t j = M.pixz + (int64_t)v * M.sx + u;
         float rA = 0.0f, rC = 0.0f;
         const float k = kap[j];
-        if (M.ws != 0.0f && k >= a.prm.tau_obs) {
+        if (ws != 0.0f && k >= a.prm.tau_obs) {
           const float pv = init ? 1.0f : p[j];
-          const float val = init == 1 ? a.ys[M.yz + (int64_t)v * M.W + u] : init == 2 ? p[j] * M.vs : e[j];
-          rC = M.ws * pv / k;
+          const float val = init == 1 ? a.ys[M.yz + (int64_t)v * M.W + u] : init == 2 ? p[j] * vs : e[j];
+          rC = ws * pv / k;
           rA = rC * val;
         }
         R[i] = make_float2(rA, rC);
@@ -603,31 +653,17 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
       s_red[0][wid] = mA;
       s_red[1][wid] = mC;
     }
-    const MemberGeom mg = member_geom(a, a.P[a.mem[G.m0].patch]);  // the group's stack
-    {  // PSF tables of the group's stack (all members share it) and the tile reset
-      const int nip = (2 * mg.ru + 1) * (2 * mg.rv + 1);
-      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[mg.ip0 + i];
-      for (int i = threadIdx.x; i < mg.ntp; i += kThreads) s_tp[i] = a.tab[mg.tp0 + i];
-      for (int i = threadIdx.x; i < nvox; i += kThreads) {
+    __syncthreads();
+    float xA = 0.0f, xC = 0.0f;  // every thread forms the same group maxima and scales
 #pragma unroll
-        for (int q = 0; q < NW; ++q) (HILO ? base + q * (kHQ / 4) : (q == 1 ? cbase : base))[i] = 0;
-      }
+    for (int i = 0; i < (kThreads >> 5); ++i) {
+      xA = fmaxf(xA, s_red[0][i]);
+      xC = fmaxf(xC, s_red[1][i]);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float xA = 0.0f, xC = 0.0f;
-      for (int i = 0; i < (kThreads >> 5); ++i) {
-        xA = fmaxf(xA, s_red[0][i]);
-        xC = fmaxf(xC, s_red[1][i]);
-      }
-      const float tpmax = a.psf[a.P[a.mem[G.m0].patch].stack].tpmax;
-      // every splat term |L tp w| <= max|r| tpmax  ->  < 2^20 units; the register window
-      // sums < 4 such terms per corner before rounding (< 2^22)
-      s_scale[0] = xA > 0.0f ? kTermMax / (xA * tpmax) : 0.0f;
-      s_scale[1] = xC > 0.0f ? kTermMax / (xC * tpmax) : 0.0f;
-    }
-    __syncthreads();
-    const float scA = s_scale[0], scC = s_scale[1];
+    // every splat term |L tp w| <= max|r| tpmax  ->  < 2^20 units; the register window
+    // sums < 4 such terms per corner before rounding (< 2^22)
+    const float scA = xA > 0.0f ? kTermMax / (xA * H.tpmax) : 0.0f;
+    const float scC = xC > 0.0f ? kTermMax / (xC * H.tpmax) : 0.0f;
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
     const Tile T{base, cbase, HILO ? base + 2 * (kHQ / 4) : nullptr,
                  HILO ? base + 3 * (kHQ / 4) : nullptr, dx, dy};
@@ -635,9 +671,9 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
     // ---- phase B: splat every owned lattice line of every member, one flattened range
     // (one tail per group); consecutive lanes take consecutive U lines of a member
     {
-      const int nl = s_nl;
-      const int w2 = 2 * mg.ru + 1;
-      const float inv_nu = 1.0f / (float)mg.nu, inv_nv = 1.0f / (float)mg.nv;
+      const int nl = H.nl;
+      const int w2 = 2 * H.ru + 1;
+      const float inv_nu = 1.0f / (float)H.nu, inv_nv = 1.0f / (float)H.nv;
       int mi = 0;
       for (int i = threadIdx.x; i < nl; i += kThreads) {
         while (i >= sbm[mi].lend) ++mi;
@@ -648,18 +684,18 @@ __global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile
         const int U = M.Ulo + iu, V = M.Vlo + iv;
         // pixels feeding lattice point U: u = (U - a) / nu with a = U mod nu (and a - nu when
         // that is within [-ru, ru]); same along V. U >= -ru > -nu: the float floor is exact.
-        const int ub = __float2int_rd(((float)U + 0.5f) * inv_nu), ra = U - ub * mg.nu;
-        const int vb = __float2int_rd(((float)V + 0.5f) * inv_nv), rb = V - vb * mg.nv;
+        const int ub = __float2int_rd(((float)U + 0.5f) * inv_nu), ra = U - ub * H.nu;
+        const int vb = __float2int_rd(((float)V + 0.5f) * inv_nv), rb = V - vb * H.nv;
         float LA = 0.0f, LC = 0.0f;
 #pragma unroll
         for (int jb = 0; jb < 2; ++jb) {
-          const int b = jb ? rb - mg.nv : rb, v = vb + jb;
-          if (b < -mg.rv || b > mg.rv || v < M.plv || v > M.phv) continue;
+          const int b = jb ? rb - H.nv : rb, v = vb + jb;
+          if (b < -H.rv || b > H.rv || v < M.plv || v > M.phv) continue;
 #pragma unroll
           for (int ja = 0; ja < 2; ++ja) {
-            const int aa = ja ? ra - mg.nu : ra, u = ub + ja;
-            if (aa < -mg.ru || aa > mg.ru || u < M.plu || u > M.phu) continue;
-            const float wt = s_ip[(b + mg.rv) * w2 + (aa + mg.ru)];
+            const int aa = ja ? ra - H.nu : ra, u = ub + ja;
+            if (aa < -H.ru || aa > H.ru || u < M.plu || u > M.phu) continue;
+            const float wt = s_ip[(b + H.rv) * w2 + (aa + H.ru)];
             const float2 rr = R[M.pbeg + (v - M.plv) * M.rw + (u - M.plu)];
             LA += wt * rr.x;
             LC += wt * rr.y;
@@ -746,16 +782,28 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
                                                         partials);
 }
 
+size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off) {
+  const size_t m = (size_t)nmembers * sizeof(BpMember);
+  if (group_off) *group_off = m;
+  return m + (size_t)ngroups * sizeof(BpGroupHdr);
+}
+
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
-                        const float* kap, const float* e, const float* p, const float* w, int init,
-                        float2* AC) {
+                        void* table, size_t group_off, bool build_table, const float* kap,
+                        const float* e, const float* p, const float* w, int init, float2* AC) {
   if (a.ngroups <= 0) return;
   configure();
+  BpMember* tm = static_cast<BpMember*>(table);
+  BpGroupHdr* th = reinterpret_cast<BpGroupHdr*>(static_cast<char*>(table) + group_off);
+  const int wpb = kThreads >> 5;
+  if (build_table) k_bp_table<<<(a.ngroups + wpb - 1) / wpb, kThreads, 0, st>>>(a, tm, th);
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
   if (init) {  // init (raw intensities) / rigidity pass: exact hi/lo words
-    k_lattice_bp<true><<<grid, kThreads, kInitTileBytes + r_bytes, st>>>(a, tile_words, kap, e, p, w, init, AC);
+    k_lattice_bp<true><<<grid, kThreads, kInitTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w,
+                                                                         init, AC);
   } else {
-    k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, kap, e, p, w, 0, AC);
+    k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, 0,
+                                                                        AC);
   }
 }
 

@@ -106,7 +106,10 @@ struct LatticeArgs {
 
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
 constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
-constexpr int kBpTileBytes = 96 * 1024;   // backprojection (iterations): 8 B/voxel tile budget
+#ifndef PVR_BP_TILE_KB
+#define PVR_BP_TILE_KB 96
+#endif
+constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;  // backprojection (iterations): 8 B/voxel tile budget
 constexpr int kInitTileBytes = 96 * 1024; // init backprojection: 16 B/voxel hi/lo tile budget
 constexpr int kRBytes = 12 * 1024;         // backprojection: per-pixel (rA, rC) buffer budget
 constexpr int kFwdTileBytes = 48 * 1024;  // forward: 4 B/voxel X tile budget
@@ -141,9 +144,13 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
                     double* partials);
 // init: 0 iteration (w p e / kappa, w p / kappa), 1 init pass (y / kappa, 1 / kappa),
 // 2 rigidity pass (p pbar / kappa, 1 / kappa; w carries pbar)
+// `table`: the plan's per-member / per-group constants (bp_table_bytes; members first, the
+// group headers at byte `group_off`), geometry only: rebuilt by this launch when
+// `build_table` (after a set_transforms / re-plan), else reused.
+size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off);
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
-                        const float* kap, const float* e, const float* p, const float* w,
-                        int init, float2* AC);
+                        void* table, size_t group_off, bool build_table, const float* kap,
+                        const float* e, const float* p, const float* w, int init, float2* AC);
 // superpixels.cu (f3): SLIC labels [K][H][W] (device) of one stack (device), synchronous
 cudaError_t slic_stack(cudaStream_t st, const float* y, int W, int H, int K, int S, int m, int iters,
                        int32_t* lab);

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libpvr.so")
+SO_PATH = os.environ.get("PVR_SO") or os.path.join(_HERE, "libpvr.so")  # PVR_SO: A/B builds
 
 PVR_OK, PVR_ERR_ARG, PVR_ERR_STATE, PVR_ERR_OOM, PVR_ERR_CUDA, PVR_ERR_NCCL, PVR_ERR_EMPTY = range(7)
 STATUS_NAMES = {0: "PVR_OK", 1: "PVR_ERR_ARG", 2: "PVR_ERR_STATE", 3: "PVR_ERR_OOM",

@@ -107,7 +107,10 @@ def test_forward_is_deterministic_and_stats_count_work(c1):
     eb, _, _, _ = b.taps()
     assert np.array_equal(ea, eb)                     # forward: fixed summation order
     s = a.stats()
-    assert s["iterations"] == 1 and s["kernel_launches"] == 6
+    # 6 per iteration, + 1 the first backprojection after set_transforms (its member tables)
+    assert s["iterations"] == 1 and s["kernel_launches"] == 7
+    a.sr_iterate(1, c1["alpha"], c1["lam"])
+    assert a.stats()["kernel_launches"] == 13
     assert s["psf_samples"] > 0 and s["ms_forward"] > 0 and s["ms_backproject"] > 0
     assert s["fwd_groups"] > 0 and s["bp_groups"] > 0
     a.close()
