@@ -282,6 +282,8 @@ typedef struct {
   int64_t fwd_smem, bp_smem;      /* dynamic shared memory per CTA (bytes)                 */
   int64_t device_replans;         /* set_transforms calls served by the device re-plan     */
   int64_t host_replans;           /* set_transforms calls that ran the host planner        */
+  int64_t replan_splits;          /* members moved into single-member backprojection groups
+                                     by device re-plans (their group outgrew the tile)       */
 } pvr_stats;
 pvr_status pvr_get_stats(const pvr_ctx* ctx, pvr_stats* out);
 pvr_status pvr_reset_stats(pvr_ctx* ctx);

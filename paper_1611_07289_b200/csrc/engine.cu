@@ -541,7 +541,8 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   const bool fwd = kind == 0;
   Trace tr;
   // the iteration backprojection plans to 90% of its tile budget: the device re-plan of a
-  // later set_transforms (k_replan) accepts growth up to 100% before falling back here
+  // later set_transforms (k_replan) accepts growth up to 100% (and splits a group that grew
+  // past it into single-member groups) before falling back here
   const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 * 9 / 10 : kInitTileBytes / 16;
   const int64_t nm = (int64_t)ng.mem.size();
   std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
@@ -736,18 +737,20 @@ pvr_status encode_tmaps(pvr_ctx* c) {
   return PVR_OK;
 }
 
-pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb) {
+// extra_groups: capacity after the plan's groups (the iteration backprojection's device
+// re-plan appends single-member groups there)
+pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb, size_t extra_groups) {
   if (pb.mem.size() > pl.mem_cap) {
     if (pl.mem) cudaFree(pl.mem);
     pl.mem = nullptr;
     CUDA_TRY(c, cudaMalloc(&pl.mem, pb.mem.size() * sizeof(MemberDev)));
     pl.mem_cap = pb.mem.size();
   }
-  if (pb.grp.size() > pl.grp_cap) {
+  if (pb.grp.size() + extra_groups > pl.grp_cap) {
     if (pl.grp) cudaFree(pl.grp);
     pl.grp = nullptr;
-    CUDA_TRY(c, cudaMalloc(&pl.grp, pb.grp.size() * sizeof(GroupDev)));
-    pl.grp_cap = pb.grp.size();
+    CUDA_TRY(c, cudaMalloc(&pl.grp, (pb.grp.size() + extra_groups) * sizeof(GroupDev)));
+    pl.grp_cap = pb.grp.size() + extra_groups;
   }
   CUDA_TRY(c, cudaMemcpyAsync(pl.mem, pb.mem.data(), pb.mem.size() * sizeof(MemberDev), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(pl.grp, pb.grp.data(), pb.grp.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, c->stream));
@@ -813,7 +816,7 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
       if (rb != PVR_OK) return rb;
     }
     tr.mark(kind == 0 ? "  plan forward" : kind == 1 ? "  plan backprojection" : "  plan init");
-    pvr_status r = upload_plan(c, pl, pb);
+    pvr_status r = upload_plan(c, pl, pb, kind == 1 ? pb.mem.size() : 0);
     if (r != PVR_OK) return r;
     tr.mark("  upload");
     if (kind == 2) continue;
@@ -1538,8 +1541,8 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
 // recompute their boxes for the new geometry on the device (k_replan). Falls back to the host
 // planner (returns non-OK) when a forward footprint outgrew its box or a group its budget.
 static pvr_status replan_on_device(pvr_ctx* c) {
-  if (!c->replan_buf) CUDA_TRY(c, cudaMalloc(&c->replan_buf, 4 * sizeof(int)));
-  CUDA_TRY(c, cudaMemsetAsync(c->replan_buf, 0, 4 * sizeof(int), c->stream));
+  if (!c->replan_buf) CUDA_TRY(c, cudaMalloc(&c->replan_buf, 8 * sizeof(int)));
+  CUDA_TRY(c, cudaMemsetAsync(c->replan_buf, 0, 8 * sizeof(int), c->stream));
   const int nshape = (int)(c->fbox.size() / 2);
   if (nshape <= 0 || nshape > kMaxBoxShapes) return PVR_ERR_ARG;
   if (!c->fbox_dev) CUDA_TRY(c, cudaMalloc(&c->fbox_dev, 2 * kMaxBoxShapes * sizeof(int)));
@@ -1547,17 +1550,25 @@ static pvr_status replan_on_device(pvr_ctx* c) {
                               c->stream));
   // forward: the planning budget + 50% (more X staged per CTA, 2-3 CTAs / SM until the next
   // host plan); backprojection: the hard tile budget (the host planned to 90% of it)
-  launch_replan(c->stream, c->fplan.mem, c->fplan.grp, c->fplan.ngroups, c->pdev, c->psf, 1, c->dims,
-                kFwdTileBytes / 4 * 3 / 2, c->fbox_dev, nshape, c->replan_buf, c->replan_buf + 1);
-  launch_replan(c->stream, c->bplan.mem, c->bplan.grp, c->bplan.ngroups, c->pdev, c->psf, 0, c->dims,
-                kBpTileBytes / 8, nullptr, 0, c->replan_buf + 2, c->replan_buf + 3);
+  launch_replan(c->stream, c->fplan.mem, c->fplan.grp, c->fplan.ngroups, (int)c->fplan.grp_cap, c->pdev, c->psf,
+                1, c->dims, kFwdTileBytes / 4 * 3 / 2, c->fbox_dev, nshape, c->replan_buf, c->replan_buf + 1,
+                nullptr);
+  // backprojection groups that outgrow the tile are split into single-member groups appended
+  // after the plan's (their Morton locality is lost until the next host plan)
+  launch_replan(c->stream, c->bplan.mem, c->bplan.grp, c->bplan.ngroups, (int)c->bplan.grp_cap, c->pdev, c->psf,
+                0, c->dims, kBpTileBytes / 8, nullptr, 0, c->replan_buf + 2, c->replan_buf + 3,
+                c->replan_buf + 4);
   CHECK_LAUNCH(c);
-  int h[4];
+  int h[5];
   CUDA_TRY(c, cudaMemcpyAsync(h, c->replan_buf, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (getenv("PVR_TRACE"))
-    fprintf(stderr, "[pvr] device replan: fwd max vox %d fail %d, bp max vox %d fail %d\n", h[0], h[1], h[2], h[3]);
+    fprintf(stderr, "[pvr] device replan: fwd max vox %d fail %d, bp max vox %d fail %d split members %d\n", h[0],
+            h[1], h[2], h[3], h[4]);
   if (h[1] || h[3]) return PVR_ERR_ARG;
+  c->bplan.ngroups += h[4];
+  c->st.bp_groups = c->bplan.ngroups;
+  c->st.replan_splits += h[4];
   c->fplan.tile_words = (h[0] + 3) & ~3;
   c->bplan.tile_words = (h[2] + 3) & ~3;
   c->st.fwd_smem = (int64_t)(c->fplan.t_floats + c->fplan.tile_words) * 4;

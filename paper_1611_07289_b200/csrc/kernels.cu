@@ -420,48 +420,80 @@ __global__ void __launch_bounds__(256) k_ratio(const float2* __restrict__ AC, in
 // the plan (shapes: the tensor maps already encoded) that holds its new footprint (x origin
 // aligned to 4); backprojection groups get fresh odd pitches. A group without a shape or over
 // the tile budget sets *fail (the host then replans from scratch).
-__global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict__ grp, int ngroups,
+// fp64 voxel bbox [lo, hi] of one member's PSF samples under the current transform (the host
+// planner's member_bbox, engine.cu)
+__device__ void replan_member_box(const MemberDev& m, const PatchDev& pt, const StackPsf& ps, int fwd, int (&lo)[3],
+                                  int (&hi)[3]) {
+  int Ulo, Uhi, Vlo, Vhi;
+  if (fwd) {
+    Ulo = ps.nu * m.u0 - ps.ru;
+    Uhi = ps.nu * (m.u0 + m.tu - 1) + ps.ru + 1;
+    Vlo = ps.nv * m.v0 - ps.rv;
+    Vhi = ps.nv * (m.v0 + m.tv - 1) + ps.rv + 1;
+  } else {
+    Ulo = ps.nu * m.u0 - ps.ru;
+    Uhi = (m.u0 + m.tu >= pt.sx) ? ps.nu * (pt.sx - 1) + ps.ru + 1 : ps.nu * (m.u0 + m.tu) - ps.ru;
+    Vlo = ps.nv * m.v0 - ps.rv;
+    Vhi = (m.v0 + m.tv >= pt.sy) ? ps.nv * (pt.sy - 1) + ps.rv + 1 : ps.nv * (m.v0 + m.tv) - ps.rv;
+  }
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int c8 = 0; c8 < 8; ++c8) {
+    const double U = (c8 & 1) ? Uhi - 1 : Ulo, V = (c8 & 2) ? Vhi - 1 : Vlo, C = (c8 & 4) ? m.c1 : m.c0;
+    for (int d = 0; d < 3; ++d) {
+      const double x = pt.t0d[d] + m.z * pt.Mzd[d] + U * pt.Qad[d] + V * pt.Qbd[d] + C * pt.Qcd[d];
+      mn[d] = fmin(mn[d], x);
+      mx[d] = fmax(mx[d], x);
+    }
+  }
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = (int)floor(mn[d] - 1e-3);
+    hi[d] = (int)floor(mx[d] + 1e-3) + 1;
+  }
+}
+
+// backprojection tile box of a voxel bbox (the host planner's group(), engine.cu): even x
+// origin, odd x / y pitches; returns its voxel count
+__device__ int64_t replan_bp_box(int (&lo)[3], const int (&hi)[3], GroupDev& G) {
+  lo[0] -= ((lo[0] % 2) + 2) % 2;
+  for (int d = 0; d < 3; ++d) G.lo[d] = lo[d];
+  G.dim[0] = (hi[0] - lo[0] + 1) | 1;
+  G.dim[1] = (hi[1] - lo[1] + 1) | 1;
+  G.dim[2] = hi[2] - lo[2] + 1;
+  return (int64_t)G.dim[0] * G.dim[1] * G.dim[2];
+}
+
+__device__ int replan_interior(const int (&lo)[3], const int (&hi)[3], int3 n) {
+  const int nn[3] = {n.x, n.y, n.z};
+  for (int d = 0; d < 3; ++d)
+    if (lo[d] < 0 || hi[d] > nn[d] - 1) return 0;
+  return 1;
+}
+
+// Device re-plan of one plan for new transforms: same groups and order, new boxes. Forward:
+// the smallest existing TMA box shape that holds the new footprint (else fail). Backprojection
+// (`nappend` != NULL): a group whose box outgrew the tile budget is emptied (nm = 0) and its
+// members appended as single-member groups at [ngroups + k] (k from *nappend, < cap); fail only
+// if a single member does not fit or the capacity is exhausted.
+__global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict__ grp, int ngroups, int cap,
                          const PatchDev* __restrict__ P, const StackPsf* __restrict__ psf, int fwd, int3 n,
                          int64_t vox_budget, const int* __restrict__ shapes, int nshape,
-                         int* __restrict__ maxvox, int* __restrict__ fail) {
+                         int* __restrict__ maxvox, int* __restrict__ fail, int* __restrict__ nappend) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ngroups) return;
   GroupDev G = grp[g];
+  if (G.nm == 0) return;  // emptied by an earlier split
   int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
   for (int i = G.m0; i < G.m0 + G.nm; ++i) {
     const MemberDev m = mem[i];
     const PatchDev& pt = P[m.patch];
-    const StackPsf ps = psf[pt.stack];
-    int Ulo, Uhi, Vlo, Vhi;
-    if (fwd) {
-      Ulo = ps.nu * m.u0 - ps.ru;
-      Uhi = ps.nu * (m.u0 + m.tu - 1) + ps.ru + 1;
-      Vlo = ps.nv * m.v0 - ps.rv;
-      Vhi = ps.nv * (m.v0 + m.tv - 1) + ps.rv + 1;
-    } else {
-      Ulo = ps.nu * m.u0 - ps.ru;
-      Uhi = (m.u0 + m.tu >= pt.sx) ? ps.nu * (pt.sx - 1) + ps.ru + 1 : ps.nu * (m.u0 + m.tu) - ps.ru;
-      Vlo = ps.nv * m.v0 - ps.rv;
-      Vhi = (m.v0 + m.tv >= pt.sy) ? ps.nv * (pt.sy - 1) + ps.rv + 1 : ps.nv * (m.v0 + m.tv) - ps.rv;
-    }
-    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
-    for (int c8 = 0; c8 < 8; ++c8) {
-      const double U = (c8 & 1) ? Uhi - 1 : Ulo, V = (c8 & 2) ? Vhi - 1 : Vlo, C = (c8 & 4) ? m.c1 : m.c0;
-      for (int d = 0; d < 3; ++d) {
-        const double x = pt.t0d[d] + m.z * pt.Mzd[d] + U * pt.Qad[d] + V * pt.Qbd[d] + C * pt.Qcd[d];
-        mn[d] = fmin(mn[d], x);
-        mx[d] = fmax(mx[d], x);
-      }
-    }
+    int ml[3], mh[3];
+    replan_member_box(m, pt, psf[pt.stack], fwd, ml, mh);
     for (int d = 0; d < 3; ++d) {
-      lo[d] = min(lo[d], (int)floor(mn[d] - 1e-3));
-      hi[d] = max(hi[d], (int)floor(mx[d] + 1e-3) + 1);
+      lo[d] = min(lo[d], ml[d]);
+      hi[d] = max(hi[d], mh[d]);
     }
   }
-  const int nn[3] = {n.x, n.y, n.z};
-  G.interior = 1;
-  for (int d = 0; d < 3; ++d)
-    if (lo[d] < 0 || hi[d] > nn[d] - 1) G.interior = 0;
+  G.interior = replan_interior(lo, hi, n);
   int64_t vox;
   if (fwd) {
     lo[0] -= ((lo[0] % 4) + 4) % 4;
@@ -482,12 +514,31 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
     G.dim[2] = hi[2] - lo[2] + 1;
     vox = (int64_t)((G.dim[0] * G.dim[1] + 31) & ~31) * G.dim[2];
   } else {
-    lo[0] -= ((lo[0] % 2) + 2) % 2;
-    for (int d = 0; d < 3; ++d) G.lo[d] = lo[d];
-    G.dim[0] = (hi[0] - lo[0] + 1) | 1;
-    G.dim[1] = (hi[1] - lo[1] + 1) | 1;
-    G.dim[2] = hi[2] - lo[2] + 1;
-    vox = (int64_t)G.dim[0] * G.dim[1] * G.dim[2];
+    vox = replan_bp_box(lo, hi, G);
+    if (vox > vox_budget && nappend && G.nm > 1) {
+      for (int i = G.m0; i < G.m0 + G.nm; ++i) {
+        const MemberDev m = mem[i];
+        const PatchDev& pt = P[m.patch];
+        int ml[3], mh[3];
+        replan_member_box(m, pt, psf[pt.stack], 0, ml, mh);
+        GroupDev S;
+        S.m0 = i;
+        S.nm = 1;
+        S.tmap = 0;
+        S.interior = replan_interior(ml, mh, n);
+        const int64_t sv = replan_bp_box(ml, mh, S);
+        const int k = atomicAdd(nappend, 1);
+        if (sv > vox_budget || ngroups + k >= cap) {
+          atomicExch(fail, 1);
+          continue;
+        }
+        atomicMax(maxvox, (int)sv);
+        grp[ngroups + k] = S;
+      }
+      G.nm = 0;  // emptied: its members now live in the appended groups
+      G.dim[0] = G.dim[1] = G.dim[2] = 0;
+      vox = 0;
+    }
   }
   if (vox > vox_budget) atomicExch(fail, 1);
   atomicMax(maxvox, (int)(vox < (1 << 30) ? vox : (1 << 30)));
@@ -553,12 +604,12 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
   k_update<<<grid, 256, 0, st>>>(X0, AC, dims, nxp, prm, em, alpha, lambda, X2);
 }
 
-void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, const PatchDev* P,
+void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, int cap, const PatchDev* P,
                    const StackPsf* psf, int fwd, int3 n, int64_t vox_budget, const int* shapes, int nshape,
-                   int* maxvox, int* fail) {
+                   int* maxvox, int* fail, int* nappend) {
   if (ngroups > 0)
-    k_replan<<<(ngroups + 255) / 256, 256, 0, st>>>(mem, grp, ngroups, P, psf, fwd, n, vox_budget, shapes, nshape,
-                                                     maxvox, fail);
+    k_replan<<<(ngroups + 255) / 256, 256, 0, st>>>(mem, grp, ngroups, cap, P, psf, fwd, n, vox_budget, shapes,
+                                                     nshape, maxvox, fail, nappend);
 }
 
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out) {

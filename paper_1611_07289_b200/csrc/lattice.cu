@@ -498,6 +498,13 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
   const int g = blockIdx.x * (kThreads >> 5) + (threadIdx.x >> 5);
   if (g >= a.ngroups) return;  // uniform per warp
   const GroupDev G = a.grp[g];
+  if (G.nm == 0) {  // emptied by a device re-plan split (engine.cu: replan_on_device)
+    if (lane == 0) {
+      BpGroupHdr h = {};
+      th[g] = h;
+    }
+    return;
+  }
   const int dx = G.dim[0], dy = G.dim[1];
   int nl = 0, np = 0;
   BpMember M;
@@ -570,8 +577,9 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
 // Dynamic shared memory: HILO (init pass): 4 x tile_words int32 (A, C, A_lo, C_lo), then R;
 // iterations: A at 0, C at the fixed byte offset kCOff (an immediate in the splat's shared
 // reductions), R after kBpTileBytes (init: after kInitTileBytes).
+// 3 CTAs per SM in the iterations (56 KB tile + R: <= 85 registers); the init tile allows 2
 template <bool HILO>
-__global__ void __launch_bounds__(kThreads) k_lattice_bp(LatticeArgs a, int tile_words,
+__global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int tile_words,
                                                          const BpMember* __restrict__ tm,
                                                          const BpGroupHdr* __restrict__ th,
                                                          const float* __restrict__ kap,

@@ -107,12 +107,16 @@ struct LatticeArgs {
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
 constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
 #ifndef PVR_BP_TILE_KB
-#define PVR_BP_TILE_KB 96
+#define PVR_BP_TILE_KB 56
 #endif
-constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;  // backprojection (iterations): 8 B/voxel tile budget
+constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;  // backprojection (iterations): 8 B/voxel tile
+                                                     // budget; 56 KB + R: 3 CTAs per SM
 constexpr int kInitTileBytes = 96 * 1024; // init backprojection: 16 B/voxel hi/lo tile budget
 constexpr int kRBytes = 12 * 1024;         // backprojection: per-pixel (rA, rC) buffer budget
-constexpr int kFwdTileBytes = 48 * 1024;  // forward: 4 B/voxel X tile budget
+#ifndef PVR_FWD_TILE_KB
+#define PVR_FWD_TILE_KB 48
+#endif
+constexpr int kFwdTileBytes = PVR_FWD_TILE_KB * 1024;  // forward: 4 B/voxel X tile budget
 constexpr int kFwdTBytes = 12 * 1024;     // forward: lattice values of a group's members
 constexpr int kMaxGroupMembers = 16;      // members per group (lattice.cu kMaxMembers)
 
@@ -180,9 +184,10 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2);
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);
 constexpr int kMaxBoxShapes = 4096;  // forward TMA box shapes the device re-plan may pick from
-void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, const PatchDev* P,
+// nappend (backprojection): counter of single-member groups appended after ngroups (< cap)
+void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, int cap, const PatchDev* P,
                    const StackPsf* psf, int fwd, int3 n, int64_t vox_budget, const int* shapes, int nshape,
-                   int* maxvox, int* fail);
+                   int* maxvox, int* fail, int* nappend);
 void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, int nxp, Params prm,
                       float* X);
 

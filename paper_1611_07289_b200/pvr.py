@@ -55,7 +55,7 @@ class pvr_stats(C.Structure):
                [("fwd_tile", C.c_int32 * 3), ("bp_tile", C.c_int32 * 3)] + \
                [(n, C.c_int64) for n in ("fwd_groups", "bp_groups", "fwd_members", "bp_members",
                                           "fwd_smem", "bp_smem",
-                                          "device_replans", "host_replans")]
+                                          "device_replans", "host_replans", "replan_splits")]
 
     def as_dict(self):
         d = {}

@@ -133,12 +133,15 @@ def test_multi_round_em_changes_the_estimates():
         assert abs(out[8][0][key] - out[1][0][key]) > 1e-3 * abs(out[1][0][key])
 
 
-@pytest.mark.parametrize("deg,mm,device", [(0.1, 0.1, True), (3.0, 2.0, False)])
-def test_new_transforms_replan(deg, mm, device):
+@pytest.mark.parametrize("deg,mm,device,split", [(0.1, 0.1, True, False), (0.5, 0.3, True, True),
+                                                 (3.0, 2.0, False, False)])
+def test_new_transforms_replan(deg, mm, device, split):
     """set_transforms with patches moved about their centres: a small registration-like
     update (0.1 deg / 0.1 mm rms) re-plans on the device (k_replan: same groups, new boxes);
-    a large one (3 deg / 2 mm) falls back to the host planner. Either way the iterations stay
-    within the parity bar against the oracle given the same new transforms."""
+    a moderate one (0.5 deg / 0.3 mm) also stays on the device, splitting the backprojection
+    groups that outgrew the tile into single-member groups; a large one (3 deg / 2 mm) falls
+    back to the host planner. Either way the iterations stay within the parity bar against the
+    oracle given the same new transforms."""
     from regprob import patch_centre_world, rigid_about
     prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
     orc = make_oracle(prob)
@@ -160,6 +163,8 @@ def test_new_transforms_replan(deg, mm, device):
         after = ctx.stats()
         assert after["device_replans"] == before["device_replans"] + int(device)
         assert after["host_replans"] == before["host_replans"] + int(not device)
+        if split:
+            assert after["replan_splits"] > before["replan_splits"]
         orc.init_volume()
         ctx.init_volume()
         from scipy import ndimage

@@ -17,3 +17,5 @@ import time
 for _ in range(3):
     t0 = time.perf_counter(); ctx.set_transforms(prob["T"]); t1 = time.perf_counter()
     print("set_transforms %.1f ms" % ((t1 - t0) * 1e3))
+s = ctx.stats()
+print("replans device/host", s["device_replans"], s["host_replans"])
