@@ -386,10 +386,14 @@ __device__ __forceinline__ void flush_word(unsigned a, float v, bool is_c) {
   }
 }
 
+// Flush one plane of the window: corner j's weight sum S_j times the line's (LA, LC) into the
+// A and C words of the 4 transverse corners (a, +sp4, +sq4, +sp4+sq4).
 template <bool HILO>
-__device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, const f2 (&P)[4], f2 mag) {
+__device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, float s1, float s2, float s3,
+                                       f2 L, f2 mag) {
   if (!HILO) {
-    const f2 t0 = add2(P[0], mag), t1 = add2(P[1], mag), t2 = add2(P[2], mag), t3 = add2(P[3], mag);
+    // L S + magic: the fixed-point rounding of each window sum (one FFMA2 per corner)
+    const f2 t0 = fma2s(s0, L, mag), t1 = fma2s(s1, L, mag), t2 = fma2s(s2, L, mag), t3 = fma2s(s3, L, mag);
     sred<0>(a, __float_as_int(lo2(t0)) - kMagicBits);
     sred<kCOff>(a, __float_as_int(hi2(t0)) - kMagicBits);
     sred<0>(a + sp4, __float_as_int(lo2(t1)) - kMagicBits);
@@ -400,25 +404,29 @@ __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, const f2 (&
     sred<kCOff>(a + sp4 + sq4, __float_as_int(hi2(t3)) - kMagicBits);
   } else {
     const unsigned ac[4] = {a, a + sp4, a + sq4, a + sp4 + sq4};
+    const float sj[4] = {s0, s1, s2, s3};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      flush_word<true>(ac[j], lo2(P[j]), false);
-      flush_word<true>(ac[j], hi2(P[j]), true);
+      const f2 v = mul2s(sj[j], L);
+      flush_word<true>(ac[j], lo2(v), false);
+      flush_word<true>(ac[j], hi2(v), true);
     }
   }
 }
 
-// Splat one lattice line with a two-plane register window along the frame's axis 0. A sample
-// at plane floor m adds (1 - f_m) of its 4 in-plane corner terms to plane m (window slot P0)
-// and f_m to plane m + 1 (slot P1). Every step first flushes P0 to the tile (one int32
-// rounding per corner per step instead of one per term and plane), then shifts: a lane whose
-// floor advanced moves P1 into P0; a lane whose floor stayed keeps P1 (its P0 restarts
-// empty); a lane whose transverse floors changed also flushes P1 and restarts. The flush is
-// uniform across the warp (all lanes issue the same 8 shared reductions); only the rarer
-// transverse restart branches. A and C travel as packed fp32 pairs (FFMA2 / FMUL2). Window
-// sums before rounding: < 4 terms of < 2^20 units each (group scale, k_lattice_bp).
-// Tile: A words at shared address tA, C words at tA + kCOff; HILO (init / rigidity passes):
-// every window sum split into exact hi / lo words (A_hi, C_hi, A_lo, C_lo planes, kHQ apart).
+// Splat one lattice line with a two-plane register window along the frame's axis 0. Every
+// sample of the line carries the same (LA, LC) (the line's adjoint values), so the window
+// holds unitless weight sums: per transverse corner j a packed pair (plane m, plane m + 1)
+// accumulating tp(c) x bilinear corner weight x (1 - f_m, f_m) with one FFMA2, scaled by
+// (LA, LC) only when a plane is flushed. Every step first flushes plane m to the tile (one
+// int32 rounding per corner and quantity per step), then shifts: a lane whose floor advanced
+// moves plane m + 1 into slot m; a lane whose floor stayed keeps slot m + 1 (slot m restarts
+// empty); a lane whose transverse floors changed also flushes plane m + 1 and restarts. The
+// flush is uniform across the warp (all lanes issue the same 8 shared reductions); only the
+// rarer transverse restart branches. Window sums before rounding: < 4 terms of < 2^20 units
+// each (group scale, k_lattice_bp). Tile: A words at shared address tA, C words at
+// tA + kCOff; HILO (init / rigidity passes): every window sum split into exact hi / lo words
+// (A_hi, C_hi, A_lo, C_lo planes, kHQ apart).
 template <bool HILO>
 __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const BpMember& M, float rm,
                                                float rp, float rq, float LA, float LC) {
@@ -437,9 +445,9 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
   int wm = mfloor(rm, fl);
   int wp = __float_as_int(lo2(add2_rd(rpq, mag))) - kMagicBits;
   int wq = __float_as_int(hi2(add2_rd(rpq, mag))) - kMagicBits;
-  f2 P0[4], P1[4];
+  f2 P[4];  // corner j: (plane wm, plane wm + 1) weight sums
 #pragma unroll
-  for (int j = 0; j < 4; ++j) P0[j] = P1[j] = pk(0.0f, 0.0f);
+  for (int j = 0; j < 4; ++j) P[j] = pk(0.0f, 0.0f);
   for (int k = 0; k < ns; ++k) {
     const float tm = __fadd_rd(rm, kMagic);
     const f2 tpq = add2_rd(rpq, mag);
@@ -450,43 +458,36 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
     const bool keep = same & (im == wm);
     const bool adv = same & (im == wm + 1);
     const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-    flush4<HILO>(a0, sp4, sq4, P0, mag);                   // plane wm
-    if (!keep && !adv) flush4<HILO>(a0 + sm4, sp4, sq4, P1, mag);  // restart: plane wm + 1 too
-    // shift: keep -> (0, P1); advance -> (P1, 0); restart (or a jump) -> (0, 0)
-    const float m0 = adv ? 1.0f : 0.0f, m1 = keep ? 1.0f : 0.0f;
+    flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag);  // plane wm
+    if (!keep && !adv)  // restart: plane wm + 1 too
+      flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag);
+    // shift: keep -> (0, m+1); advance -> (m+1, 0); restart (or a jump) -> (0, 0)
+    const f2 sh = pk(adv ? 1.0f : 0.0f, keep ? 1.0f : 0.0f);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      P0[j] = mul2s(m0, P1[j]);
-      P1[j] = mul2s(m1, P1[j]);
-    }
+    for (int j = 0; j < 4; ++j) P[j] = mul2s(hi2(P[j]), sh);
     wm = im;
     wp = ip;
     wq = iq;
-    // this sample's terms
+    // this sample's weights
     float t;
     asm("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(ta));
     const float flm = __fsub_rn(tm, kMagic);
     const f2 fpq = sub2(rpq, sub2(tpq, mag));
     const float fm = rm - flm, fp = lo2(fpq), fq = hi2(fpq);
-    const f2 V = mul2s(t, L);                       // (vA, vC)
+    const f2 TM = mul2s(t, fma2s(fm, m1p1, one0));  // t (1 - fm, fm)
     const f2 WP = fma2s(fp, m1p1, one0);            // (1 - fp, fp)
     const f2 w01 = mul2s(1.0f - fq, WP), w23 = mul2s(fq, WP);
-    const f2 VL = mul2s(1.0f - fm, V), VH = mul2s(fm, V);
-    P0[0] = fma2s(lo2(w01), VL, P0[0]);
-    P0[1] = fma2s(hi2(w01), VL, P0[1]);
-    P0[2] = fma2s(lo2(w23), VL, P0[2]);
-    P0[3] = fma2s(hi2(w23), VL, P0[3]);
-    P1[0] = fma2s(lo2(w01), VH, P1[0]);
-    P1[1] = fma2s(hi2(w01), VH, P1[1]);
-    P1[2] = fma2s(lo2(w23), VH, P1[2]);
-    P1[3] = fma2s(hi2(w23), VH, P1[3]);
+    P[0] = fma2s(lo2(w01), TM, P[0]);
+    P[1] = fma2s(hi2(w01), TM, P[1]);
+    P[2] = fma2s(lo2(w23), TM, P[2]);
+    P[3] = fma2s(hi2(w23), TM, P[3]);
     rm += qm;
     rpq = add2(rpq, qpq);
     ta += dta;
   }
   const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-  flush4<HILO>(a0, sp4, sq4, P0, mag);
-  flush4<HILO>(a0 + sm4, sp4, sq4, P1, mag);
+  flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag);
+  flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag);
 }
 
 // Member tables of all groups of a backprojection plan (geometry only: rebuilt after every
