@@ -92,6 +92,9 @@ struct FwdMember {  // per-member constants in shared memory
   int ob[3];
   int LU, LV, t0, p0;  // lattice extent, offset into sT, first pixel index in the group order
   int patch, z, u0, v0, tu, tv;
+  int strip;           // lattice point order: 1 = strips of 4 U columns (V fastest in blocks of
+                       // 4 U), 0 = rows (U fastest); see the lattice pass
+  float inv_LU, inv_s4;  // 1 / LU, 1 / (4 LV)
 };
 
 template <int MODE>
@@ -170,6 +173,13 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         f.qc[d] = pt.Qc[d];
       }
       f.patch = m.patch; f.z = m.z; f.u0 = m.u0; f.v0 = m.v0; f.tu = m.tu; f.tv = m.tv;
+      // V along the tile's y axis (axial-like stacks): a warp of row-ordered points straddles
+      // two lattice rows one tile row (dx floats) apart -> bank conflicts; blocks of 4 U x 8 V
+      // points hit 32 distinct banks (rows 4 (mod 8) banks apart). Other stacks keep rows.
+      const float ab0 = fabsf(pt.Qb[0]), ab1 = fabsf(pt.Qb[1]), ab2 = fabsf(pt.Qb[2]);
+      f.strip = (MODE == 0 && ab1 >= ab0 && ab1 >= ab2 && f.LU >= 4) ? 1 : 0;
+      f.inv_LU = 1.0f / (float)f.LU;
+      f.inv_s4 = 1.0f / (float)(4 * f.LV);
     }
     {
       const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
@@ -209,7 +219,18 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       while (k + 1 < G.nm && i >= sm[k + 1].t0) ++k;
       const FwdMember& f = sm[k];
       const int li = i - f.t0;
-      const float U = (float)(li % f.LU), V = (float)(li / f.LU);
+      int iu, iv;
+      if (f.strip) {  // strip sidx of 4 U columns (the last one narrower), V-major inside
+        const int sidx = (int)(((float)li + 0.5f) * f.inv_s4);
+        const int r = li - sidx * 4 * f.LV;
+        const int ws = min(4, f.LU - 4 * sidx);
+        iv = ws == 4 ? (r >> 2) : (int)(((float)r + 0.5f) / (float)ws);
+        iu = 4 * sidx + (r - iv * ws);
+      } else {
+        iv = (int)(((float)li + 0.5f) * f.inv_LU);
+        iu = li - iv * f.LU;
+      }
+      const float U = (float)iu, V = (float)iv;
       float rx = f.of[0] + U * f.qa[0] + V * f.qb[0];
       float ry = f.of[1] + U * f.qa[1] + V * f.qb[1];
       float rz = f.of[2] + U * f.qa[2] + V * f.qb[2];
@@ -240,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         rxy = add2(rxy, qcxy);
         rz += qcz;
       }
-      sT[i] = acc;
+      sT[f.t0 + iv * f.LU + iu] = acc;
     }
     __syncthreads();
     // pixels of all members: yhat = sum_ab ip(a,b) T(nu u + a, nv v + b) / kappa
