@@ -745,21 +745,20 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
     // ---- phase C: flush the tile, one red.v4 per in-grid (even, odd) voxel pair along x
     const double iA = scA > 0.0f ? 1.0 / scA : 0.0, iC = scC > 0.0f ? 1.0 / scC : 0.0;
     const float fA = (float)iA, fC = (float)iC;
-    const int hx = (dx + 1) >> 1;
-    // flat pair index i = (zz * dy + yy) * hx + px over all threads, advanced by kThreads
-    // without per-element division
-    const int qs = kThreads / hx, rs = kThreads - qs * hx;
-    int px = threadIdx.x % hx, yy = threadIdx.x / hx, zz = 0;
-    while (yy >= dy) { yy -= dy; ++zz; }
-    for (int i = threadIdx.x; i < hx * dy * dz; i += kThreads) {
-      const int pl = px, yl = yy, zl = zz;
-      px += rs;
-      yy += qs;
-      if (px >= hx) { px -= hx; ++yy; }
-      while (yy >= dy) { yy -= dy; ++zz; }
+    const int hx = (dx + 1) >> 1, npair = hx * dy * dz;
+    const float inv_hx = 1.0f / (float)hx, inv_dy = 1.0f / (float)dy;
+    // flat pair index i = (zl * dy + yl) * hx + pl, decoded by float reciprocals (exact for
+    // these small integers); 32-bit voxel offsets (the volume has < 2^31 voxels)
+    const int gbase = (G.lo[2] * n.y + G.lo[1]) * a.nxp + G.lo[0];
+    for (int i = threadIdx.x; i < npair; i += kThreads) {
+      const int row = (int)(((float)i + 0.5f) * inv_hx);
+      const int pl = i - row * hx;
+      const int zl = (int)(((float)row + 0.5f) * inv_dy);
+      const int yl = row - zl * dy;
       const int gy = G.lo[1] + yl, gz = G.lo[2] + zl, gx = G.lo[0] + 2 * pl;
-      if (gy < 0 || gy >= n.y || gz < 0 || gz >= n.z || gx < 0 || gx >= a.nxp) continue;
-      const int k = (zl * dy + yl) * dx + 2 * pl;
+      if ((unsigned)gy >= (unsigned)n.y || (unsigned)gz >= (unsigned)n.z || (unsigned)gx >= (unsigned)a.nxp)
+        continue;
+      const int k = row * dx + 2 * pl;
       const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
       const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
       int al0 = 0, al1 = 0, cl0 = 0, cl1 = 0;
@@ -778,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
         A0 = (float)ah0 * fA; A1 = (float)ah1 * fA;
         C0 = (float)ch0 * fC; C1 = (float)ch1 * fC;
       }
-      red_v4(AC + ((size_t)gz * n.y + gy) * a.nxp + gx, A0, C0, A1, C1);
+      red_v4(AC + (gbase + (zl * n.y + yl) * a.nxp + 2 * pl), A0, C0, A1, C1);
     }
   }
 }
