@@ -86,6 +86,10 @@ __device__ __forceinline__ void lattice_origin(const PatchDev& pt, int z, int U0
 // of all members (T values into shared memory), then one pass over all their pixels.
 // Dynamic shared memory: [t_floats] lattice values T of all members, then the X tile.
 constexpr int kMaxMembers = 16;
+#ifndef PVR_FWD_UNROLL
+#define PVR_FWD_UNROLL 4
+#endif
+constexpr int kFwdUnroll = PVR_FWD_UNROLL;  // samples per iteration of the forward's c loop
 
 struct FwdMember {  // per-member constants in shared memory
   float of[3], qa[3], qb[3], qc[3];
@@ -241,6 +245,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       const f2 mag = pk(kMagic, kMagic);
       const float* sXo = sX + f.ob[2] * dxy + f.ob[1] * dx + f.ob[0];
       float acc = 0.0f;
+#pragma unroll kFwdUnroll
       for (int c = 0; c < ntp; ++c) {
         const f2 txy = add2_rd(rxy, mag);
         const float tz = __fadd_rd(rz, kMagic);
@@ -389,6 +394,10 @@ __device__ __forceinline__ int pick3i(const int (&v)[3], int ax) {
   return ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]);
 }
 
+#ifndef PVR_BP_UNROLL
+#define PVR_BP_UNROLL 4
+#endif
+constexpr int kBpUnroll = PVR_BP_UNROLL;  // steps per iteration of the splat window loop
 constexpr int kCOff = kBpTileBytes / 2;  // byte offset of the C plane in the iteration tile
 // init / rigidity tile (HILO): A_hi, C_hi, A_lo, C_lo planes at fixed byte offsets
 constexpr int kHQ = kInitTileBytes / 4;
@@ -469,6 +478,7 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
   f2 P[4];  // corner j: (plane wm, plane wm + 1) weight sums
 #pragma unroll
   for (int j = 0; j < 4; ++j) P[j] = pk(0.0f, 0.0f);
+#pragma unroll kBpUnroll
   for (int k = 0; k < ns; ++k) {
     const float tm = __fadd_rd(rm, kMagic);
     const f2 tpq = add2_rd(rpq, mag);
