@@ -173,6 +173,7 @@ struct pvr_ctx {
   int patch_mixture = 0;        // f4 two-Gaussian patch classification (reading Q31)
   int32_t* nlivep = nullptr;    // live pixels per local patch (mixture validity)
   uint8_t* mask = nullptr;      // f3: per-pixel patch mask of the local shard (NULL = all)
+  std::vector<uint8_t> mask_host;  // its host copy: the planners drop fully masked member tiles
   EmDev* em = nullptr;
   // stats; with PVR_PARAM_PROFILE every iteration records EV_N events into a slot of the
   // pool, drained (synchronised) only by pvr_get_stats or when the pool is large
@@ -467,13 +468,28 @@ void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, 
   ng.TU = TU; ng.TV = TV; ng.nseg = nseg; ng.fwd = fwd;
   std::vector<MemberDev> mem;
   std::vector<std::pair<uint64_t, int32_t>> keys;
+  // f3 (reading Q32): a member whose pixels are all masked out is never observed (kappa, e and
+  // R stay 0) and is not planned at all. A backprojection member's owned lattice points also
+  // collect the pixels one beside its tile (ru < nu: owned_range in lattice.cu), so its test
+  // covers the tile grown by one pixel
+  const uint8_t* mk = c->mask_host.empty() ? nullptr : c->mask_host.data();
+  const int grow = fwd ? 0 : 1;
   for (int64_t s : which) {
     const HostPatch& hp = c->patches[c->first + s];
     const StackPsf& ps = c->stacks[hp.stack].psf;
     const int ntp = 2 * ps.cmax + 1, seg = (ntp + nseg - 1) / nseg;
+    const int64_t pbase = c->pix0_global[c->first + s] - c->first_pix;
+    auto masked_out = [&](int z, int u0, int v0) {
+      if (!mk) return false;
+      for (int v = std::max(0, v0 - grow); v < std::min(v0 + TV + grow, hp.sy); ++v)
+        for (int u = std::max(0, u0 - grow); u < std::min(u0 + TU + grow, hp.sx); ++u)
+          if (mk[pbase + ((int64_t)z * hp.sy + v) * hp.sx + u]) return false;
+      return true;
+    };
     for (int z = 0; z < hp.sz; ++z)
       for (int v0 = 0; v0 < hp.sy; v0 += TV)
-        for (int u0 = 0; u0 < hp.sx; u0 += TU)
+        for (int u0 = 0; u0 < hp.sx; u0 += TU) {
+          if (masked_out(z, u0, v0)) continue;
           for (int k = 0; k < (fwd ? 1 : nseg); ++k) {
             const int c0 = -ps.cmax + k * seg, c1 = fwd ? ps.cmax : std::min(ps.cmax, c0 + seg - 1);
             if (c0 > c1) continue;
@@ -485,6 +501,7 @@ void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, 
             keys.emplace_back(key, (int32_t)mem.size());
             mem.push_back(m);
           }
+        }
   }
   std::sort(keys.begin(), keys.end());
   ng.mem.clear();
@@ -1071,6 +1088,7 @@ static pvr_status begin_extraction(pvr_ctx* c) {
   c->rpart = nullptr;
   c->nlivep = nullptr;
   c->mask = nullptr;
+  c->mask_host.clear();
   for (pvr_ctx::Plan* pl : {&c->fplan, &c->bplan, &c->iplan}) {
     pl->mem = nullptr;
     pl->grp = nullptr;
@@ -1296,6 +1314,10 @@ static pvr_status install_patches(pvr_ctx* c, const uint8_t* mask, int64_t* n_ou
     CUDA_TRY(c, cudaMalloc(&c->mask, np));
     CUDA_TRY(c, cudaMemcpyAsync(c->mask, mask + c->first_pix, c->nloc_pix,
                                 is_device_ptr(mask) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    c->mask_host.resize(c->nloc_pix);
+    CUDA_TRY(c, cudaMemcpyAsync(c->mask_host.data(), c->mask, c->nloc_pix, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    c->mask_host.clear();
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->st.pixels = c->nloc_pix;

@@ -112,7 +112,10 @@ constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics 
 constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;  // backprojection (iterations): 8 B/voxel tile
                                                      // budget; 56 KB + R: 3 CTAs per SM
 constexpr int kInitTileBytes = 96 * 1024; // init backprojection: 16 B/voxel hi/lo tile budget
-constexpr int kRBytes = 12 * 1024;         // backprojection: per-pixel (rA, rC) buffer budget
+#ifndef PVR_R_KB
+#define PVR_R_KB 12
+#endif
+constexpr int kRBytes = PVR_R_KB * 1024;   // backprojection: per-pixel (rA, rC) buffer budget
 #ifndef PVR_FWD_TILE_KB
 #define PVR_FWD_TILE_KB 48
 #endif
