@@ -96,9 +96,10 @@ struct FwdMember {  // per-member constants in shared memory
   int ob[3];
   int LU, LV, t0, p0;  // lattice extent, offset into sT, first pixel index in the group order
   int patch, z, u0, v0, tu, tv;
-  int strip;           // lattice point order: 1 = strips of 4 U columns (V fastest in blocks of
-                       // 4 U), 0 = rows (U fastest); see the lattice pass
-  float inv_LU, inv_s4;  // 1 / LU, 1 / (4 LV)
+  int sh;              // lattice point order: strips of 2^sh U columns, V-major inside
+                       // (sh = 2 axial-like, 3 x-normal), 0 = rows (U fastest); see the lattice pass
+  int skew;            // x-normal members: the c loop of point (U, V) starts at phase V & 3
+  float inv_LU, inv_s4;  // 1 / LU, 1 / (2^sh LV)
 };
 
 template <int MODE>
@@ -111,7 +112,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
   extern __shared__ __align__(128) float4 fsm4[];
   float* sT = reinterpret_cast<float*>(fsm4);
   float* sX = sT + t_floats;  // t_floats is a multiple of 32: 128-byte aligned TMA slabs
-  __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
+  __shared__ float s_ip[kMaxIp];
+  __shared__ float2 s_tpc[2 * kMaxTp + 4];  // (tp(i mod ntp), i mod ntp): phase-shifted c loops
   __shared__ FwdMember sm[kMaxMembers];
   __shared__ int s_nt, s_np;  // lattice points / pixels of the group
   __shared__ __align__(8) uint64_t s_bar;  // TMA completion barrier (MODE 0)
@@ -179,17 +181,28 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       f.patch = m.patch; f.z = m.z; f.u0 = m.u0; f.v0 = m.v0; f.tu = m.tu; f.tv = m.tv;
       // V along the tile's y axis (axial-like stacks): a warp of row-ordered points straddles
       // two lattice rows one tile row (dx floats) apart -> bank conflicts; blocks of 4 U x 8 V
-      // points hit 32 distinct banks (rows 4 (mod 8) banks apart). Other stacks keep rows.
+      // points hit 32 distinct banks (rows 4 (mod 8) banks apart). x-normal stacks (c along
+      // x): lanes differ only in y and z, whose tile offsets are multiples of 4 floats (TMA row
+      // pitch), so a warp reaches 8 banks (4 wavefronts per load); blocks of 8 U x 4 V with the
+      // c loop of row V started at phase V & 3 spread the lanes over 4 x offsets
+      // (tools/banksim_forward.py: 4.0 -> 1.5 wavefronts). Other stacks keep rows.
       const float ab0 = fabsf(pt.Qb[0]), ab1 = fabsf(pt.Qb[1]), ab2 = fabsf(pt.Qb[2]);
-      f.strip = (MODE == 0 && ab1 >= ab0 && ab1 >= ab2 && f.LU >= 4) ? 1 : 0;
+      const float ac0 = fabsf(pt.Qc[0]), ac1 = fabsf(pt.Qc[1]), ac2 = fabsf(pt.Qc[2]);
+      const bool xn = MODE == 0 && ac0 >= ac1 && ac0 >= ac2;
+      f.sh = (MODE == 0 && ab1 >= ab0 && ab1 >= ab2 && f.LU >= 4) ? 2 : (xn && f.LU >= 8 ? 3 : 0);
+      f.skew = xn ? 1 : 0;
       f.inv_LU = 1.0f / (float)f.LU;
-      f.inv_s4 = 1.0f / (float)(4 * f.LV);
+      f.inv_s4 = 1.0f / (float)((1 << f.sh) * f.LV);
     }
     {
       const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
       const int nip = (2 * ps.ru + 1) * (2 * ps.rv + 1);
       for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[ps.ip0 + i];
-      for (int i = threadIdx.x; i < 2 * ps.cmax + 1; i += kThreads) s_tp[i] = a.tab[ps.tp0 + i];
+      const int nt = 2 * ps.cmax + 1;
+      for (int i = threadIdx.x; i < 2 * nt + 4; i += kThreads) {
+        const int c = i % nt;
+        s_tpc[i] = make_float2(a.tab[ps.tp0 + c], (float)c);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -224,12 +237,13 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       const FwdMember& f = sm[k];
       const int li = i - f.t0;
       int iu, iv;
-      if (f.strip) {  // strip sidx of 4 U columns (the last one narrower), V-major inside
+      if (f.sh) {  // strip sidx of 2^sh U columns (the last one narrower), V-major inside
+        const int sw = 1 << f.sh;
         const int sidx = (int)(((float)li + 0.5f) * f.inv_s4);
-        const int r = li - sidx * 4 * f.LV;
-        const int ws = min(4, f.LU - 4 * sidx);
-        iv = ws == 4 ? (r >> 2) : (int)(((float)r + 0.5f) / (float)ws);
-        iu = 4 * sidx + (r - iv * ws);
+        const int r = li - sidx * sw * f.LV;
+        const int ws = min(sw, f.LU - sw * sidx);
+        iv = ws == sw ? (r >> f.sh) : (int)(((float)r + 0.5f) / (float)ws);
+        iu = sw * sidx + (r - iv * ws);
       } else {
         iv = (int)(((float)li + 0.5f) * f.inv_LU);
         iu = li - iv * f.LU;
@@ -238,22 +252,28 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       float rx = f.of[0] + U * f.qa[0] + V * f.qb[0];
       float ry = f.of[1] + U * f.qa[1] + V * f.qb[1];
       float rz = f.of[2] + U * f.qa[2] + V * f.qb[2];
-      // (x, y) travel as a packed pair; the lerps run on (z0, z1) pairs (FADD2 / FFMA2)
-      f2 rxy = pk(rx, ry);
+      // (x, y) travel as a packed pair; the lerps run on (z0, z1) pairs (FADD2 / FFMA2). The
+      // samples are visited from phase ph (x-normal members: V & 3, else 0) with wrap-around:
+      // s_tpc[ph + k] = (tp(c), c), c = (ph + k) mod ntp, and the position is r0 + c qc.
+      const f2 rxy0 = pk(rx, ry);
       const f2 qcxy = pk(f.qc[0], f.qc[1]);
       const float qcz = f.qc[2];
       const f2 mag = pk(kMagic, kMagic);
       const float* sXo = sX + f.ob[2] * dxy + f.ob[1] * dx + f.ob[0];
+      const float2* tpc = s_tpc + (f.skew ? (iv & 3) : 0);
       float acc = 0.0f;
 #pragma unroll kFwdUnroll
-      for (int c = 0; c < ntp; ++c) {
+      for (int k = 0; k < ntp; ++k) {
+        const float2 q = tpc[k];
+        const f2 rxy = fma2s(q.y, qcxy, rxy0);
+        const float rzc = fmaf(q.y, qcz, rz);
         const f2 txy = add2_rd(rxy, mag);
-        const float tz = __fadd_rd(rz, kMagic);
+        const float tz = __fadd_rd(rzc, kMagic);
         const int ix = __float_as_int(lo2(txy)) - kMagicBits;
         const int iy = __float_as_int(hi2(txy)) - kMagicBits;
         const int iz = __float_as_int(tz) - kMagicBits;
         const f2 fxy = sub2(rxy, sub2(txy, mag));
-        const float fz = rz - __fsub_rn(tz, kMagic);
+        const float fz = rzc - __fsub_rn(tz, kMagic);
         const float* p = sXo + iz * dxy + iy * dx + ix;
         const f2 x00 = pk(p[0], p[dxy]), x10 = pk(p[1], p[dxy + 1]);            // (z0, z1) at y0
         const f2 x01 = pk(p[dx], p[dxy + dx]), x11 = pk(p[dx + 1], p[dxy + dx + 1]);  // at y1
@@ -262,9 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         const f2 cy1 = fma2s(fx, sub2(x11, x01), x01);   // at y1
         const f2 cz = fma2s(fy, sub2(cy1, cy0), cy0);    // y-lerp: (z0, z1)
         const float c0 = lo2(cz), c1 = hi2(cz);
-        acc = fmaf(s_tp[c], fmaf(fz, c1 - c0, c0), acc);
-        rxy = add2(rxy, qcxy);
-        rz += qcz;
+        acc = fmaf(q.x, fmaf(fz, c1 - c0, c0), acc);
       }
       sT[f.t0 + iv * f.LU + iu] = acc;
     }
