@@ -289,84 +289,119 @@ __global__ void k_mix_weights(const int32_t* __restrict__ nlive, int64_t M, cons
 // X1 = clip(X0 + alpha A / C) where C > tau_C; X2 = X1 + alpha lambda sum_{d in D13}
 // [b_d(k)(X1_{k+d} - X1_k) + b_d(k-d)(X1_{k-d} - X1_k)], b from X0: the two terms of each
 // axis pair d, -d are the 26 neighbours, each weighted by its own b.
-// One CTA per 32 x 8 x 4 voxel tile: X0, A, C of the tile plus a 1-voxel halo are read once
-// (coalesced rows), X1 and the covered flag c = [C > tau_C] are formed in shared memory, and
-// every voxel of the tile sums its 26 neighbours from there.
-constexpr int kUX = 32, kUY = 8, kUZ = 4;
+// One CTA per 32 x 8 x 8 voxel tile: X0, A, C of the tile plus a 1-voxel halo are read once
+// (a warp per halo row, lanes on the 32-aligned interior columns, two lanes on the halo
+// columns), X1 and the covered flag c = [C > tau_C] are formed in shared memory, and every
+// voxel of the tile sums its 26 neighbours from there as 13 axis pairs (d, -d) of equal weight.
+// Tiles whose halo is entirely covered and in the grid (most of the volume) skip the
+// per-neighbour coverage tests.
+constexpr int kUX = 32, kUY = 8, kUZ = 8;
 constexpr int kHX = kUX + 2, kHY = kUY + 2, kHZ = kUZ + 2;
+
+__device__ __forceinline__ float rsqrt_ftz(float x) {  // x >= 1 here: no denormal handling
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// sum over the pair (d, -d) at shared offset O (weight W = |d|_1) of b (X1_n - X1_k),
+// b = rsqrt(W (W + g^2)), g = (X0_n - X0_k) / delta
+template <int O, int W, bool CHECK>
+__device__ __forceinline__ void nb_pair(const float* c0, const float* c1, f2 X0p, f2 X1p, f2 id2, f2& sum) {
+  const f2 d0 = sub2(pk(c0[-O], c0[O]), X0p);
+  f2 t = fma2(mul2(d0, d0), id2, pk((float)W, (float)W));  // W + g^2
+  if (W > 1) t = mul2s((float)W, t);
+  const f2 b = pk(rsqrt_ftz(lo2(t)), rsqrt_ftz(hi2(t)));
+  f2 dv = sub2(pk(c1[-O], c1[O]), X1p);
+  if (CHECK) {  // neighbour uncovered / off-grid (NaN X1): no term
+    const float v0 = lo2(dv) == lo2(dv) ? lo2(dv) : 0.0f, v1 = hi2(dv) == hi2(dv) ? hi2(dv) : 0.0f;
+    dv = pk(v0, v1);
+  }
+  sum = fma2(b, dv, sum);
+}
+
+template <bool CHECK>
+__device__ __forceinline__ float nb_sum(const float* c0, const float* c1, float x0, float x1, float id) {
+  constexpr int X = 1, Y = kHX, Z = kHX * kHY;
+  const f2 X0p = pk(x0, x0), X1p = pk(x1, x1), id2 = pk(id * id, id * id);
+  f2 s = pk(0.0f, 0.0f);
+  nb_pair<X, 1, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<Y, 1, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<Z, 1, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X + Y, 2, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X - Y, 2, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X + Z, 2, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X - Z, 2, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<Y + Z, 2, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<Y - Z, 2, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X + Y + Z, 3, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X + Y - Z, 3, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X - Y + Z, 3, CHECK>(c0, c1, X0p, X1p, id2, s);
+  nb_pair<X - Y - Z, 3, CHECK>(c0, c1, X0p, X1p, id2, s);
+  return lo2(s) + hi2(s);
+}
 
 __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
                                                 const float2* __restrict__ AC, int3 n, int nxp,
                                                 Params prm, const EmDev* __restrict__ em,
                                                 float alpha, float lambda, float* __restrict__ X2) {
-  __shared__ float s0[kHZ][kHY][kHX];  // X0
-  __shared__ float s1[kHZ][kHY][kHX];  // X1, NaN where C <= tau_C (uncovered) or off-grid
+  __shared__ float s0[kHZ * kHY * kHX];  // X0
+  __shared__ float s1[kHZ * kHY * kHX];  // X1, NaN where C <= tau_C (uncovered) or off-grid
   const float lo = (float)em->lo, hi = (float)em->hi;
   const int bx = blockIdx.x * kUX - 1, by = blockIdx.y * kUY - 1, bz = blockIdx.z * kUZ - 1;
-  for (int t = threadIdx.x; t < kHX * kHY * kHZ; t += blockDim.x) {
-    const int hx = t % kHX, hy = (t / kHX) % kHY, hz = t / (kHX * kHY);
-    const int i = bx + hx, j = by + hy, l = bz + hz;
-    float x0 = 0.0f, x1 = __int_as_float(0x7fc00000);
-    if (i >= 0 && i < n.x && j >= 0 && j < n.y && l >= 0 && l < n.z) {
-      x0 = X0[((size_t)l * n.y + j) * nxp + i];
-      const float2 ac = AC[((size_t)l * n.y + j) * nxp + i];
-      if (ac.y > prm.tau_C) {
-        float x = x0 + alpha * __fdividef(ac.x, ac.y);  // a6: X1 = clip(X0 + alpha A / C)
-        if (prm.clamp) x = fminf(fmaxf(x, lo), hi);
-        x1 = x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool cov = true;
+  for (int r = wid; r < kHY * kHZ; r += 8) {
+    const int hz = r / kHY, hy = r - hz * kHY;
+    const int j = by + hy, l = bz + hz;
+    const bool rin = (unsigned)j < (unsigned)n.y && (unsigned)l < (unsigned)n.z;
+    const int row = (l * n.y + j) * nxp;  // < 2^31 voxels
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (q == 1 && lane >= 2) break;
+      const int hx = q == 0 ? lane + 1 : (lane == 0 ? 0 : kHX - 1);
+      const int i = bx + hx;
+      float x0 = 0.0f, x1 = __int_as_float(0x7fc00000);
+      if (rin && (unsigned)i < (unsigned)n.x) {
+        x0 = X0[row + i];
+        const float2 ac = AC[row + i];
+        if (ac.y > prm.tau_C) {
+          float x = fmaf(alpha * ac.x, rcp_ftz(ac.y), x0);  // a6: X1 = clip(X0 + alpha A / C)
+          if (prm.clamp) x = fminf(fmaxf(x, lo), hi);
+          x1 = x;
+        }
       }
+      cov = cov && (x1 == x1);
+      s0[r * kHX + hx] = x0;
+      s1[r * kHX + hx] = x1;
     }
-    s0[hz][hy][hx] = x0;
-    s1[hz][hy][hx] = x1;
   }
-  __syncthreads();
+  const bool allc = __syncthreads_and(cov);
   const float al = alpha * lambda;
-  // b_d = phi / sqrt(1 + phi g^2), g = dX0 / delta  ==  rsqrt(1/phi^2 + (1/phi) g^2): one
-  // FFMA + MUFU per neighbour with g in units of delta; two neighbours per packed pair
   const float id = 1.0f / prm.delta;
-  for (int t = threadIdx.x; t < kUX * kUY * kUZ; t += blockDim.x) {
-    const int tx = t % kUX, ty = (t / kUX) % kUY, tz = t / (kUX * kUY);
-    const int i = bx + 1 + tx, j = by + 1 + ty, l = bz + 1 + tz;
-    if (i >= n.x || j >= n.y || l >= n.z) continue;
-    const int hx = tx + 1, hy = ty + 1, hz = tz + 1;
-    const float x0 = s0[hz][hy][hx], x1 = s1[hz][hy][hx];
+  const int i = bx + 1 + lane, j = by + 1 + wid;
+  if (i >= n.x || j >= n.y) return;
+#pragma unroll 2
+  for (int tz = 0; tz < kUZ; ++tz) {
+    const int l = bz + 1 + tz;
+    if (l >= n.z) break;
+    const int c = ((tz + 1) * kHY + (wid + 1)) * kHX + lane + 1;
+    const float x0 = s0[c], x1 = s1[c];
     float out;
     if (x1 != x1) {  // uncovered: X2 = X1 = X0
       out = x0;
     } else {
       // a7 (reading Q17): sum over the 26 neighbours d of b_d (X1_{k+d} - X1_k),
       // b_d = phi_d / sqrt(1 + phi_d ((X0_{k+d} - X0_k) / delta)^2), phi_d = 1/|d|_1
-      f2 sum2 = pk(0.0f, 0.0f);
-      const f2 X0p = pk(x0, x0), X1p = pk(x1, x1), idp = pk(id, id);
-      float pend_x0 = 0.0f, pend_x1 = 0.0f;
-      int pend_w = 0;
-      bool have = false;
-#pragma unroll
-      for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-          for (int dx = -1; dx <= 1; ++dx) {
-            if (!dx && !dy && !dz) continue;
-            const int w = (dx != 0) + (dy != 0) + (dz != 0);  // |d|_1 = 1 / phi
-            const float xn0 = s0[hz + dz][hy + dy][hx + dx], xn1 = s1[hz + dz][hy + dy][hx + dx];
-            if (!have) {
-              pend_x0 = xn0; pend_x1 = xn1; pend_w = w; have = true;
-              continue;
-            }
-            // the pair (pending neighbour, this neighbour)
-            const f2 g = mul2(sub2(pk(pend_x0, xn0), X0p), idp);
-            const f2 c = pk((float)pend_w, (float)w), a = pk((float)(pend_w * pend_w), (float)(w * w));
-            const f2 q = fma2(mul2(c, g), g, a);  // 1/phi^2 + (1/phi) g^2
-            const f2 dv = sub2(pk(pend_x1, xn1), X1p);
-            const float d0 = lo2(dv) == lo2(dv) ? lo2(dv) : 0.0f;  // neighbour uncovered / off-grid
-            const float d1 = hi2(dv) == hi2(dv) ? hi2(dv) : 0.0f;
-            sum2 = fma2(pk(rsqrtf(lo2(q)), rsqrtf(hi2(q))), pk(d0, d1), sum2);
-            have = false;
-          }
-      out = x1 + al * (lo2(sum2) + hi2(sum2));
+      const float sum = allc ? nb_sum<false>(s0 + c, s1 + c, x0, x1, id) : nb_sum<true>(s0 + c, s1 + c, x0, x1, id);
+      out = fmaf(al, sum, x1);
     }
-    X2[((size_t)l * n.y + j) * nxp + i] = out;
+    X2[(l * n.y + j) * nxp + i] = out;
   }
 }
 
