@@ -100,6 +100,7 @@ struct FwdMember {  // per-member constants in shared memory
                        // (sh = 2 axial-like, 3 x-normal), 0 = rows (U fastest); see the lattice pass
   int skew;            // x-normal members: the c loop of point (U, V) starts at phase V & 3
   float inv_LU, inv_s4;  // 1 / LU, 1 / (2^sh LV)
+  float inv_tu;          // 1 / tu (pixel index decode)
 };
 
 template <int MODE>
@@ -127,30 +128,34 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned phase = 0;
+  // X footprint of group gg by TMA (thread 0): one 3D tensor copy (box dx x dy x 1) per z
+  // slab, zero fill outside the grid, completion on the mbarrier. Issued for the CTA's first
+  // group here and for each next group as soon as the current one's lattice pass is done (the
+  // pixel pass does not read sX), so the copy overlaps the pixel pass.
+  auto issue_tma = [&](int gg) {
+    const GroupDev Gt = a.grp[gg];
+    const int tdx = Gt.dim[0], tdy = Gt.dim[1], tdz = Gt.dim[2], tdxy = (tdx * tdy + 31) & ~31;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // sX reads -> async writes
+    const char* tm = tmaps + 128 * Gt.tmap;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(tdz * tdx * tdy * 4)
+                 : "memory");
+    for (int z = 0; z < tdz; ++z)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sX0 + 4u * (unsigned)(z * tdxy)),
+          "l"(tm), "r"(Gt.lo[0]), "r"(Gt.lo[1]), "r"(Gt.lo[2] + z), "r"(bar)
+          : "memory");
+  };
+  if (MODE == 0 && threadIdx.x == 0 && (int)blockIdx.x < a.ngroups) issue_tma(blockIdx.x);
 
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
     const GroupDev G = a.grp[g];
     // tile: rows of pitch dx (the group's TMA box width), z slabs of dxy floats (128-byte
     // aligned); the box covers the group footprint (engine.cu: size_groups)
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = (dx * dy + 31) & ~31;
-    __syncthreads();  // the previous group's readers of sX / sT / tables / sm are done
-    if (MODE == 0) {
-      // X footprint by TMA: one 3D tensor copy (box dx x dy x 1) per z slab, zero fill
-      // outside the grid, completion on an mbarrier
-      if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // sX reads -> async writes
-        const char* tm = tmaps + 128 * G.tmap;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(dz * dx * dy * 4)
-                     : "memory");
-        for (int z = 0; z < dz; ++z)
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sX0 + 4u * (unsigned)(z * dxy)),
-              "l"(tm), "r"(G.lo[0]), "r"(G.lo[1]), "r"(G.lo[2] + z), "r"(bar)
-              : "memory");
-      }
-    } else if (!G.interior) {
+    __syncthreads();  // the previous group's readers of sT / tables / sm are done
+    if (MODE == 1 && !G.interior) {
       // the grid indicator over the same layout (interior groups: kappa = 1, no lattice pass)
       int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
       while (ly >= dy) { ly -= dy; ++lz; }
@@ -193,6 +198,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       f.skew = xn ? 1 : 0;
       f.inv_LU = 1.0f / (float)f.LU;
       f.inv_s4 = 1.0f / (float)((1 << f.sh) * f.LV);
+      f.inv_tu = 1.0f / (float)f.tu;
     }
     {
       const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
@@ -231,8 +237,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     const int ntp = 2 * ps.cmax + 1;
     // lattice points of all members: T(U, V) = sum_c tp(c) trilerp(X, x(U, V, c))
     const bool skip = MODE == 1 && G.interior;
+    int k = 0;  // the member of lattice point / pixel i (i only grows)
     for (int i = skip ? s_nt : threadIdx.x; i < s_nt; i += kThreads) {
-      int k = 0;
       while (k + 1 < G.nm && i >= sm[k + 1].t0) ++k;
       const FwdMember& f = sm[k];
       const int li = i - f.t0;
@@ -287,14 +293,15 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       sT[f.t0 + iv * f.LU + iu] = acc;
     }
     __syncthreads();
+    if (MODE == 0 && threadIdx.x == 0 && g + (int)gridDim.x < a.ngroups) issue_tma(g + gridDim.x);
     // pixels of all members: yhat = sum_ab ip(a,b) T(nu u + a, nv v + b) / kappa
     const int w2 = 2 * ps.ru + 1;
+    k = 0;
     for (int i = threadIdx.x; i < s_np; i += kThreads) {
-      int k = 0;
       while (k + 1 < G.nm && i >= sm[k + 1].p0) ++k;
       const FwdMember& f = sm[k];
       const int li = i - f.p0;
-      const int du = li % f.tu, dv = li / f.tu;
+      const int dv = (int)(((float)li + 0.5f) * f.inv_tu), du = li - dv * f.tu;  // li < 2^16: exact
       const int u = f.u0 + du, v = f.v0 + dv;
       float s = 0.0f;
       if (skip) {
