@@ -119,7 +119,9 @@ def oracle_sample(cfg, slices):
 
 def time_oracle(cfg, steps, warmup, slices):
     import numpy as np
+    import synth
     from oracle import Oracle
+    slices = max(slices, synth.CONFIGS[cfg].get("depth", 1))  # 3D patches (c4) need >= depth slices
     prob = oracle_sample(cfg, slices)
     orc = Oracle(prob["dims"], prob["spacing"], prob["origin"])
     for st in prob["stacks"]:

@@ -44,6 +44,7 @@ constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
 constexpr int kMagicBits = 0x4B400000;
 constexpr float kLoScale = 1048576.0f;  // 2^20: resolution of the lo word in hi units
 constexpr float kTermMax = 1048576.0f;  // 2^20: largest splat term in hi units
+constexpr float kWindowMax = 4194304.0f;  // 2^22: largest window plane sum (exact magic rounding)
 
 // Member geometry shared by both kernels.
 struct MemberGeom {
@@ -409,7 +410,8 @@ struct __align__(16) BpGroupHdr {  // per-group totals and the group's stack PSF
   int nl, np;              // lattice lines / pixels of all members
   int nu, nv, ru, rv, ip0, tp0, ntp;
   float tpmax;
-  int pad[2];
+  float tmax;              // largest splat term in fixed-point units (window bound, k_bp_table)
+  int pad;
 };
 
 __device__ __forceinline__ float pick3(const float (&v)[3], int ax) {
@@ -608,6 +610,14 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     nl = M.nU * (o.Vhi - o.Vlo);
     np = M.rw * (o.phv - o.plv + 1);
   }
+  // window bound: a flushed plane sums the terms of all samples whose floor along m is
+  // m - 1 (<= ceil(1 / qm) of them, qm = the step along m >= |qc| / sqrt 3) and of one at
+  // floor m; nterm tmax <= 2^22 keeps the magic rounding exact (c3: qm ~ 0.89, nterm = 3,
+  // tmax = 2^20; ns bounds nterm for a degenerate step)
+  float nterm = 1.0f;
+  if (lane < G.nm) nterm = fminf(ceilf(1.0f / fmaxf(M.dc[0], 1e-6f)), (float)M.ns) + 1.0f;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) nterm = fmaxf(nterm, __shfl_xor_sync(0xffffffffu, nterm, d));
   int sl = nl, sp = np;  // inclusive scans over the members
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -626,7 +636,8 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     h.nu = mg.nu; h.nv = mg.nv; h.ru = mg.ru; h.rv = mg.rv;
     h.ip0 = mg.ip0; h.tp0 = mg.tp0; h.ntp = mg.ntp;
     h.tpmax = a.psf[a.P[a.mem[G.m0].patch].stack].tpmax;
-    h.pad[0] = h.pad[1] = 0;
+    h.tmax = fminf(kTermMax, kWindowMax / nterm);
+    h.pad = 0;
     th[g] = h;
   }
 }
@@ -725,10 +736,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
       xA = fmaxf(xA, s_red[0][i]);
       xC = fmaxf(xC, s_red[1][i]);
     }
-    // every splat term |L tp w| <= max|r| tpmax  ->  < 2^20 units; the register window
-    // sums < 4 such terms per corner before rounding (< 2^22)
-    const float scA = xA > 0.0f ? kTermMax / (xA * H.tpmax) : 0.0f;
-    const float scC = xC > 0.0f ? kTermMax / (xC * H.tpmax) : 0.0f;
+    // every splat term |L tp w| <= max|r| tpmax  ->  <= H.tmax units; a register window
+    // plane sums at most nterm such terms before rounding (<= 2^22; k_bp_table)
+    const float scA = xA > 0.0f ? H.tmax / (xA * H.tpmax) : 0.0f;
+    const float scC = xC > 0.0f ? H.tmax / (xC * H.tpmax) : 0.0f;
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
     const Tile T{base, cbase, HILO ? base + 2 * (kHQ / 4) : nullptr,
                  HILO ? base + 3 * (kHQ / 4) : nullptr, dx, dy};
