@@ -921,7 +921,7 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   cudaError_t e2 = cudaMalloc(&c->X[1], c->Vp * sizeof(float));
   cudaError_t e3 = cudaMalloc(&c->AC, (c->Vp + 2) * sizeof(float2));
   cudaError_t e4 = cudaMalloc(&c->em, sizeof(EmDev));
-  cudaError_t e5 = cudaMalloc(&c->partials, (size_t)kStatBlocks * 5 * sizeof(double));
+  cudaError_t e5 = cudaMalloc(&c->partials, ((size_t)kStatBlocks * 5 + 1) * sizeof(double));  // + fwd group counter
   if (e1 || e2 || e3 || e4 || e5) {
     cudaGetLastError();
     free_dev(c);

@@ -104,13 +104,18 @@ struct FwdMember {  // per-member constants in shared memory
   float inv_tu;          // 1 / tu (pixel index decode)
 };
 
+#ifndef PVR_FWD_DYN
+#define PVR_FWD_DYN 1
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_floats,
                                                           const char* __restrict__ tmaps,
                                                           const float* __restrict__ kap,
                                                           const float* __restrict__ pprev,
                                                           float* __restrict__ out,
-                                                          double* __restrict__ partials) {
+                                                          double* __restrict__ partials,
+                                                          int* __restrict__ next) {
   extern __shared__ __align__(128) float4 fsm4[];
   float* sT = reinterpret_cast<float*>(fsm4);
   float* sX = sT + t_floats;  // t_floats is a multiple of 32: 128-byte aligned TMA slabs
@@ -148,9 +153,22 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
           "l"(tm), "r"(Gt.lo[0]), "r"(Gt.lo[1]), "r"(Gt.lo[2] + z), "r"(bar)
           : "memory");
   };
-  if (MODE == 0 && threadIdx.x == 0 && (int)blockIdx.x < a.ngroups) issue_tma(blockIdx.x);
+  // MODE 0 with PVR_FWD_DYN: thread 0 claims each CTA's next group from a launch counter (reset
+  // before the launch) when it issues that group's TMA copy; groups differ in cost, so a static
+  // stride leaves SMs idle at the end. s_gn is published by the barrier at the loop top.
+  constexpr bool kDyn = MODE == 0 && PVR_FWD_DYN;
+  __shared__ int s_gn;
+  if (MODE == 0 && threadIdx.x == 0) {
+    s_gn = kDyn ? atomicAdd(next, 1) : (int)blockIdx.x;
+    if (s_gn < a.ngroups) issue_tma(s_gn);
+  }
 
-  for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
+  for (int g = blockIdx.x;; g += gridDim.x) {
+    if (kDyn) {
+      __syncthreads();
+      g = s_gn;
+    }
+    if (g >= a.ngroups) break;
     const GroupDev G = a.grp[g];
     // tile: rows of pitch dx (the group's TMA box width), z slabs of dxy floats (128-byte
     // aligned); the box covers the group footprint (engine.cu: size_groups)
@@ -294,7 +312,10 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       sT[f.t0 + iv * f.LU + iu] = acc;
     }
     __syncthreads();
-    if (MODE == 0 && threadIdx.x == 0 && g + (int)gridDim.x < a.ngroups) issue_tma(g + gridDim.x);
+    if (MODE == 0 && threadIdx.x == 0) {
+      s_gn = kDyn ? atomicAdd(next, 1) : g + (int)gridDim.x;
+      if (s_gn < a.ngroups) issue_tma(s_gn);
+    }
     // pixels of all members: yhat = sum_ab ip(a,b) T(nu u + a, nv v + b) / kappa
     const int w2 = 2 * ps.ru + 1;
     k = 0;
@@ -642,6 +663,10 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
   }
 }
 
+#ifndef PVR_BP_DYN
+#define PVR_BP_DYN 1
+#endif
+
 // Dynamic shared memory: HILO (init pass): 4 x tile_words int32 (A, C, A_lo, C_lo), then R;
 // iterations: A at 0, C at the fixed byte offset kCOff (an immediate in the splat's shared
 // reductions), R after kBpTileBytes (init: after kInitTileBytes).
@@ -654,7 +679,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
                                                          const float* __restrict__ e,
                                                          const float* __restrict__ p,
                                                          const float* __restrict__ w, int init,
-                                                         float2* __restrict__ AC) {
+                                                         float2* __restrict__ AC,
+                                                         int* __restrict__ next) {
   extern __shared__ int4 bsm4[];
   int* base = reinterpret_cast<int*>(bsm4);
   constexpr int NW = HILO ? 4 : 2;
@@ -668,7 +694,20 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
   const unsigned tA = (unsigned)__cvta_generic_to_shared(base);
   const unsigned tpA = (unsigned)__cvta_generic_to_shared(s_tp);
 
+#if PVR_BP_DYN
+  // persistent CTAs (resident count per SM x SMs) take the next group from the plan's launch
+  // counter (after the group headers, reset before every launch): groups differ in cost, and a
+  // static stride left SMs idle at the end (bp 14.59 -> 14.22 ms at c3)
+  __shared__ int s_next;
+  for (;;) {
+    __syncthreads();  // everyone has read s_next of the previous group
+    if (threadIdx.x == 0) s_next = atomicAdd(next, 1);
+    __syncthreads();
+    const int g = s_next;
+    if (g >= a.ngroups) break;
+#else
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
+#endif
     const GroupDev G = a.grp[g];
     const BpGroupHdr H = th[g];
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
@@ -846,21 +885,23 @@ void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_
   configure();
   const int smem = (t_floats + x_floats) * 4;
   k_lattice_fwd<1><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, nullptr, nullptr, nullptr, kap,
-                                                        partials);
+                                                        partials, nullptr);
 }
 
 void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, const void* tmaps,
                     const float* kap, const float* p, float* e, double* partials) {
   configure();
   const int smem = (t_floats + x_floats) * 4;
+  int* next = reinterpret_cast<int*>(partials + kStatBlocks * 5);  // the launch's group counter
+  if (PVR_FWD_DYN) cudaMemsetAsync(next, 0, sizeof(int), st);
   k_lattice_fwd<0><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, (const char*)tmaps, kap, p, e,
-                                                        partials);
+                                                        partials, next);
 }
 
 size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off) {
   const size_t m = (size_t)nmembers * sizeof(BpMember);
   if (group_off) *group_off = m;
-  return m + (size_t)ngroups * sizeof(BpGroupHdr);
+  return m + (size_t)ngroups * sizeof(BpGroupHdr) + 16;  // + the launch's group counter
 }
 
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
@@ -870,15 +911,30 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
   configure();
   BpMember* tm = static_cast<BpMember*>(table);
   BpGroupHdr* th = reinterpret_cast<BpGroupHdr*>(static_cast<char*>(table) + group_off);
+  int* next = reinterpret_cast<int*>(th + a.ngroups);
   const int wpb = kThreads >> 5;
   if (build_table) k_bp_table<<<(a.ngroups + wpb - 1) / wpb, kThreads, 0, st>>>(a, tm, th);
+#if PVR_BP_DYN
+  static int resident[2] = {0, 0}, nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident[0], k_lattice_bp<false>, kThreads, kBpTileBytes + kRBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident[1], k_lattice_bp<true>, kThreads, kInitTileBytes + kRBytes);
+  }
+  const int per = nsm * (resident[init ? 1 : 0] > 0 ? resident[init ? 1 : 0] : 1);
+  const int grid = a.ngroups < per ? a.ngroups : per;
+  cudaMemsetAsync(next, 0, sizeof(int), st);
+#else
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
+#endif
   if (init) {  // init (raw intensities) / rigidity pass: exact hi/lo words
     k_lattice_bp<true><<<grid, kThreads, kInitTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w,
-                                                                         init, AC);
+                                                                         init, AC, next);
   } else {
     k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, 0,
-                                                                        AC);
+                                                                        AC, next);
   }
 }
 

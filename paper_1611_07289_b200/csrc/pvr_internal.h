@@ -152,8 +152,8 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
 // init: 0 iteration (w p e / kappa, w p / kappa), 1 init pass (y / kappa, 1 / kappa),
 // 2 rigidity pass (p pbar / kappa, 1 / kappa; w carries pbar)
 // `table`: the plan's per-member / per-group constants (bp_table_bytes; members first, the
-// group headers at byte `group_off`), geometry only: rebuilt by this launch when
-// `build_table` (after a set_transforms / re-plan), else reused.
+// group headers at byte `group_off`, then the launch's int group counter), geometry only:
+// rebuilt by this launch when `build_table` (after a set_transforms / re-plan), else reused.
 size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off);
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         void* table, size_t group_off, bool build_table, const float* kap,
