@@ -10,6 +10,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libpvro.so")
+_SO_OVERRIDE = os.environ.get("PVRO_SO")  # tools/mutation_probe.py: a mutant build of pvro.c
 _SRC = os.path.join(_HERE, "pvro.c")
 
 PARAM = {
@@ -34,8 +35,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(_SO)
+        if _SO_OVERRIDE:
+            L = C.CDLL(_SO_OVERRIDE)
+        else:
+            build()
+            L = C.CDLL(_SO)
         d, i32, i64, vp = C.c_double, C.c_int32, C.c_int64, C.c_void_p
         L.pvro_sinc_taylor.restype = d
         L.pvro_sinc_taylor.argtypes = [d]
