@@ -87,6 +87,17 @@ enum {
                                  P:209 "an inlier and outlier probability for each y_s",
                                  reading Q31): w = inlier posterior r if r >= 1/2, else 0;
                                  0: the threshold rule of Q13 [0]                          */
+  ,PVR_PARAM_BP_EXACT = 16    /* (extract) precision of the backprojection's shared tiles
+                                 (DESIGN.md 7). 1 [default]: exact hi/lo int32 word pairs
+                                 (~2^-41 of the group's largest splat term) for every group
+                                 that can reach the rim of the coverage -- members on a stack
+                                 border, on a patch border or next to a masked pixel (explicit
+                                 patches), of stacks with slice gaps, or whose footprint leaves
+                                 the grid -- where confidences fall to tau_C; one int32 word
+                                 (2^-20 of the largest term) elsewhere, where every cell's
+                                 confidence is that of a covered interior. 2: exact everywhere.
+                                 0: one word everywhere (a timing reference, not parity-tested
+                                 below tau_C = 1e-3)                                          */
 };
 
 /* Version string of the library build. */

@@ -38,6 +38,7 @@ struct HostStack {
   double theta;
   double u[3], v[3], w[3], h[3];  // in-plane axes, slice normal, PSF lattice steps (mm)
   int S = 0;                       // PSF samples (direct count)
+  bool gappy = false;              // through-plane coverage dips between slices (build_psf)
   StackPsf psf;                    // separable factors (offsets into the float table)
   float* y_dev = nullptr;          // device copy of the slices (until extract)
   int64_t y_off = 0;               // offset in the concatenated stack buffer
@@ -120,6 +121,8 @@ struct pvr_ctx {
   // parameters
   double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-3, tau_obs = 0.5;
   int clamp = 1, psf_mode = 0, profile = 0;
+  int bp_exact = kBpRim;  // backprojection tile precision (PVR_PARAM_BP_EXACT)
+  bool explicit_patches = false;  // patches from pvr_set_patches / superpixels (not windows)
   double s2floor = 1e-6, nsigma = 3.0, quality = 1.0;
   // stacks / patches
   std::vector<HostStack> stacks;
@@ -247,6 +250,30 @@ int psf_steps(double pitch, double s, double q) {  // reading Q5: n = max(2, cei
   return std::max(2, n);
 }
 
+// Through-plane coverage of a stack: P(z) = sum_k sum_c tp(c) tent((z - k step - c h_w) / s)
+// over one slice period in the middle of the stack. A stack whose coverage dips below 1/4 of
+// its peak between slices (slice gaps, thin slices far apart) leaves cells of small confidence
+// inside its footprint, so all its backprojection members get exact tiles (the border rule of
+// build_natural covers the outer rim only).
+bool stack_gappy(const HostStack& st, const std::vector<double>& tp, double hw, double s) {
+  if (st.K < 2) return true;
+  const double step = std::fabs(st.G[2] * st.w[0] + st.G[6] * st.w[1] + st.G[10] * st.w[2]);
+  const int cmax = ((int)tp.size() - 1) / 2;
+  double mn = 1e300, mx = 0.0;
+  for (int i = 0; i < 64; ++i) {
+    const double z = step * i / 64.0;
+    double v = 0.0;
+    for (int k = -4; k <= 4; ++k)
+      for (int c = -cmax; c <= cmax; ++c) {
+        const double t = std::fabs(z - k * step - c * hw) / s;
+        if (t < 1.0) v += tp[c + cmax] * (1.0 - t);
+      }
+    mn = std::min(mn, v);
+    mx = std::max(mx, v);
+  }
+  return !(mn >= 0.25 * mx);
+}
+
 // PSF of one stack: psi(a,b,c) ~ sinc(pi R) exp(-(c h_w)^2 / 2 sw^2) with
 // R = |(a/n_u, b/n_v)| < 1 (main lobe, Q2), |c h_w| <= nsigma sw (Q3), normalised to 1.
 // Stored as its two factors ip(a,b) = sinc / sum sinc and tp(c) = g / sum g, whose product is
@@ -261,6 +288,7 @@ pvr_status build_psf(pvr_ctx* c, HostStack& st) {
     st.S = 1;
     const double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
     st.h[0] = norm3(c0); st.h[1] = norm3(c1); st.h[2] = 0.0;  // Qa = Mu, Qb = Mv
+    st.gappy = stack_gappy(st, std::vector<double>{1.0}, 0.0, c->s);
     return PVR_OK;
   }
   const double c0[3] = {st.G[0], st.G[4], st.G[8]}, c1[3] = {st.G[1], st.G[5], st.G[9]};
@@ -314,6 +342,7 @@ pvr_status build_psf(pvr_ctx* c, HostStack& st) {
   }
   ps.tpmax = (float)tpmax;
   st.S = disk * (2 * cmax + 1);
+  st.gappy = stack_gappy(st, tp, st.h[2], c->s);
   return PVR_OK;
 }
 
@@ -486,6 +515,29 @@ void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, 
           if (mk[pbase + ((int64_t)z * hp.sy + v) * hp.sx + u]) return false;
       return true;
     };
+    // Rim members (exact backprojection tiles, GroupDev::exact): cells of small confidence lie at
+    // the rim of the coverage, which only these members reach: a tile on its stack's border
+    // (windows of extract_patches cover every pixel of the stack, so inner patch borders are
+    // covered by the neighbouring windows) or, for explicit patches, on its patch's border or
+    // with a masked-out pixel in its grown tile; every member of a stack with slice gaps
+    // (stack_gappy) or with PVR_PARAM_BP_EXACT = 2. Footprints that leave the grid are added
+    // per geometry (size_groups, k_replan).
+    const HostStack& hst = c->stacks[hp.stack];
+    auto rim_member = [&](const MemberDev& m, const HostPatch& p) {
+      if (c->bp_exact == kBpAll || hst.gappy) return true;
+      if (c->bp_exact == kBpSingle) return false;
+      if (c->explicit_patches) {
+        if (m.u0 == 0 || m.v0 == 0 || m.u0 + m.tu >= p.sx || m.v0 + m.tv >= p.sy || m.z == 0 || m.z == p.sz - 1)
+          return true;
+        if (mk)
+          for (int v = std::max(0, m.v0 - 1); v < std::min(m.v0 + m.tv + 1, p.sy); ++v)
+            for (int u = std::max(0, m.u0 - 1); u < std::min(m.u0 + m.tu + 1, p.sx); ++u)
+              if (!mk[pbase + ((int64_t)m.z * p.sy + v) * p.sx + u]) return true;
+        return false;
+      }
+      return p.x0 + m.u0 == 0 || p.y0 + m.v0 == 0 || p.x0 + m.u0 + m.tu >= hst.W || p.y0 + m.v0 + m.tv >= hst.H ||
+             p.z0 + m.z == 0 || p.z0 + m.z == hst.K - 1;
+    };
     for (int z = 0; z < hp.sz; ++z)
       for (int v0 = 0; v0 < hp.sy; v0 += TV)
         for (int u0 = 0; u0 < hp.sx; u0 += TU) {
@@ -493,7 +545,8 @@ void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, 
           for (int k = 0; k < (fwd ? 1 : nseg); ++k) {
             const int c0 = -ps.cmax + k * seg, c1 = fwd ? ps.cmax : std::min(ps.cmax, c0 + seg - 1);
             if (c0 > c1) continue;
-            const MemberDev m{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0), c0, c1};
+            MemberDev m{(int32_t)s, z, u0, v0, std::min(TU, hp.sx - u0), std::min(TV, hp.sy - v0), c0, c1, 0};
+            if (!fwd && rim_member(m, hp)) m.flags |= kMemberRim;
             // group key: stack | slice | c segment | stack row | stack column | tile shape
             const uint64_t key = ((uint64_t)hp.stack << 58) | ((uint64_t)(hp.z0 + z) << 44) |
                                  ((uint64_t)k << 38) | ((uint64_t)(hp.y0 + v0) << 24) |
@@ -560,7 +613,9 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   // the iteration backprojection plans to 90% of its tile budget: the device re-plan of a
   // later set_transforms (k_replan) accepts growth up to 100% (and splits a group that grew
   // past it into single-member groups) before falling back here
-  const int64_t vox_budget = fwd ? kFwdTileBytes / 4 : kind == 1 ? kBpTileBytes / 8 * 9 / 10 : kInitTileBytes / 16;
+  // shared-memory budget in bytes: forward 4 B per staged voxel; backprojection 16 B per cell
+  // for exact groups (hi / lo words), 8 B for single-word groups; the init plan is all exact
+  const int64_t byte_budget = fwd ? kFwdTileBytes : kind == 1 ? (int64_t)kBpTileBytes * 9 / 10 : kBpTileBytes;
   const int64_t nm = (int64_t)ng.mem.size();
   std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
 #pragma omp parallel for schedule(static)
@@ -586,6 +641,9 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     g.interior = 1;
     for (int d = 0; d < 3; ++d)
       if (lo[d] < 0 || hi[d] > n3[d] - 1) g.interior = 0;
+    int rim = 0;
+    for (int i = a; i < b; ++i) rim |= ng.mem[i].flags & kMemberRim;
+    g.exact = !fwd && (kind == 2 || c->bp_exact == kBpAll || (c->bp_exact == kBpRim && (rim || !g.interior)));
     if (fwd) {
       // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
       // (measured: a box starting at an x not a multiple of 4 floats faults with an illegal
@@ -614,6 +672,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   std::vector<int64_t> nvox(ngrp);
 #pragma omp parallel for schedule(static)
   for (int gi = 0; gi < ngrp; ++gi) nvox[gi] = group(ng.start[gi], ng.start[gi + 1], nat[gi]);
+  auto fits = [&](const GroupDev& g, int64_t vox) { return vox * (fwd ? 4 : g.exact ? 16 : 8) <= byte_budget; };
   out.grp.clear();
   out.grp.reserve(ngrp);
   out.max_tile_vox = 0;
@@ -624,7 +683,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   int fit = 0;
   for (int gi = 0; gi < ngrp; ++gi) {
     const int a = ng.start[gi], b = ng.start[gi + 1];
-    if (nvox[gi] <= vox_budget) {
+    if (fits(nat[gi], nvox[gi])) {
       ++fit;
       out.grp.push_back(nat[gi]);
       out.max_tile_vox = std::max(out.max_tile_vox, nvox[gi]);
@@ -634,7 +693,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     for (int i = a; i < b; ++i) {
       GroupDev g;
       const int64_t vox = group(i, i + 1, g);
-      if (vox > vox_budget) out.all_fit = false;
+      if (!fits(g, vox)) out.all_fit = false;
       out.grp.push_back(g);
       out.max_tile_vox = std::max(out.max_tile_vox, vox);
     }
@@ -980,7 +1039,8 @@ pvr_status pvr_comm_init(pvr_ctx* c, int nranks, int rank, const void* uid) {
 
 pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
   GUARD(c);
-  const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA || key == PVR_PARAM_PSF_QUALITY;
+  const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA || key == PVR_PARAM_PSF_QUALITY ||
+                           key == PVR_PARAM_BP_EXACT;
   if (extract_key && c->state >= PATCHED)
     return fail(c, PVR_ERR_STATE, "parameter %d must be set before extract_patches", key);
   switch (key) {
@@ -1002,6 +1062,7 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
     case PVR_PARAM_EM_TOL: if (!(v >= 0)) goto bad; c->em_tol = v; break;
     case PVR_PARAM_PATCH_MIXTURE: if (v != 0 && v != 1) goto bad; c->patch_mixture = (int)v; break;
     case PVR_PARAM_PROFILE: c->profile = v != 0; break;
+    case PVR_PARAM_BP_EXACT: if (v != 0 && v != 1 && v != 2) goto bad; c->bp_exact = (int)v; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }
   return PVR_OK;
@@ -1120,6 +1181,7 @@ pvr_status pvr_extract_patches(pvr_ctx* c, int size, int stride, int depth, int 
                   st.W, st.H, st.K);
   pvr_status rb = begin_extraction(c);
   if (rb != PVR_OK) return rb;
+  c->explicit_patches = false;
   // patch list, order stack, z0, y0, x0
   c->patches.clear();
   for (int si = 0; si < (int)c->stacks.size(); ++si) {
@@ -1152,6 +1214,7 @@ pvr_status pvr_set_patches(pvr_ctx* c, int64_t n, const int32_t* rects, const ui
   }
   pvr_status rb = begin_extraction(c);
   if (rb != PVR_OK) return rb;
+  c->explicit_patches = true;
   c->patches.swap(list);
   return install_patches(c, mask, n_out);
 }
@@ -1251,6 +1314,7 @@ pvr_status pvr_superpixel_patches(pvr_ctx* c, int S, int m, int iters, int gamma
   if (list.empty()) return fail(c, PVR_ERR_EMPTY, "no superpixels");
   pvr_status rb = begin_extraction(c);
   if (rb != PVR_OK) return rb;
+  c->explicit_patches = true;
   c->patches.swap(list);
   return install_patches(c, mask.data(), n_out);
 }
@@ -1513,17 +1577,32 @@ pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const Latt
   return PVR_OK;
 }
 
-pvr_status pvr_init_volume(pvr_ctx* c) {
-  GUARD(c);
-  if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
+// The plan of the one-off exact passes (init, rigidity): the iteration's own plan when all its
+// groups are exact (PVR_PARAM_BP_EXACT = 2), else the lazily built all-exact init plan (its
+// groups fit the 16 B per cell budget).
+static pvr_status exact_plan(pvr_ctx* c, pvr_ctx::Plan** pl) {
+  if (c->bp_exact == kBpAll) {
+    *pl = &c->bplan;
+    return PVR_OK;
+  }
   if (!c->iplan_valid) {
     pvr_status rp = build_plans(c, c->geo, 2, 3);
     if (rp != PVR_OK) return rp;
     c->iplan_valid = true;
   }
-  const LatticeArgs lb = lattice_args(c, c->iplan);
+  *pl = &c->iplan;
+  return PVR_OK;
+}
+
+pvr_status pvr_init_volume(pvr_ctx* c) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "init_volume needs set_transforms");
+  pvr_ctx::Plan* pl = nullptr;
+  pvr_status rp = exact_plan(c, &pl);
+  if (rp != PVR_OK) return rp;
+  const LatticeArgs lb = lattice_args(c, *pl);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
-  pvr_status rb = backproject(c, c->stream, c->iplan, lb, c->w, 1);
+  pvr_status rb = backproject(c, c->stream, *pl, lb, c->w, 1);
   if (rb != PVR_OK) return rb;
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;
@@ -1537,15 +1616,13 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "rigidity_map needs set_transforms");
   if (!out || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
-  if (!c->iplan_valid) {
-    pvr_status rp = build_plans(c, c->geo, 2, 3);
-    if (rp != PVR_OK) return rp;
-    c->iplan_valid = true;
-  }
-  const LatticeArgs lb = lattice_args(c, c->iplan);
+  pvr_ctx::Plan* pl = nullptr;
+  pvr_status rp = exact_plan(c, &pl);
+  if (rp != PVR_OK) return rp;
+  const LatticeArgs lb = lattice_args(c, *pl);
   CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
-  // W^T (p pbar) and W^T 1 with the exact hi/lo tiles of the init pass (pbar rides in w)
-  pvr_status rb = backproject(c, c->stream, c->iplan, lb, c->pbar, 2);
+  // W^T (p pbar) and W^T 1 with exact hi/lo tiles (pbar rides in w)
+  pvr_status rb = backproject(c, c->stream, *pl, lb, c->pbar, 2);
   if (rb != PVR_OK) return rb;
   pvr_status r = allreduce_ac(c);
   if (r != PVR_OK) return r;
@@ -1574,12 +1651,12 @@ static pvr_status replan_on_device(pvr_ctx* c) {
   // host plan); backprojection: the hard tile budget (the host planned to 90% of it)
   launch_replan(c->stream, c->fplan.mem, c->fplan.grp, c->fplan.ngroups, (int)c->fplan.grp_cap, c->pdev, c->psf,
                 1, c->dims, kFwdTileBytes / 4 * 3 / 2, c->fbox_dev, nshape, c->replan_buf, c->replan_buf + 1,
-                nullptr);
+                nullptr, c->bp_exact);
   // backprojection groups that outgrow the tile are split into single-member groups appended
   // after the plan's (their Morton locality is lost until the next host plan)
   launch_replan(c->stream, c->bplan.mem, c->bplan.grp, c->bplan.ngroups, (int)c->bplan.grp_cap, c->pdev, c->psf,
-                0, c->dims, kBpTileBytes / 8, nullptr, 0, c->replan_buf + 2, c->replan_buf + 3,
-                c->replan_buf + 4);
+                0, c->dims, kBpTileBytes, nullptr, 0, c->replan_buf + 2, c->replan_buf + 3, c->replan_buf + 4,
+                c->bp_exact);
   CHECK_LAUNCH(c);
   int h[5];
   CUDA_TRY(c, cudaMemcpyAsync(h, c->replan_buf, sizeof(h), cudaMemcpyDeviceToHost, c->stream));

@@ -512,23 +512,30 @@ __device__ int replan_interior(const int (&lo)[3], const int (&hi)[3], int3 n) {
 __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict__ grp, int ngroups, int cap,
                          const PatchDev* __restrict__ P, const StackPsf* __restrict__ psf, int fwd, int3 n,
                          int64_t vox_budget, const int* __restrict__ shapes, int nshape,
-                         int* __restrict__ maxvox, int* __restrict__ fail, int* __restrict__ nappend) {
+                         int* __restrict__ maxvox, int* __restrict__ fail, int* __restrict__ nappend,
+                         int bp_mode) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ngroups) return;
   GroupDev G = grp[g];
   if (G.nm == 0) return;  // emptied by an earlier split
   int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+  int rim = 0;
   for (int i = G.m0; i < G.m0 + G.nm; ++i) {
     const MemberDev m = mem[i];
     const PatchDev& pt = P[m.patch];
     int ml[3], mh[3];
     replan_member_box(m, pt, psf[pt.stack], fwd, ml, mh);
+    rim |= m.flags & kMemberRim;
     for (int d = 0; d < 3; ++d) {
       lo[d] = min(lo[d], ml[d]);
       hi[d] = max(hi[d], mh[d]);
     }
   }
   G.interior = replan_interior(lo, hi, n);
+  // backprojection tile precision (engine.cu: size_groups): exact for rim members and
+  // footprints that leave the grid; the byte budget then buys half the cells
+  G.exact = !fwd && (bp_mode == kBpAll || (bp_mode == kBpRim && (rim || !G.interior)));
+  const int64_t cell_bytes = G.exact ? 16 : 8;
   int64_t vox;
   if (fwd) {
     lo[0] -= ((lo[0] % 4) + 4) % 4;
@@ -550,7 +557,7 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
     vox = (int64_t)((G.dim[0] * G.dim[1] + 31) & ~31) * G.dim[2];
   } else {
     vox = replan_bp_box(lo, hi, G);
-    if (vox > vox_budget && nappend && G.nm > 1) {
+    if (vox * cell_bytes > vox_budget && nappend && G.nm > 1) {
       for (int i = G.m0; i < G.m0 + G.nm; ++i) {
         const MemberDev m = mem[i];
         const PatchDev& pt = P[m.patch];
@@ -561,9 +568,10 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
         S.nm = 1;
         S.tmap = 0;
         S.interior = replan_interior(ml, mh, n);
+        S.exact = bp_mode == kBpAll || (bp_mode == kBpRim && ((m.flags & kMemberRim) || !S.interior));
         const int64_t sv = replan_bp_box(ml, mh, S);
         const int k = atomicAdd(nappend, 1);
-        if (sv > vox_budget || ngroups + k >= cap) {
+        if (sv * (S.exact ? 16 : 8) > vox_budget || ngroups + k >= cap) {
           atomicExch(fail, 1);
           continue;
         }
@@ -575,7 +583,7 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
       vox = 0;
     }
   }
-  if (vox > vox_budget) atomicExch(fail, 1);
+  if ((fwd ? vox : vox * cell_bytes) > vox_budget) atomicExch(fail, 1);
   atomicMax(maxvox, (int)(vox < (1 << 30) ? vox : (1 << 30)));
   grp[g] = G;
 }
@@ -641,10 +649,10 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
 
 void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, int cap, const PatchDev* P,
                    const StackPsf* psf, int fwd, int3 n, int64_t vox_budget, const int* shapes, int nshape,
-                   int* maxvox, int* fail, int* nappend) {
+                   int* maxvox, int* fail, int* nappend, int bp_mode) {
   if (ngroups > 0)
     k_replan<<<(ngroups + 255) / 256, 256, 0, st>>>(mem, grp, ngroups, cap, P, psf, fwd, n, vox_budget, shapes,
-                                                     nshape, maxvox, fail, nappend);
+                                                     nshape, maxvox, fail, nappend, bp_mode);
 }
 
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out) {

@@ -30,6 +30,7 @@
 // coalesced red.global.add.v4.f32 (voxel pairs), skipping cells outside the grid.
 #include <cfloat>
 #include <cmath>
+#include <mutex>
 
 #include "device_util.cuh"
 #include "pvr_internal.h"
@@ -392,14 +393,6 @@ __device__ __forceinline__ Owned owned_range(const MemberDev& m, const PatchDev&
   return o;
 }
 
-// value (hi units, |v| < 2^22) -> exact hi/lo int32 pair: v = hi + lo 2^-20 (+ < 2^-21)
-__device__ __forceinline__ void split_hilo(float v, int& hi, int& lo) {
-  const float t = __fadd_rn(v, kMagic);
-  hi = __float_as_int(t) - kMagicBits;
-  const float r = __fsub_rn(v, __fsub_rn(t, kMagic));  // exact (Sterbenz)
-  lo = __float_as_int(__fmaf_rn(r, kLoScale, kMagic)) - kMagicBits;
-}
-
 struct Tile {  // planar int32 accumulators of the group bbox: A, C (+ lo words for HILO)
   int *ah, *ch, *al, *cl;
   int dx, dy;
@@ -416,9 +409,10 @@ struct __align__(16) BpMember {
   int o[3];                // integer origin in the tile (frame)
   int s[3];                // tile strides (frame)
   int ti0, dti, ns;        // tp index of the first sample, its step (+-1), samples per line
-  int Ulo, Vlo, nU;
-  float inv_nU, inv_rw;
-  int lbeg, lend;          // flattened line range of the member in the group
+  int Ulo, Vlo, nU, nV;    // owned lattice range [Ulo, Ulo + nU) x [Vlo, Vlo + nV)
+  int nU3, nUV3;           // line colouring: ceil(nU / 3), ceil(nU / 3) ceil(nV / 3)
+  float inv_nU3, inv_nUV3, inv_rw, inv_nU;
+  int lbeg, lend;          // flattened (padded, colour-ordered) line range of the member
   int pbeg, pend;          // flattened pixel range (== its R range)
   int plu, plv, phu, phv, rw;
   int64_t pixz, yz;        // first pixel of slice z in the local arrays / in the stacks
@@ -431,8 +425,9 @@ struct __align__(16) BpGroupHdr {  // per-group totals and the group's stack PSF
   int nl, np;              // lattice lines / pixels of all members
   int nu, nv, ru, rv, ip0, tp0, ntp;
   float tpmax;
-  float tmax;              // largest splat term in fixed-point units (window bound, k_bp_table)
-  int pad;
+  float tmax;              // largest splat term in fixed-point units (k_bp_table: window and
+                           // per-cell total bounds)
+  float lsc;               // lo-word scale (2^20, lower if a cell could take > 4096 flushes)
 };
 
 __device__ __forceinline__ float pick3(const float (&v)[3], int ax) {
@@ -442,33 +437,25 @@ __device__ __forceinline__ int pick3i(const int (&v)[3], int ax) {
   return ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]);
 }
 
+#ifndef PVR_BP_COLOUR
+#define PVR_BP_COLOUR 0  // 1: lines in colour classes (U mod 3, V mod 3): no same-cell lanes
+#endif                    // (measured slower: the bank conflicts remain, plus padding)
+#ifndef PVR_BP_PHASES
+#define PVR_BP_PHASES 2   // lanes start their line at sample (lane mod P) ns / P (wrapping)
+#endif
 #ifndef PVR_BP_UNROLL
 #define PVR_BP_UNROLL 4
 #endif
 constexpr int kBpUnroll = PVR_BP_UNROLL;  // steps per iteration of the splat window loop
-constexpr int kCOff = kBpTileBytes / 2;  // byte offset of the C plane in the iteration tile
-// init / rigidity tile (HILO): A_hi, C_hi, A_lo, C_lo planes at fixed byte offsets
-constexpr int kHQ = kInitTileBytes / 4;
-
-template <bool HILO>
-__device__ __forceinline__ void flush_word(unsigned a, float v, bool is_c) {
-  if (HILO) {
-    int h, l;
-    split_hilo(v, h, l);
-    if (is_c) { sred<kHQ>(a, h); sred<3 * kHQ>(a, l); }
-    else      { sred<0>(a, h);   sred<2 * kHQ>(a, l); }
-  } else {
-    const int q = __float_as_int(__fadd_rn(v, kMagic)) - kMagicBits;
-    if (is_c) sred<kCOff>(a, q);
-    else      sred<0>(a, q);
-  }
-}
+constexpr int kCOff = kBpTileBytes / 2;  // single-word tile: byte offset of the C plane
+// exact tile (HILO): A_hi, C_hi, A_lo, C_lo planes at fixed byte offsets kHQ apart
+constexpr int kHQ = kBpTileBytes / 4;
 
 // Flush one plane of the window: corner j's weight sum S_j times the line's (LA, LC) into the
 // A and C words of the 4 transverse corners (a, +sp4, +sq4, +sp4+sq4).
 template <bool HILO>
 __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, float s1, float s2, float s3,
-                                       f2 L, f2 mag) {
+                                       f2 L, f2 mag, f2 lsc) {
   if (!HILO) {
     // L S + magic: the fixed-point rounding of each window sum (one FFMA2 per corner)
     const f2 t0 = fma2s(s0, L, mag), t1 = fma2s(s1, L, mag), t2 = fma2s(s2, L, mag), t3 = fma2s(s3, L, mag);
@@ -481,13 +468,22 @@ __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, f
     sred<0>(a + sp4 + sq4, __float_as_int(lo2(t3)) - kMagicBits);
     sred<kCOff>(a + sp4 + sq4, __float_as_int(hi2(t3)) - kMagicBits);
   } else {
+    // exact hi / lo words of S L (A and C as a packed pair): t = S L + magic rounds to the hi
+    // integer h = t - magic (exact); the FMA S L - h is the exact remainder r, |r| <= 1/2, and
+    // lo = round(r lsc), lsc = 2^20 (k_bp_table). hi + lo / lsc equals S L to 1 / (2 lsc) hi
+    // units: the word pair resolves ~2^-41 of the group's largest splat term, whatever the
+    // cell's own total.
     const unsigned ac[4] = {a, a + sp4, a + sq4, a + sp4 + sq4};
     const float sj[4] = {s0, s1, s2, s3};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const f2 v = mul2s(sj[j], L);
-      flush_word<true>(ac[j], lo2(v), false);
-      flush_word<true>(ac[j], hi2(v), true);
+      const f2 t = fma2s(sj[j], L, mag);
+      const f2 r = fma2s(sj[j], L, sub2(mag, t));
+      const f2 l = fma2(r, lsc, mag);
+      sred<0>(ac[j], __float_as_int(lo2(t)) - kMagicBits);
+      sred<kHQ>(ac[j], __float_as_int(hi2(t)) - kMagicBits);
+      sred<2 * kHQ>(ac[j], __float_as_int(lo2(l)) - kMagicBits);
+      sred<3 * kHQ>(ac[j], __float_as_int(hi2(l)) - kMagicBits);
     }
   }
 }
@@ -503,47 +499,57 @@ __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, f
 // flush is uniform across the warp (all lanes issue the same 8 shared reductions); only the
 // rarer transverse restart branches. Window sums before rounding: < 4 terms of < 2^20 units
 // each (group scale, k_lattice_bp). Tile: A words at shared address tA, C words at
-// tA + kCOff; HILO (init / rigidity passes): every window sum split into exact hi / lo words
+// tA + kCOff; HILO (exact groups): every window sum split into exact hi / lo words
 // (A_hi, C_hi, A_lo, C_lo planes, kHQ apart).
 template <bool HILO>
-__device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const BpMember& M, float rm,
-                                               float rp, float rq, float LA, float LC) {
-  f2 rpq = pk(rp, rq);
+__device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const BpMember& M, float rm0,
+                                               float rp, float rq, float LA, float LC, float lo_scale,
+                                               int ph) {
+  const f2 rpq0 = pk(rp, rq);
   const float qm = M.dc[0];
   const f2 qpq = pk(M.dc[1], M.dc[2]);
   const f2 mag = pk(kMagic, kMagic);
   const f2 L = pk(LA, LC);
+  const f2 lsc = pk(lo_scale, lo_scale);
   const f2 one0 = pk(1.0f, 0.0f), m1p1 = pk(-1.0f, 1.0f);
   const int sm4 = 4 * M.s[0], sp4 = 4 * M.s[1], sq4 = 4 * M.s[2];
   const unsigned org = tA + (unsigned)(M.o[0] * sm4 + M.o[1] * sp4 + M.o[2] * sq4);
-  unsigned ta = s_tp + 4u * M.ti0;
+  const unsigned ta0 = s_tp + 4u * M.ti0;
   const int dta = 4 * M.dti;
   const int ns = M.ns;
-  float fl;
-  int wm = mfloor(rm, fl);
-  int wp = __float_as_int(lo2(add2_rd(rpq, mag))) - kMagicBits;
-  int wq = __float_as_int(hi2(add2_rd(rpq, mag))) - kMagicBits;
+  const float nsf = (float)ns;
+  // samples are visited from index ph with wrap-around (ph = 0 for phase 0 lanes): lanes of a
+  // warp that walk neighbouring lines then sit in different planes of the tile, so their
+  // same-floor cells are different addresses and their banks are offset (the wrap costs one
+  // restart flush)
+  float kf = (float)ph;
+  unsigned ta = ta0 + (unsigned)(dta * ph);
+  int wm = 0, wp = 0, wq = 0;
   f2 P[4];  // corner j: (plane wm, plane wm + 1) weight sums
 #pragma unroll
   for (int j = 0; j < 4; ++j) P[j] = pk(0.0f, 0.0f);
 #pragma unroll kBpUnroll
   for (int k = 0; k < ns; ++k) {
+    const float rm = fmaf(kf, qm, rm0);
+    const f2 rpq = fma2s(kf, qpq, rpq0);
     const float tm = __fadd_rd(rm, kMagic);
     const f2 tpq = add2_rd(rpq, mag);
     const int im = __float_as_int(tm) - kMagicBits;
     const int ip = __float_as_int(lo2(tpq)) - kMagicBits;
     const int iq = __float_as_int(hi2(tpq)) - kMagicBits;
-    const bool same = (ip == wp) & (iq == wq);
-    const bool keep = same & (im == wm);
-    const bool adv = same & (im == wm + 1);
-    const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-    flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag);  // plane wm
-    if (!keep && !adv)  // restart: plane wm + 1 too
-      flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag);
-    // shift: keep -> (0, m+1); advance -> (m+1, 0); restart (or a jump) -> (0, 0)
-    const f2 sh = pk(adv ? 1.0f : 0.0f, keep ? 1.0f : 0.0f);
+    if (k > 0) {  // (uniform) the first sample only opens the window
+      const bool same = (ip == wp) & (iq == wq);
+      const bool keep = same & (im == wm);
+      const bool adv = same & (im == wm + 1);
+      const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
+      flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);  // plane wm
+      if (!keep && !adv)  // restart (transverse change, the wrap, a jump): plane wm + 1 too
+        flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
+      // shift: keep -> (0, m+1); advance -> (m+1, 0); restart -> (0, 0)
+      const f2 sh = pk(adv ? 1.0f : 0.0f, keep ? 1.0f : 0.0f);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) P[j] = mul2s(hi2(P[j]), sh);
+      for (int j = 0; j < 4; ++j) P[j] = mul2s(hi2(P[j]), sh);
+    }
     wm = im;
     wp = ip;
     wq = iq;
@@ -560,13 +566,16 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
     P[1] = fma2s(hi2(w01), TM, P[1]);
     P[2] = fma2s(lo2(w23), TM, P[2]);
     P[3] = fma2s(hi2(w23), TM, P[3]);
-    rm += qm;
-    rpq = add2(rpq, qpq);
+    kf += 1.0f;
     ta += dta;
+    if (kf == nsf) {  // wrap to the line's first sample
+      kf = 0.0f;
+      ta = ta0;
+    }
   }
   const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-  flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag);
-  flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag);
+  flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);
+  flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
 }
 
 // Member tables of all groups of a backprojection plan (geometry only: rebuilt after every
@@ -619,6 +628,11 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     M.Ulo = o.Ulo;
     M.Vlo = o.Vlo;
     M.nU = o.Uhi - o.Ulo;
+    M.nV = o.Vhi - o.Vlo;
+    M.nU3 = (M.nU + 2) / 3;
+    M.nUV3 = M.nU3 * ((M.nV + 2) / 3);
+    M.inv_nU3 = 1.0f / (float)M.nU3;
+    M.inv_nUV3 = 1.0f / (float)M.nUV3;
     M.inv_nU = 1.0f / (float)M.nU;
     M.plu = o.plu; M.phu = o.phu; M.plv = o.plv; M.phv = o.phv;
     M.rw = o.phu - o.plu + 1;
@@ -628,7 +642,11 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     M.sx = pt.sx;
     M.W = pt.W;
     M.patch = m.patch;
-    nl = M.nU * (o.Vhi - o.Vlo);
+#if PVR_BP_COLOUR
+    nl = 9 * M.nUV3;  // 9 colour classes (U mod 3, V mod 3), padded to whole classes
+#else
+    nl = M.nU * M.nV;
+#endif
     np = M.rw * (o.phv - o.plv + 1);
   }
   // window bound: a flushed plane sums the terms of all samples whose floor along m is
@@ -636,9 +654,31 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
   // floor m; nterm tmax <= 2^22 keeps the magic rounding exact (c3: qm ~ 0.89, nterm = 3,
   // tmax = 2^20; ns bounds nterm for a degenerate step)
   float nterm = 1.0f;
-  if (lane < G.nm) nterm = fminf(ceilf(1.0f / fmaxf(M.dc[0], 1e-6f)), (float)M.ns) + 1.0f;
+  // Per-cell totals (int32 words): a cell k takes, from one member, the lines whose transverse
+  // position lies within 1 voxel of it -- lattice points of the (du, dv) transverse lattice in
+  // a 2 x 2 square: <= (2 + |du_t| + |dv_t|)^2 / |du_t x dv_t| -- each flushing the plane of k
+  // at most ceil(2 / qm) + 2 times, with weights along m summing to <= 1 / qm + 1. So the hi
+  // total is <= sum_members (1 / qm + 1) nlines tmax and the lo total (|lo| <= lsc / 2 per
+  // flush) <= sum_members (ceil(2 / qm) + 2) nlines lsc / 2; both are kept below 2^30.
+  float hib = 0.0f, flb = 0.0f;
+  if (lane < G.nm) {
+    const float qm = fmaxf(M.dc[0], 1e-6f);
+    nterm = fminf(ceilf(1.0f / qm), (float)M.ns) + 1.0f;
+    const float at = fabsf(M.du[1] * M.dv[2] - M.du[2] * M.dv[1]);
+    const float lu = sqrtf(M.du[1] * M.du[1] + M.du[2] * M.du[2]);
+    const float lv = sqrtf(M.dv[1] * M.dv[1] + M.dv[2] * M.dv[2]);
+    const float nlines = fminf((2.0f + lu + lv) * (2.0f + lu + lv) / fmaxf(at, 1e-12f),
+                               (float)(M.nU * M.nV));
+    const float steps = fminf(1.0f / qm + 1.0f, (float)M.ns);
+    hib = steps * nlines;
+    flb = fminf(ceilf(2.0f / qm) + 2.0f, (float)M.ns + 1.0f) * nlines;
+  }
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) nterm = fmaxf(nterm, __shfl_xor_sync(0xffffffffu, nterm, d));
+  for (int d = 16; d > 0; d >>= 1) {
+    nterm = fmaxf(nterm, __shfl_xor_sync(0xffffffffu, nterm, d));
+    hib += __shfl_xor_sync(0xffffffffu, hib, d);
+    flb += __shfl_xor_sync(0xffffffffu, flb, d);
+  }
   int sl = nl, sp = np;  // inclusive scans over the members
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -657,8 +697,8 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     h.nu = mg.nu; h.nv = mg.nv; h.ru = mg.ru; h.rv = mg.rv;
     h.ip0 = mg.ip0; h.tp0 = mg.tp0; h.ntp = mg.ntp;
     h.tpmax = a.psf[a.P[a.mem[G.m0].patch].stack].tpmax;
-    h.tmax = fminf(kTermMax, kWindowMax / nterm);
-    h.pad = 0;
+    h.tmax = fminf(fminf(kTermMax, kWindowMax / nterm), 1073741824.0f / fmaxf(hib, 1.0f));
+    h.lsc = fminf(kLoScale, 2147483648.0f / fmaxf(flb, 1.0f));
     th[g] = h;
   }
 }
@@ -667,12 +707,10 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
 #define PVR_BP_DYN 1
 #endif
 
-// Dynamic shared memory: HILO (init pass): 4 x tile_words int32 (A, C, A_lo, C_lo), then R;
-// iterations: A at 0, C at the fixed byte offset kCOff (an immediate in the splat's shared
-// reductions), R after kBpTileBytes (init: after kInitTileBytes).
-// 3 CTAs per SM in the iterations (56 KB tile + R: <= 85 registers); the init tile allows 2
-template <bool HILO>
-__global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int tile_words,
+// Dynamic shared memory: the tile (exact group: planes A_hi, C_hi, A_lo, C_lo at byte offsets
+// kHQ apart; single-word group: A at 0, C at kCOff; offsets are immediates of the splat's
+// shared reductions), then R after kBpTileBytes. kBpCtasPerSm CTAs per SM.
+__global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeArgs a, int tile_words,
                                                          const BpMember* __restrict__ tm,
                                                          const BpGroupHdr* __restrict__ th,
                                                          const float* __restrict__ kap,
@@ -683,9 +721,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
                                                          int* __restrict__ next) {
   extern __shared__ int4 bsm4[];
   int* base = reinterpret_cast<int*>(bsm4);
-  constexpr int NW = HILO ? 4 : 2;
-  int* cbase = HILO ? base + kHQ / 4 : base + kCOff / 4;
-  float2* R = reinterpret_cast<float2*>(base + (HILO ? kInitTileBytes : kBpTileBytes) / 4);
+
+  float2* R = reinterpret_cast<float2*>(base + kBpTileBytes / 4);
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
   __shared__ float s_red[2][kThreads >> 5];
   __shared__ BpMember sbm[kMaxMembers];
@@ -710,6 +747,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
 #endif
     const GroupDev G = a.grp[g];
     const BpGroupHdr H = th[g];
+    const bool ex = init || G.exact;  // CTA-uniform: this group's tile precision
+    const int NW = ex ? 4 : 2;
+    int* cbase = ex ? base + kHQ / 4 : base + kCOff / 4;
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
     __syncthreads();  // previous group's flush is done with the tile / R / tables / sbm
@@ -724,8 +764,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
       const int4 z4 = make_int4(0, 0, 0, 0);
       const int nv4 = (nvox + 3) >> 2;  // tile_words is a multiple of 4
 #pragma unroll
-      for (int q = 0; q < NW; ++q) {
-        int4* t4 = reinterpret_cast<int4*>(HILO ? base + q * (kHQ / 4) : (q == 1 ? cbase : base));
+      for (int q = 0; q < 4; ++q) {
+        if (q >= NW) break;
+        int4* t4 = reinterpret_cast<int4*>(ex ? base + q * (kHQ / 4) : (q == 1 ? cbase : base));
         for (int i = threadIdx.x; i < nv4; i += kThreads) t4[i] = z4;
       }
     }
@@ -780,8 +821,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
     const float scA = xA > 0.0f ? H.tmax / (xA * H.tpmax) : 0.0f;
     const float scC = xC > 0.0f ? H.tmax / (xC * H.tpmax) : 0.0f;
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
-    const Tile T{base, cbase, HILO ? base + 2 * (kHQ / 4) : nullptr,
-                 HILO ? base + 3 * (kHQ / 4) : nullptr, dx, dy};
+    const Tile T{base, cbase, base + 2 * (kHQ / 4), base + 3 * (kHQ / 4), dx, dy};
 
     // ---- phase B: splat every owned lattice line of every member, one flattened range
     // (one tail per group); consecutive lanes take consecutive U lines of a member
@@ -793,9 +833,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
       for (int i = threadIdx.x; i < nl; i += kThreads) {
         while (i >= sbm[mi].lend) ++mi;
         const BpMember& M = sbm[mi];
+        // colour-ordered lines: class (U mod 3, V mod 3), then rows of the class. The lanes of
+        // a warp take lines >= 3 lattice steps (~2.5 voxels) apart, so no two lanes flush the
+        // same tile cell in one shared reduction (adjacent lines 0.83 voxel apart did: 2.4
+        // wavefronts per ATOMS, 58% of them conflicts; ncu v14)
         const int li = i - M.lbeg;
+#if PVR_BP_COLOUR
+        const int cls = (int)(((float)li + 0.5f) * M.inv_nUV3);
+        const int r = li - cls * M.nUV3;
+        const int b3 = (int)(((float)r + 0.5f) * M.inv_nU3);
+        const int cv = (int)(((float)cls + 0.5f) * (1.0f / 3.0f));
+        const int iu = (cls - 3 * cv) + 3 * (r - b3 * M.nU3);
+        const int iv = cv + 3 * b3;
+        if (iu >= M.nU || iv >= M.nV) continue;  // padding of the class grid
+#else
         const int iv = (int)(((float)li + 0.5f) * M.inv_nU);
         const int iu = li - iv * M.nU;
+#endif
         const int U = M.Ulo + iu, V = M.Vlo + iv;
         // pixels feeding lattice point U: u = (U - a) / nu with a = U mod nu (and a - nu when
         // that is within [-ru, ru]); same along V. U >= -ru > -nu: the float floor is exact.
@@ -823,12 +877,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
         const float rm = M.r[0] + fU * M.du[0] + fV * M.dv[0];
         const float rp = M.r[1] + fU * M.du[1] + fV * M.dv[1];
         const float rq = M.r[2] + fU * M.du[2] + fV * M.dv[2];
-        splat_line_win<HILO>(tA, tpA, M, rm, rp, rq, LA, LC);
+        const int ph = PVR_BP_PHASES > 1 ? ((lane & (PVR_BP_PHASES - 1)) * M.ns) / PVR_BP_PHASES : 0;
+        if (ex)
+          splat_line_win<true>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
+        else
+          splat_line_win<false>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
       }
     }
     __syncthreads();
     // ---- phase C: flush the tile, one red.v4 per in-grid (even, odd) voxel pair along x
     const double iA = scA > 0.0f ? 1.0 / scA : 0.0, iC = scC > 0.0f ? 1.0 / scC : 0.0;
+    const double ilo = 1.0 / (double)H.lsc;
     const float fA = (float)iA, fC = (float)iC;
     const int hx = (dx + 1) >> 1, npair = hx * dy * dz;
     const float inv_hx = 1.0f / (float)hx, inv_dy = 1.0f / (float)dy;
@@ -847,17 +906,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
       const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
       const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
       int al0 = 0, al1 = 0, cl0 = 0, cl1 = 0;
-      if (HILO) {
+      if (ex) {
         al0 = T.al[k]; al1 = two ? T.al[k + 1] : 0;
         cl0 = T.cl[k]; cl1 = two ? T.cl[k + 1] : 0;
       }
       if ((ah0 | ah1 | ch0 | ch1 | al0 | al1 | cl0 | cl1) == 0) continue;
       float A0, A1, C0, C1;
-      if (HILO) {
-        A0 = (float)(((double)ah0 + (double)al0 * (1.0 / kLoScale)) * iA);
-        A1 = (float)(((double)ah1 + (double)al1 * (1.0 / kLoScale)) * iA);
-        C0 = (float)(((double)ch0 + (double)cl0 * (1.0 / kLoScale)) * iC);
-        C1 = (float)(((double)ch1 + (double)cl1 * (1.0 / kLoScale)) * iC);
+      if (ex) {
+        A0 = (float)(((double)ah0 + (double)al0 * ilo) * iA);
+        A1 = (float)(((double)ah1 + (double)al1 * ilo) * iA);
+        C0 = (float)(((double)ch0 + (double)cl0 * ilo) * iC);
+        C1 = (float)(((double)ch1 + (double)cl1 * ilo) * iC);
       } else {
         A0 = (float)ah0 * fA; A1 = (float)ah1 * fA;
         C0 = (float)ch0 * fC; C1 = (float)ch1 * fC;
@@ -870,19 +929,33 @@ __global__ void __launch_bounds__(kThreads, 3) k_lattice_bp(LatticeArgs a, int t
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
-static void configure() {
-  static bool done = false;
-  if (done) return;
-  cudaFuncSetAttribute(k_lattice_bp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_lattice_bp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_lattice_fwd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_lattice_fwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  done = true;
+// Per-device kernel attributes and occupancy (cudaFuncSetAttribute applies to the current
+// device only; contexts on several GPUs of one process each configure theirs once).
+struct DevConfig {
+  int nsm = 0, resident = 0;
+};
+constexpr int kMaxDevices = 64;
+static DevConfig g_dev[kMaxDevices];
+static std::once_flag g_dev_once[kMaxDevices];
+
+static const DevConfig& configure() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  std::call_once(g_dev_once[dev], [dev] {
+    DevConfig& c = g_dev[dev];
+    cudaFuncSetAttribute(k_lattice_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lattice_fwd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lattice_fwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.resident, k_lattice_bp, kThreads, kBpTileBytes + kRBytes);
+  });
+  return g_dev[dev];
 }
 
 void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, float* kap,
                      double* partials) {
-  configure();
+  (void)configure();
   const int smem = (t_floats + x_floats) * 4;
   k_lattice_fwd<1><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, nullptr, nullptr, nullptr, kap,
                                                         partials, nullptr);
@@ -890,7 +963,7 @@ void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_
 
 void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, const void* tmaps,
                     const float* kap, const float* p, float* e, double* partials) {
-  configure();
+  (void)configure();
   const int smem = (t_floats + x_floats) * 4;
   int* next = reinterpret_cast<int*>(partials + kStatBlocks * 5);  // the launch's group counter
   if (PVR_FWD_DYN) cudaMemsetAsync(next, 0, sizeof(int), st);
@@ -908,34 +981,21 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
                         void* table, size_t group_off, bool build_table, const float* kap,
                         const float* e, const float* p, const float* w, int init, float2* AC) {
   if (a.ngroups <= 0) return;
-  configure();
+  const DevConfig& dc = configure();
   BpMember* tm = static_cast<BpMember*>(table);
   BpGroupHdr* th = reinterpret_cast<BpGroupHdr*>(static_cast<char*>(table) + group_off);
   int* next = reinterpret_cast<int*>(th + a.ngroups);
   const int wpb = kThreads >> 5;
   if (build_table) k_bp_table<<<(a.ngroups + wpb - 1) / wpb, kThreads, 0, st>>>(a, tm, th);
 #if PVR_BP_DYN
-  static int resident[2] = {0, 0}, nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident[0], k_lattice_bp<false>, kThreads, kBpTileBytes + kRBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident[1], k_lattice_bp<true>, kThreads, kInitTileBytes + kRBytes);
-  }
-  const int per = nsm * (resident[init ? 1 : 0] > 0 ? resident[init ? 1 : 0] : 1);
+  const int per = dc.nsm * (dc.resident > 0 ? dc.resident : 1);
   const int grid = a.ngroups < per ? a.ngroups : per;
   cudaMemsetAsync(next, 0, sizeof(int), st);
 #else
+  (void)dc;
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
 #endif
-  if (init) {  // init (raw intensities) / rigidity pass: exact hi/lo words
-    k_lattice_bp<true><<<grid, kThreads, kInitTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w,
-                                                                         init, AC, next);
-  } else {
-    k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, 0,
-                                                                        AC, next);
-  }
+  k_lattice_bp<<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC, next);
 }
 
 }  // namespace pvr

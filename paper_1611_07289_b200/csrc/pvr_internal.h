@@ -47,7 +47,10 @@ struct MemberDev {
   int32_t patch;            // local patch index
   int32_t z, u0, v0, tu, tv;
   int32_t c0, c1;           // through-plane lattice range [c0, c1] (backprojection segments)
+  int32_t flags;            // kMemberRim: the member may touch cells at the rim of the
+                            // coverage (engine.cu: build_natural) -> exact tile words
 };
+constexpr int32_t kMemberRim = 1;
 struct GroupDev {
   int32_t m0, nm;           // members [m0, m0 + nm)
   int32_t lo[3];            // voxel bbox origin (not clipped to the grid; lo[0] even, forward:
@@ -55,8 +58,11 @@ struct GroupDev {
   int32_t dim[3];           // voxel bbox size (row / plane pitches of the shared tile: odd;
                             // forward: dim[0] = 4 x odd, the TMA box width)
   int32_t tmap;             // forward: index of the group's TMA box tensor map
-  int32_t interior;         // forward: 1 if every PSF sample's 8 trilinear corners are in the
-                            // grid (kappa = sum psi = 1 exactly; coverage skips the lattice)
+  int32_t interior;         // 1 if every PSF sample's 8 trilinear corners are in the grid
+                            // (forward: kappa = sum psi = 1 exactly; coverage skips the lattice)
+  int32_t exact;            // backprojection: hi/lo tile words (a rim member, a footprint that
+                            // leaves the grid, or PVR_PARAM_BP_EXACT = 2), 16 B per cell; else
+                            // one word per quantity, 8 B per cell
 };
 
 // EM state on the device (written by k_em_params / k_range_finish, read by later kernels).
@@ -107,11 +113,16 @@ struct LatticeArgs {
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
 constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
 #ifndef PVR_BP_TILE_KB
-#define PVR_BP_TILE_KB 56
+#define PVR_BP_TILE_KB 96
 #endif
-constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;  // backprojection (iterations): 8 B/voxel tile
-                                                     // budget; 56 KB + R: 3 CTAs per SM
-constexpr int kInitTileBytes = 96 * 1024; // init backprojection: 16 B/voxel hi/lo tile budget
+// Backprojection tile budget (shared memory). An exact group (GroupDev::exact) uses four int32
+// planes A_hi, C_hi, A_lo, C_lo of kBpTileBytes / 4 bytes each (16 B per voxel); a
+// single-word group two planes A, C of kBpTileBytes / 2 bytes (8 B per voxel).
+constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;
+// Backprojection tile precision (PVR_PARAM_BP_EXACT): 0 one word everywhere (a timing
+// reference), 1 exact hi/lo words for rim groups only (default), 2 exact everywhere.
+enum { kBpSingle = 0, kBpRim = 1, kBpAll = 2 };
+constexpr int kBpCtasPerSm = PVR_BP_TILE_KB <= 56 ? 3 : 2;
 #ifndef PVR_R_KB
 #define PVR_R_KB 12
 #endif
@@ -155,6 +166,7 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
 // group headers at byte `group_off`, then the launch's int group counter), geometry only:
 // rebuilt by this launch when `build_table` (after a set_transforms / re-plan), else reused.
 size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off);
+// Each group's tile precision is GroupDev::exact (init / rigidity passes: always exact).
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         void* table, size_t group_off, bool build_table, const float* kap,
                         const float* e, const float* p, const float* w, int init, float2* AC);
@@ -188,9 +200,11 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);
 constexpr int kMaxBoxShapes = 4096;  // forward TMA box shapes the device re-plan may pick from
 // nappend (backprojection): counter of single-member groups appended after ngroups (< cap)
+// bp_mode (backprojection): PVR_PARAM_BP_EXACT; vox_budget: forward voxels, backprojection
+// tile bytes (a group needs 16 B per cell if exact, else 8)
 void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, int cap, const PatchDev* P,
                    const StackPsf* psf, int fwd, int3 n, int64_t vox_budget, const int* shapes, int nshape,
-                   int* maxvox, int* fail, int* nappend);
+                   int* maxvox, int* fail, int* nappend, int bp_mode);
 void launch_init_fill(cudaStream_t st, const float2* AC, const int3 dims, int nxp, Params prm,
                       float* X);
 

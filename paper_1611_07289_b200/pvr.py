@@ -20,7 +20,8 @@ STATUS_NAMES = {0: "PVR_OK", 1: "PVR_ERR_ARG", 2: "PVR_ERR_STATE", 3: "PVR_ERR_O
                 4: "PVR_ERR_CUDA", 5: "PVR_ERR_NCCL", 6: "PVR_ERR_EMPTY"}
 PARAM = {"delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
          "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "profile": 11, "psf_quality": 12,
-         "em_rounds": 13, "em_tol": 14, "patch_mixture": 15}
+         "em_rounds": 13, "em_tol": 14, "patch_mixture": 15,
+         "bp_exact": 16}
 
 # every symbol include/pvr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", "pvr_comm_init",
