@@ -132,7 +132,7 @@ def time_oracle(cfg, steps, warmup, slices):
     orc.set_volume(np.full(orc.V, 300.0))
     _, kap, _, _ = orc.taps()
     S = len(orc.psf(0)[1])
-    samples = int((kap >= 0.5).sum()) * S  # observed pixels (tau_obs, Q25)
+    samples = int((kap >= 0.01).sum()) * S  # observed pixels (tau_obs = 0.01, Q25)
     for _ in range(warmup):
         orc.sr_iterate(1, prob["alpha"], prob["lam"])
     ts = []
@@ -142,11 +142,22 @@ def time_oracle(cfg, steps, warmup, slices):
         ts.append(time.perf_counter() - t0)
     t = statistics.mean(ts)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return dict(value=samples / t, unit=UNIT, cores=cores, kind="oracle",
+    return dict(value=samples / t, unit=UNIT, cores=cores, kind="oracle", cpu_model=cpu_model(),
                 sample=f"{cfg} with {slices} slice(s) per stack: M={orc.M} patches, "
                        f"{samples:.3e} observed PSF samples per iteration, full {prob['dims'][0]}^3 "
                        f"volume update; fp64, mean of {steps} iteration(s)",
                 seconds_per_iteration=t)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def config_block(cfg, prob=None, extra=None):
@@ -173,7 +184,7 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded analytic phantom acquisition; synth/)",
             "config": config_block(args.config, extra={"reference_sample": r["sample"]}),
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")},
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -279,8 +290,21 @@ def run_ours(args):
     breakdown["em_params"] = {"ms": st["ms_em"] / st["n_em"], "share": st["ms_em"] / st["n_em"] / ms}
     if ws > 1:
         breakdown["allreduce_AC"] = {"ms": st["ms_allreduce"] / max(st["n_allreduce"], 1)}
-    hbm_iter = (st["bytes_alg_forward"] + st["bytes_alg_estep"] + st["bytes_alg_backproject"]
-                + st["bytes_alg_update"]) / (ms * 1e-3) / 1e9
+    # iteration-level HBM fraction on SURVEY 8(d)'s B_alg = 24 P + 28 V + 48 M bytes (the fused
+    # minimum per iteration), and, labelled apart, on the sum of the kernels' algorithmic bytes
+    P_all = int(ctx.M) * prob["patch"]["size"] ** 2 * prob["patch"]["depth"]  # every window is full size
+    V_all = int(st["voxels"])
+    M_all = int(ctx.M)
+    b_alg = 24 * P_all + 28 * V_all + 48 * M_all
+    kernel_bytes = (st["bytes_alg_forward"] + st["bytes_alg_estep"] + st["bytes_alg_backproject"]
+                    + st["bytes_alg_update"])
+    hbm_iter = {"B_alg_bytes": b_alg, "frac": b_alg / (ms_max * 1e-3) / (pk["hbm_gbs"] * 1e9),
+                "definition": "SURVEY 8(d): B_alg = 24 P + 28 V + 48 M bytes per iteration / t_iter / HBM peak",
+                "kernel_bytes_sum": kernel_bytes,
+                "kernel_bytes_frac": kernel_bytes / (ms * 1e-3) / (pk["hbm_gbs"] * 1e9)}
+    plan = {k: st[k] for k in ("fwd_tile", "bp_tile", "fwd_groups", "bp_groups", "fwd_members", "bp_members",
+                               "fwd_smem", "bp_smem", "bp_exact_groups", "fwd_split", "bp_split",
+                               "device_replans", "host_replans", "replan_splits")}
 
     # ---- end to end through the C ABI with host buffers: per step the step's inputs (the
     # patch transforms from registration) go host -> device and the step's result metrics
@@ -389,7 +413,7 @@ def run_ours(args):
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
             r = time_oracle(args.config, 1, 0, args.ref_slices)
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "s_per_iteration": ms_max * 1e-3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -398,7 +422,7 @@ def run_ours(args):
                     "M": int(ctx.M), "P": int(st["pixels"]) if ws == 1 else None,
                     "psf_samples_per_iteration": samples, "parallelism": f"patch-shard x{ws}",
                     "psf_quality": args.psf_quality}),
-                "roofline": roof, "iteration_hbm_frac_alg": hbm_iter / pk["hbm_gbs"],
+                "roofline": roof, "iteration_hbm": hbm_iter, "plan": plan,
                 "kernels": breakdown, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(st["kernel_launches"]), "cpu_baseline": cpu,
                 "extras": {"f2_rigidity_map": rigidity, "f1_registration": registration,

@@ -68,8 +68,8 @@ enum {
   PVR_PARAM_TAU_PATCH = 1,    /* patch kept iff pbar >= tau_patch [0.5] (Q13)             */
   PVR_PARAM_C0 = 2,           /* inlier proportion c at the first iteration [0.9] (Q10)    */
   PVR_PARAM_TAU_LIVE = 3,     /* pixel in the EM statistics iff kappa >= tau_live [0.99]   */
-  PVR_PARAM_TAU_C = 4,        /* voxel updated iff C > tau_C [1e-3] (Q24)                  */
-  PVR_PARAM_TAU_OBS = 5,      /* pixel observed iff kappa >= tau_obs [0.5] (Q25)           */
+  PVR_PARAM_TAU_C = 4,        /* voxel updated iff C > tau_C [1e-6] (Q24)                  */
+  PVR_PARAM_TAU_OBS = 5,      /* pixel observed iff kappa >= tau_obs [0.01] (Q25)          */
   PVR_PARAM_CLAMP = 6,        /* 1: clamp X1 to the live-y range +-10% [1] (Q19)           */
   PVR_PARAM_PSF_MODE = 7,     /* (extract) 0: PVR PSF; 1: delta PSF (tests only) [0]       */
   PVR_PARAM_SIGMA2_FLOOR = 9, /* sigma2 >= floor * (ymax - ymin)^2 [1e-6] (Q10)            */
@@ -87,6 +87,12 @@ enum {
                                  P:209 "an inlier and outlier probability for each y_s",
                                  reading Q31): w = inlier posterior r if r >= 1/2, else 0;
                                  0: the threshold rule of Q13 [0]                          */
+  ,PVR_PARAM_EXCHANGE = 17     /* multi-rank exchange scheme PVR_EXCHANGE_* [0]; set it before
+                                 pvr_comm_init / pvr_comm_init_host                          */
+  ,PVR_PARAM_COMM_TIMEOUT = 18 /* seconds a wait on NCCL work may take before the library
+                                 aborts the communicator (ncclCommAbort) and returns
+                                 PVR_ERR_NCCL; NCCL asynchronous errors are polled while
+                                 waiting [300]                                               */
   ,PVR_PARAM_BP_EXACT = 16    /* (extract) precision of the backprojection's shared tiles
                                  (DESIGN.md 7). 1 [default]: exact hi/lo int32 word pairs
                                  (~2^-41 of the group's largest splat term) for every group
@@ -121,6 +127,32 @@ const char* pvr_last_error(const pvr_ctx* ctx);
 pvr_status pvr_comm_init(pvr_ctx* ctx, int nranks, int rank, const void* nccl_unique_id);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */
 pvr_status pvr_comm_unique_id(void* out128);
+
+/* Host-collective transport, the alternative to pvr_comm_init (same place in the call
+ * sequence): every exchange step of the iteration runs as a call of `fn` on a pinned HOST
+ * buffer the library owns, copied from the device before and back after the call. The
+ * caller implements the collective with any transport (tests back it with torch.distributed
+ * gloo across processes that may share one GPU: no kernel ever waits on another rank).
+ *   op PVR_COLL_ALLREDUCE_SUM / _MAX: buf holds count elements, reduced in place over ranks;
+ *   op PVR_COLL_ALLGATHER: buf holds nranks * count elements; every rank's count elements at
+ *     [rank * count] are gathered into all ranks' buffers.
+ * dtype: PVR_DT_F32 / PVR_DT_F64 / PVR_DT_I64. fn returns 0 on success; anything else poisons
+ * the context (PVR_ERR_NCCL). */
+typedef enum { PVR_COLL_ALLREDUCE_SUM = 0, PVR_COLL_ALLREDUCE_MAX = 1, PVR_COLL_ALLGATHER = 2 } pvr_coll_op;
+typedef enum { PVR_DT_F32 = 0, PVR_DT_F64 = 1, PVR_DT_I64 = 2 } pvr_dtype;
+typedef int (*pvr_host_collective_fn)(void* user, void* buf, int64_t count, int dtype, int op);
+pvr_status pvr_comm_init_host(pvr_ctx* ctx, int nranks, int rank, pvr_host_collective_fn fn, void* user);
+
+/* Exchange schemes of (A, C) per iteration (PVR_PARAM_EXCHANGE):
+ *  PVR_EXCHANGE_ALLREDUCE: sum-allreduce of (A, C), every rank runs the whole update (the
+ *    1-rank operator up to summation order; reading Q21) [default];
+ *  PVR_EXCHANGE_SLABS: reduce-scatter of (A, C) over z slabs (+ one halo plane from each
+ *    neighbour), each rank updates its slab, all-gather of the new X: 12 V (N-1)/N bytes per
+ *    rank instead of 16 V (N-1)/N, and the update split N ways (same operator);
+ *  PVR_EXCHANGE_AVERAGE: the paper's "averaging of the resulting sub reconstruction volumes
+ *    on the master GPU", for comparison only: each rank updates X with its own
+ *    patches' (A, C), then X = mean over ranks (NOT the 1-rank operator). */
+enum { PVR_EXCHANGE_ALLREDUCE = 0, PVR_EXCHANGE_SLABS = 1, PVR_EXCHANGE_AVERAGE = 2 };
 
 /* Add one stack of slices ("stacks of 2D images").
  * slices: float32 [K][H][W], host or device, copied.
@@ -262,6 +294,12 @@ pvr_status pvr_get_weights(pvr_ctx* ctx, float* pixel_p, float* patch_w, float* 
 /* Debug taps of the last iteration: residual e and coverage kappa [n_local_pixels] of this
  * shard, and the (reduced) addon A and confidence C [V]; any may be NULL. */
 pvr_status pvr_get_taps(pvr_ctx* ctx, float* e, float* kappa, float* addon, float* confidence);
+/* Confidence map C_k = sum_s w_s sum_j W_jk p_j of the last iteration (north_star
+ * "confidence map"), the denominator of the SR update (P:185,
+ * reading Q16): float32 [nz][ny][nx], host or device pointer (device copies stay on the
+ * device). After pvr_init_volume it is W^T 1 over the observed pixels. Errors: PVR_ERR_ARG
+ * (nvox != nx ny nz), PVR_ERR_STATE (before set_transforms). */
+pvr_status pvr_get_confidence(pvr_ctx* ctx, float* out, size_t nvox);
 /* EM state after the last iteration: sigma^2, c, m, iteration counter t, and the clamp
  * range [lo, hi]. Any output may be NULL. */
 pvr_status pvr_get_em_state(pvr_ctx* ctx, double* sigma2, double* c, double* m, int64_t* iter,
@@ -295,6 +333,10 @@ typedef struct {
   int64_t host_replans;           /* set_transforms calls that ran the host planner        */
   int64_t replan_splits;          /* members moved into single-member backprojection groups
                                      by device re-plans (their group outgrew the tile)       */
+  int64_t bp_exact_groups;        /* backprojection groups with exact hi/lo tiles (rim)    */
+  int64_t fwd_split, bp_split;    /* host plan: natural groups not kept whole (an outlying
+                                     member left, or the union did not fit) + members split
+                                     into smaller pixel tiles                                */
 } pvr_stats;
 pvr_status pvr_get_stats(const pvr_ctx* ctx, pvr_stats* out);
 pvr_status pvr_reset_stats(pvr_ctx* ctx);

@@ -348,8 +348,10 @@ pvro_ctx* pvro_create(const int32_t dims[3], double spacing, const double origin
   pvro_ctx* x = (pvro_ctx*)calloc(1, sizeof(pvro_ctx));
   for (int d = 0; d < 3; ++d) { x->n[d] = dims[d]; x->o[d] = origin[d]; }
   x->s = spacing;
-  x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-3;
-  x->tau_obs = 0.5; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0; x->quality = 1.0;
+  /* thresholds (reading Q24 / Q25): tau_C = 1e-6 (SURVEY.md:678); observed iff kappa > 0
+     (SURVEY.md:652) with a 1e-2 floor against 1/kappa amplification of pixels >= 99% outside */
+  x->delta = 150.0; x->tau_patch = 0.5; x->c0 = 0.9; x->tau_live = 0.99; x->tau_C = 1e-6;
+  x->tau_obs = 0.01; x->clamp = 1; x->psf_mode = 0; x->s2floor = 1e-6; x->nsigma = 3.0; x->quality = 1.0;
   x->em_rounds = 1.0; x->em_tol = 1e-6; x->patch_mixture = 0.0;
   int64_t V = (int64_t)dims[0] * dims[1] * dims[2];
   x->X = (double*)calloc(V, sizeof(double));
@@ -794,36 +796,74 @@ int pvro_forward(const pvro_ctx* x, const double* X, double* yhat, double* kappa
   return pvro_forward_range(x, X, 0, x->M, yhat, kappa);
 }
 
+/* Steps 2-3 for the pixels of one patch s (yhat, kappa indexed by global pixel). */
+static void forward_patch(const pvro_ctx* x, const double* X, int64_t s, double* yhat, double* kappa) {
+  const int32_t* pt = &x->patch[7 * s];
+  const ostack* st = &x->st[pt[0]];
+  const double* T = &x->T[12 * s];
+  int64_t j = x->pix0[s];
+  for (int z = 0; z < pt[6]; ++z)
+    for (int v = 0; v < pt[5]; ++v)
+      for (int u = 0; u < pt[4]; ++u, ++j) {
+        double kap = 0.0, acc = 0.0;
+        for (int q = 0; q < st->S; ++q) {
+          double pos[3], wt[8];
+          int64_t idx[8];
+          sample_pos(x, pt, T, u, v, z, q, pos);
+          int nc = trilinear(x, pos, idx, wt);
+          for (int c = 0; c < nc; ++c) {
+            kap += st->psi[q] * wt[c];
+            acc += st->psi[q] * wt[c] * X[idx[c]];
+          }
+        }
+        if (x->mask && !x->mask[j]) kap = 0.0;  /* f3: masked-out pixel (Q32) */
+        kappa[j] = kap;
+        yhat[j] = (kap >= x->tau_obs) ? acc / kap : 0.0;
+      }
+}
+
 /* Forward of patches [first, first+count) only (yhat, kappa indexed by global pixel). */
 int pvro_forward_range(const pvro_ctx* x, const double* X, int64_t first, int64_t count,
                        double* yhat, double* kappa) {
   if (x->state < 2 || first < 0 || first + count > x->M) return -1;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t s = first; s < first + count; ++s) {
-    const int32_t* pt = &x->patch[7 * s];
-    const ostack* st = &x->st[pt[0]];
-    const double* T = &x->T[12 * s];
-    int64_t j = x->pix0[s];
-    for (int z = 0; z < pt[6]; ++z)
-      for (int v = 0; v < pt[5]; ++v)
-        for (int u = 0; u < pt[4]; ++u, ++j) {
-          double kap = 0.0, acc = 0.0;
-          for (int q = 0; q < st->S; ++q) {
-            double pos[3], wt[8];
-            int64_t idx[8];
-            sample_pos(x, pt, T, u, v, z, q, pos);
-            int nc = trilinear(x, pos, idx, wt);
-            for (int c = 0; c < nc; ++c) {
-              kap += st->psi[q] * wt[c];
-              acc += st->psi[q] * wt[c] * X[idx[c]];
-            }
-          }
-          if (x->mask && !x->mask[j]) kap = 0.0;  /* f3: masked-out pixel (Q32) */
-          kappa[j] = kap;
-          yhat[j] = (kap >= x->tau_obs) ? acc / kap : 0.0;
-        }
-  }
+  for (int64_t s = first; s < first + count; ++s) forward_patch(x, X, s, yhat, kappa);
   return 0;
+}
+
+/* Coverage kappa (step 2) of a list of patches into the context (test hook for full-size
+ * checks that never run the whole coverage pass: set_transforms with PVRO_LAZY). */
+int pvro_coverage_subset(pvro_ctx* x, const int64_t* patches, int64_t n) {
+  if (x->state < 3) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    if (patches[i] < 0 || patches[i] >= x->M) return -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < n; ++i) forward_patch(x, x->X, patches[i], x->yhat, x->kappa);
+  return 0;
+}
+
+/* Adjoint of step 3 for one patch: out_k += sum_j W_jk r_j over its observed pixels. */
+static void adjoint_patch(const pvro_ctx* x, const double* r, int64_t s, double* out) {
+  const int32_t* pt = &x->patch[7 * s];
+  const ostack* st = &x->st[pt[0]];
+  const double* T = &x->T[12 * s];
+  int64_t j = x->pix0[s];
+  for (int z = 0; z < pt[6]; ++z)
+    for (int v = 0; v < pt[5]; ++v)
+      for (int u = 0; u < pt[4]; ++u, ++j) {
+        if (!(x->kappa[j] >= x->tau_obs) || r[j] == 0.0) continue;
+        for (int q = 0; q < st->S; ++q) {
+          double pos[3], wt[8];
+          int64_t idx[8];
+          sample_pos(x, pt, T, u, v, z, q, pos);
+          int nc = trilinear(x, pos, idx, wt);
+          for (int c = 0; c < nc; ++c) {
+            double add = st->psi[q] * wt[c] / x->kappa[j] * r[j];
+#pragma omp atomic
+            out[idx[c]] += add;
+          }
+        }
+      }
 }
 
 /* Adjoint of step 3 (north_star "backprojection"): out_k += sum_j W_jk r_j over the
@@ -831,28 +871,17 @@ int pvro_forward_range(const pvro_ctx* x, const double* X, int64_t first, int64_
 int pvro_adjoint(const pvro_ctx* x, const double* r, int64_t first, int64_t count, double* out) {
   if (x->state < 3 || first < 0 || first + count > x->M) return -1;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t s = first; s < first + count; ++s) {
-    const int32_t* pt = &x->patch[7 * s];
-    const ostack* st = &x->st[pt[0]];
-    const double* T = &x->T[12 * s];
-    int64_t j = x->pix0[s];
-    for (int z = 0; z < pt[6]; ++z)
-      for (int v = 0; v < pt[5]; ++v)
-        for (int u = 0; u < pt[4]; ++u, ++j) {
-          if (!(x->kappa[j] >= x->tau_obs) || r[j] == 0.0) continue;
-          for (int q = 0; q < st->S; ++q) {
-            double pos[3], wt[8];
-            int64_t idx[8];
-            sample_pos(x, pt, T, u, v, z, q, pos);
-            int nc = trilinear(x, pos, idx, wt);
-            for (int c = 0; c < nc; ++c) {
-              double add = st->psi[q] * wt[c] / x->kappa[j] * r[j];
-#pragma omp atomic
-              out[idx[c]] += add;
-            }
-          }
-        }
-  }
+  for (int64_t s = first; s < first + count; ++s) adjoint_patch(x, r, s, out);
+  return 0;
+}
+
+/* The same adjoint over a list of patches. */
+int pvro_adjoint_subset(const pvro_ctx* x, const double* r, const int64_t* patches, int64_t n, double* out) {
+  if (x->state < 3) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    if (patches[i] < 0 || patches[i] >= x->M) return -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < n; ++i) adjoint_patch(x, r, patches[i], out);
   return 0;
 }
 

@@ -44,8 +44,8 @@ enum {
   PVRO_TAU_PATCH = 1,    /* patch inlier threshold on pbar (0.5)                     */
   PVRO_C0 = 2,           /* initial inlier proportion c at t = 1 (0.9)               */
   PVRO_TAU_LIVE = 3,     /* live pixel: kappa >= tau_live (0.99)                     */
-  PVRO_TAU_C = 4,        /* voxel updated iff C > tau_C (1e-3)                       */
-  PVRO_TAU_OBS = 5,      /* observed pixel: kappa >= tau_obs (0.5)                   */
+  PVRO_TAU_C = 4,        /* voxel updated iff C > tau_C (1e-6)                       */
+  PVRO_TAU_OBS = 5,      /* observed pixel: kappa >= tau_obs (0.01)                  */
   PVRO_CLAMP = 6,        /* 1: clamp X1 to [lo, hi] (default 1)                      */
   PVRO_PSF_MODE = 7,     /* 0: PVR PSF; 1: delta PSF (S = 1, delta_q = 0), test only */
   PVRO_SIGMA2_FLOOR = 9, /* sigma2_min = floor * (ymax - ymin)^2 (1e-6)              */
@@ -153,6 +153,10 @@ int pvro_forward_range(const pvro_ctx*, const double* X, int64_t first, int64_t 
 /* adjoint operator: out[k] = sum_j W_jk r[j] over observed pixels of patches
    [first, first + count) (out is accumulated into, caller zeroes it) */
 int pvro_adjoint(const pvro_ctx*, const double* r, int64_t first, int64_t count, double* out);
+/* The adjoint over a list of patches (accumulates into out), and the coverage kappa of a list of
+ * patches into the context: test hooks for full-size region-of-interest checks. */
+int pvro_adjoint_subset(const pvro_ctx*, const double* r, const int64_t* patches, int64_t n, double* out);
+int pvro_coverage_subset(pvro_ctx*, const int64_t* patches, int64_t n);
 int pvro_init_volume(pvro_ctx*);
 /* Rigidity map ("Integrating p and pbar into a 3D volume using the same PSF as for
  * the reconstruction"; reading Q28): out_k = [W^T (p pbar_s)]_k /

@@ -89,6 +89,8 @@ def lib():
         L.pvro_forward.argtypes = [vp, vp, vp, vp]
         L.pvro_forward_range.argtypes = [vp, vp, i64, i64, vp, vp]
         L.pvro_adjoint.argtypes = [vp, vp, i64, i64, vp]
+        L.pvro_adjoint_subset.argtypes = [vp, vp, vp, i64, vp]
+        L.pvro_coverage_subset.argtypes = [vp, vp, i64]
         L.pvro_init_volume.argtypes = [vp]
         L.pvro_rigidity_map.argtypes = [vp, vp]
         L.pvro_set_weights.argtypes = [vp, vp, vp]
@@ -318,6 +320,20 @@ class Oracle:
         out = np.zeros(self.V)
         _chk(lib().pvro_adjoint(self.h, _p(r), first, count, _p(out)), "adjoint")
         return out.reshape(self.dims[::-1])
+
+    def adjoint_subset(self, r, patches, out=None):
+        """W^T r over the patches listed (accumulated into out, a new zero volume if None)."""
+        r = np.ascontiguousarray(r, np.float64)
+        pl = np.ascontiguousarray(patches, np.int64)
+        if out is None:
+            out = np.zeros(self.V)
+        _chk(lib().pvro_adjoint_subset(self.h, _p(r), _p(pl), len(pl), _p(out)), "adjoint_subset")
+        return out
+
+    def coverage_subset(self, patches):
+        """kappa of the listed patches into the context (after a lazy set_transforms)."""
+        pl = np.ascontiguousarray(patches, np.int64)
+        _chk(lib().pvro_coverage_subset(self.h, _p(pl), len(pl)), "coverage_subset")
 
     def init_volume(self):
         _chk(lib().pvro_init_volume(self.h), "init_volume")

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <parallel/algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdlib>
 #include <memory>
 #include <cmath>
@@ -73,6 +74,15 @@ struct Nccl {
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -84,7 +94,16 @@ struct Nccl {
     AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
     CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
     GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString) {
+    ReduceScatter = (decltype(ReduceScatter))dlsym(h, "ncclReduceScatter");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    Send = (decltype(Send))dlsym(h, "ncclSend");
+    Recv = (decltype(Recv))dlsym(h, "ncclRecv");
+    GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
+    CommGetAsyncError = (decltype(CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    CommAbort = (decltype(CommAbort))dlsym(h, "ncclCommAbort");
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString || !ReduceScatter ||
+        !AllGather || !Send || !Recv || !GroupStart || !GroupEnd || !CommGetAsyncError || !CommAbort) {
       err = "libnccl is missing a required symbol";
       return false;
     }
@@ -119,7 +138,8 @@ struct pvr_ctx {
   bool poisoned = false;
   std::string err;
   // parameters
-  double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-3, tau_obs = 0.5;
+  // thresholds: readings Q24 / Q25 (SURVEY.md:652, 678)
+  double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-6, tau_obs = 0.01;
   int clamp = 1, psf_mode = 0, profile = 0;
   int bp_exact = kBpRim;  // backprojection tile precision (PVR_PARAM_BP_EXACT)
   bool explicit_patches = false;  // patches from pvr_set_patches / superpixels (not windows)
@@ -155,9 +175,17 @@ struct pvr_ctx {
   std::vector<int> fbox;   // forward TMA box shapes (width, height) of the current plan
   char* tmaps = nullptr;   // device: CUtensorMap [2 X buffers][box shapes]
   size_t tmaps_cap = 0;
-  // comm
+  // comm: NCCL (pvr_comm_init) or a host-collective callback (pvr_comm_init_host)
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  pvr_host_collective_fn host_fn = nullptr;
+  void* host_user = nullptr;
+  char* host_buf = nullptr;     // pinned staging buffer of the host collectives
+  size_t host_cap = 0;
+  int exchange = PVR_EXCHANGE_ALLREDUCE;  // C2 scheme (PVR_PARAM_EXCHANGE)
+  double comm_timeout = 300.0;  // seconds an NCCL wait may take before the communicator is aborted
+  int nzp = 0;                  // planes of X / (A, C) allocated: nz rounded up to nranks slabs
+  int z0 = 0, z1 = 0;           // this rank's slab of planes (PVR_EXCHANGE_SLABS)
   // device buffers
   float* X[2] = {nullptr, nullptr};
   int cur = 0;
@@ -387,44 +415,126 @@ pvr_status nccl_check(pvr_ctx* c, ncclResult_t r, const char* what) {
   return fail(c, PVR_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
 }
 
+// ---- collectives: NCCL on the context's stream, or the host-collective callback on a pinned
+// staging copy (pvr_comm_init_host). All are no-ops on one rank.
+pvr_status coll(pvr_ctx* c, void* dev, int64_t count, int dtype, int op) {
+  if (c->nranks <= 1 || count <= 0) return PVR_OK;
+  const size_t esz = dtype == PVR_DT_F32 ? 4 : 8;
+  const size_t bytes = (op == PVR_COLL_ALLGATHER ? (size_t)c->nranks : 1) * (size_t)count * esz;
+  if (c->host_fn) {
+    if (bytes > c->host_cap) {
+      if (c->host_buf) cudaFreeHost(c->host_buf);
+      c->host_buf = nullptr;
+      c->host_cap = 0;
+      CUDA_TRY(c, cudaMallocHost(&c->host_buf, bytes));
+      c->host_cap = bytes;
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->host_buf, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->host_fn(c->host_user, c->host_buf, count, dtype, op) != 0)
+      return fail(c, PVR_ERR_NCCL, "host collective (op %d, %lld elements) failed", op, (long long)count);
+    CUDA_TRY(c, cudaMemcpyAsync(dev, c->host_buf, bytes, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // the staging buffer is reused by the next call
+    return PVR_OK;
+  }
+  const ncclDataType_t t = dtype == PVR_DT_F32 ? ncclFloat32 : dtype == PVR_DT_F64 ? ncclFloat64 : ncclInt64;
+  if (op == PVR_COLL_ALLGATHER)
+    return nccl_check(c, g_nccl.AllGather(static_cast<char*>(dev) + (size_t)c->rank * count * esz, dev, count, t,
+                                          c->comm, c->stream),
+                      "ncclAllGather");
+  return nccl_check(c, g_nccl.AllReduce(dev, dev, count, t, op == PVR_COLL_ALLREDUCE_MAX ? ncclMax : ncclSum,
+                                        c->comm, c->stream),
+                    "ncclAllReduce");
+}
+
+// Wait for the context's stream. With NCCL, poll the communicator's asynchronous error state
+// while waiting and abort it (ncclCommAbort) on an error or after PVR_PARAM_COMM_TIMEOUT
+// seconds, so a failed or hung peer poisons the context instead of hanging the call.
+pvr_status comm_wait(pvr_ctx* c) {
+  if (c->nranks <= 1 || !c->comm) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return PVR_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) return PVR_OK;
+    if (q != cudaErrorNotReady) return fail(c, PVR_ERR_CUDA, "stream: %s", cudaGetErrorString(q));
+    ncclResult_t ar = ncclSuccess;
+    g_nccl.CommGetAsyncError(c->comm, &ar);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ar != ncclSuccess && ar != ncclInProgress) || dt > c->comm_timeout) {
+      g_nccl.CommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(c, PVR_ERR_NCCL, "NCCL %s after %.1f s: communicator aborted",
+                  ar != ncclSuccess && ar != ncclInProgress ? g_nccl.GetErrorString(ar) : "timeout", dt);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 // EM statistics allreduce (C1): SUM over stats[0..2], MAX over stats[3..4].
 pvr_status allreduce_stats(pvr_ctx* c) {
-  if (c->nranks <= 1) return PVR_OK;
-  double* s = c->em->stats;
-  pvr_status r = nccl_check(c, g_nccl.AllReduce(s, s, 3, ncclFloat64, ncclSum, c->comm, c->stream),
-                            "ncclAllReduce(stats sum)");
+  pvr_status r = coll(c, c->em->stats, 3, PVR_DT_F64, PVR_COLL_ALLREDUCE_SUM);
   if (r != PVR_OK) return r;
-  return nccl_check(c, g_nccl.AllReduce(s + 3, s + 3, 2, ncclFloat64, ncclMax, c->comm, c->stream),
-                    "ncclAllReduce(stats max)");
+  return coll(c, c->em->stats + 3, 2, PVR_DT_F64, PVR_COLL_ALLREDUCE_MAX);
 }
 
 // f4 multi-round EM: SUM of the E-step partials {sum p e^2, sum p, LL} before each M-step.
-pvr_status allreduce_stats2(pvr_ctx* c) {
-  if (c->nranks <= 1) return PVR_OK;
-  double* s = c->em->stats2;
-  return nccl_check(c, g_nccl.AllReduce(s, s, 3, ncclFloat64, ncclSum, c->comm, c->stream),
-                    "ncclAllReduce(E-step stats)");
-}
+pvr_status allreduce_stats2(pvr_ctx* c) { return coll(c, c->em->stats2, 3, PVR_DT_F64, PVR_COLL_ALLREDUCE_SUM); }
 
 // f4 patch mixture sums: stage 0 = {n, sum pbar, sum pbar^2 | max, -min}; 1 = 7 round sums.
 constexpr int kMixRounds = 50;
 pvr_status allreduce_mix(pvr_ctx* c, int stage) {
-  if (c->nranks <= 1) return PVR_OK;
   double* s = c->em->mix_stats;
   if (stage == 0) {
-    pvr_status r = nccl_check(c, g_nccl.AllReduce(s, s, 3, ncclFloat64, ncclSum, c->comm, c->stream), "mix sums");
+    pvr_status r = coll(c, s, 3, PVR_DT_F64, PVR_COLL_ALLREDUCE_SUM);
     if (r != PVR_OK) return r;
-    return nccl_check(c, g_nccl.AllReduce(s + 3, s + 3, 2, ncclFloat64, ncclMax, c->comm, c->stream), "mix max");
+    return coll(c, s + 3, 2, PVR_DT_F64, PVR_COLL_ALLREDUCE_MAX);
   }
-  return nccl_check(c, g_nccl.AllReduce(s, s, 7, ncclFloat64, ncclSum, c->comm, c->stream), "mix round sums");
+  return coll(c, s, 7, PVR_DT_F64, PVR_COLL_ALLREDUCE_SUM);
 }
 
 // Addon / confidence allreduce (C2): SUM over the interleaved, row-padded (A, C) volume.
-pvr_status allreduce_ac(pvr_ctx* c) {
-  if (c->nranks <= 1) return PVR_OK;
-  return nccl_check(c, g_nccl.AllReduce(c->AC, c->AC, (size_t)c->Vp * 2, ncclFloat32, ncclSum,
-                                        c->comm, c->stream),
-                    "ncclAllReduce(A,C)");
+pvr_status allreduce_ac(pvr_ctx* c) { return coll(c, c->AC, c->Vp * 2, PVR_DT_F32, PVR_COLL_ALLREDUCE_SUM); }
+
+// The iteration's (A, C) exchange (PVR_PARAM_EXCHANGE). Slabs with NCCL: reduce-scatter of
+// the z slabs (in place) and one halo plane from each neighbour (ncclSend / ncclRecv), so each
+// rank holds the reduced (A, C) of its slab and the planes its update stencil reads; with the
+// host transport the same slab update runs on an allreduced (A, C). Averaging: no exchange.
+pvr_status exchange_ac(pvr_ctx* c) {
+  if (c->nranks <= 1 || c->exchange == PVR_EXCHANGE_AVERAGE) return PVR_OK;
+  if (c->exchange == PVR_EXCHANGE_ALLREDUCE || c->host_fn) return allreduce_ac(c);
+  const size_t plane = (size_t)c->nxp * c->dims.y * 2;  // floats per (A, C) plane
+  const int slab = c->nzp / c->nranks;
+  float* ac = reinterpret_cast<float*>(c->AC);
+  pvr_status r = nccl_check(c, g_nccl.ReduceScatter(ac, ac + (size_t)c->rank * slab * plane, slab * plane, ncclFloat32,
+                                                    ncclSum, c->comm, c->stream),
+                            "ncclReduceScatter(A,C)");
+  if (r != PVR_OK) return r;
+  r = nccl_check(c, g_nccl.GroupStart(), "ncclGroupStart");
+  if (r != PVR_OK) return r;
+  if (c->rank > 0) {
+    g_nccl.Send(ac + (size_t)c->z0 * plane, plane, ncclFloat32, c->rank - 1, c->comm, c->stream);
+    g_nccl.Recv(ac + (size_t)(c->z0 - 1) * plane, plane, ncclFloat32, c->rank - 1, c->comm, c->stream);
+  }
+  if (c->rank < c->nranks - 1) {
+    g_nccl.Send(ac + (size_t)(c->z1 - 1) * plane, plane, ncclFloat32, c->rank + 1, c->comm, c->stream);
+    g_nccl.Recv(ac + (size_t)c->z1 * plane, plane, ncclFloat32, c->rank + 1, c->comm, c->stream);
+  }
+  return nccl_check(c, g_nccl.GroupEnd(), "ncclGroupEnd (halo planes)");
+}
+
+// After the update: slabs -> all-gather the new X (in place); averaging -> X = mean over ranks.
+pvr_status exchange_x(pvr_ctx* c, float* X2) {
+  if (c->nranks <= 1 || c->exchange == PVR_EXCHANGE_ALLREDUCE) return PVR_OK;
+  const int64_t plane = (int64_t)c->nxp * c->dims.y;
+  if (c->exchange == PVR_EXCHANGE_SLABS)
+    return coll(c, X2, (int64_t)(c->nzp / c->nranks) * plane, PVR_DT_F32, PVR_COLL_ALLGATHER);
+  pvr_status r = coll(c, X2, (int64_t)c->nzp * plane, PVR_DT_F32, PVR_COLL_ALLREDUCE_SUM);
+  if (r != PVR_OK) return r;
+  launch_scale(c->stream, X2, (int64_t)c->nzp * plane, 1.0f / (float)c->nranks);
+  return PVR_OK;
 }
 
 void free_dev(pvr_ctx* c) {
@@ -616,33 +726,37 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   // shared-memory budget in bytes: forward 4 B per staged voxel; backprojection 16 B per cell
   // for exact groups (hi / lo words), 8 B for single-word groups; the init plan is all exact
   const int64_t byte_budget = fwd ? kFwdTileBytes : kind == 1 ? (int64_t)kBpTileBytes * 9 / 10 : kBpTileBytes;
+  // member pool: the natural members, then sub-members made by splitting a member whose own
+  // footprint does not fit (below); mlo / mhi: their fp64 voxel bboxes
+  std::vector<MemberDev> pool(ng.mem);
   const int64_t nm = (int64_t)ng.mem.size();
   std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < nm; ++i) {
-    const MemberDev& m = ng.mem[i];
+  auto bbox_of = [&](const MemberDev& m, int* lo, int* hi) {
     const HostPatch& hp = c->patches[c->first + m.patch];
-    int lo[3], hi[3];
     member_bbox(m, hp, c->stacks[hp.stack].psf, geo[m.patch], fwd, lo, hi);
-    for (int d = 0; d < 3; ++d) { mlo[3 * i + d] = lo[d]; mhi[3 * i + d] = hi[d]; }
-  }
+  };
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nm; ++i) bbox_of(ng.mem[i], &mlo[3 * i], &mhi[3 * i]);
   tr.mark("    member bboxes");
   const int n3[3] = {c->dims.x, c->dims.y, c->dims.z};
-  auto group = [&](int a, int b, GroupDev& g) {  // union bbox of members [a, b)
+  // union bbox of the pool members listed in ix[0, n) -> tile box g (m0 / nm set by the caller)
+  auto group = [&](const int32_t* ix, int n, GroupDev& g) {
     int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
-    for (int i = a; i < b; ++i)
+    int rim = 0;
+    for (int k = 0; k < n; ++k) {
+      const int i = ix[k];
       for (int d = 0; d < 3; ++d) {
         lo[d] = std::min(lo[d], mlo[3 * i + d]);
         hi[d] = std::max(hi[d], mhi[3 * i + d]);
       }
-    g.m0 = a;  // natural member index; renumbered below
-    g.nm = b - a;
+      rim |= pool[i].flags & kMemberRim;
+    }
+    g.m0 = 0;
+    g.nm = n;
     g.tmap = 0;
     g.interior = 1;
     for (int d = 0; d < 3; ++d)
       if (lo[d] < 0 || hi[d] > n3[d] - 1) g.interior = 0;
-    int rim = 0;
-    for (int i = a; i < b; ++i) rim |= ng.mem[i].flags & kMemberRim;
     g.exact = !fwd && (kind == 2 || c->bp_exact == kBpAll || (c->bp_exact == kBpRim && (rim || !g.interior)));
     if (fwd) {
       // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
@@ -666,13 +780,53 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     g.dim[2] = hi[2] - lo[2] + 1;
     return (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
   };
-  // natural groups (parallel); a group over the tile budget is split into single members
+  auto fits = [&](const GroupDev& g, int64_t vox) { return vox * (fwd ? 4 : g.exact ? 16 : 8) <= byte_budget; };
+  // Outlying members of a natural group: a member whose footprint centre lies more than a
+  // quarter of the group's median footprint extent (and 4 voxels) from the median centre on
+  // some axis (a patch
+  // misregistered far from the neighbours that share its stack pixels: c4's gross errors). Two
+  // members that far apart are both taken out. Bit k of the mask: member a + k.
+  auto outliers = [&](int a, int b) -> uint32_t {
+    const int n = b - a;
+    if (n < 2) return 0u;
+    uint32_t mask = 0u;
+    for (int d = 0; d < 3; ++d) {
+      double cen[kMaxGroupMembers], ext[kMaxGroupMembers];
+      for (int i = 0; i < n; ++i) {
+        cen[i] = 0.5 * (mlo[3 * (a + i) + d] + mhi[3 * (a + i) + d]);
+        ext[i] = mhi[3 * (a + i) + d] - mlo[3 * (a + i) + d] + 1;
+      }
+      double sc[kMaxGroupMembers], se[kMaxGroupMembers];
+      std::copy(cen, cen + n, sc);
+      std::copy(ext, ext + n, se);
+      std::sort(sc, sc + n);
+      std::sort(se, se + n);
+      const double mc = n % 2 ? sc[n / 2] : 0.5 * (sc[n / 2 - 1] + sc[n / 2]);
+      const double me = n % 2 ? se[n / 2] : 0.5 * (se[n / 2 - 1] + se[n / 2]);
+      for (int i = 0; i < n; ++i)
+        if (std::fabs(cen[i] - mc) > std::max(0.25 * me, 4.0)) mask |= 1u << i;
+    }
+    return mask;
+  };
+  // Natural groups, in parallel: the common case is a group without outlying members whose
+  // union fits (status 0: one tile). Otherwise (status 1) it is resolved below: outlying
+  // members leave the group, so they cannot inflate the shared tile; the rest forms the group
+  // if it fits, else single members; a member that does not fit alone is split into halves of
+  // its pixel tile until it does.
   const int ngrp = (int)ng.start.size() - 1;
   std::vector<GroupDev> nat(ngrp);
   std::vector<int64_t> nvox(ngrp);
+  std::vector<uint8_t> status(ngrp);
+  std::vector<uint32_t> omask(ngrp);
+  std::vector<int32_t> seq(nm);
+  for (int64_t i = 0; i < nm; ++i) seq[i] = (int32_t)i;
 #pragma omp parallel for schedule(static)
-  for (int gi = 0; gi < ngrp; ++gi) nvox[gi] = group(ng.start[gi], ng.start[gi + 1], nat[gi]);
-  auto fits = [&](const GroupDev& g, int64_t vox) { return vox * (fwd ? 4 : g.exact ? 16 : 8) <= byte_budget; };
+  for (int gi = 0; gi < ngrp; ++gi) {
+    const int a = ng.start[gi], b = ng.start[gi + 1];
+    omask[gi] = outliers(a, b);
+    nvox[gi] = group(&seq[a], b - a, nat[gi]);
+    status[gi] = (!omask[gi] && fits(nat[gi], nvox[gi])) ? 0 : 1;
+  }
   out.grp.clear();
   out.grp.reserve(ngrp);
   out.max_tile_vox = 0;
@@ -680,24 +834,77 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   out.max_t_floats = ng.max_t_floats;
   out.nsplit = 0;
   out.all_fit = true;
+  std::vector<int32_t> ix;          // pool indices of every output group, concatenated
+  std::vector<int32_t> gstart;      // output group k lists ix[gstart[k], gstart[k + 1])
+  ix.reserve(nm);
+  gstart.reserve(ngrp + 1);
   int fit = 0;
+  auto emit = [&](const GroupDev& g, int64_t vox, const int32_t* list, int n) {
+    gstart.push_back((int32_t)ix.size());
+    ix.insert(ix.end(), list, list + n);
+    out.grp.push_back(g);
+    out.max_tile_vox = std::max(out.max_tile_vox, vox);
+  };
+  std::vector<int32_t> work;
+  auto emit_single = [&](int32_t i0) {  // a member alone, halving its pixel tile until it fits
+    work.assign(1, i0);
+    while (!work.empty()) {
+      const int32_t i = work.back();
+      work.pop_back();
+      GroupDev g;
+      const int64_t vox = group(&i, 1, g);
+      const MemberDev m = pool[i];
+      if (fits(g, vox) || (m.tu == 1 && m.tv == 1)) {
+        if (!fits(g, vox)) out.all_fit = false;
+        emit(g, vox, &i, 1);
+        continue;
+      }
+      const int hu = m.tu > 1 ? (m.tu + 1) / 2 : m.tu, hv = m.tv > 1 ? (m.tv + 1) / 2 : m.tv;
+      for (int sv = 0; sv < m.tv; sv += hv)
+        for (int su = 0; su < m.tu; su += hu) {
+          MemberDev q = m;
+          q.u0 = m.u0 + su;
+          q.v0 = m.v0 + sv;
+          q.tu = std::min(hu, m.tu - su);
+          q.tv = std::min(hv, m.tv - sv);
+          pool.push_back(q);
+          mlo.resize(3 * pool.size());
+          mhi.resize(3 * pool.size());
+          const int32_t k = (int32_t)pool.size() - 1;
+          bbox_of(q, &mlo[3 * k], &mhi[3 * k]);
+          work.push_back(k);
+        }
+      ++out.nsplit;
+    }
+  };
+  std::vector<int32_t> core;
   for (int gi = 0; gi < ngrp; ++gi) {
     const int a = ng.start[gi], b = ng.start[gi + 1];
-    if (fits(nat[gi], nvox[gi])) {
+    if (status[gi] == 0) {
       ++fit;
-      out.grp.push_back(nat[gi]);
-      out.max_tile_vox = std::max(out.max_tile_vox, nvox[gi]);
+      emit(nat[gi], nvox[gi], &seq[a], b - a);
       continue;
     }
-    if (b - a > 1) ++out.nsplit;
+    core.clear();
     for (int i = a; i < b; ++i) {
-      GroupDev g;
-      const int64_t vox = group(i, i + 1, g);
-      if (!fits(g, vox)) out.all_fit = false;
-      out.grp.push_back(g);
-      out.max_tile_vox = std::max(out.max_tile_vox, vox);
+      if (omask[gi] >> (i - a) & 1u) emit_single(i);
+      else core.push_back(i);
     }
+    if (core.empty()) {  // all members outlying: not a tile-size failure
+      ++fit;
+      continue;
+    }
+    GroupDev g;
+    const int64_t vox = group(core.data(), (int)core.size(), g);
+    if (fits(g, vox)) {
+      ++fit;
+      emit(g, vox, core.data(), (int)core.size());
+      continue;
+    }
+    if (core.size() > 1) ++out.nsplit;
+    for (int32_t i : core) emit_single(i);
   }
+  gstart.push_back((int32_t)ix.size());
   out.fit_frac = ngrp ? (double)fit / ngrp : 1.0;
   tr.mark("    group boxes");
   // Order the CTAs' work along a Morton curve of the groups' bbox centres (16-voxel cells), so
@@ -725,8 +932,9 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   out.mem.resize(m0[ng2]);
 #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < ng2; ++k) {
-    GroupDev g = out.grp[order[k].second];
-    for (int i = 0; i < g.nm; ++i) out.mem[m0[k] + i] = ng.mem[g.m0 + i];
+    const int32_t src = order[k].second;
+    GroupDev g = out.grp[src];
+    for (int i = 0; i < g.nm; ++i) out.mem[m0[k] + i] = pool[ix[gstart[src] + i]];
     g.m0 = m0[k];
     grp[k] = g;
   }
@@ -851,8 +1059,10 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
   const int64_t step = std::max<int64_t>(1, c->nloc / 128);
   for (int64_t s = 0; s < c->nloc; s += step) sample.push_back(s);
   static const int fcand[][3] = {{16, 16, 1}, {16, 8, 1}, {8, 8, 1}, {8, 4, 1}, {4, 4, 1}, {2, 2, 1}, {1, 1, 1}};
-  static const int bcand[][3] = {{16, 16, 1}, {16, 8, 1}, {16, 8, 2}, {8, 8, 1}, {8, 8, 2}, {8, 4, 2},
-                                 {4, 4, 2},   {4, 4, 4},  {2, 2, 4},  {2, 2, 8}, {1, 1, 8}, {1, 1, 32}};
+  // through-plane segments cost a line setup and two window flushes each: fewer segments at a
+  // smaller pixel tile first (c3: 8 x 8 x 1 17.8 ms vs 16 x 8 x 2 20.5 ms per backprojection)
+  static const int bcand[][3] = {{16, 16, 1}, {16, 8, 1}, {8, 8, 1}, {8, 4, 1}, {16, 8, 2}, {8, 8, 2},
+                                 {8, 4, 2},   {4, 4, 2},  {4, 4, 4}, {2, 2, 4}, {2, 2, 8},  {1, 1, 8}, {1, 1, 32}};
   auto natural = [&](int TU, int TV, int nseg, bool fwd, bool smp) -> const NaturalGroups& {
     for (auto& ng : c->ngcache)
       if (ng->TU == TU && ng->TV == TV && ng->nseg == nseg && ng->fwd == fwd && ng->sample == smp) return *ng;
@@ -881,6 +1091,9 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
         if (!(pb.all_fit && pb.fit_frac >= 0.9)) continue;
       }
       size_groups(c, geo, natural(cand[k][0], cand[k][1], cand[k][2], fwd, false), kind, pb);
+      if (tr.on)
+        fprintf(stderr, "[pvr]   plan kind %d tile %dx%dx%d: fit %.3f all_fit %d groups %zu split %d\n", kind,
+                cand[k][0], cand[k][1], cand[k][2], pb.fit_frac, (int)pb.all_fit, pb.grp.size(), pb.nsplit);
       if (pb.all_fit && pb.fit_frac >= 0.9) { pick = k; break; }
     }
     if (pick < 0) return fail(c, PVR_ERR_ARG, "no tiling fits the shared-memory budget (extreme transforms?)");
@@ -899,6 +1112,12 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
     int32_t* tile = fwd ? c->st.fwd_tile : c->st.bp_tile;
     tile[0] = pl.TU; tile[1] = pl.TV; tile[2] = pl.nseg;
     (fwd ? c->st.fwd_groups : c->st.bp_groups) = pl.ngroups;
+    (fwd ? c->st.fwd_split : c->st.bp_split) = pb.nsplit;
+    if (!fwd) {
+      int64_t ne = 0;
+      for (const GroupDev& g : pb.grp) ne += g.exact;
+      c->st.bp_exact_groups = ne;
+    }
     (fwd ? c->st.fwd_members : c->st.bp_members) = (int64_t)pb.mem.size();
     (fwd ? c->st.fwd_smem : c->st.bp_smem) =
         fwd ? (int64_t)(pl.t_floats + pl.tile_words) * 4 : (int64_t)kBpTileBytes + pl.r_bytes;
@@ -966,6 +1185,9 @@ pvr_status pvr_create_volume(const pvr_geometry* g, int cuda_device, void* cuda_
   for (int d = 0; d < 3; ++d) c->o[d] = g->origin_mm[d];
   c->V = (int64_t)g->dims[0] * g->dims[1] * g->dims[2];
   c->Vp = (int64_t)c->nxp * g->dims[1] * g->dims[2];
+  c->nzp = g->dims[2];
+  c->z0 = 0;
+  c->z1 = g->dims[2];
   cudaSetDevice(cuda_device);
   if (cuda_stream) {
     c->stream = (cudaStream_t)cuda_stream;
@@ -1006,6 +1228,7 @@ pvr_status pvr_destroy(pvr_ctx* c) {
     for (auto& slot : *pool)
       for (auto e : slot) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->host_buf) cudaFreeHost(c->host_buf);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return PVR_OK;
@@ -1022,19 +1245,63 @@ pvr_status pvr_comm_unique_id(void* out128) {
   return PVR_OK;
 }
 
+// Common part of the two comm inits: rank, shard and the padded volume layout (nz rounded up
+// to nranks equal slabs of planes, for reduce-scatter / all-gather; X kept).
+static pvr_status comm_setup(pvr_ctx* c, int nranks, int rank) {
+  c->nranks = nranks;
+  c->rank = rank;
+  const int nzp = (c->dims.z + nranks - 1) / nranks * nranks;
+  if (nzp != c->nzp) {
+    const int64_t plane = (int64_t)c->nxp * c->dims.y;
+    const int64_t Vp = plane * nzp;
+    float* X[2] = {nullptr, nullptr};
+    float2* AC = nullptr;
+    CUDA_TRY(c, cudaMalloc(&X[0], Vp * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&X[1], Vp * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&AC, (Vp + 2) * sizeof(float2)));
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(c, cudaMemsetAsync(X[b], 0, Vp * sizeof(float), c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(X[b], c->X[b], c->Vp * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CUDA_TRY(c, cudaMemsetAsync(AC, 0, (Vp + 2) * sizeof(float2), c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaFree(c->X[0]);
+    cudaFree(c->X[1]);
+    cudaFree(c->AC);
+    c->X[0] = X[0];
+    c->X[1] = X[1];
+    c->AC = AC;
+    c->Vp = Vp;
+    c->nzp = nzp;
+  }
+  const int slab = c->nzp / nranks;
+  c->z0 = std::min(rank * slab, c->dims.z);
+  c->z1 = std::min((rank + 1) * slab, c->dims.z);
+  return PVR_OK;
+}
+
 pvr_status pvr_comm_init(pvr_ctx* c, int nranks, int rank, const void* uid) {
   GUARD(c);
   if (c->state >= PATCHED) return fail(c, PVR_ERR_STATE, "pvr_comm_init must precede extract_patches");
   if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !uid))
     return fail(c, PVR_ERR_ARG, "invalid nranks/rank/unique id");
-  c->nranks = nranks;
-  c->rank = rank;
-  if (nranks == 1) return PVR_OK;
+  pvr_status r = comm_setup(c, nranks, rank);
+  if (r != PVR_OK || nranks == 1) return r;
   std::string err;
   if (!g_nccl.load(err)) return fail(c, PVR_ERR_NCCL, "%s", err.c_str());
   ncclUniqueId id;
   memcpy(&id, uid, sizeof(id));
   return nccl_check(c, g_nccl.CommInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+}
+
+pvr_status pvr_comm_init_host(pvr_ctx* c, int nranks, int rank, pvr_host_collective_fn fn, void* user) {
+  GUARD(c);
+  if (c->state >= PATCHED) return fail(c, PVR_ERR_STATE, "pvr_comm_init_host must precede extract_patches");
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !fn))
+    return fail(c, PVR_ERR_ARG, "invalid nranks/rank/collective callback");
+  c->host_fn = fn;
+  c->host_user = user;
+  return comm_setup(c, nranks, rank);
 }
 
 pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
@@ -1063,6 +1330,11 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
     case PVR_PARAM_PATCH_MIXTURE: if (v != 0 && v != 1) goto bad; c->patch_mixture = (int)v; break;
     case PVR_PARAM_PROFILE: c->profile = v != 0; break;
     case PVR_PARAM_BP_EXACT: if (v != 0 && v != 1 && v != 2) goto bad; c->bp_exact = (int)v; break;
+    case PVR_PARAM_EXCHANGE:
+      if (v != PVR_EXCHANGE_ALLREDUCE && v != PVR_EXCHANGE_SLABS && v != PVR_EXCHANGE_AVERAGE) goto bad;
+      c->exchange = (int)v;
+      break;
+    case PVR_PARAM_COMM_TIMEOUT: if (!(v > 0)) goto bad; c->comm_timeout = v; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }
   return PVR_OK;
@@ -1920,11 +2192,15 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     r = backproject(c, s, c->bplan, lb, c->w, 0);
     if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_BP1], s);
-    r = allreduce_ac(c);
+    r = exchange_ac(c);
     if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_AR1], s);
-    launch_update(s, X0, c->AC, c->dims, c->nxp, prm, c->em, alpha, lambda, X2);
+    const bool slabs = c->nranks > 1 && c->exchange == PVR_EXCHANGE_SLABS;
+    launch_update(s, X0, c->AC, c->dims, c->nxp, prm, c->em, alpha, lambda, X2, slabs ? c->z0 : 0,
+                  slabs ? c->z1 : c->dims.z);
     CHECK_LAUNCH(c);
+    r = exchange_x(c, X2);
+    if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_UPD1], s);
     c->cur = 1 - c->cur;
     c->st.iterations += 1;
@@ -1935,9 +2211,33 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     if (c->nranks > 1) c->st.n_allreduce += 1;
     if (c->prof_pending.size() >= 512) prof_drain(c);
   }
+  if (c->comm) {  // poll NCCL's asynchronous errors while the iterations drain (comm_wait)
+    pvr_status rw = comm_wait(c);
+    if (rw != PVR_OK) return rw;
+  }
   if ((double)alpha * lambda > 3.0 / 44.0)
     c->err = "warning: alpha*lambda > 3/44, the regulariser's maximum principle does not hold";
   return PVR_OK;
+}
+
+// One quantity (0: A, 1: C) of the interleaved, row-padded (A, C) volume into a caller
+// buffer [nz][ny][nx]: unpacked on the device (k_unpack_ac) straight into a device output, or
+// into the scratch X buffer and copied to a host output.
+static pvr_status unpack_ac(pvr_ctx* c, int which, float* out) {
+  const bool dev = is_device_ptr(out);
+  float* dst = dev ? out : c->X[1 - c->cur];  // scratch between iterations
+  launch_unpack_ac(c->stream, c->AC, c->dims, c->nxp, which, dst);
+  CHECK_LAUNCH(c);
+  if (!dev) CUDA_TRY(c, cudaMemcpyAsync(out, dst, c->V * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_get_confidence(pvr_ctx* c, float* out, size_t nvox) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "no confidence before set_transforms");
+  if (!out || (int64_t)nvox != c->V) return fail(c, PVR_ERR_ARG, "volume has %lld voxels", (long long)c->V);
+  return unpack_ac(c, 1, out);
 }
 
 pvr_status pvr_get_volume(pvr_ctx* c, float* out, size_t nvox) {
@@ -1974,28 +2274,8 @@ pvr_status pvr_get_taps(pvr_ctx* c, float* e, float* kap, float* A, float* C) {
   pvr_status r;
   if ((r = copy_out(c, e, c->e, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
   if ((r = copy_out(c, kap, c->kap, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
-  if (A || C) {
-    std::vector<float2> ac(c->Vp);
-    CUDA_TRY(c, cudaMemcpyAsync(ac.data(), c->AC, c->Vp * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    std::vector<float> a(c->V), cc(c->V);
-    const int nx = c->dims.x;
-    for (int64_t row = 0; row < (int64_t)c->dims.y * c->dims.z; ++row)
-      for (int i = 0; i < nx; ++i) {
-        a[row * nx + i] = ac[row * c->nxp + i].x;
-        cc[row * nx + i] = ac[row * c->nxp + i].y;
-      }
-    float* dsts[2] = {A, C};
-    const std::vector<float>* srcs[2] = {&a, &cc};
-    for (int i = 0; i < 2; ++i) {
-      if (!dsts[i]) continue;
-      if (is_device_ptr(dsts[i])) {
-        CUDA_TRY(c, cudaMemcpy(dsts[i], srcs[i]->data(), c->V * sizeof(float), cudaMemcpyHostToDevice));
-      } else {
-        memcpy(dsts[i], srcs[i]->data(), c->V * sizeof(float));
-      }
-    }
-  }
+  if (A && (r = unpack_ac(c, 0, A)) != PVR_OK) return r;
+  if (C && (r = unpack_ac(c, 1, C)) != PVR_OK) return r;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
 }
@@ -2040,6 +2320,8 @@ pvr_status pvr_reset_stats(pvr_ctx* c) {
   c->st.fwd_groups = keep.fwd_groups; c->st.bp_groups = keep.bp_groups;
   c->st.fwd_members = keep.fwd_members; c->st.bp_members = keep.bp_members;
   c->st.fwd_smem = keep.fwd_smem; c->st.bp_smem = keep.bp_smem;
+  c->st.bp_exact_groups = keep.bp_exact_groups;
+  c->st.fwd_split = keep.fwd_split; c->st.bp_split = keep.bp_split;
   return PVR_OK;
 }
 

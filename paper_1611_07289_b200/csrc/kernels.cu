@@ -349,11 +349,12 @@ __device__ __forceinline__ float nb_sum(const float* c0, const float* c1, float 
 __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
                                                 const float2* __restrict__ AC, int3 n, int nxp,
                                                 Params prm, const EmDev* __restrict__ em,
-                                                float alpha, float lambda, float* __restrict__ X2) {
+                                                float alpha, float lambda, float* __restrict__ X2,
+                                                int zlo, int zhi) {
   __shared__ float s0[kHZ * kHY * kHX];  // X0
   __shared__ float s1[kHZ * kHY * kHX];  // X1, NaN where C <= tau_C (uncovered) or off-grid
   const float lo = (float)em->lo, hi = (float)em->hi;
-  const int bx = blockIdx.x * kUX - 1, by = blockIdx.y * kUY - 1, bz = blockIdx.z * kUZ - 1;
+  const int bx = blockIdx.x * kUX - 1, by = blockIdx.y * kUY - 1, bz = zlo + blockIdx.z * kUZ - 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   bool cov = true;
   for (int r = wid; r < kHY * kHZ; r += 8) {
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
 #pragma unroll 2
   for (int tz = 0; tz < kUZ; ++tz) {
     const int l = bz + 1 + tz;
-    if (l >= n.z) break;
+    if (l >= zhi) break;  // this launch's planes [zlo, zhi) (a rank's slab, or all)
     const int c = ((tz + 1) * kHY + (wid + 1)) * kHX + lane + 1;
     const float x0 = s0[c], x1 = s1[c];
     float out;
@@ -588,6 +589,22 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
   grp[g] = G;
 }
 
+// One quantity of the interleaved, row-padded (A, C) volume into a contiguous [nz][ny][nx]
+// array (pvr_get_confidence, the taps).
+__global__ void k_unpack_ac(const float2* __restrict__ AC, int3 n, int nxp, int which, float* __restrict__ out) {
+  const int64_t V = (int64_t)n.x * n.y * n.z;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < V; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = k / n.x;
+    const float2 ac = AC[row * nxp + (k - row * n.x)];
+    out[k] = which ? ac.y : ac.x;
+  }
+}
+
+__global__ void k_scale(float* __restrict__ x, int64_t n, float f) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= f;
+}
+
 __global__ void k_fill(float* __restrict__ x, int64_t n, float v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = v;
@@ -595,6 +612,14 @@ __global__ void k_fill(float* __restrict__ x, int64_t n, float v) {
 
 // --------------------------------------------------------------------------------------
 // launchers
+
+void launch_unpack_ac(cudaStream_t st, const float2* AC, int3 dims, int nxp, int which, float* out) {
+  k_unpack_ac<<<148 * 8, 256, 0, st>>>(AC, dims, nxp, which, out);
+}
+
+void launch_scale(cudaStream_t st, float* x, int64_t n, float f) {
+  if (n > 0) k_scale<<<148 * 8, 256, 0, st>>>(x, n, f);
+}
 
 void launch_fill(cudaStream_t st, float* x, int64_t n, float v) {
   if (n > 0) k_fill<<<148 * 8, 256, 0, st>>>(x, n, v);
@@ -642,9 +667,10 @@ void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double t
 }
 
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
-                   Params prm, const EmDev* em, float alpha, float lambda, float* X2) {
-  const dim3 grid((dims.x + kUX - 1) / kUX, (dims.y + kUY - 1) / kUY, (dims.z + kUZ - 1) / kUZ);
-  k_update<<<grid, 256, 0, st>>>(X0, AC, dims, nxp, prm, em, alpha, lambda, X2);
+                   Params prm, const EmDev* em, float alpha, float lambda, float* X2, int zlo, int zhi) {
+  if (zhi <= zlo) return;
+  const dim3 grid((dims.x + kUX - 1) / kUX, (dims.y + kUY - 1) / kUY, (zhi - zlo + kUZ - 1) / kUZ);
+  k_update<<<grid, 256, 0, st>>>(X0, AC, dims, nxp, prm, em, alpha, lambda, X2, zlo, zhi);
 }
 
 void launch_replan(cudaStream_t st, const MemberDev* mem, GroupDev* grp, int ngroups, int cap, const PatchDev* P,

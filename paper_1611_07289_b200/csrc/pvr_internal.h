@@ -195,8 +195,11 @@ void launch_mix_round(cudaStream_t st, const float* pbar, const int32_t* nlive, 
 void launch_mix_update(cudaStream_t st, EmDev* em, int round, double tol);
 void launch_mix_weights(cudaStream_t st, const int32_t* nlive, int64_t npatch, const EmDev* em, float* w);
 void launch_em_round(cudaStream_t st, Params prm, EmDev* em, int round, double tol);
+// planes [zlo, zhi) only (a rank's slab; the stencil reads the planes on either side)
 void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int3 dims, int nxp,
-                   Params prm, const EmDev* em, float alpha, float lambda, float* X2);
+                   Params prm, const EmDev* em, float alpha, float lambda, float* X2, int zlo, int zhi);
+void launch_unpack_ac(cudaStream_t st, const float2* AC, int3 dims, int nxp, int which, float* out);
+void launch_scale(cudaStream_t st, float* x, int64_t n, float f);
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);
 constexpr int kMaxBoxShapes = 4096;  // forward TMA box shapes the device re-plan may pick from
 // nappend (backprojection): counter of single-member groups appended after ngroups (< cap)

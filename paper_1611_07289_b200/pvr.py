@@ -21,16 +21,21 @@ STATUS_NAMES = {0: "PVR_OK", 1: "PVR_ERR_ARG", 2: "PVR_ERR_STATE", 3: "PVR_ERR_O
 PARAM = {"delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
          "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "profile": 11, "psf_quality": 12,
          "em_rounds": 13, "em_tol": 14, "patch_mixture": 15,
-         "bp_exact": 16}
+         "bp_exact": 16, "exchange": 17, "comm_timeout": 18}
+EXCHANGE = {"allreduce": 0, "slabs": 1, "average": 2}
+COLL_ALLREDUCE_SUM, COLL_ALLREDUCE_MAX, COLL_ALLGATHER = 0, 1, 2
+DT_F32, DT_F64, DT_I64 = 0, 1, 2
+# int fn(void* user, void* buf, int64_t count, int dtype, int op)
+HOST_COLLECTIVE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int)
 
 # every symbol include/pvr.h declares (checked by tests/test_abi.py)
-EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", "pvr_comm_init",
+EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", "pvr_comm_init", "pvr_comm_init_host",
            "pvr_comm_unique_id", "pvr_add_stack", "pvr_extract_patches", "pvr_plan_shards",
            "pvr_get_shard", "pvr_get_patches", "pvr_set_transforms", "pvr_set_volume",
            "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume", "pvr_rigidity_map",
            "pvr_register_patches", "pvr_patch_cc", "pvr_set_patches", "pvr_superpixels",
            "pvr_superpixel_patches", "pvr_get_mask",
-           "pvr_get_weights", "pvr_get_taps", "pvr_get_em_state", "pvr_get_stats",
+           "pvr_get_weights", "pvr_get_taps", "pvr_get_confidence", "pvr_get_em_state", "pvr_get_stats",
            "pvr_reset_stats"]
 
 
@@ -56,7 +61,8 @@ class pvr_stats(C.Structure):
                [("fwd_tile", C.c_int32 * 3), ("bp_tile", C.c_int32 * 3)] + \
                [(n, C.c_int64) for n in ("fwd_groups", "bp_groups", "fwd_members", "bp_members",
                                           "fwd_smem", "bp_smem",
-                                          "device_replans", "host_replans", "replan_splits")]
+                                          "device_replans", "host_replans", "replan_splits",
+                                          "bp_exact_groups", "fwd_split", "bp_split")]
 
     def as_dict(self):
         d = {}
@@ -85,6 +91,8 @@ def lib():
             "pvr_last_error": (C.c_char_p, [vp]),
             "pvr_comm_init": (i32, [vp, i32, i32, vp]),
             "pvr_comm_unique_id": (i32, [vp]),
+            "pvr_comm_init_host": (i32, [vp, i32, i32, HOST_COLLECTIVE, vp]),
+            "pvr_get_confidence": (i32, [vp, vp, C.c_size_t]),
             "pvr_add_stack": (i32, [vp, vp, i32, i32, i32, vp, d, C.POINTER(i32)]),
             "pvr_extract_patches": (i32, [vp, i32, i32, i32, i32, C.POINTER(i64)]),
             "pvr_plan_shards": (i32, [vp, i64, i32, vp]),
@@ -166,6 +174,30 @@ def pvr_comm_unique_id():
 def pvr_comm_init(ctx, nranks, rank, unique_id):
     buf = (C.c_char * 128).from_buffer_copy(unique_id) if unique_id is not None else None
     _check(ctx, lib().pvr_comm_init(ctx, nranks, rank, buf))
+
+
+def pvr_comm_init_host(ctx, nranks, rank, fn):
+    """fn(buf: numpy array view of the library's host buffer, op) performs the collective in
+    place (see pvr.h); returns the ctypes callback object, which must outlive the context."""
+    dt = {DT_F32: np.float32, DT_F64: np.float64, DT_I64: np.int64}
+
+    def tramp(user, buf, count, dtype, op):
+        try:
+            n = count * (nranks if op == COLL_ALLGATHER else 1)
+            arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(np.ctypeslib.as_ctypes_type(dt[dtype]))), (n,))
+            fn(arr, op)
+            return 0
+        except Exception as ex:  # the library turns a nonzero return into PVR_ERR_NCCL
+            print("pvr host collective failed:", ex)
+            return 1
+    cb = HOST_COLLECTIVE(tramp)
+    _check(ctx, lib().pvr_comm_init_host(ctx, nranks, rank, cb, None))
+    return cb
+
+
+def pvr_get_confidence(ctx, out):
+    _check(ctx, lib().pvr_get_confidence(ctx, _ptr(out), out.size if isinstance(out, np.ndarray) else out.numel()))
+    return out
 
 
 def pvr_add_stack(ctx, slices, index_to_world, thickness_mm):
@@ -292,6 +324,14 @@ class Context:
 
     def comm_init(self, nranks, rank, uid):
         pvr_comm_init(self.h, nranks, rank, uid)
+
+    def comm_init_host(self, nranks, rank, fn):
+        self._coll = pvr_comm_init_host(self.h, nranks, rank, fn)  # keep the callback alive
+
+    def confidence(self, out=None):
+        if out is None:
+            out = np.empty(tuple(self.dims)[::-1], np.float32)
+        return pvr_get_confidence(self.h, out)
 
     def add_stack(self, slices, G, thickness):
         return pvr_add_stack(self.h, slices, G, thickness)

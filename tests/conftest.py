@@ -17,3 +17,17 @@ def pytest_configure(config):
 def _built():
     import __graft_entry__
     __graft_entry__.build()
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Dump the errors the parity checks measured (tests/helpers.py ERRORS) to $PVR_PARITY_LOG."""
+    path = os.environ.get("PVR_PARITY_LOG")
+    if not path:
+        return
+    try:
+        import json
+        from helpers import ERRORS
+        with open(path, "w") as f:
+            json.dump(ERRORS, f, indent=0, default=float)
+    except Exception as ex:  # diagnostics only
+        print("parity log not written:", ex)

@@ -1,0 +1,111 @@
+"""The product's sharded path on one GPU: two processes, each a rank with
+its own libpvr context on cuda:0 and its shard of the patches, joined by the host-collective
+transport (pvr_comm_init_host) backed by torch.distributed gloo. No kernel waits on another
+rank (every exchange is a host call between kernels), so sharing one GPU is safe.
+
+Checked against one rank running the whole problem:
+  * PVR_EXCHANGE_ALLREDUCE and PVR_EXCHANGE_SLABS give the 1-rank volume up to fp32
+    summation order (<= 1e-5 relative), with bit-identical volumes on both ranks;
+  * PVR_EXCHANGE_AVERAGE (the paper's averaging of sub-reconstructions, kept for comparison)
+    does not: its volume differs from the 1-rank operator by far more.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ITERS = 2
+
+
+def _problem():
+    import synth
+    return synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
+
+
+def _run(nranks, rank, exchange, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_07289_b200 import Context, load_problem, pvr
+    if nranks > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=nranks)
+
+    def collective(buf, op):
+        t = torch.from_numpy(buf)
+        if op == pvr.COLL_ALLGATHER:
+            parts = list(t.chunk(nranks))
+            gathered = [torch.empty_like(parts[0]) for _ in range(nranks)]
+            dist.all_gather(gathered, parts[rank].clone())
+            t.copy_(torch.cat(gathered))
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == pvr.COLL_ALLREDUCE_MAX else dist.ReduceOp.SUM)
+
+    prob = _problem()
+    ctx = Context(prob["dims"], prob["spacing"], prob["origin"], 0)
+    try:
+        ctx.set_param("exchange", pvr.EXCHANGE[exchange])
+        if nranks > 1:
+            ctx.comm_init_host(nranks, rank, collective)
+        load_problem(ctx, prob)
+        ctx.init_volume()
+        ctx.sr_iterate(ITERS, prob["alpha"], prob["lam"])
+        X = ctx.volume()
+        first, nloc, _, _ = pvr.pvr_get_shard(ctx.h)
+        np.save(out, X)
+        np.save(out + ".shard.npy", np.array([first, nloc]))
+    finally:
+        ctx.close()
+        if nranks > 1:
+            dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(nranks, exchange, tmp_path):
+    import torch.multiprocessing as mp
+    port = _free_port()
+    outs = [str(tmp_path / f"{exchange}_{nranks}_{r}.npy") for r in range(nranks)]
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_run, args=(nranks, r, exchange, port, outs[r])) for r in range(nranks)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0, f"rank process failed ({p.exitcode})"
+    return [np.load(o) for o in outs], [np.load(o + ".shard.npy") for o in outs]
+
+
+@pytest.fixture(scope="module")
+def one_rank(tmp_path_factory):
+    (X,), _ = _spawn(1, "allreduce", tmp_path_factory.mktemp("r1"))
+    return X.astype(np.float64)
+
+
+@pytest.mark.parametrize("exchange", ["allreduce", "slabs"])
+def test_two_ranks_match_one(exchange, one_rank, tmp_path):
+    Xs, shards = _spawn(2, exchange, tmp_path)
+    assert np.array_equal(Xs[0], Xs[1]), "ranks disagree"
+    (f0, n0), (f1, n1) = shards
+    assert f0 == 0 and n0 > 0 and f1 == n0 and n1 > 0          # contiguous shards
+    rel = np.linalg.norm(Xs[0] - one_rank) / np.linalg.norm(one_rank)
+    print(f"{exchange}: 2 ranks vs 1, rel L2 {rel:.2e}")
+    assert rel <= 1e-5
+
+
+def test_paper_averaging_is_not_the_one_rank_operator(one_rank, tmp_path):
+    """P:233's averaging of the ranks' sub-reconstructions (PVR_EXCHANGE_AVERAGE): each rank
+    updates X from its own patches only, then X is the mean; a voxel seen by one rank's patches
+    moves half as far. Reading Q21 sums (A, C) instead, which reproduces one rank."""
+    Xs, _ = _spawn(2, "average", tmp_path)
+    assert np.array_equal(Xs[0], Xs[1])
+    rel = np.linalg.norm(Xs[0] - one_rank) / np.linalg.norm(one_rank)
+    print(f"average: 2 ranks vs 1, rel L2 {rel:.2e}")
+    assert rel > 1e-3

@@ -1,17 +1,59 @@
 """GPU (libpvr, fp32 CUDA) vs oracle (fp64 CPU) parity on seeded synthetic problems.
 
-Tolerances are north_star's (BASELINE.json): volume within 1e-4 relative L2 after every
-iteration (free-running, both sides iterate from the same start); pixel posteriors and
-patch weights within 1e-3 absolute. Stage taps (e, kappa, A, C, EM scalars) are checked
-with the tolerances DESIGN.md §Parity derives from fp32 arithmetic.
+Every case runs at both threshold sets of DESIGN.md Q24 / Q25 (tests/helpers.py THRESHOLDS:
+the defaults tau_C = 1e-6, tau_obs = 0.01 of SURVEY.md:652/678, and the round-1 readings 1e-3 /
+0.5). Acceptance (north_star, BASELINE.json): volume within 1e-4 relative L2 after every
+iteration (free-running, both sides iterate from the same start); pixel posteriors and patch
+weights within 1e-3 absolute. Stage bars (helpers.TOL: <= 10x the measured fp32
+error): X, e, A, C relative L2; kappa, p, w absolute; sigma2, c, m relative. Voxels whose
+confidence sits within fp32 reach of tau_C (helpers.tau_c_tie_band) may take either side of the
+threshold; they and their 26-neighbours are left out of the stage X bar, and any flip outside
+that band fails.
 """
 import numpy as np
 import pytest
 
 import synth
-from helpers import make_gpu, make_oracle, rel_l2, weight_mismatch
+from helpers import THRESHOLDS, TOL, make_gpu, make_oracle, record, rel_l2, tau_c_tie_band, weight_mismatch
 
 pytestmark = pytest.mark.gpu
+
+
+def check_iteration(ctx, orc, prob, params, it, check_taps=True):
+    """Compare one iteration's outputs; returns the measured errors."""
+    tau_C = (params or {}).get("tau_C", 1e-6)
+    Xo, Xg = orc.volume().ravel(), ctx.volume().ravel().astype(np.float64)
+    eo, ko, Ao, Co = orc.taps()
+    eg, kg, Ag, Cg = ctx.taps()
+    Co, Cg = Co.ravel(), np.asarray(Cg, np.float64).ravel()
+    band, near = tau_c_tie_band(Co, tau_C, prob["dims"])
+    band, near = band.ravel(), near.ravel()
+    flips = (Co > tau_C) != (Cg > tau_C)
+    assert not (flips & ~band).any(), f"{int((flips & ~band).sum())} tau_C decisions differ outside the fp32 tie band"
+    keep = ~near
+    err = {"X": rel_l2(Xg[keep], Xo[keep]), "X_all": rel_l2(Xg, Xo), "flips": int(flips.sum()),
+           "band": int(band.sum())}
+    po, pbo, wo = orc.weights()
+    pg, pbg, wg = ctx.weights()
+    err["p"], err["w"], err["w_near_threshold"] = weight_mismatch(pg, po, pbg, pbo, wg, wo)
+    emo, emg = orc.em_state(), ctx.em_state()
+    assert emg["t"] == emo["t"] == it + 1
+    err["em"] = max(abs(emg[k] - emo[k]) / max(abs(emo[k]), 1e-30) for k in ("sigma2", "c", "m"))
+    if check_taps:
+        err["e"] = rel_l2(eg, eo)
+        err["A"] = rel_l2(Ag, Ao)
+        err["C"] = rel_l2(Cg, Co)
+        err["kappa"] = float(np.abs(kg - ko).max())
+    record(dict(err, iteration=it + 1))
+    print(f"iteration {it + 1}: " + " ".join(f"{k} {v:.2e}" if isinstance(v, float) else f"{k} {v}"
+                                              for k, v in err.items()))
+    # north_star acceptance (tie-band flips aside, which the stage check below isolates)
+    assert err["X"] <= 1e-4, f"iteration {it + 1}: volume rel L2 {err['X']:.3e}"
+    assert err["p"] <= 1e-3 and err["w"] <= 1e-3, err
+    # stage bars
+    for k in ("X", "p", "w", "em") + (("e", "A", "C", "kappa") if check_taps else ()):
+        assert err[k] <= TOL[k], f"iteration {it + 1}: {k} {err[k]:.3e} > {TOL[k]:.1e}"
+    return err
 
 
 def run_pair(prob, iters, params=None, init=True, X0=None, check_taps=True):
@@ -25,71 +67,85 @@ def run_pair(prob, iters, params=None, init=True, X0=None, check_taps=True):
             orc.init_volume()
             ctx.init_volume()
         rel0 = rel_l2(ctx.volume(), orc.volume())
-        assert rel0 <= 1e-5, f"initial volume rel L2 {rel0:.3e}"
-        # coverage is geometry only: kappa parity and threshold margins
+        assert rel0 <= TOL["X"], f"initial volume rel L2 {rel0:.3e}"
+        # coverage is geometry only
         _, kap_o, _, _ = orc.taps()
         _, kap_g, _, _ = ctx.taps()
-        assert np.abs(kap_g - kap_o).max() <= 2e-5
+        assert np.abs(kap_g - kap_o).max() <= TOL["kappa"]
         hist = []
         for it in range(iters):
             orc.sr_iterate(1, prob["alpha"], prob["lam"])
             ctx.sr_iterate(1, prob["alpha"], prob["lam"])
-            Xo, Xg = orc.volume(), ctx.volume()
-            rel = rel_l2(Xg, Xo)
-            po, pbo, wo = orc.weights()
-            pg, pbg, wg = ctx.weights()
-            dp, dw, near = weight_mismatch(pg, po, pbg, pbo, wg, wo)
-            emo, emg = orc.em_state(), ctx.em_state()
-            hist.append((rel, dp, dw, near))
-            assert emg["t"] == emo["t"] == it + 1
-            for key in ("sigma2", "c", "m"):
-                assert abs(emg[key] - emo[key]) <= 1e-4 * max(abs(emo[key]), 1e-30), (key, emg, emo)
-            if check_taps:
-                eo, _, Ao, Co = orc.taps()
-                eg, _, Ag, Cg = ctx.taps()
-                assert rel_l2(eg, eo) <= 1e-3, "residual e"
-                assert rel_l2(Cg, Co) <= 1e-4, "confidence C"
-                assert rel_l2(Ag, Ao) <= 2e-3, "addon A"
-            assert rel <= 1e-4, f"iteration {it + 1}: volume rel L2 {rel:.3e}"
-            assert dp <= 1e-3, f"iteration {it + 1}: max |dp| {dp:.3e}"
-            assert dw <= 1e-3, f"iteration {it + 1}: max |dw| {dw:.3e}"
+            hist.append(check_iteration(ctx, orc, prob, params, it, check_taps))
         return hist
     finally:
         ctx.close()
 
 
-def test_c1_phantom_two_iterations():
+SETS = pytest.mark.parametrize("thr", list(THRESHOLDS))
+
+
+@SETS
+def test_c1_phantom_two_iterations(thr):
     prob = synth.make_problem("c1")
-    run_pair(prob, prob["iters"])
+    run_pair(prob, prob["iters"], THRESHOLDS[thr])
 
 
-def test_c1_more_iterations():
+@SETS
+def test_c1_more_iterations(thr):
     prob = synth.make_problem("c1")
-    run_pair(prob, 6)
+    run_pair(prob, 6, THRESHOLDS[thr])
 
 
-def test_c2_svr_mode():
+@SETS
+def test_c2_svr_mode(thr):
     prob = synth.make_problem("c2")
-    run_pair(prob, 3)
+    run_pair(prob, 3, THRESHOLDS[thr])
 
 
-def test_c3_structure_small():
+@SETS
+def test_c3_structure_small(thr):
     """c3's structure (4 stacks, 64x64 patches at 50% overlap, breathing motion with
     per-patch mismatch) on a cropped grid the oracle finishes in seconds."""
     prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
-    run_pair(prob, 2)
+    run_pair(prob, 2, THRESHOLDS[thr])
 
 
-def test_c4_3d_patches_corrupted_small():
+@SETS
+def test_c4_3d_patches_corrupted_small(thr):
     """c4's structure: 3D 4-slice patches, per-slab affine motion, 10% gross errors."""
     prob = synth.make_problem("c4", scale=(96, 96, 16), size=32, stride=16)
-    run_pair(prob, 2)
+    run_pair(prob, 2, THRESHOLDS[thr])
 
 
-def test_oblique_stacks_small():
+@SETS
+def test_oblique_stacks_small(thr):
     """c5's oblique stacks (30 deg about x, 45 deg about y) and dense 75% overlap."""
     prob = synth.make_problem("c5", scale=(64, 64, 12), size=16, stride=4)
-    run_pair(prob, 1)
+    run_pair(prob, 1, THRESHOLDS[thr])
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_backprojection_precision_modes(mode):
+    """PVR_PARAM_BP_EXACT = 2 (exact tiles everywhere) is held to the same bars; 0 (one word
+    everywhere, the timing reference) only at the round-1 thresholds, where no confidence
+    sits near tau_C."""
+    prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
+    params = dict(THRESHOLDS["survey" if mode == 2 else "round1"], bp_exact=mode)
+    if mode == 0:
+        orc = make_oracle(prob, params)
+        ctx = make_gpu(prob, params)
+        try:
+            orc.init_volume()
+            ctx.init_volume()
+            for _ in range(2):
+                orc.sr_iterate(1, prob["alpha"], prob["lam"])
+                ctx.sr_iterate(1, prob["alpha"], prob["lam"])
+            assert rel_l2(ctx.volume(), orc.volume()) <= 1e-4
+        finally:
+            ctx.close()
+    else:
+        run_pair(prob, 2, params)
 
 
 @pytest.mark.parametrize("cfg,kw,iters", [("c1", {}, 2),
@@ -167,24 +223,10 @@ def test_new_transforms_replan(deg, mm, device, split):
             assert after["replan_splits"] > before["replan_splits"]
         orc.init_volume()
         ctx.init_volume()
-        from scipy import ndimage
         for it in range(2):
             orc.sr_iterate(1, prob["alpha"], prob["lam"])
             ctx.sr_iterate(1, prob["alpha"], prob["lam"])
-            # sparse random patches leave voxels whose confidence C sits at tau_C = 1e-3: a
-            # float decision either side may take; compare outside them and their 26-neighbours
-            _, _, _, Co = orc.taps()
-            near = np.abs(Co.reshape(prob["dims"][::-1]) - 1e-3) <= 1e-6
-            keep = ~ndimage.binary_dilation(near, np.ones((3, 3, 3), bool))
-            if it == 0:
-                keep0 = keep
-            keep &= keep0
-            assert near.sum() < 1e-3 * near.size
-            assert rel_l2(ctx.volume()[keep], orc.volume()[keep]) <= 1e-4
-            po, pbo, wo = orc.weights()
-            pg, pbg, wg = ctx.weights()
-            dp, dw, _ = weight_mismatch(pg, po, pbg, pbo, wg, wo)
-            assert dp <= 1e-3 and dw <= 1e-3
+            check_iteration(ctx, orc, prob, None, it)
     finally:
         ctx.close()
 
@@ -198,9 +240,13 @@ def test_patch_mixture(cfg, kw, iters):
     run_pair(prob, iters, params={"patch_mixture": 1})
 
 
-def test_explicit_masked_patches():
+@SETS
+def test_explicit_masked_patches(thr):
     """f3 step 1 (reading Q32): explicit rectangles of assorted sizes with random per-pixel
-    masks (pvr_set_patches / pvro_set_patches); same parity bar, masked pixels unobserved."""
+    masks (pvr_set_patches / pvro_set_patches); same parity bar, masked pixels unobserved.
+    Random rectangles and a 30% random mask leave many cells of small confidence: every
+    member touches a patch border or a masked pixel, so all groups are exact."""
+    thr = THRESHOLDS[thr]
     from oracle import Oracle
     from paper_1611_07289_b200 import Context
     prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
@@ -219,6 +265,9 @@ def test_explicit_masked_patches():
     orc = Oracle(prob["dims"], prob["spacing"], prob["origin"])
     ctx = Context(prob["dims"], prob["spacing"], prob["origin"])
     try:
+        for k, v in thr.items():
+            orc.set_param(k, v)
+            ctx.set_param(k, v)
         for st in prob["stacks"]:
             orc.add_stack(st["slices"], st["G"], st["thickness"])
             ctx.add_stack(st["slices"], st["G"], st["thickness"])
@@ -229,36 +278,23 @@ def test_explicit_masked_patches():
         ctx.set_transforms(T)
         _, ko, _, _ = orc.taps()
         _, kg, _, _ = ctx.taps()
-        assert (kg[mask == 0] == 0).all() and np.abs(kg - ko).max() <= 2e-5
+        assert (kg[mask == 0] == 0).all() and np.abs(kg - ko).max() <= TOL["kappa"]
         orc.init_volume()
         ctx.init_volume()
-        from scipy import ndimage
         for it in range(2):
             orc.sr_iterate(1, prob["alpha"], prob["lam"])
             ctx.sr_iterate(1, prob["alpha"], prob["lam"])
-            # sparse random patches leave voxels whose confidence C sits at tau_C = 1e-3: a
-            # float decision either side may take; compare outside them and their 26-neighbours
-            _, _, _, Co = orc.taps()
-            near = np.abs(Co.reshape(prob["dims"][::-1]) - 1e-3) <= 1e-6
-            keep = ~ndimage.binary_dilation(near, np.ones((3, 3, 3), bool))
-            if it == 0:
-                keep0 = keep
-            keep &= keep0
-            assert near.sum() < 1e-3 * near.size
-            assert rel_l2(ctx.volume()[keep], orc.volume()[keep]) <= 1e-4
-            po, pbo, wo = orc.weights()
-            pg, pbg, wg = ctx.weights()
-            dp, dw, _ = weight_mismatch(pg, po, pbg, pbo, wg, wo)
-            assert dp <= 1e-3 and dw <= 1e-3
+            check_iteration(ctx, orc, prob, thr, it)
     finally:
         ctx.close()
 
 
-def test_odd_volume_dims_small_patches():
+@SETS
+def test_odd_volume_dims_small_patches(thr):
     """Edge shapes: a 37^3 volume (rows padded to 40 floats for the TMA pitch), 29x29 stacks
     of 5 slices, 8x8 patches at stride 4 (ragged last windows)."""
     prob = synth.make_problem("c3", scale=(37, 29, 5), size=8, stride=4)
-    run_pair(prob, 2)
+    run_pair(prob, 2, THRESHOLDS[thr])
 
 
 def test_delta_psf_mode():
@@ -268,11 +304,12 @@ def test_delta_psf_mode():
     run_pair(prob, 2, params={"psf_mode": 1})
 
 
-def test_patches_partly_outside_the_volume():
+@SETS
+def test_patches_partly_outside_the_volume(thr):
     """Transforms that move a quarter of the patches 14 mm out along x: their pixels are
     partly unobserved (kappa < tau_obs) or graze the grid border."""
     prob = synth.make_problem("c2", scale=(64, 64, 12))
     T = np.asarray(prob["T"], np.float64).reshape(-1, 3, 4).copy()
     T[::4, 0, 3] += 14.0
     prob["T"] = T
-    run_pair(prob, 2)
+    run_pair(prob, 2, THRESHOLDS[thr])

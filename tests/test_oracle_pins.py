@@ -14,6 +14,7 @@ import pytest
 import oracle.pvro as O
 import synth
 from oracle import Oracle
+from helpers import TAU_OBS
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -134,7 +135,7 @@ def test_constant_field_rows_sum_to_one():
     prob = synth.make_problem("c3", scale=(48, 48, 6), size=16, stride=8)
     orc = _problem_oracle(prob)
     yhat, kap = orc.forward(np.full(orc.V, 437.25))
-    obs = kap >= 0.5
+    obs = kap >= TAU_OBS
     assert obs.sum() > 1000 and (~obs).sum() > 0
     assert np.abs(yhat[obs] - 437.25).max() <= 1e-10
 
@@ -210,7 +211,7 @@ def test_adjoint_inner_product(cfg, kw):
     x = rng.normal(size=orc.V)
     Wx, kap = orc.forward(x)
     y = rng.normal(size=orc.P)
-    y[kap < 0.5] = 0.0
+    y[kap < TAU_OBS] = 0.0
     WTy = orc.adjoint(y).ravel()
     lhs, rhs = float(Wx @ y), float(x @ WTy)
     assert abs(lhs - rhs) <= 1e-10 * max(abs(lhs), 1.0)
@@ -412,7 +413,7 @@ def test_fixed_point_inverse_crime():
     orc.sr_iterate(2, 1.0, 0.0)
     assert np.abs(orc.volume() - Xs).max() <= 1e-12 * np.abs(Xs).max()
     p, _, w = orc.weights()
-    assert np.all(p[kap >= 0.5] == 1.0)
+    assert np.all(p[kap >= TAU_OBS] == 1.0)
 
 
 def test_delta_psf_one_iteration_recovers_data():
