@@ -93,6 +93,13 @@ enum {
                                  aborts the communicator (ncclCommAbort) and returns
                                  PVR_ERR_NCCL; NCCL asynchronous errors are polled while
                                  waiting [300]                                               */
+  ,PVR_PARAM_DETERMINISTIC = 19 /* (extract) 1: every reduction is order-independent, so X, p
+                                 and w are bit-identical from run to run and for any number of
+                                 ranks: the EM sums add terms rounded to fixed grids (exact in
+                                 fp64), the backprojection uses one global tile scale with
+                                 three int32 words per value (24 B per cell) and int64 (A, C)
+                                 accumulators. Slower (~1.5x the backprojection); the
+                                 two-Gaussian patch mixture (f4) is not covered [0]           */
   ,PVR_PARAM_BP_EXACT = 16    /* (extract) precision of the backprojection's shared tiles
                                  (DESIGN.md 7). 1 [default]: exact hi/lo int32 word pairs
                                  (~2^-41 of the group's largest splat term) for every group

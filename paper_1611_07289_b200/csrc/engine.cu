@@ -142,6 +142,8 @@ struct pvr_ctx {
   double delta = 150.0, tau_patch = 0.5, c0 = 0.9, tau_live = 0.99, tau_C = 1e-6, tau_obs = 0.01;
   int clamp = 1, psf_mode = 0, profile = 0;
   int bp_exact = kBpRim;  // backprojection tile precision (PVR_PARAM_BP_EXACT)
+  int det = 0;            // PVR_PARAM_DETERMINISTIC
+  unsigned long long* ACd = nullptr;  // deterministic mode: int64 (A, C) accumulators [4 Vp]
   bool explicit_patches = false;  // patches from pvr_set_patches / superpixels (not windows)
   double s2floor = 1e-6, nsigma = 3.0, quality = 1.0;
   // stacks / patches
@@ -391,6 +393,7 @@ Params make_params(const pvr_ctx* c) {
   p.c0 = (float)c->c0;
   p.delta = (float)c->delta;
   p.clamp = c->clamp;
+  p.det = c->det;
   return p;
 }
 
@@ -407,6 +410,8 @@ LatticeArgs lattice_args(const pvr_ctx* c, const pvr_ctx::Plan& pl) {
   a.ys = c->ys;
   a.mask = c->mask;
   a.prm = make_params(c);
+  a.det_scale = c->em ? c->em->det_scale : nullptr;
+  a.ACd = c->ACd;
   return a;
 }
 
@@ -543,7 +548,8 @@ void free_dev(pvr_ctx* c) {
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
-                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep, c->mask};
+                  c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep, c->mask,
+                  c->ACd};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -757,7 +763,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     g.interior = 1;
     for (int d = 0; d < 3; ++d)
       if (lo[d] < 0 || hi[d] > n3[d] - 1) g.interior = 0;
-    g.exact = !fwd && (kind == 2 || c->bp_exact == kBpAll || (c->bp_exact == kBpRim && (rim || !g.interior)));
+    g.exact = !fwd && (kind == 2 || c->det || c->bp_exact == kBpAll || (c->bp_exact == kBpRim && (rim || !g.interior)));
     if (fwd) {
       // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
       // (measured: a box starting at an x not a multiple of 4 floats faults with an illegal
@@ -780,7 +786,9 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     g.dim[2] = hi[2] - lo[2] + 1;
     return (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
   };
-  auto fits = [&](const GroupDev& g, int64_t vox) { return vox * (fwd ? 4 : g.exact ? 16 : 8) <= byte_budget; };
+  auto fits = [&](const GroupDev& g, int64_t vox) {
+    return vox * (fwd ? 4 : c->det ? 24 : g.exact ? 16 : 8) <= byte_budget;
+  };
   // Outlying members of a natural group: a member whose footprint centre lies more than a
   // quarter of the group's median footprint extent (and 4 voxels) from the median centre on
   // some axis (a patch
@@ -1307,7 +1315,7 @@ pvr_status pvr_comm_init_host(pvr_ctx* c, int nranks, int rank, pvr_host_collect
 pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
   GUARD(c);
   const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA || key == PVR_PARAM_PSF_QUALITY ||
-                           key == PVR_PARAM_BP_EXACT;
+                           key == PVR_PARAM_BP_EXACT || key == PVR_PARAM_DETERMINISTIC;
   if (extract_key && c->state >= PATCHED)
     return fail(c, PVR_ERR_STATE, "parameter %d must be set before extract_patches", key);
   switch (key) {
@@ -1335,6 +1343,7 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
       c->exchange = (int)v;
       break;
     case PVR_PARAM_COMM_TIMEOUT: if (!(v > 0)) goto bad; c->comm_timeout = v; break;
+    case PVR_PARAM_DETERMINISTIC: if (v != 0 && v != 1) goto bad; c->det = (int)v; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }
   return PVR_OK;
@@ -1849,11 +1858,45 @@ pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const Latt
   return PVR_OK;
 }
 
+// Backprojection into (A, C) and its exchange over ranks (init / rigidity: a sum-allreduce;
+// iterations: PVR_PARAM_EXCHANGE). Deterministic mode: the global maxima of the inputs
+// (atomicMax per rank, max-allreduce) fix one tile scale for every group, the tiles add into
+// int64 accumulators (sum-allreduced exactly), and (A, C) is formed from them.
+pvr_status backproject_reduce(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const float* w, int init,
+                              bool iteration) {
+  const LatticeArgs lb0 = lattice_args(c, pl);
+  if (!c->det) {
+    CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
+    pvr_status r = backproject(c, s, pl, lb0, w, init);
+    if (r != PVR_OK) return r;
+    return iteration ? exchange_ac(c) : allreduce_ac(c);
+  }
+  if (!c->ACd) CUDA_TRY(c, cudaMalloc(&c->ACd, (size_t)(c->Vp + 2) * 4 * sizeof(unsigned long long)));
+  const LatticeArgs lb = lattice_args(c, pl);
+  CUDA_TRY(c, cudaMemsetAsync(c->em->det_max, 0, sizeof(c->em->det_max), s));
+  launch_bp_maxima(s, c->pdev, c->nloc, lb.prm, c->kap, c->e, c->p, w, c->ys, init, c->em);
+  CHECK_LAUNCH(c);
+  pvr_status r = coll(c, c->em->det_max, 2, PVR_DT_F32, PVR_COLL_ALLREDUCE_MAX);
+  if (r != PVR_OK) return r;
+  launch_det_scales(s, c->em);
+  CUDA_TRY(c, cudaMemsetAsync(c->ACd, 0, (size_t)(c->Vp + 2) * 4 * sizeof(unsigned long long), s));
+  r = backproject(c, s, pl, lb, w, init);
+  if (r != PVR_OK) return r;
+  if (!(iteration && c->exchange == PVR_EXCHANGE_AVERAGE)) {
+    r = coll(c, c->ACd, c->Vp * 4, PVR_DT_I64, PVR_COLL_ALLREDUCE_SUM);
+    if (r != PVR_OK) return r;
+  }
+  launch_det_to_float(s, c->ACd, c->Vp, c->em, c->AC);
+  CHECK_LAUNCH(c);
+  c->st.kernel_launches += 3;
+  return PVR_OK;
+}
+
 // The plan of the one-off exact passes (init, rigidity): the iteration's own plan when all its
 // groups are exact (PVR_PARAM_BP_EXACT = 2), else the lazily built all-exact init plan (its
 // groups fit the 16 B per cell budget).
 static pvr_status exact_plan(pvr_ctx* c, pvr_ctx::Plan** pl) {
-  if (c->bp_exact == kBpAll) {
+  if (c->bp_exact == kBpAll || c->det) {
     *pl = &c->bplan;
     return PVR_OK;
   }
@@ -1873,10 +1916,7 @@ pvr_status pvr_init_volume(pvr_ctx* c) {
   pvr_status rp = exact_plan(c, &pl);
   if (rp != PVR_OK) return rp;
   const LatticeArgs lb = lattice_args(c, *pl);
-  CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
-  pvr_status rb = backproject(c, c->stream, *pl, lb, c->w, 1);
-  if (rb != PVR_OK) return rb;
-  pvr_status r = allreduce_ac(c);
+  pvr_status r = backproject_reduce(c, c->stream, *pl, c->w, 1, false);
   if (r != PVR_OK) return r;
   launch_init_fill(c->stream, c->AC, c->dims, c->nxp, lb.prm, c->X[c->cur]);
   CHECK_LAUNCH(c);
@@ -1891,12 +1931,8 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
   pvr_ctx::Plan* pl = nullptr;
   pvr_status rp = exact_plan(c, &pl);
   if (rp != PVR_OK) return rp;
-  const LatticeArgs lb = lattice_args(c, *pl);
-  CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), c->stream));
   // W^T (p pbar) and W^T 1 with exact hi/lo tiles (pbar rides in w)
-  pvr_status rb = backproject(c, c->stream, *pl, lb, c->pbar, 2);
-  if (rb != PVR_OK) return rb;
-  pvr_status r = allreduce_ac(c);
+  pvr_status r = backproject_reduce(c, c->stream, *pl, c->pbar, 2, false);
   if (r != PVR_OK) return r;
   float* tmp = c->X[1 - c->cur];  // scratch between iterations
   launch_ratio(c->stream, c->AC, c->dims, c->nxp, (float)c->tau_C, tmp);
@@ -1923,12 +1959,12 @@ static pvr_status replan_on_device(pvr_ctx* c) {
   // host plan); backprojection: the hard tile budget (the host planned to 90% of it)
   launch_replan(c->stream, c->fplan.mem, c->fplan.grp, c->fplan.ngroups, (int)c->fplan.grp_cap, c->pdev, c->psf,
                 1, c->dims, kFwdTileBytes / 4 * 3 / 2, c->fbox_dev, nshape, c->replan_buf, c->replan_buf + 1,
-                nullptr, c->bp_exact);
+                nullptr, c->det ? kBpDet : c->bp_exact);
   // backprojection groups that outgrow the tile are split into single-member groups appended
   // after the plan's (their Morton locality is lost until the next host plan)
   launch_replan(c->stream, c->bplan.mem, c->bplan.grp, c->bplan.ngroups, (int)c->bplan.grp_cap, c->pdev, c->psf,
                 0, c->dims, kBpTileBytes, nullptr, 0, c->replan_buf + 2, c->replan_buf + 3, c->replan_buf + 4,
-                c->bp_exact);
+                c->det ? kBpDet : c->bp_exact);
   CHECK_LAUNCH(c);
   int h[5];
   CUDA_TRY(c, cudaMemcpyAsync(h, c->replan_buf, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -2188,12 +2224,9 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
       c->st.kernel_launches += 3 + 2 * kMixRounds;
     }
     if (prof) cudaEventRecord((*ev)[EV_EST1], s);
-    CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
-    r = backproject(c, s, c->bplan, lb, c->w, 0);
+    r = backproject_reduce(c, s, c->bplan, c->w, 0, true);
     if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_BP1], s);
-    r = exchange_ac(c);
-    if (r != PVR_OK) return r;
     if (prof) cudaEventRecord((*ev)[EV_AR1], s);
     const bool slabs = c->nranks > 1 && c->exchange == PVR_EXCHANGE_SLABS;
     launch_update(s, X0, c->AC, c->dims, c->nxp, prm, c->em, alpha, lambda, X2, slabs ? c->z0 : 0,

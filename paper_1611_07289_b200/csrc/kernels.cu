@@ -118,7 +118,37 @@ __global__ void k_em_round(Params prm, EmDev* em, int round, double tol) {
 
 // --------------------------------------------------------------------------------------
 // a4: p_j (observed pixels; 0 elsewhere), pbar_s = sqrt(sum_live p^2 / N_live),
-// w_s = pbar_s if pbar_s >= tau_patch else 0 (reading Q13). One CTA per patch.
+// w_s = pbar_s if pbar_s >= tau_patch else 0 (reading Q13). One CTA per patch; pixels read as
+// float4 where the patch's pixel range is 16-byte aligned (every window of extract_patches with
+// a width divisible by 4). ROUNDS (f4 multi-round EM, reading Q30) also forms the next M-step's
+// partials {sum p e^2, sum p, LL}; the single-round default skips them and the log-likelihood's
+// two transcendentals per pixel.
+template <bool ROUNDS>
+__device__ __forceinline__ void estep_pixel(float k, float ev, const Params& prm, int mode, float logk,
+                                            float inv2s2, float lnbm, float& pv, double (&s)[5]) {
+  float ll = 0.0f;
+  pv = 0.0f;
+  if (k >= prm.tau_obs) {
+    if (mode == 1) {
+      pv = 1.0f;
+    } else if (mode == 0) {
+      const float z = logk + ev * ev * inv2s2;
+      pv = 1.0f / (1.0f + expf(z));
+      if (ROUNDS) ll = lnbm + log1pf(expf(-z));  // ln(c G + (1 - c) m) = ln((1-c) m) + ln(1 + e^-z)
+    }
+  }
+  if (k >= prm.tau_live) {
+    s[0] += (double)pv * (double)pv;
+    s[1] += 1.0;
+    if (ROUNDS) {
+      s[2] += (double)pv * (double)ev * (double)ev;
+      s[3] += (double)pv;
+      s[4] += (double)ll;
+    }
+  }
+}
+
+template <bool ROUNDS>
 __global__ void __launch_bounds__(256) k_estep(const PatchDev* __restrict__ P, Params prm,
                                                EmDev* __restrict__ em,
                                                const float* __restrict__ kap,
@@ -134,28 +164,28 @@ __global__ void __launch_bounds__(256) k_estep(const PatchDev* __restrict__ P, P
   // live-pixel sums: {sum p^2, N} for pbar, and {sum p e^2, sum p, LL} for the next M-step
   double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   float mx[1] = {0.0f};
-  for (int q = threadIdx.x; q < npix; q += blockDim.x) {
-    const int64_t j = pt.pix0 + q;
-    const float k = kap[j];
-    float pv = 0.0f, ll = 0.0f;
-    const float ev = e[j];
-    if (k >= prm.tau_obs) {
-      if (mode == 1) {
-        pv = 1.0f;
-      } else if (mode == 0) {
-        const float z = logk + ev * ev * inv2s2;
-        pv = 1.0f / (1.0f + expf(z));
-        ll = lnbm + log1pf(expf(-z));  // ln(c G + (1 - c) m) = ln((1-c) m) + ln(1 + e^-z)
-      }
+  const int64_t j0 = pt.pix0;
+  int q0 = 0;
+  if ((j0 & 3) == 0) {  // aligned: float4 loads and stores over the multiple-of-4 body
+    const int n4 = npix >> 2;
+    const float4* k4 = reinterpret_cast<const float4*>(kap + j0);
+    const float4* e4 = reinterpret_cast<const float4*>(e + j0);
+    float4* p4 = reinterpret_cast<float4*>(p + j0);
+    for (int q = threadIdx.x; q < n4; q += blockDim.x) {
+      const float4 kk = __ldg(k4 + q), ee = __ldg(e4 + q);
+      float4 pp;
+      estep_pixel<ROUNDS>(kk.x, ee.x, prm, mode, logk, inv2s2, lnbm, pp.x, s);
+      estep_pixel<ROUNDS>(kk.y, ee.y, prm, mode, logk, inv2s2, lnbm, pp.y, s);
+      estep_pixel<ROUNDS>(kk.z, ee.z, prm, mode, logk, inv2s2, lnbm, pp.z, s);
+      estep_pixel<ROUNDS>(kk.w, ee.w, prm, mode, logk, inv2s2, lnbm, pp.w, s);
+      p4[q] = pp;
     }
-    p[j] = pv;
-    if (k >= prm.tau_live) {
-      s[0] += (double)pv * (double)pv;
-      s[1] += 1.0;
-      s[2] += (double)pv * (double)ev * (double)ev;
-      s[3] += (double)pv;
-      s[4] += (double)ll;
-    }
+    q0 = n4 << 2;
+  }
+  for (int q = q0 + threadIdx.x; q < npix; q += blockDim.x) {
+    float pv;
+    estep_pixel<ROUNDS>(kap[j0 + q], e[j0 + q], prm, mode, logk, inv2s2, lnbm, pv, s);
+    p[j0 + q] = pv;
   }
   __shared__ double res[6];
   block_reduce_store<5, 1>(s, mx, res);
@@ -165,9 +195,12 @@ __global__ void __launch_bounds__(256) k_estep(const PatchDev* __restrict__ P, P
     w[blockIdx.x] = pb >= prm.tau_patch ? pb : 0.0f;
     if (nlive) nlive[blockIdx.x] = (int32_t)res[1];
     if (rpart) {
-      rpart[3 * blockIdx.x] = res[2];
-      rpart[3 * blockIdx.x + 1] = res[3];
-      rpart[3 * blockIdx.x + 2] = res[4];
+      // deterministic mode: each patch's sums on fixed grids (2^-4, 2^-24, 2^-10), so the sums
+      // over patches are exact in fp64 and independent of their order and of the sharding
+      const bool d = prm.det;
+      rpart[3 * blockIdx.x] = d ? rint(res[2] * 16.0) / 16.0 : res[2];
+      rpart[3 * blockIdx.x + 1] = d ? rint(res[3] * 16777216.0) / 16777216.0 : res[3];
+      rpart[3 * blockIdx.x + 2] = d ? rint(res[4] * 1024.0) / 1024.0 : res[4];
     }
   }
 }
@@ -535,8 +568,8 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
   G.interior = replan_interior(lo, hi, n);
   // backprojection tile precision (engine.cu: size_groups): exact for rim members and
   // footprints that leave the grid; the byte budget then buys half the cells
-  G.exact = !fwd && (bp_mode == kBpAll || (bp_mode == kBpRim && (rim || !G.interior)));
-  const int64_t cell_bytes = G.exact ? 16 : 8;
+  G.exact = !fwd && (bp_mode >= kBpAll || (bp_mode == kBpRim && (rim || !G.interior)));
+  const int64_t cell_bytes = bp_mode == kBpDet ? 24 : G.exact ? 16 : 8;
   int64_t vox;
   if (fwd) {
     lo[0] -= ((lo[0] % 4) + 4) % 4;
@@ -569,10 +602,10 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
         S.nm = 1;
         S.tmap = 0;
         S.interior = replan_interior(ml, mh, n);
-        S.exact = bp_mode == kBpAll || (bp_mode == kBpRim && ((m.flags & kMemberRim) || !S.interior));
+        S.exact = bp_mode >= kBpAll || (bp_mode == kBpRim && ((m.flags & kMemberRim) || !S.interior));
         const int64_t sv = replan_bp_box(ml, mh, S);
         const int k = atomicAdd(nappend, 1);
-        if (sv * (S.exact ? 16 : 8) > vox_budget || ngroups + k >= cap) {
+        if (sv * (bp_mode == kBpDet ? 24 : S.exact ? 16 : 8) > vox_budget || ngroups + k >= cap) {
           atomicExch(fail, 1);
           continue;
         }
@@ -587,6 +620,58 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
   if ((fwd ? vox : vox * cell_bytes) > vox_budget) atomicExch(fail, 1);
   atomicMax(maxvox, (int)(vox < (1 << 30) ? vox : (1 << 30)));
   grp[g] = G;
+}
+
+// ---- deterministic mode (PVR_PARAM_DETERMINISTIC) -----------------------------------------
+// Per patch: the maxima over its observed pixels of |rA| and rC (the backprojection's per-pixel
+// inputs, the same formulas as k_lattice_bp's phase A), into em->det_max by atomicMax on the
+// (non-negative) float bits: order-independent.
+__global__ void k_bp_maxima(const PatchDev* __restrict__ P, Params prm, const float* __restrict__ kap,
+                            const float* __restrict__ e, const float* __restrict__ p,
+                            const float* __restrict__ w, const float* __restrict__ ys, int init,
+                            EmDev* __restrict__ em) {
+  const PatchDev& pt = P[blockIdx.x];
+  const float ws = init == 1 ? 1.0f : (init == 2 ? 1.0f : w[blockIdx.x]);
+  const float vs = init == 2 ? w[blockIdx.x] : 1.0f;
+  if (ws == 0.0f) return;
+  float mA = 0.0f, mC = 0.0f;
+  const int npix = pt.sx * pt.sy * pt.sz;
+  for (int q = threadIdx.x; q < npix; q += blockDim.x) {
+    const int64_t j = pt.pix0 + q;
+    const float k = kap[j];
+    if (!(k >= prm.tau_obs)) continue;
+    const int u = q % pt.sx, v = (q / pt.sx) % pt.sy, z = q / (pt.sx * pt.sy);
+    const float pv = init ? 1.0f : p[j];
+    const float val = init == 1 ? ys[pt.y0off + (int64_t)z * pt.HW + (int64_t)v * pt.W + u]
+                                : init == 2 ? p[j] * vs : e[j];
+    const float rC = ws * pv / k;
+    mA = fmaxf(mA, fabsf(rC * val));
+    mC = fmaxf(mC, rC);
+  }
+  mA = warp_max(mA);
+  mC = warp_max(mC);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(reinterpret_cast<int*>(&em->det_max[0]), __float_as_int(mA));
+    atomicMax(reinterpret_cast<int*>(&em->det_max[1]), __float_as_int(mC));
+  }
+}
+
+// The global scales: the largest splat term maps to kDetTermMax units (tp <= 1).
+__global__ void k_det_scales(EmDev* em) {
+  if (threadIdx.x != 0) return;
+  for (int q = 0; q < 2; ++q) em->det_scale[q] = em->det_max[q] > 0.0f ? kDetTermMax / (double)em->det_max[q] : 0.0;
+}
+
+// (A, C) = int64 totals / scale: {A hi, A lo 2^20 + lo2, C hi, C lo 2^20 + lo2} per voxel.
+__global__ void k_det_to_float(const unsigned long long* __restrict__ ACd, int64_t Vp, const EmDev* __restrict__ em,
+                               float2* __restrict__ AC) {
+  const double iA = em->det_scale[0] > 0.0 ? 1.0 / em->det_scale[0] : 0.0;
+  const double iC = em->det_scale[1] > 0.0 ? 1.0 / em->det_scale[1] : 0.0;
+  const double l2 = 1.0 / (1048576.0 * 1048576.0);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < Vp; k += (int64_t)gridDim.x * blockDim.x) {
+    const long long* v = reinterpret_cast<const long long*>(ACd + 4 * k);
+    AC[k] = make_float2((float)(((double)v[0] + (double)v[1] * l2) * iA), (float)(((double)v[2] + (double)v[3] * l2) * iC));
+  }
 }
 
 // One quantity of the interleaved, row-padded (A, C) volume into a contiguous [nz][ny][nx]
@@ -612,6 +697,17 @@ __global__ void k_fill(float* __restrict__ x, int64_t n, float v) {
 
 // --------------------------------------------------------------------------------------
 // launchers
+
+void launch_bp_maxima(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, const float* kap,
+                      const float* e, const float* p, const float* w, const float* ys, int init, EmDev* em) {
+  if (npatch > 0) k_bp_maxima<<<(unsigned)npatch, 256, 0, st>>>(P, prm, kap, e, p, w, ys, init, em);
+}
+
+void launch_det_scales(cudaStream_t st, EmDev* em) { k_det_scales<<<1, 32, 0, st>>>(em); }
+
+void launch_det_to_float(cudaStream_t st, const unsigned long long* ACd, int64_t Vp, const EmDev* em, float2* AC) {
+  k_det_to_float<<<148 * 8, 256, 0, st>>>(ACd, Vp, em, AC);
+}
 
 void launch_unpack_ac(cudaStream_t st, const float2* AC, int3 dims, int nxp, int which, float* out) {
   k_unpack_ac<<<148 * 8, 256, 0, st>>>(AC, dims, nxp, which, out);
@@ -641,7 +737,10 @@ void launch_estep(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm
                   const float* kap, const float* e, float* p, float* pbar, float* w, int round,
                   double* rpart, int32_t* nlive) {
   if (npatch <= 0) return;
-  k_estep<<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w, round, rpart, nlive);
+  if (rpart)
+    k_estep<true><<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w, round, rpart, nlive);
+  else
+    k_estep<false><<<(unsigned)npatch, 256, 0, st>>>(P, prm, em, kap, e, p, pbar, w, round, rpart, nlive);
 }
 
 void launch_em_reduce3(cudaStream_t st, const double* rpart, int64_t npatch, EmDev* em) {

@@ -357,8 +357,15 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
           ev = y - s / kk;
           if (kk >= a.prm.tau_live) {
             const double pp = pprev[j];
-            acc_s[0] += pp * (double)ev * (double)ev;
-            acc_s[1] += pp;
+            if (a.prm.det) {
+              // deterministic mode: every term on a fixed grid (2^-4, 2^-24): the fp64 sums of
+              // these integers (< 2^53) are exact in any order, on any number of ranks
+              acc_s[0] += rint(pp * (double)ev * (double)ev * 16.0) * 0.0625;
+              acc_s[1] += rint(pp * 16777216.0) * (1.0 / 16777216.0);
+            } else {
+              acc_s[0] += pp * (double)ev * (double)ev;
+              acc_s[1] += pp;
+            }
             acc_s[2] += 1.0;
             acc_m[0] = fmaxf(acc_m[0], ev);
             acc_m[1] = fmaxf(acc_m[1], -ev);
@@ -452,11 +459,16 @@ constexpr int kCOff = kBpTileBytes / 2;  // single-word tile: byte offset of the
 constexpr int kHQ = kBpTileBytes / 4;
 
 // Flush one plane of the window: corner j's weight sum S_j times the line's (LA, LC) into the
-// A and C words of the 4 transverse corners (a, +sp4, +sq4, +sp4+sq4).
-template <bool HILO>
+// A and C words of the 4 transverse corners (a, +sp4, +sq4, +sp4+sq4). PREC: kPrecSingle one
+// word per quantity (A at 0, C at kCOff), kPrecHiLo two (planes kHQ apart), kPrecDet three
+// (planes kH6 apart: deterministic mode's global scale).
+constexpr int kPrecSingle = 0, kPrecHiLo = 1, kPrecDet = 2;
+constexpr int kH6 = kBpTileBytes / 6;  // deterministic tile: A_hi, C_hi, A_lo, C_lo, A_lo2, C_lo2
+static_assert(kH6 % 16 == 0, "tile planes must stay 16-byte aligned");
+template <int PREC>
 __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, float s1, float s2, float s3,
                                        f2 L, f2 mag, f2 lsc) {
-  if (!HILO) {
+  if (PREC == kPrecSingle) {
     // L S + magic: the fixed-point rounding of each window sum (one FFMA2 per corner)
     const f2 t0 = fma2s(s0, L, mag), t1 = fma2s(s1, L, mag), t2 = fma2s(s2, L, mag), t3 = fma2s(s3, L, mag);
     sred<0>(a, __float_as_int(lo2(t0)) - kMagicBits);
@@ -468,22 +480,29 @@ __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, f
     sred<0>(a + sp4 + sq4, __float_as_int(lo2(t3)) - kMagicBits);
     sred<kCOff>(a + sp4 + sq4, __float_as_int(hi2(t3)) - kMagicBits);
   } else {
-    // exact hi / lo words of S L (A and C as a packed pair): t = S L + magic rounds to the hi
-    // integer h = t - magic (exact); the FMA S L - h is the exact remainder r, |r| <= 1/2, and
+    // hi / lo words of S L (A and C as a packed pair): t = S L + magic rounds to the hi
+    // integer h = t - magic (exact); the FMA S L - h is the remainder r, |r| <= 1/2, and
     // lo = round(r lsc), lsc = 2^20 (k_bp_table). hi + lo / lsc equals S L to 1 / (2 lsc) hi
     // units: the word pair resolves ~2^-41 of the group's largest splat term, whatever the
-    // cell's own total.
+    // cell's own total. Deterministic mode adds lo2 = round((r lsc - lo) lsc): ~2^-61 of the
+    // global scale's largest term, for one scale shared by every group (grouping-independent).
     const unsigned ac[4] = {a, a + sp4, a + sq4, a + sp4 + sq4};
     const float sj[4] = {s0, s1, s2, s3};
+    constexpr int Q = PREC == kPrecDet ? kH6 : kHQ;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const f2 t = fma2s(sj[j], L, mag);
       const f2 r = fma2s(sj[j], L, sub2(mag, t));
       const f2 l = fma2(r, lsc, mag);
       sred<0>(ac[j], __float_as_int(lo2(t)) - kMagicBits);
-      sred<kHQ>(ac[j], __float_as_int(hi2(t)) - kMagicBits);
-      sred<2 * kHQ>(ac[j], __float_as_int(lo2(l)) - kMagicBits);
-      sred<3 * kHQ>(ac[j], __float_as_int(hi2(l)) - kMagicBits);
+      sred<Q>(ac[j], __float_as_int(hi2(t)) - kMagicBits);
+      sred<2 * Q>(ac[j], __float_as_int(lo2(l)) - kMagicBits);
+      sred<3 * Q>(ac[j], __float_as_int(hi2(l)) - kMagicBits);
+      if (PREC == kPrecDet) {
+        const f2 l2 = fma2(fma2(r, lsc, sub2(mag, l)), lsc, mag);
+        sred<4 * Q>(ac[j], __float_as_int(lo2(l2)) - kMagicBits);
+        sred<5 * Q>(ac[j], __float_as_int(hi2(l2)) - kMagicBits);
+      }
     }
   }
 }
@@ -501,7 +520,7 @@ __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, f
 // each (group scale, k_lattice_bp). Tile: A words at shared address tA, C words at
 // tA + kCOff; HILO (exact groups): every window sum split into exact hi / lo words
 // (A_hi, C_hi, A_lo, C_lo planes, kHQ apart).
-template <bool HILO>
+template <int PREC>
 __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const BpMember& M, float rm0,
                                                float rp, float rq, float LA, float LC, float lo_scale,
                                                int ph) {
@@ -542,9 +561,9 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
       const bool keep = same & (im == wm);
       const bool adv = same & (im == wm + 1);
       const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-      flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);  // plane wm
+      flush4<PREC>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);  // plane wm
       if (!keep && !adv)  // restart (transverse change, the wrap, a jump): plane wm + 1 too
-        flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
+        flush4<PREC>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
       // shift: keep -> (0, m+1); advance -> (m+1, 0); restart -> (0, 0)
       const f2 sh = pk(adv ? 1.0f : 0.0f, keep ? 1.0f : 0.0f);
 #pragma unroll
@@ -574,8 +593,8 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
     }
   }
   const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
-  flush4<HILO>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);
-  flush4<HILO>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
+  flush4<PREC>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);
+  flush4<PREC>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
 }
 
 // Member tables of all groups of a backprojection plan (geometry only: rebuilt after every
@@ -747,9 +766,12 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
 #endif
     const GroupDev G = a.grp[g];
     const BpGroupHdr H = th[g];
-    const bool ex = init || G.exact;  // CTA-uniform: this group's tile precision
-    const int NW = ex ? 4 : 2;
-    int* cbase = ex ? base + kHQ / 4 : base + kCOff / 4;
+    // CTA-uniform: this group's tile precision (deterministic mode: three words everywhere)
+    const int prec = a.prm.det ? kPrecDet : (init || G.exact) ? kPrecHiLo : kPrecSingle;
+    const bool ex = prec != kPrecSingle;
+    const int NW = prec == kPrecDet ? 6 : ex ? 4 : 2;
+    const int QW = prec == kPrecDet ? kH6 / 4 : kHQ / 4;  // words between the exact planes
+    int* cbase = ex ? base + QW : base + kCOff / 4;
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
     __syncthreads();  // previous group's flush is done with the tile / R / tables / sbm
@@ -764,9 +786,9 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
       const int4 z4 = make_int4(0, 0, 0, 0);
       const int nv4 = (nvox + 3) >> 2;  // tile_words is a multiple of 4
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 6; ++q) {
         if (q >= NW) break;
-        int4* t4 = reinterpret_cast<int4*>(ex ? base + q * (kHQ / 4) : (q == 1 ? cbase : base));
+        int4* t4 = reinterpret_cast<int4*>(ex ? base + q * QW : (q == 1 ? cbase : base));
         for (int i = threadIdx.x; i < nv4; i += kThreads) t4[i] = z4;
       }
     }
@@ -818,10 +840,14 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     }
     // every splat term |L tp w| <= max|r| tpmax  ->  <= H.tmax units; a register window
     // plane sums at most nterm such terms before rounding (<= 2^22; k_bp_table)
-    const float scA = xA > 0.0f ? H.tmax / (xA * H.tpmax) : 0.0f;
-    const float scC = xC > 0.0f ? H.tmax / (xC * H.tpmax) : 0.0f;
+    float scA = xA > 0.0f ? H.tmax / (xA * H.tpmax) : 0.0f;
+    float scC = xC > 0.0f ? H.tmax / (xC * H.tpmax) : 0.0f;
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
-    const Tile T{base, cbase, base + 2 * (kHQ / 4), base + 3 * (kHQ / 4), dx, dy};
+    if (prec == kPrecDet) {  // one scale for every group (k_det_scales), grouping-independent
+      scA = xA > 0.0f ? (float)a.det_scale[0] : 0.0f;
+      scC = xC > 0.0f ? (float)a.det_scale[1] : 0.0f;
+    }
+    const Tile T{base, cbase, base + 2 * QW, base + 3 * QW, dx, dy};
 
     // ---- phase B: splat every owned lattice line of every member, one flattened range
     // (one tail per group); consecutive lanes take consecutive U lines of a member
@@ -878,10 +904,12 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
         const float rp = M.r[1] + fU * M.du[1] + fV * M.dv[1];
         const float rq = M.r[2] + fU * M.du[2] + fV * M.dv[2];
         const int ph = PVR_BP_PHASES > 1 ? ((lane & (PVR_BP_PHASES - 1)) * M.ns) / PVR_BP_PHASES : 0;
-        if (ex)
-          splat_line_win<true>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
+        if (prec == kPrecHiLo)
+          splat_line_win<kPrecHiLo>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
+        else if (prec == kPrecSingle)
+          splat_line_win<kPrecSingle>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
         else
-          splat_line_win<false>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
+          splat_line_win<kPrecDet>(tA, tpA, M, rm, rp, rq, LA, LC, kLoScale, ph);
       }
     }
     __syncthreads();
@@ -904,6 +932,23 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
         continue;
       const int k = row * dx + 2 * pl;
       const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
+      if (prec == kPrecDet) {
+        // deterministic mode: exact int64 totals per voxel and quantity, hi and (lo 2^20 + lo2)
+        // parts at the global scale, accumulated by integer reductions (order-independent)
+        for (int h = 0; h < (two ? 2 : 1); ++h) {
+          const int kk = k + h;
+          long long v[4];
+          for (int qn = 0; qn < 2; ++qn) {
+            v[2 * qn] = base[qn * QW + kk];
+            v[2 * qn + 1] = (long long)base[(2 + qn) * QW + kk] * 1048576LL + base[(4 + qn) * QW + kk];
+          }
+          if ((v[0] | v[1] | v[2] | v[3]) == 0) continue;
+          unsigned long long* d = a.ACd + 4 * (size_t)(gbase + (zl * n.y + yl) * a.nxp + 2 * pl + h);
+          for (int qn = 0; qn < 4; ++qn)
+            if (v[qn]) atomicAdd(d + qn, (unsigned long long)v[qn]);
+        }
+        continue;
+      }
       const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
       int al0 = 0, al1 = 0, cl0 = 0, cl1 = 0;
       if (ex) {

@@ -87,12 +87,17 @@ struct EmDev {
   double mix_mu[2], mix_v[2], mix_pi, mix_ll_prev;  // [0] inliers, [1] outliers
   double mix_stats[7];         // reduced round sums (see kernels.cu k_mix_round)
   int32_t mix_done, mix_degenerate;
+  // deterministic mode: global maxima of the backprojection inputs |rA|, rC (float bits,
+  // atomicMax over the ranks' patches) and the global tile scales formed from them
+  float det_max[2];
+  double det_scale[2];
 };
 
 struct Params {
   float tau_live, tau_obs, tau_C, tau_patch;
   float c0, delta;
   int clamp;
+  int det;  // PVR_PARAM_DETERMINISTIC: order-independent (integer) reductions everywhere
 };
 
 // Everything a lattice kernel needs about the problem (passed by value).
@@ -108,6 +113,10 @@ struct LatticeArgs {
   const float* ys;         // concatenated stacks
   const uint8_t* mask;     // f3: per-pixel patch mask (local shard; NULL = all pixels)
   Params prm;
+  // deterministic mode: the global tile scales (A, C) and the int64 accumulators, per voxel
+  // {A hi, A lo 2^20 + lo2, C hi, C lo 2^20 + lo2} (k_det_to_float forms A, C)
+  const double* det_scale;
+  unsigned long long* ACd;
 };
 
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
@@ -121,7 +130,7 @@ constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics 
 constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;
 // Backprojection tile precision (PVR_PARAM_BP_EXACT): 0 one word everywhere (a timing
 // reference), 1 exact hi/lo words for rim groups only (default), 2 exact everywhere.
-enum { kBpSingle = 0, kBpRim = 1, kBpAll = 2 };
+enum { kBpSingle = 0, kBpRim = 1, kBpAll = 2, kBpDet = 3 /* deterministic mode: three words, 24 B */ };
 constexpr int kBpCtasPerSm = PVR_BP_TILE_KB <= 56 ? 3 : 2;
 #ifndef PVR_R_KB
 #define PVR_R_KB 12
@@ -200,6 +209,15 @@ void launch_update(cudaStream_t st, const float* X0, const float2* AC, const int
                    Params prm, const EmDev* em, float alpha, float lambda, float* X2, int zlo, int zhi);
 void launch_unpack_ac(cudaStream_t st, const float2* AC, int3 dims, int nxp, int which, float* out);
 void launch_scale(cudaStream_t st, float* x, int64_t n, float f);
+// deterministic mode: per-patch maxima of the backprojection inputs into em->det_max (init:
+// 0 iteration, 1 init, 2 rigidity, as launch_backproject), the global scales from them, and the
+// int64 accumulators into the float (A, C) volume
+void launch_bp_maxima(cudaStream_t st, const PatchDev* P, int64_t npatch, Params prm, const float* kap,
+                      const float* e, const float* p, const float* w, const float* ys, int init, EmDev* em);
+void launch_det_scales(cudaStream_t st, EmDev* em);
+void launch_det_to_float(cudaStream_t st, const unsigned long long* ACd, int64_t Vp, const EmDev* em, float2* AC);
+constexpr float kDetTermMax = 16384.0f;  // 2^14: deterministic mode's largest splat term (window
+                                         // sums < 2^22 for lines of up to 255 samples)
 void launch_ratio(cudaStream_t st, const float2* AC, const int3 dims, int nxp, float tau_C, float* out);
 constexpr int kMaxBoxShapes = 4096;  // forward TMA box shapes the device re-plan may pick from
 // nappend (backprojection): counter of single-member groups appended after ngroups (< cap)

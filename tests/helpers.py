@@ -44,7 +44,7 @@ def make_oracle(prob, params=None):
     from oracle import Oracle
     orc = Oracle(prob["dims"], prob["spacing"], prob["origin"])
     for k, v in (params or {}).items():
-        if k not in ("profile", "bp_exact"):   # product-only parameters
+        if k not in ("profile", "bp_exact", "deterministic", "exchange", "comm_timeout"):  # product-only
             orc.set_param(k, v)
     for st in prob["stacks"]:
         orc.add_stack(st["slices"], st["G"], st["thickness"])

@@ -180,9 +180,10 @@ def roi_check(prob, roi_lo, roi_size, params=None):
     dX = np.abs(X1[box][sl] - X2[sl])
     ok = ~near[sl]
     assert (dX[ok] <= dX2[sl][ok] + 1e-5 * np.abs(X2[sl][ok]) + 1e-4).all(), "X beyond its fp32 bound"
-    # the rim: cells whose C is a grazing sum, below 10% of their neighbourhood's mean C (and
-    # their 26-neighbours), where the bound is large relative to X
-    grazing = ndimage.binary_dilation(Co[box] < 0.1 * envC / 27.0, np.ones((3, 3, 3), bool))
+    # the rim: cells whose C is a grazing sum -- below 10% of their neighbourhood's mean C, or
+    # below 1e-2 (1% of one observation's weight) -- and their 26-neighbours, where the fp32
+    # geometry error of the small trilinear weights dominates
+    grazing = ndimage.binary_dilation((Co[box] < 0.1 * envC / 27.0) | (Co[box] < 1e-2), np.ones((3, 3, 3), bool))
     resolved = ok & ~grazing[sl]
     rx = rel_l2(X1[box][sl][resolved], X2[sl][resolved])
     rim = int((ok & ~resolved).sum())

@@ -25,7 +25,7 @@ def _problem():
     return synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
 
 
-def _run(nranks, rank, exchange, port, out):
+def _run(nranks, rank, exchange, port, out, det=0):
     import torch
     import torch.distributed as dist
 
@@ -48,6 +48,7 @@ def _run(nranks, rank, exchange, port, out):
     ctx = Context(prob["dims"], prob["spacing"], prob["origin"], 0)
     try:
         ctx.set_param("exchange", pvr.EXCHANGE[exchange])
+        ctx.set_param("deterministic", det)
         if nranks > 1:
             ctx.comm_init_host(nranks, rank, collective)
         load_problem(ctx, prob)
@@ -69,12 +70,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _spawn(nranks, exchange, tmp_path):
+def _spawn(nranks, exchange, tmp_path, det=0):
     import torch.multiprocessing as mp
     port = _free_port()
-    outs = [str(tmp_path / f"{exchange}_{nranks}_{r}.npy") for r in range(nranks)]
+    outs = [str(tmp_path / f"{exchange}_{nranks}_{det}_{r}.npy") for r in range(nranks)]
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=_run, args=(nranks, r, exchange, port, outs[r])) for r in range(nranks)]
+    procs = [ctx.Process(target=_run, args=(nranks, r, exchange, port, outs[r], det)) for r in range(nranks)]
     for p in procs:
         p.start()
     for p in procs:

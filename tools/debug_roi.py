@@ -43,16 +43,20 @@ X1o, X2 = O.update_regularise(X0[box], Ao[box], Co[box], prob["alpha"], prob["la
                               clamp=True, lo=em["lo"], hi=em["hi"])
 X1g1, _ = O.update_regularise(X0[box], A[box], C[box], prob["alpha"], prob["lam"], 150.0, tau_C=1e-6,
                               clamp=True, lo=em["lo"], hi=em["hi"])
+from scipy import ndimage
+envC = ndimage.uniform_filter(Co[box], size=3, mode="constant") * 27.0
+grazing = ndimage.binary_dilation(Co[box] < 0.1 * envC / 27.0, np.ones((3, 3, 3), bool))
 d = np.abs(X1[box] - X2)
+d[grazing] = 0
 d[:1] = d[-1:] = 0
 d[:, :1] = d[:, -1:] = 0
 d[:, :, :1] = d[:, :, -1:] = 0
 idx = np.argsort(d.ravel())[::-1][:15]
 print("em", em)
-print("rel X", np.linalg.norm(d) / np.linalg.norm(X2))
+print("rel X (resolved)", np.linalg.norm(d) / np.linalg.norm(X2[~grazing]))
 for k in idx:
     z, y, x = np.unravel_index(k, d.shape)
     print(f"({x + glo[0]},{y + glo[1]},{z + glo[2]}) dX {d[z, y, x]:.3e} Xg {X1[box][z, y, x]:.3f} Xo {X2[z, y, x]:.3f} "
           f"X0 {X0[box][z, y, x]:.3f} Cg {C[box][z, y, x]:.4e} Co {Co[box][z, y, x]:.4e} "
           f"Ag/Cg {A[box][z, y, x] / max(C[box][z, y, x], 1e-30):.4f} Ao/Co {Ao[box][z, y, x] / max(Co[box][z, y, x], 1e-30):.4f} "
-          f"X1o {X1o[z, y, x]:.3f} X1(gpu A,C) {X1g1[z, y, x]:.3f}")
+          f"X1o {X1o[z, y, x]:.3f} X1(gpu A,C) {X1g1[z, y, x]:.3f} envC/27 {envC[z, y, x] / 27:.3e}")
