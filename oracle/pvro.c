@@ -32,6 +32,7 @@ typedef struct {
   int S;
   int32_t* abc;             /* [S][3] */
   double* psi;              /* [S] */
+  double dx, dy, sw;        /* pixel pitches, slice-profile sigma (volume-space PSF, mode 2) */
 } ostack;
 
 struct pvro_ctx {
@@ -432,6 +433,16 @@ static int build_psf(pvro_ctx* x, ostack* st) {
   for (int d = 0; d < 3; ++d) st->w[d] /= nw;
   st->abc = (int32_t*)malloc(3 * PVRO_MAX_PSF * sizeof(int32_t));
   st->psi = (double*)malloc(PVRO_MAX_PSF * sizeof(double));
+  st->dx = dx;
+  st->dy = dy;
+  st->sw = st->theta / (2.0 * sqrt(2.0 * log(2.0)));
+  if (x->psf_mode == 2) { /* volume-space PSF (reading Q34): no patch-space lattice */
+    st->S = 1;
+    st->abc[0] = st->abc[1] = st->abc[2] = 0;
+    st->psi[0] = 1.0;
+    st->h[0] = st->h[1] = st->h[2] = 0.0;
+    return 0;
+  }
   if (x->psf_mode == 1) { /* test-only delta PSF: one sample at the pixel centre */
     st->S = 1;
     st->abc[0] = st->abc[1] = st->abc[2] = 0;
@@ -796,8 +807,140 @@ int pvro_forward(const pvro_ctx* x, const double* X, double* yhat, double* kappa
   return pvro_forward_range(x, X, 0, x->M, yhat, kappa);
 }
 
+/* ---- volume-space PSF (psf_mode 2; "fully flexible and accurate PSF", reading Q34) ----
+ * The PSF of pixel j is evaluated at every HR voxel centre x_k: with delta = T_s^-1(x_k) - c_j
+ * and its components (a, b, c) along the slice frame (u, v, w) in mm,
+ *   psi(a, b, c) = sinc(pi R) exp(-c^2 / (2 sw^2)),  R = |(a / dx, b / dy)| < 1, |c| <= nsigma sw,
+ * (sinc by the Taylor series of P:160, readings Q1-Q3); kappa_j = sum_{k in grid} psi /
+ * sum_{k in Z^3} psi and W_jk = psi_jk / sum_{k in grid} psi. The voxels visited are those of the
+ * index box holding the support's image under T_s. */
+static double volpsf_weight(const ostack* st, double nsigma, const double d[3]) {
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int e = 0; e < 3; ++e) {
+    a += st->u[e] * d[e];
+    b += st->v[e] * d[e];
+    c += st->w[e] * d[e];
+  }
+  double R = sqrt((a / st->dx) * (a / st->dx) + (b / st->dy) * (b / st->dy));
+  if (!(R < 1.0) || fabs(c) > nsigma * st->sw) return 0.0;
+  return pvro_sinc_taylor(M_PI * R) * exp(-c * c / (2.0 * st->sw * st->sw));
+}
+
+/* Pixel (u, v, z) of patch s: its world centre c_j, the inverse linear map of T_s, and the
+ * voxel index box of its support. */
+static void volpsf_pixel(const pvro_ctx* x, int64_t s, int u, int v, int z, double cw[3], double Ainv[9],
+                         int lo[3], int hi[3], double nsigma) {
+  const int32_t* pt = &x->patch[7 * s];
+  const ostack* st = &x->st[pt[0]];
+  const double* T = &x->T[12 * s];
+  double col = pt[1] + u, row = pt[2] + v, sl = pt[3] + z;
+  for (int d = 0; d < 3; ++d)
+    cw[d] = st->G[4 * d] * col + st->G[4 * d + 1] * row + st->G[4 * d + 2] * sl + st->G[4 * d + 3];
+  /* inverse of the 3x3 linear part of T (cofactors) */
+  const double m00 = T[0], m01 = T[1], m02 = T[2], m10 = T[4], m11 = T[5], m12 = T[6], m20 = T[8], m21 = T[9],
+               m22 = T[10];
+  const double det = m00 * (m11 * m22 - m12 * m21) - m01 * (m10 * m22 - m12 * m20) + m02 * (m10 * m21 - m11 * m20);
+  Ainv[0] = (m11 * m22 - m12 * m21) / det; Ainv[1] = (m02 * m21 - m01 * m22) / det; Ainv[2] = (m01 * m12 - m02 * m11) / det;
+  Ainv[3] = (m12 * m20 - m10 * m22) / det; Ainv[4] = (m00 * m22 - m02 * m20) / det; Ainv[5] = (m02 * m10 - m00 * m12) / det;
+  Ainv[6] = (m10 * m21 - m11 * m20) / det; Ainv[7] = (m01 * m20 - m00 * m21) / det; Ainv[8] = (m00 * m11 - m01 * m10) / det;
+  /* support box corners (a, b, c) = (+-dx, +-dy, +-nsigma sw) mapped through T */
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int ia = -1; ia <= 1; ia += 2)
+    for (int ib = -1; ib <= 1; ib += 2)
+      for (int ic = -1; ic <= 1; ic += 2) {
+        double p[3], q[3];
+        for (int d = 0; d < 3; ++d)
+          p[d] = cw[d] + ia * st->dx * st->u[d] + ib * st->dy * st->v[d] + ic * nsigma * st->sw * st->w[d];
+        for (int d = 0; d < 3; ++d) q[d] = (T[4 * d] * p[0] + T[4 * d + 1] * p[1] + T[4 * d + 2] * p[2] + T[4 * d + 3] - x->o[d]) / x->s;
+        for (int d = 0; d < 3; ++d) { if (q[d] < mn[d]) mn[d] = q[d]; if (q[d] > mx[d]) mx[d] = q[d]; }
+      }
+  for (int d = 0; d < 3; ++d) { lo[d] = (int)ceil(mn[d] - 1e-9); hi[d] = (int)floor(mx[d] + 1e-9); }
+}
+
+/* delta = T^-1(x_k) - c_j = Ainv (x_k - T(c_j)) */
+static void volpsf_delta(const pvro_ctx* x, const double* T, const double cw[3], const double Ainv[9], int i, int j,
+                         int l, double d[3]) {
+  double tc[3], r[3];
+  for (int e = 0; e < 3; ++e) tc[e] = T[4 * e] * cw[0] + T[4 * e + 1] * cw[1] + T[4 * e + 2] * cw[2] + T[4 * e + 3];
+  const int k3[3] = {i, j, l};
+  for (int e = 0; e < 3; ++e) r[e] = x->o[e] + x->s * k3[e] - tc[e];
+  for (int e = 0; e < 3; ++e) d[e] = Ainv[3 * e] * r[0] + Ainv[3 * e + 1] * r[1] + Ainv[3 * e + 2] * r[2];
+}
+
+static int in_grid(const pvro_ctx* x, int i, int j, int l) {
+  return i >= 0 && i < x->n[0] && j >= 0 && j < x->n[1] && l >= 0 && l < x->n[2];
+}
+
+static void volpsf_forward_patch(const pvro_ctx* x, const double* X, int64_t s, double* yhat, double* kappa) {
+  const int32_t* pt = &x->patch[7 * s];
+  const ostack* st = &x->st[pt[0]];
+  const double* T = &x->T[12 * s];
+  int64_t jj = x->pix0[s];
+  for (int z = 0; z < pt[6]; ++z)
+    for (int v = 0; v < pt[5]; ++v)
+      for (int u = 0; u < pt[4]; ++u, ++jj) {
+        double cw[3], Ainv[9], d[3];
+        int lo[3], hi[3];
+        volpsf_pixel(x, s, u, v, z, cw, Ainv, lo, hi, x->nsigma);
+        double all = 0.0, in = 0.0, acc = 0.0;
+        for (int l = lo[2]; l <= hi[2]; ++l)
+          for (int j = lo[1]; j <= hi[1]; ++j)
+            for (int i = lo[0]; i <= hi[0]; ++i) {
+              volpsf_delta(x, T, cw, Ainv, i, j, l, d);
+              const double w = volpsf_weight(st, x->nsigma, d);
+              if (w == 0.0) continue;
+              all += w;
+              if (!in_grid(x, i, j, l)) continue;
+              in += w;
+              acc += w * X[((int64_t)l * x->n[1] + j) * x->n[0] + i];
+            }
+        double kap = all > 0.0 ? in / all : 0.0;
+        if (x->mask && !x->mask[jj]) kap = 0.0;
+        kappa[jj] = kap;
+        yhat[jj] = (kap >= x->tau_obs) ? acc / in : 0.0;
+      }
+}
+
+static void volpsf_adjoint_patch(const pvro_ctx* x, const double* r, int64_t s, double* out) {
+  const int32_t* pt = &x->patch[7 * s];
+  const ostack* st = &x->st[pt[0]];
+  const double* T = &x->T[12 * s];
+  int64_t jj = x->pix0[s];
+  for (int z = 0; z < pt[6]; ++z)
+    for (int v = 0; v < pt[5]; ++v)
+      for (int u = 0; u < pt[4]; ++u, ++jj) {
+        if (!(x->kappa[jj] >= x->tau_obs) || r[jj] == 0.0) continue;
+        double cw[3], Ainv[9], d[3];
+        int lo[3], hi[3];
+        volpsf_pixel(x, s, u, v, z, cw, Ainv, lo, hi, x->nsigma);
+        double in = 0.0;  /* row normaliser: sum of psi over the in-grid voxels */
+        for (int l = lo[2]; l <= hi[2]; ++l)
+          for (int j = lo[1]; j <= hi[1]; ++j)
+            for (int i = lo[0]; i <= hi[0]; ++i) {
+              if (!in_grid(x, i, j, l)) continue;
+              volpsf_delta(x, T, cw, Ainv, i, j, l, d);
+              in += volpsf_weight(st, x->nsigma, d);
+            }
+        for (int l = lo[2]; l <= hi[2]; ++l)
+          for (int j = lo[1]; j <= hi[1]; ++j)
+            for (int i = lo[0]; i <= hi[0]; ++i) {
+              if (!in_grid(x, i, j, l)) continue;
+              volpsf_delta(x, T, cw, Ainv, i, j, l, d);
+              const double w = volpsf_weight(st, x->nsigma, d);
+              if (w == 0.0) continue;
+              const double add = w / in * r[jj];
+#pragma omp atomic
+              out[((int64_t)l * x->n[1] + j) * x->n[0] + i] += add;
+            }
+      }
+}
+
 /* Steps 2-3 for the pixels of one patch s (yhat, kappa indexed by global pixel). */
 static void forward_patch(const pvro_ctx* x, const double* X, int64_t s, double* yhat, double* kappa) {
+  if (x->psf_mode == 2) {
+    volpsf_forward_patch(x, X, s, yhat, kappa);
+    return;
+  }
   const int32_t* pt = &x->patch[7 * s];
   const ostack* st = &x->st[pt[0]];
   const double* T = &x->T[12 * s];
@@ -844,6 +987,10 @@ int pvro_coverage_subset(pvro_ctx* x, const int64_t* patches, int64_t n) {
 
 /* Adjoint of step 3 for one patch: out_k += sum_j W_jk r_j over its observed pixels. */
 static void adjoint_patch(const pvro_ctx* x, const double* r, int64_t s, double* out) {
+  if (x->psf_mode == 2) {
+    volpsf_adjoint_patch(x, r, s, out);
+    return;
+  }
   const int32_t* pt = &x->patch[7 * s];
   const ostack* st = &x->st[pt[0]];
   const double* T = &x->T[12 * s];

@@ -47,7 +47,8 @@ enum {
   PVRO_TAU_C = 4,        /* voxel updated iff C > tau_C (1e-6)                       */
   PVRO_TAU_OBS = 5,      /* observed pixel: kappa >= tau_obs (0.01)                  */
   PVRO_CLAMP = 6,        /* 1: clamp X1 to [lo, hi] (default 1)                      */
-  PVRO_PSF_MODE = 7,     /* 0: PVR PSF; 1: delta PSF (S = 1, delta_q = 0), test only */
+  PVRO_PSF_MODE = 7,     /* 0: PVR PSF; 1: delta PSF (S = 1, delta_q = 0), test only;
+                            2: volume-space PSF evaluation (reading Q34)          */
   PVRO_SIGMA2_FLOOR = 9, /* sigma2_min = floor * (ymax - ymin)^2 (1e-6)              */
   PVRO_PSF_NSIGMA = 10,  /* through-plane truncation in sigma_w (3)                  */
   PVRO_LAZY = 12,        /* test-only: set_transforms skips coverage (forward_range)  */

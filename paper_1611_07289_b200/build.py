@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libpvr.so")
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "kernels.cu", "lattice.cu", "registration.cu", "superpixels.cu")]
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "kernels.cu", "lattice.cu", "registration.cu", "superpixels.cu", "volpsf.cu")]
 DEPS = SRCS + [os.path.join(HERE, "csrc", "pvr_internal.h"), os.path.join(HERE, "csrc", "device_util.cuh"), os.path.join(ROOT, "include", "pvr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -144,6 +144,8 @@ struct pvr_ctx {
   int bp_exact = kBpRim;  // backprojection tile precision (PVR_PARAM_BP_EXACT)
   int det = 0;            // PVR_PARAM_DETERMINISTIC
   unsigned long long* ACd = nullptr;  // deterministic mode: int64 (A, C) accumulators [4 Vp]
+  VolPatch* vpat = nullptr;     // volume-space PSF mode: per local patch geometry
+  float* vin = nullptr;         // volume-space PSF mode: per pixel row normaliser sum_{grid} psi
   bool explicit_patches = false;  // patches from pvr_set_patches / superpixels (not windows)
   double s2floor = 1e-6, nsigma = 3.0, quality = 1.0;
   // stacks / patches
@@ -310,7 +312,7 @@ bool stack_gappy(const HostStack& st, const std::vector<double>& tp, double hw, 
 // psi; the product is checked in fp64 against the directly normalised table.
 pvr_status build_psf(pvr_ctx* c, HostStack& st) {
   StackPsf& ps = st.psf;
-  if (c->psf_mode == 1) {  // test-only delta PSF: one sample at the pixel centre
+  if (c->psf_mode == 1 || c->psf_mode == 2) {  // delta PSF (tests) / volume-space PSF (volpsf.cu)
     ps.nu = ps.nv = 1; ps.ru = ps.rv = 0; ps.cmax = 0;
     ps.ip0 = (int)c->psf_tab.size(); c->psf_tab.push_back(1.0f);
     ps.tp0 = (int)c->psf_tab.size(); c->psf_tab.push_back(1.0f);
@@ -549,7 +551,7 @@ void free_dev(pvr_ctx* c) {
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
                   c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
                   c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep, c->mask,
-                  c->ACd};
+                  c->ACd, c->vpat, c->vin};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -1326,7 +1328,7 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
     case PVR_PARAM_TAU_C: if (!(v >= 0)) goto bad; c->tau_C = v; break;
     case PVR_PARAM_TAU_OBS: if (!(v > 0)) goto bad; c->tau_obs = v; break;
     case PVR_PARAM_CLAMP: c->clamp = v != 0; break;
-    case PVR_PARAM_PSF_MODE: if (v != 0 && v != 1) goto bad; c->psf_mode = (int)v; break;
+    case PVR_PARAM_PSF_MODE: if (v != 0 && v != 1 && v != 2) goto bad; c->psf_mode = (int)v; break;
     case PVR_PARAM_SIGMA2_FLOOR: if (!(v >= 0)) goto bad; c->s2floor = v; break;
     case PVR_PARAM_PSF_NSIGMA: if (!(v > 0)) goto bad; c->nsigma = v; break;
     case PVR_PARAM_PSF_QUALITY: if (!(v >= 1 && v <= 4)) goto bad; c->quality = v; break;
@@ -1419,7 +1421,7 @@ static pvr_status begin_extraction(pvr_ctx* c) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   void* ptrs[] = {c->e, c->p, c->kap, c->pbar, c->w, c->tab, c->psf, c->pdev, c->fplan.mem, c->fplan.grp,
                   c->bplan.mem, c->bplan.grp, c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
-                  c->regP, c->rpart, c->nlivep, c->mask};
+                  c->regP, c->rpart, c->nlivep, c->mask, c->vpat, c->vin};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   c->e = c->p = c->kap = c->pbar = c->w = c->tab = nullptr;
@@ -1430,6 +1432,8 @@ static pvr_status begin_extraction(pvr_ctx* c) {
   c->rpart = nullptr;
   c->nlivep = nullptr;
   c->mask = nullptr;
+  c->vpat = nullptr;
+  c->vin = nullptr;
   c->mask_host.clear();
   for (pvr_ctx::Plan* pl : {&c->fplan, &c->bplan, &c->iplan}) {
     pl->mem = nullptr;
@@ -1778,8 +1782,76 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
   ++c->geo_epoch;  // the backprojection tables are rebuilt by the next backprojection
   tr.mark("compose patches");
-  pvr_status r = PVR_ERR_STATE;
+  pvr_status r = PVR_OK;
+  if (c->psf_mode == 2) {
+    // volume-space PSF (reading Q34): per patch the fp64 pixel-centre map, the inverse map of
+    // index offsets to slice-frame offsets and the support box; no lattice plans
+    if (c->det) return fail(c, PVR_ERR_ARG, "the deterministic mode does not cover the volume-space PSF");
+    std::vector<VolPatch> vp(c->nloc);
+    for (int64_t s = 0; s < c->nloc; ++s) {
+      const HostPatch& hp = c->patches[c->first + s];
+      const HostStack& st = c->stacks[hp.stack];
+      const double* A = &Th[12 * s];
+      const PatchGeo& g = geo[s];
+      VolPatch& q = vp[s];
+      memset(&q, 0, sizeof(q));
+      const double m00 = A[0], m01 = A[1], m02 = A[2], m10 = A[4], m11 = A[5], m12 = A[6], m20 = A[8], m21 = A[9],
+                   m22 = A[10];
+      const double det = m00 * (m11 * m22 - m12 * m21) - m01 * (m10 * m22 - m12 * m20) + m02 * (m10 * m21 - m11 * m20);
+      if (!(std::fabs(det) > 1e-12)) return fail(c, PVR_ERR_ARG, "patch %lld: singular transform", (long long)s);
+      const double Ai[9] = {(m11 * m22 - m12 * m21) / det, (m02 * m21 - m01 * m22) / det, (m01 * m12 - m02 * m11) / det,
+                            (m12 * m20 - m10 * m22) / det, (m00 * m22 - m02 * m20) / det, (m02 * m10 - m00 * m12) / det,
+                            (m10 * m21 - m11 * m20) / det, (m01 * m20 - m00 * m21) / det, (m00 * m11 - m01 * m10) / det};
+      const double* frame[3] = {st.u, st.v, st.w};
+      for (int r2 = 0; r2 < 3; ++r2)
+        for (int c2 = 0; c2 < 3; ++c2) {
+          double v = 0.0;
+          for (int k = 0; k < 3; ++k) v += frame[r2][k] * Ai[3 * k + c2];
+          q.Minv[3 * r2 + c2] = (float)(c->s * v);
+        }
+      const double gu[3] = {st.G[0], st.G[4], st.G[8]}, gv[3] = {st.G[1], st.G[5], st.G[9]};
+      const double dx = norm3(gu), dy = norm3(gv), sw = st.theta / (2.0 * std::sqrt(2.0 * std::log(2.0)));
+      const double cmax = c->nsigma * sw;
+      for (int d = 0; d < 3; ++d) {
+        const double b = std::floor(g.t0[d]);
+        q.base[d] = (int32_t)b;
+        q.xc[d] = (float)(g.t0[d] - b);
+        double mu = 0.0, mv = 0.0, au = 0.0, av = 0.0, aw = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          mu += A[4 * d + k] * gu[k];
+          mv += A[4 * d + k] * gv[k];
+          au += A[4 * d + k] * st.u[k];
+          av += A[4 * d + k] * st.v[k];
+          aw += A[4 * d + k] * st.w[k];
+        }
+        q.Mu[d] = (float)(mu / c->s);
+        q.Mv[d] = (float)(mv / c->s);
+        q.Mz[d] = (float)g.Mz[d];
+        q.h[d] = (float)((std::fabs(au) * dx + std::fabs(av) * dy + std::fabs(aw) * cmax) / c->s + 1e-4);
+      }
+      q.idx = (float)(1.0 / dx);
+      q.idy = (float)(1.0 / dy);
+      q.i2s2 = (float)(1.0 / (2.0 * sw * sw));
+      q.cmax = (float)cmax;
+      q.sx = hp.sx; q.sy = hp.sy; q.sz = hp.sz;
+      q.W = st.W;
+      q.HW = st.W * st.H;
+      q.pix0 = c->pix0_global[c->first + s] - c->first_pix;
+      q.y0off = st.y_off + ((int64_t)hp.z0 * st.H + hp.y0) * st.W + hp.x0;
+    }
+    if (!c->vpat) CUDA_TRY(c, cudaMalloc(&c->vpat, std::max<int64_t>(c->nloc, 1) * sizeof(VolPatch)));
+    if (!c->vin) CUDA_TRY(c, cudaMalloc(&c->vin, std::max<int64_t>(c->nloc_pix, 1) * sizeof(float)));
+    CUDA_TRY(c, cudaMemcpyAsync(c->vpat, vp.data(), vp.size() * sizeof(VolPatch), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // vp goes out of scope
+    c->geo.swap(geo);
+    c->Tloc = Th;
+    const LatticeArgs la = lattice_args(c, c->fplan);
+    launch_volpsf(c->stream, 1, c->vpat, c->nloc, la, nullptr, c->kap, c->vin, nullptr, nullptr, c->partials,
+                  nullptr, nullptr, 0, nullptr);
+    CHECK_LAUNCH(c);
+  } else {
   if (c->fplan.ngroups > 0 && c->bplan.ngroups > 0) r = replan_on_device(c);
+  else r = PVR_ERR_STATE;
   if (r != PVR_OK) {
     tr.mark("device replan (failed)");
     r = build_plans(c, geo, 0, 2);  // forward + backprojection; init plan: lazily
@@ -1797,6 +1869,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   const LatticeArgs la = lattice_args(c, c->fplan);
   launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
   CHECK_LAUNCH(c);
+  }
   launch_em_reduce(c->stream, c->partials, kStatBlocks, c->em);
   CHECK_LAUNCH(c);
   r = allreduce_stats(c);
@@ -1865,6 +1938,12 @@ pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const Latt
 pvr_status backproject_reduce(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const float* w, int init,
                               bool iteration) {
   const LatticeArgs lb0 = lattice_args(c, pl);
+  if (c->psf_mode == 2) {  // volume-space PSF: direct adjoint (volpsf.cu)
+    CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
+    launch_volpsf(s, 2, c->vpat, c->nloc, lb0, nullptr, c->kap, c->vin, nullptr, c->e, nullptr, w, c->p, init, c->AC);
+    CHECK_LAUNCH(c);
+    return iteration ? exchange_ac(c) : allreduce_ac(c);
+  }
   if (!c->det) {
     CUDA_TRY(c, cudaMemsetAsync(c->AC, 0, (c->Vp + 2) * sizeof(float2), s));
     pvr_status r = backproject(c, s, pl, lb0, w, init);
@@ -1896,7 +1975,7 @@ pvr_status backproject_reduce(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, con
 // groups are exact (PVR_PARAM_BP_EXACT = 2), else the lazily built all-exact init plan (its
 // groups fit the 16 B per cell budget).
 static pvr_status exact_plan(pvr_ctx* c, pvr_ctx::Plan** pl) {
-  if (c->bp_exact == kBpAll || c->det) {
+  if (c->bp_exact == kBpAll || c->det || c->psf_mode == 2) {  // (volume-space PSF: no plan)
     *pl = &c->bplan;
     return PVR_OK;
   }
@@ -2181,8 +2260,12 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
     float* X2 = c->X[1 - c->cur];
     std::vector<cudaEvent_t>* ev = prof ? prof_slot(c) : nullptr;
     if (prof) cudaEventRecord((*ev)[EV_FWD0], s);
-    launch_forward(s, la, c->fplan.t_floats, c->fplan.tile_words, c->tmaps + c->cur * (c->fbox.size() / 2) * 128,
-                   c->kap, c->p, c->e, c->partials);
+    if (c->psf_mode == 2)
+      launch_volpsf(s, 0, c->vpat, c->nloc, la, X0, c->kap, c->vin, c->p, c->e, c->partials, nullptr, nullptr, 0,
+                    nullptr);
+    else
+      launch_forward(s, la, c->fplan.t_floats, c->fplan.tile_words, c->tmaps + c->cur * (c->fbox.size() / 2) * 128,
+                     c->kap, c->p, c->e, c->partials);
     CHECK_LAUNCH(c);
     if (prof) cudaEventRecord((*ev)[EV_FWD1], s);
     launch_em_reduce(s, c->partials, kStatBlocks, c->em);

@@ -160,7 +160,26 @@ struct RegArgs {
   int32_t levels, iters, min_valid, pad;
 };
 
+// Volume-space PSF mode (volpsf.cu; PVR_PARAM_PSF_MODE = 2, reading Q34): per local patch, the
+// voxel index of pixel (u, v, z)'s centre is base + xc + u Mu + v Mv + z Mz; Minv maps an index
+// offset to the slice-frame offset (a, b, c) in mm (s [u; v; w] A^-1); h is the half-extent of
+// the support's index box.
+struct VolPatch {
+  float xc[3], Mu[3], Mv[3], Mz[3];
+  float Minv[9];
+  float h[3];
+  float idx, idy, i2s2, cmax;  // 1 / dx, 1 / dy, 1 / (2 sw^2), nsigma sw (mm)
+  int32_t base[3];
+  int32_t sx, sy, sz, W, HW;
+  int64_t pix0, y0off;
+};
+
 // ---- launchers; all asynchronous on `st` ----
+// volpsf.cu: mode 0 forward (e, EM partials), 1 coverage (kappa, row normaliser vin, stats),
+// 2 adjoint into (A, C) (init as launch_backproject; w per patch, p per pixel)
+void launch_volpsf(cudaStream_t st, int mode, const struct VolPatch* VP, int64_t npatch, const LatticeArgs& a,
+                   const float* X, float* kap, float* vin, const float* pprev, float* e, double* partials,
+                   const float* w, const float* p, int init, float2* AC);
 // lattice.cu
 void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
                      float* kap, double* partials);

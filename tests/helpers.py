@@ -22,7 +22,10 @@ THRESHOLDS = {"survey": {}, "round1": {"tau_C": 1e-3, "tau_obs": 0.5}}
 # (profiles/r02_parity_errors.txt): X 4.2e-7, e 1.2e-6, A 9.5e-6, C 8.9e-7 (rel L2; X away
 # from the tau_C tie band), kappa 1.6e-6, p 1.4e-5, w 1.3e-6 (abs), sigma2 / c / m 2.4e-7 (rel).
 # The north_star bars (X 1e-4 rel L2, p and w 1e-3 abs) are asserted as well.
-TOL = {"X": 5e-6, "e": 1.2e-5, "A": 1e-4, "C": 9e-6, "kappa": 1.7e-5, "p": 1.4e-4, "w": 1.3e-5, "em": 2.5e-6}
+# m = 1 / (max e - min e) is a ratio of two extreme residuals, each off by up to ~1e-6 of its
+# pixel's yhat, so its relative error scales with max|yhat| / range(e) (~5 on these phantoms):
+# the EM bar is 1e-5 rather than 10x the lattice mode's 2.4e-7 (volume-space PSF mode: 4.3e-6).
+TOL = {"X": 5e-6, "e": 1.2e-5, "A": 1e-4, "C": 9e-6, "kappa": 1.7e-5, "p": 1.4e-4, "w": 1.3e-5, "em": 1e-5}
 
 
 def tau_c_tie_band(Co, tau_C, dims):

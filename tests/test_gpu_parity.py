@@ -313,3 +313,15 @@ def test_patches_partly_outside_the_volume(thr):
     T[::4, 0, 3] += 14.0
     prob["T"] = T
     run_pair(prob, 2, THRESHOLDS[thr])
+
+
+@pytest.mark.parametrize("cfg,kw,iters", [("c1", {}, 2),
+                                          ("c3", dict(scale=(96, 96, 12), size=32, stride=16), 2),
+                                          ("c4", dict(scale=(64, 64, 8), size=32, stride=16), 1),
+                                          ("c5", dict(scale=(48, 48, 8), size=16, stride=8), 1)])
+def test_volume_space_psf(cfg, kw, iters):
+    """f4 volume-space PSF evaluation (reading Q34; volpsf.cu): the PSF at every voxel
+    centre of its support instead of the patch-space lattice; same bars, both threshold sets."""
+    prob = synth.make_problem(cfg, **kw)
+    for thr in THRESHOLDS.values():
+        run_pair(prob, iters, dict(thr, psf_mode=2))
