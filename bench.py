@@ -209,6 +209,9 @@ def run_ours(args):
     prob = synth.make_problem(args.config)
     ctx = Context(prob["dims"], prob["spacing"], prob["origin"], local, stream.cuda_stream)
     if ws > 1:
+        # SURVEY 8(e) lever 3: reduce-scatter (A, C) over z slabs, slab update, all-gather X
+        # (12 V (N-1)/N bytes per rank instead of the allreduce's 16 V (N-1)/N)
+        ctx.set_param("exchange", pvr.EXCHANGE[args.exchange])
         uid = [pvr.pvr_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.comm_init(ws, rank, uid[0])
@@ -420,7 +423,8 @@ def run_ours(args):
                 "data": "synthetic (seeded analytic phantom acquisition; synth/)",
                 "config": config_block(args.config, extra={
                     "M": int(ctx.M), "P": int(st["pixels"]) if ws == 1 else None,
-                    "psf_samples_per_iteration": samples, "parallelism": f"patch-shard x{ws}",
+                    "psf_samples_per_iteration": samples,
+                    "parallelism": f"patch-shard x{ws}" + (f", exchange {args.exchange}" if ws > 1 else ""),
                     "psf_quality": args.psf_quality}),
                 "roofline": roof, "iteration_hbm": hbm_iter, "plan": plan,
                 "kernels": breakdown, "clocks": clk.summary(), "e2e": e2e,
@@ -445,6 +449,8 @@ def main():
     ap.add_argument("--one-call", action="store_true", help="time one pvr_sr_iterate(K) call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the f3 superpixel measurement")
+    ap.add_argument("--exchange", default="slabs", choices=["allreduce", "slabs"],
+                    help="multi-GPU (A, C) exchange (PVR_PARAM_EXCHANGE); default slabs")
     ap.add_argument("--psf-quality", type=float, default=1.0,
                     help="f4 PSF lattice density q (2 = the q = 2 quality mode); default 1")
     args = ap.parse_args()

@@ -1808,6 +1808,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
           double v = 0.0;
           for (int k = 0; k < 3; ++k) v += frame[r2][k] * Ai[3 * k + c2];
           q.Minv[3 * r2 + c2] = (float)(c->s * v);
+          q.Minvd[3 * r2 + c2] = c->s * v;
         }
       const double gu[3] = {st.G[0], st.G[4], st.G[8]}, gv[3] = {st.G[1], st.G[5], st.G[9]};
       const double dx = norm3(gu), dy = norm3(gv), sw = st.theta / (2.0 * std::sqrt(2.0 * std::log(2.0)));
@@ -1816,6 +1817,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
         const double b = std::floor(g.t0[d]);
         q.base[d] = (int32_t)b;
         q.xc[d] = (float)(g.t0[d] - b);
+        q.xcd[d] = g.t0[d] - b;
         double mu = 0.0, mv = 0.0, au = 0.0, av = 0.0, aw = 0.0;
         for (int k = 0; k < 3; ++k) {
           mu += A[4 * d + k] * gu[k];
@@ -1827,12 +1829,18 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
         q.Mu[d] = (float)(mu / c->s);
         q.Mv[d] = (float)(mv / c->s);
         q.Mz[d] = (float)g.Mz[d];
+        q.Mud[d] = mu / c->s;
+        q.Mvd[d] = mv / c->s;
+        q.Mzd[d] = g.Mz[d];
         q.h[d] = (float)((std::fabs(au) * dx + std::fabs(av) * dy + std::fabs(aw) * cmax) / c->s + 1e-4);
       }
       q.idx = (float)(1.0 / dx);
       q.idy = (float)(1.0 / dy);
       q.i2s2 = (float)(1.0 / (2.0 * sw * sw));
       q.cmax = (float)cmax;
+      q.dxd = dx;
+      q.dyd = dy;
+      q.cmaxd = cmax;
       q.sx = hp.sx; q.sy = hp.sy; q.sz = hp.sz;
       q.W = st.W;
       q.HW = st.W * st.H;

@@ -172,6 +172,9 @@ struct VolPatch {
   int32_t base[3];
   int32_t sx, sy, sz, W, HW;
   int64_t pix0, y0off;
+  // fp64 copies for the support decisions of voxels within 1e-3 of its edge (R = 1, |c| = cmax)
+  double xcd[3], Mud[3], Mvd[3], Mzd[3], Minvd[9];
+  double dxd, dyd, cmaxd;
 };
 
 // ---- launchers; all asynchronous on `st` ----

@@ -21,11 +21,26 @@ namespace pvr {
 
 namespace {
 
-// PSF value at slice-frame offsets (a, b, c) mm; 0 outside the support
-__device__ __forceinline__ float vpsf(const VolPatch& V, float a, float b, float c) {
+// PSF value at slice-frame offsets (a, b, c) mm; 0 outside the support. The support test
+// (R < 1, |c| <= nsigma sw) is an exact decision of the reading: a voxel within 1e-3 of its
+// edge is decided again from fp64 offsets (the fp32 ones carry ~1e-5 of rounding), so the
+// kernel includes the same voxels as the fp64 oracle.
+__device__ __forceinline__ float vpsf(const VolPatch& V, float a, float b, float c, const double (&cd)[3],
+                                      int i, int j, int l) {
   const float ra = a * V.idx, rb = b * V.idy;
-  const float R2 = ra * ra + rb * rb;
-  if (!(R2 < 1.0f) || fabsf(c) > V.cmax) return 0.0f;
+  float R2 = ra * ra + rb * rb;
+  if (fabsf(R2 - 1.0f) < 1e-3f || fabsf(fabsf(c) - V.cmax) < 1e-3f) {
+    const double dx = i - cd[0], dy = j - cd[1], dz = l - cd[2];
+    const double ad = V.Minvd[0] * dx + V.Minvd[1] * dy + V.Minvd[2] * dz;
+    const double bd = V.Minvd[3] * dx + V.Minvd[4] * dy + V.Minvd[5] * dz;
+    const double cd2 = V.Minvd[6] * dx + V.Minvd[7] * dy + V.Minvd[8] * dz;
+    const double R2d = (ad / V.dxd) * (ad / V.dxd) + (bd / V.dyd) * (bd / V.dyd);
+    if (!(sqrt(R2d) < 1.0) || fabs(cd2) > V.cmaxd) return 0.0f;
+    R2 = fminf((float)R2d, 0.99999994f);
+    c = (float)cd2;
+  } else if (!(R2 < 1.0f) || fabsf(c) > V.cmax) {
+    return 0.0f;
+  }
   const float R = sqrtf(R2);
   const float s = R > 1e-4f ? sinpif(R) / (3.14159265358979f * R) : 1.0f - 1.6449341f * R2;
   return s * __expf(-c * c * V.i2s2);
@@ -72,10 +87,12 @@ __global__ void __launch_bounds__(256) k_volpsf(const VolPatch* __restrict__ VP,
       }
       // pixel centre (index units, relative to the patch base) and its support box
       float c[3];
+      double cd[3];
       int lo[3], hi[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        c[d] = V.xc[d] + u * V.Mu[d] + v * V.Mv[d] + z * V.Mz[d];
+        cd[d] = V.xcd[d] + u * V.Mud[d] + v * V.Mvd[d] + z * V.Mzd[d];
+        c[d] = (float)cd[d];
         lo[d] = (int)ceilf(c[d] - V.h[d]);
         hi[d] = (int)floorf(c[d] + V.h[d]);
       }
@@ -100,7 +117,7 @@ __global__ void __launch_bounds__(256) k_volpsf(const VolPatch* __restrict__ VP,
             const float pa = V.Minv[0] * dx + V.Minv[1] * dy + V.Minv[2] * dz;
             const float pb = V.Minv[3] * dx + V.Minv[4] * dy + V.Minv[5] * dz;
             const float pc = V.Minv[6] * dx + V.Minv[7] * dy + V.Minv[8] * dz;
-            const float wt = vpsf(V, pa, pb, pc);
+            const float wt = vpsf(V, pa, pb, pc, cd, i, jj, l);
             if (wt == 0.0f) continue;
             if (MODE == 1) {
               all += wt;
