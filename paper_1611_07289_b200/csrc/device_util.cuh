@@ -6,6 +6,20 @@
 
 namespace pvr {
 
+// Debug builds (-DPVR_CHECKS=1, tools/ab_build.py): device-side bounds checks of the shared
+// tiles and the global reductions; a violation traps (the launch fails with an error). The
+// compute-sanitizer is closed on this GPU pool, so these stand in for memcheck.
+#ifdef PVR_CHECKS
+#define PVR_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define PVR_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

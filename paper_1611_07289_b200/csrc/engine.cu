@@ -789,7 +789,8 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     return (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
   };
   auto fits = [&](const GroupDev& g, int64_t vox) {
-    return vox * (fwd ? 4 : c->det ? 24 : g.exact ? 16 : 8) <= byte_budget;
+    if (!fwd && c->det) return vox * 4 <= (int64_t)kBpDetPlane * (kind == 1 ? 9 : 10) / 10;
+    return vox * (fwd ? 4 : g.exact ? 16 : 8) <= byte_budget;
   };
   // Outlying members of a natural group: a member whose footprint centre lies more than a
   // quarter of the group's median footprint extent (and 4 voxels) from the median centre on

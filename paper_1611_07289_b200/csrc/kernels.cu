@@ -569,6 +569,7 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
   // backprojection tile precision (engine.cu: size_groups): exact for rim members and
   // footprints that leave the grid; the byte budget then buys half the cells
   G.exact = !fwd && (bp_mode >= kBpAll || (bp_mode == kBpRim && (rim || !G.interior)));
+  // (deterministic mode: 4 B per cell in each of 6 planes of kBpDetPlane bytes)
   const int64_t cell_bytes = bp_mode == kBpDet ? 24 : G.exact ? 16 : 8;
   int64_t vox;
   if (fwd) {
@@ -605,7 +606,8 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
         S.exact = bp_mode >= kBpAll || (bp_mode == kBpRim && ((m.flags & kMemberRim) || !S.interior));
         const int64_t sv = replan_bp_box(ml, mh, S);
         const int k = atomicAdd(nappend, 1);
-        if (sv * (bp_mode == kBpDet ? 24 : S.exact ? 16 : 8) > vox_budget || ngroups + k >= cap) {
+        if (sv * (bp_mode == kBpDet ? 24 : S.exact ? 16 : 8) > vox_budget ||
+            (bp_mode == kBpDet && sv * 4 > kBpDetPlane) || ngroups + k >= cap) {
           atomicExch(fail, 1);
           continue;
         }
@@ -617,7 +619,8 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
       vox = 0;
     }
   }
-  if ((fwd ? vox : vox * cell_bytes) > vox_budget) atomicExch(fail, 1);
+  if ((fwd ? vox : vox * cell_bytes) > vox_budget || (bp_mode == kBpDet && vox * 4 > kBpDetPlane))
+    atomicExch(fail, 1);
   atomicMax(maxvox, (int)(vox < (1 << 30) ? vox : (1 << 30)));
   grp[g] = G;
 }

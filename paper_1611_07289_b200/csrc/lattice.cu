@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         const f2 fxy = sub2(rxy, sub2(txy, mag));
         const float fz = rzc - __fsub_rn(tz, kMagic);
         const float* p = sXo + iz * dxy + iy * dx + ix;
+        PVR_CHECK(p >= sX && p + dxy + dx + 1 < sX + dz * dxy);
         const f2 x00 = pk(p[0], p[dxy]), x10 = pk(p[1], p[dxy + 1]);            // (z0, z1) at y0
         const f2 x01 = pk(p[dx], p[dxy + dx]), x11 = pk(p[dx + 1], p[dxy + dx + 1]);  // at y1
         const float fx = lo2(fxy), fy = hi2(fxy);
@@ -463,7 +464,9 @@ constexpr int kHQ = kBpTileBytes / 4;
 // word per quantity (A at 0, C at kCOff), kPrecHiLo two (planes kHQ apart), kPrecDet three
 // (planes kH6 apart: deterministic mode's global scale).
 constexpr int kPrecSingle = 0, kPrecHiLo = 1, kPrecDet = 2;
-constexpr int kH6 = kBpTileBytes / 6;  // deterministic tile: A_hi, C_hi, A_lo, C_lo, A_lo2, C_lo2
+__shared__ int s_cells;  // cells of the current group's tile (PVR_CHECK bounds)
+// deterministic tile: A_hi, C_hi, A_lo, C_lo, A_lo2, C_lo2 planes of kBpDetPlane bytes
+constexpr int kH6 = kBpDetPlane;
 static_assert(kH6 % 16 == 0, "tile planes must stay 16-byte aligned");
 template <int PREC>
 __device__ __forceinline__ void flush4(unsigned a, int sp4, int sq4, float s0, float s1, float s2, float s3,
@@ -561,6 +564,7 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
       const bool keep = same & (im == wm);
       const bool adv = same & (im == wm + 1);
       const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
+      PVR_CHECK(a0 >= tA && a0 + sm4 + sp4 + sq4 < tA + 4u * (unsigned)s_cells);
       flush4<PREC>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);  // plane wm
       if (!keep && !adv)  // restart (transverse change, the wrap, a jump): plane wm + 1 too
         flush4<PREC>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
@@ -593,6 +597,7 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
     }
   }
   const unsigned a0 = org + wm * sm4 + wp * sp4 + wq * sq4;
+  PVR_CHECK(a0 >= tA && a0 + sm4 + sp4 + sq4 < tA + 4u * (unsigned)s_cells);
   flush4<PREC>(a0, sp4, sq4, lo2(P[0]), lo2(P[1]), lo2(P[2]), lo2(P[3]), L, mag, lsc);
   flush4<PREC>(a0 + sm4, sp4, sq4, hi2(P[0]), hi2(P[1]), hi2(P[2]), hi2(P[3]), L, mag, lsc);
 }
@@ -729,6 +734,9 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
 // Dynamic shared memory: the tile (exact group: planes A_hi, C_hi, A_lo, C_lo at byte offsets
 // kHQ apart; single-word group: A at 0, C at kCOff; offsets are immediates of the splat's
 // shared reductions), then R after kBpTileBytes. kBpCtasPerSm CTAs per SM.
+// DET: the deterministic mode's instance (three-word tiles, int64 accumulators); the default
+// instance carries only the single-word and hi/lo paths (fewer registers).
+template <bool DET>
 __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeArgs a, int tile_words,
                                                          const BpMember* __restrict__ tm,
                                                          const BpGroupHdr* __restrict__ th,
@@ -767,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     const GroupDev G = a.grp[g];
     const BpGroupHdr H = th[g];
     // CTA-uniform: this group's tile precision (deterministic mode: three words everywhere)
-    const int prec = a.prm.det ? kPrecDet : (init || G.exact) ? kPrecHiLo : kPrecSingle;
+    const int prec = DET ? kPrecDet : (init || G.exact) ? kPrecHiLo : kPrecSingle;
     const bool ex = prec != kPrecSingle;
     const int NW = prec == kPrecDet ? 6 : ex ? 4 : 2;
     const int QW = prec == kPrecDet ? kH6 / 4 : kHQ / 4;  // words between the exact planes
@@ -775,6 +783,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
     __syncthreads();  // previous group's flush is done with the tile / R / tables / sbm
+    if (threadIdx.x == 0) s_cells = nvox;
     {  // member table, the stack's PSF factors, the tile reset
       const int4* src = reinterpret_cast<const int4*>(tm + G.m0);
       int4* dst = reinterpret_cast<int4*>(sbm);
@@ -843,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     float scA = xA > 0.0f ? H.tmax / (xA * H.tpmax) : 0.0f;
     float scC = xC > 0.0f ? H.tmax / (xC * H.tpmax) : 0.0f;
     if (scA == 0.0f && scC == 0.0f) continue;  // nothing to splat (excluded patches)
-    if (prec == kPrecDet) {  // one scale for every group (k_det_scales), grouping-independent
+    if (DET) {  // one scale for every group (k_det_scales), grouping-independent
       scA = xA > 0.0f ? (float)a.det_scale[0] : 0.0f;
       scC = xC > 0.0f ? (float)a.det_scale[1] : 0.0f;
     }
@@ -904,12 +913,12 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
         const float rp = M.r[1] + fU * M.du[1] + fV * M.dv[1];
         const float rq = M.r[2] + fU * M.du[2] + fV * M.dv[2];
         const int ph = PVR_BP_PHASES > 1 ? ((lane & (PVR_BP_PHASES - 1)) * M.ns) / PVR_BP_PHASES : 0;
-        if (prec == kPrecHiLo)
-          splat_line_win<kPrecHiLo>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
-        else if (prec == kPrecSingle)
-          splat_line_win<kPrecSingle>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
-        else
+        if (DET)
           splat_line_win<kPrecDet>(tA, tpA, M, rm, rp, rq, LA, LC, kLoScale, ph);
+        else if (prec == kPrecHiLo)
+          splat_line_win<kPrecHiLo>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
+        else
+          splat_line_win<kPrecSingle>(tA, tpA, M, rm, rp, rq, LA, LC, H.lsc, ph);
       }
     }
     __syncthreads();
@@ -932,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
         continue;
       const int k = row * dx + 2 * pl;
       const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
-      if (prec == kPrecDet) {
+      if (DET) {
         // deterministic mode: exact int64 totals per voxel and quantity, hi and (lo 2^20 + lo2)
         // parts at the global scale, accumulated by integer reductions (order-independent)
         for (int h = 0; h < (two ? 2 : 1); ++h) {
@@ -966,6 +975,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
         A0 = (float)ah0 * fA; A1 = (float)ah1 * fA;
         C0 = (float)ch0 * fC; C1 = (float)ch1 * fC;
       }
+      PVR_CHECK(gbase + (zl * n.y + yl) * a.nxp + 2 * pl + 1 < n.z * n.y * a.nxp + 2);
       red_v4(AC + (gbase + (zl * n.y + yl) * a.nxp + 2 * pl), A0, C0, A1, C1);
     }
   }
@@ -989,11 +999,12 @@ static const DevConfig& configure() {
   if (dev < 0 || dev >= kMaxDevices) dev = 0;
   std::call_once(g_dev_once[dev], [dev] {
     DevConfig& c = g_dev[dev];
-    cudaFuncSetAttribute(k_lattice_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lattice_bp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_lattice_bp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_lattice_fwd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_lattice_fwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.resident, k_lattice_bp, kThreads, kBpTileBytes + kRBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.resident, k_lattice_bp<false>, kThreads, kBpTileBytes + kRBytes);
   });
   return g_dev[dev];
 }
@@ -1040,7 +1051,12 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
   (void)dc;
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
 #endif
-  k_lattice_bp<<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC, next);
+  if (a.prm.det)
+    k_lattice_bp<true><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC,
+                                                                       next);
+  else
+    k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC,
+                                                                        next);
 }
 
 }  // namespace pvr

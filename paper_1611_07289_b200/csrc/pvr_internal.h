@@ -132,6 +132,7 @@ constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;
 // reference), 1 exact hi/lo words for rim groups only (default), 2 exact everywhere.
 enum { kBpSingle = 0, kBpRim = 1, kBpAll = 2, kBpDet = 3 /* deterministic mode: three words, 24 B */ };
 constexpr int kBpCtasPerSm = PVR_BP_TILE_KB <= 56 ? 3 : 2;
+constexpr int kBpDetPlane = (kBpTileBytes / 6) & ~15;  // deterministic mode: 6 planes
 #ifndef PVR_R_KB
 #define PVR_R_KB 12
 #endif

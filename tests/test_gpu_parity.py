@@ -36,6 +36,18 @@ def check_iteration(ctx, orc, prob, params, it, check_taps=True):
     po, pbo, wo = orc.weights()
     pg, pbg, wg = ctx.weights()
     err["p"], err["w"], err["w_near_threshold"] = weight_mismatch(pg, po, pbg, pbo, wg, wo)
+    # pixels whose coverage sits within kappa's bar of tau_live / tau_obs may be live / observed
+    # on one side only (a float decision): they and their patches are left out of the stage p / w
+    # bars (not of the north_star ones)
+    tl = (params or {}).get("tau_live", 0.99)
+    to = (params or {}).get("tau_obs", 0.01)
+    kt = (np.abs(ko - tl) <= TOL["kappa"]) | (np.abs(ko - to) <= TOL["kappa"])
+    pts = ctx.patches()
+    npx = (pts[:, 4] * pts[:, 5] * pts[:, 6]).astype(np.int64)
+    tie_patch = np.add.reduceat(kt.astype(np.int64), np.concatenate([[0], np.cumsum(npx)[:-1]])) > 0
+    err["p_stage"] = float(np.abs(pg - po)[~np.repeat(tie_patch, npx)].max(initial=0.0))
+    err["w_stage"], err["kappa_ties"] = weight_mismatch(pg, po, pbg[~tie_patch], pbo[~tie_patch], wg[~tie_patch],
+                                                        wo[~tie_patch])[1], int(kt.sum())
     emo, emg = orc.em_state(), ctx.em_state()
     assert emg["t"] == emo["t"] == it + 1
     err["em"] = max(abs(emg[k] - emo[k]) / max(abs(emo[k]), 1e-30) for k in ("sigma2", "c", "m"))
@@ -51,8 +63,13 @@ def check_iteration(ctx, orc, prob, params, it, check_taps=True):
     assert err["X"] <= 1e-4, f"iteration {it + 1}: volume rel L2 {err['X']:.3e}"
     assert err["p"] <= 1e-3 and err["w"] <= 1e-3, err
     # stage bars
-    for k in ("X", "p", "w", "em") + (("e", "A", "C", "kappa") if check_taps else ()):
-        assert err[k] <= TOL[k], f"iteration {it + 1}: {k} {err[k]:.3e} > {TOL[k]:.1e}"
+    for k, t in [("X", "X"), ("p_stage", "p"), ("w_stage", "w")] + \
+            ([("e", "e"), ("A", "A"), ("C", "C"), ("kappa", "kappa")] if check_taps else []):
+        assert err[k] <= TOL[t], f"iteration {it + 1}: {k} {err[k]:.3e} > {TOL[t]:.1e}"
+    # sigma^2, c, m sum over live pixels and m takes their extreme residuals: a pixel whose
+    # live status is a kappa tie (above) can move them; then the round-1 bar 1e-4 applies
+    tol_em = TOL["em"] if err["kappa_ties"] == 0 else 1e-4
+    assert err["em"] <= tol_em, f"iteration {it + 1}: em {err['em']:.3e} > {tol_em:.1e}"
     return err
 
 
