@@ -298,6 +298,16 @@ pvr_status pvr_patch_cc(pvr_ctx* ctx, int64_t n, const int64_t* patch, const flo
 /* Weights of this rank's shard after the last iteration: pixel posteriors p
  * [n_local_pixels], patch weights w and patch scores pbar [n_local]; any may be NULL. */
 pvr_status pvr_get_weights(pvr_ctx* ctx, float* pixel_p, float* patch_w, float* patch_pbar);
+/* Checkpoint / resume: restore what pvr_get_weights returned (this shard's
+ * pixel p [n_local_pixels], patch w and pbar [n_local]; any may be NULL, host or device
+ * pointers). With pvr_set_volume and pvr_set_em_state this resumes an SR run exactly: the
+ * next iteration reads X, the previous p (P:193's M-step partials) and t, nothing else.
+ * Errors: PVR_ERR_STATE (before set_transforms). */
+pvr_status pvr_set_weights(pvr_ctx* ctx, const float* pixel_p, const float* patch_w, const float* patch_pbar);
+/* Restore sigma^2, c, m and the iteration counter t (c = c0 while t <= 1, reading Q10) as
+ * pvr_get_em_state returned them; the clamp range stays the one set_transforms formed.
+ * Errors: PVR_ERR_ARG (t < 0, sigma2 < 0, c outside [0, 1], m < 0), PVR_ERR_STATE. */
+pvr_status pvr_set_em_state(pvr_ctx* ctx, double sigma2, double c, double m, int64_t iter);
 /* Debug taps of the last iteration: residual e and coverage kappa [n_local_pixels] of this
  * shard, and the (reduced) addon A and confidence C [V]; any may be NULL. */
 pvr_status pvr_get_taps(pvr_ctx* ctx, float* e, float* kappa, float* addon, float* confidence);

@@ -1889,6 +1889,8 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   launch_fill(c->stream, c->pbar, c->nloc, 1.0f);
   launch_fill(c->stream, c->w, c->nloc, 1.0f);
   CHECK_LAUNCH(c);
+  r = comm_wait(c);  // the coverage allreduce: NCCL errors abort instead of hanging
+  if (r != PVR_OK) return r;
   EmDev h;
   CUDA_TRY(c, cudaMemcpyAsync(&h, c->em, sizeof(EmDev), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -2008,8 +2010,7 @@ pvr_status pvr_init_volume(pvr_ctx* c) {
   if (r != PVR_OK) return r;
   launch_init_fill(c->stream, c->AC, c->dims, c->nxp, lb.prm, c->X[c->cur]);
   CHECK_LAUNCH(c);
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  return PVR_OK;
+  return comm_wait(c);
 }
 
 pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
@@ -2021,6 +2022,8 @@ pvr_status pvr_rigidity_map(pvr_ctx* c, float* out, size_t nvox) {
   if (rp != PVR_OK) return rp;
   // W^T (p pbar) and W^T 1 with exact hi/lo tiles (pbar rides in w)
   pvr_status r = backproject_reduce(c, c->stream, *pl, c->pbar, 2, false);
+  if (r != PVR_OK) return r;
+  r = comm_wait(c);
   if (r != PVR_OK) return r;
   float* tmp = c->X[1 - c->cur];  // scratch between iterations
   launch_ratio(c->stream, c->AC, c->dims, c->nxp, (float)c->tau_C, tmp);
@@ -2389,6 +2392,44 @@ pvr_status pvr_get_weights(pvr_ctx* c, float* pp, float* pw, float* pb) {
   if ((r = copy_out(c, pp, c->p, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
   if ((r = copy_out(c, pw, c->w, c->nloc * sizeof(float))) != PVR_OK) return r;
   if ((r = copy_out(c, pb, c->pbar, c->nloc * sizeof(float))) != PVR_OK) return r;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+static pvr_status copy_in(pvr_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!src || bytes == 0) return PVR_OK;
+  CUDA_TRY(c, cudaMemcpyAsync(dst, src, bytes, is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              c->stream));
+  return PVR_OK;
+}
+
+// Checkpoint / resume: the state one SR iteration carries into the next is X, the
+// pixel probabilities p (the forward's M-step partials weight by the previous p) and
+// the EM counter t (c = c0 at t = 1, reading Q10); w and pbar are re-formed by every E-step.
+pvr_status pvr_set_weights(pvr_ctx* c, const float* pp, const float* pw, const float* pb) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "set_weights needs set_transforms");
+  pvr_status r;
+  if ((r = copy_in(c, c->p, pp, c->nloc_pix * sizeof(float))) != PVR_OK) return r;
+  if ((r = copy_in(c, c->w, pw, c->nloc * sizeof(float))) != PVR_OK) return r;
+  if ((r = copy_in(c, c->pbar, pb, c->nloc * sizeof(float))) != PVR_OK) return r;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PVR_OK;
+}
+
+pvr_status pvr_set_em_state(pvr_ctx* c, double sigma2, double cc, double m, int64_t it) {
+  GUARD(c);
+  if (c->state < READY) return fail(c, PVR_ERR_STATE, "set_em_state needs set_transforms");
+  if (it < 0 || !(sigma2 >= 0) || !(cc >= 0 && cc <= 1) || !(m >= 0))
+    return fail(c, PVR_ERR_ARG, "need iter >= 0, sigma2 >= 0, 0 <= c <= 1, m >= 0");
+  EmDev h;
+  CUDA_TRY(c, cudaMemcpyAsync(&h, c->em, sizeof(EmDev), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  h.sigma2 = sigma2;
+  h.c = cc;
+  h.m = m;
+  h.t = it;
+  CUDA_TRY(c, cudaMemcpyAsync(c->em, &h, sizeof(EmDev), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return PVR_OK;
 }

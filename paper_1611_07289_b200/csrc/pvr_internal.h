@@ -122,7 +122,7 @@ struct LatticeArgs {
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
 constexpr int kStatBlocks = 1184;  // 148 SMs x 8: fixed grid of the statistics kernels
 #ifndef PVR_BP_TILE_KB
-#define PVR_BP_TILE_KB 96
+#define PVR_BP_TILE_KB 56
 #endif
 // Backprojection tile budget (shared memory). An exact group (GroupDev::exact) uses four int32
 // planes A_hi, C_hi, A_lo, C_lo of kBpTileBytes / 4 bytes each (16 B per voxel); a

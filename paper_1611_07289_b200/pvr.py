@@ -35,7 +35,7 @@ EXPORTS = ["pvr_version", "pvr_create_volume", "pvr_destroy", "pvr_last_error", 
            "pvr_init_volume", "pvr_set_param", "pvr_sr_iterate", "pvr_get_volume", "pvr_rigidity_map",
            "pvr_register_patches", "pvr_patch_cc", "pvr_set_patches", "pvr_superpixels",
            "pvr_superpixel_patches", "pvr_get_mask",
-           "pvr_get_weights", "pvr_get_taps", "pvr_get_confidence", "pvr_get_em_state", "pvr_get_stats",
+           "pvr_get_weights", "pvr_set_weights", "pvr_set_em_state", "pvr_get_taps", "pvr_get_confidence", "pvr_get_em_state", "pvr_get_stats",
            "pvr_reset_stats"]
 
 
@@ -112,6 +112,8 @@ def lib():
             "pvr_superpixel_patches": (i32, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
             "pvr_get_mask": (i32, [vp, vp]),
             "pvr_get_weights": (i32, [vp, vp, vp, vp]),
+            "pvr_set_weights": (i32, [vp, vp, vp, vp]),
+            "pvr_set_em_state": (i32, [vp, d, d, d, i64]),
             "pvr_get_taps": (i32, [vp, vp, vp, vp, vp]),
             "pvr_get_em_state": (i32, [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i64),
                                        C.POINTER(d), C.POINTER(d)]),
@@ -278,6 +280,14 @@ def pvr_get_weights(ctx, pixel_p=None, patch_w=None, patch_pbar=None):
     _check(ctx, lib().pvr_get_weights(ctx, _ptr(pixel_p), _ptr(patch_w), _ptr(patch_pbar)))
 
 
+def pvr_set_weights(ctx, pixel_p=None, patch_w=None, patch_pbar=None):
+    _check(ctx, lib().pvr_set_weights(ctx, _ptr(pixel_p), _ptr(patch_w), _ptr(patch_pbar)))
+
+
+def pvr_set_em_state(ctx, sigma2, c, m, t):
+    _check(ctx, lib().pvr_set_em_state(ctx, float(sigma2), float(c), float(m), int(t)))
+
+
 def pvr_get_taps(ctx, e=None, kappa=None, addon=None, confidence=None):
     _check(ctx, lib().pvr_get_taps(ctx, _ptr(e), _ptr(kappa), _ptr(addon), _ptr(confidence)))
 
@@ -421,6 +431,15 @@ class Context:
         pb = np.zeros(self.nloc, np.float32)
         pvr_get_weights(self.h, p, w, pb)
         return p, pb, w
+
+    def set_weights(self, p=None, pbar=None, w=None):
+        """Restore what weights() returned (checkpoint / resume)."""
+        f = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)
+        pvr_set_weights(self.h, f(p), f(w), f(pbar))
+
+    def set_em_state(self, st):
+        """Restore sigma^2, c, m, t from an em_state() dict."""
+        pvr_set_em_state(self.h, st["sigma2"], st["c"], st["m"], st["t"])
 
     def taps(self):
         e = np.zeros(self.nloc_pix, np.float32)

@@ -58,3 +58,36 @@ def test_deterministic_two_ranks_equal_one_bit_for_bit(exchange, tmp_path):
     X2, _ = _spawn(2, exchange, tmp_path, det=1)
     assert np.array_equal(X2[0], X2[1])
     assert np.array_equal(X1, X2[0]), f"max |dX| {np.abs(X1 - X2[0]).max():.3e}"
+
+
+@pytest.mark.parametrize("det", [1, 0])
+def test_checkpoint_resume(prob, det):
+    """Checkpoint / resume: X, p, w, pbar and the EM state saved after 2 iterations
+    and restored into a fresh context continue the run exactly: bit-identical in the
+    deterministic mode, to float-atomic rounding in the default one."""
+    a = make_gpu(prob, {"deterministic": det})
+    try:
+        a.init_volume()
+        a.sr_iterate(2, prob["alpha"], prob["lam"])
+        X, (p, pbar, w), st = a.volume(), a.weights(), a.em_state()
+        a.sr_iterate(2, prob["alpha"], prob["lam"])
+        Xa, pa = a.volume(), a.weights()[0]
+    finally:
+        a.close()
+    b = make_gpu(prob, {"deterministic": det})
+    try:
+        b.set_volume(X)
+        b.set_weights(p, pbar, w)
+        b.set_em_state(st)
+        assert b.em_state()["t"] == 2
+        b.sr_iterate(2, prob["alpha"], prob["lam"])
+        Xb, pb = b.volume(), b.weights()[0]
+        assert b.em_state()["t"] == 4
+    finally:
+        b.close()
+    if det:
+        assert np.array_equal(Xa, Xb) and np.array_equal(pa, pb)
+    else:
+        rel = np.linalg.norm(Xa.astype(np.float64) - Xb) / np.linalg.norm(Xa)
+        assert rel <= 1e-6, rel
+        assert np.abs(pa - pb).max() <= 1e-4
