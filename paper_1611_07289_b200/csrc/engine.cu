@@ -116,8 +116,9 @@ Nccl g_nccl;
 struct Trace {
   bool on = getenv("PVR_TRACE") != nullptr;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
+  void mark(const char* what, cudaStream_t sync = nullptr) {
     if (!on) return;
+    if (sync) cudaStreamSynchronize(sync);  // attribute the device work queued so far
     const auto n = std::chrono::steady_clock::now();
     fprintf(stderr, "[pvr] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
     t = n;
@@ -185,6 +186,9 @@ struct pvr_ctx {
   pvr_host_collective_fn host_fn = nullptr;
   void* host_user = nullptr;
   char* host_buf = nullptr;     // pinned staging buffer of the host collectives
+  PatchDev* pd_host = nullptr;  // pinned staging of the composed patch geometry (set_transforms)
+  int64_t pd_host_n = 0;
+  cudaEvent_t pd_copied = nullptr;  // its last host -> device copy (reuse waits on it)
   size_t host_cap = 0;
   int exchange = PVR_EXCHANGE_ALLREDUCE;  // C2 scheme (PVR_PARAM_EXCHANGE)
   double comm_timeout = 300.0;  // seconds an NCCL wait may take before the communicator is aborted
@@ -1240,6 +1244,8 @@ pvr_status pvr_destroy(pvr_ctx* c) {
       for (auto e : slot) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
   if (c->host_buf) cudaFreeHost(c->host_buf);
+  if (c->pd_host) cudaFreeHost(c->pd_host);
+  if (c->pd_copied) cudaEventDestroy(c->pd_copied);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return PVR_OK;
@@ -1727,9 +1733,19 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   }
   // compose, per patch, in fp64: voxel index of lattice point (a,b,c) of pixel (u,v,z) is
   // g(T_s(G (x0+u, y0+v, z0+z, 1) + a h_u u^ + b h_v v^ + c h_w w^)), g(x) = (x - o) / s
-  std::vector<PatchDev> pd(c->nloc);
+  if (!c->pd_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&c->pd_copied, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventSynchronize(c->pd_copied));  // the previous copy out of the buffer is done
+  if (c->pd_host_n < c->nloc) {
+    if (c->pd_host) cudaFreeHost(c->pd_host);
+    c->pd_host = nullptr;
+    c->pd_host_n = 0;
+    CUDA_TRY(c, cudaMallocHost(&c->pd_host, std::max<int64_t>(c->nloc, 1) * sizeof(PatchDev)));
+    c->pd_host_n = c->nloc;
+  }
+  PatchDev* pd = c->pd_host;
   std::vector<PatchGeo> geo(c->nloc);
   const double is = 1.0 / c->s;
+#pragma omp parallel for schedule(static) if (c->nloc >= 2048)
   for (int64_t s = 0; s < c->nloc; ++s) {
     const HostPatch& hp = c->patches[c->first + s];
     const HostStack& st = c->stacks[hp.stack];
@@ -1780,9 +1796,10 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
       q.Qcd[d] = g.Qc[d];
     }
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd.data(), pd.size() * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->pdev, pd, c->nloc * sizeof(PatchDev), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->pd_copied, c->stream));
   ++c->geo_epoch;  // the backprojection tables are rebuilt by the next backprojection
-  tr.mark("compose patches");
+  tr.mark("compose patches", c->stream);
   pvr_status r = PVR_OK;
   if (c->psf_mode == 2) {
     // volume-space PSF (reading Q34): per patch the fp64 pixel-centre map, the inverse map of
@@ -1870,7 +1887,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   c->iplan_valid = false;
   c->geo.swap(geo);
   c->Tloc = Th;
-  tr.mark("build plans");
+  tr.mark("build plans", c->stream);
   r = encode_tmaps(c);
   if (r != PVR_OK) return r;
   tr.mark("tensor maps");
@@ -1878,6 +1895,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   const LatticeArgs la = lattice_args(c, c->fplan);
   launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
   CHECK_LAUNCH(c);
+  tr.mark("coverage", c->stream);
   }
   launch_em_reduce(c->stream, c->partials, kStatBlocks, c->em);
   CHECK_LAUNCH(c);

@@ -27,7 +27,9 @@ __global__ void k_range_finish(double s2floor, EmDev* em) {
   em->m = 0.0;
 }
 
-// Deterministic reduction of the forward partials into em->stats (one CTA).
+// Fixed-order reduction of the forward's per-block partials into em->stats (one CTA). The blocks
+// claim groups dynamically, so the partials (and sigma^2, c, m) reproduce bit for bit only in
+// PVR_PARAM_DETERMINISTIC mode, where every term sits on a fixed grid (reading Q35).
 __global__ void k_em_reduce(const double* partials, int nblk, EmDev* em) {
   __shared__ double sh[5][32];
   double a[5] = {0.0, 0.0, 0.0, -DBL_MAX, -DBL_MAX};

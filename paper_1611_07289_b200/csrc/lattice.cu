@@ -175,19 +175,6 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     // aligned); the box covers the group footprint (engine.cu: size_groups)
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = (dx * dy + 31) & ~31;
     __syncthreads();  // the previous group's readers of sT / tables / sm are done
-    if (MODE == 1 && !G.interior) {
-      // the grid indicator over the same layout (interior groups: kappa = 1, no lattice pass)
-      int ly = threadIdx.x >> 5, lz = 0;  // row = lz * dy + ly, advanced without division
-      while (ly >= dy) { ly -= dy; ++lz; }
-      for (int row = threadIdx.x >> 5; row < dy * dz; row += kThreads >> 5) {
-        const int gy = G.lo[1] + ly, gz = G.lo[2] + lz;
-        const bool rin = (unsigned)gy < (unsigned)n.y && (unsigned)gz < (unsigned)n.z;
-        for (int lx = threadIdx.x & 31; lx < dx; lx += 32)
-          sX[lz * dxy + ly * dx + lx] = (rin && (unsigned)(G.lo[0] + lx) < (unsigned)n.x) ? 1.0f : 0.0f;
-        ly += kThreads >> 5;
-        while (ly >= dy) { ly -= dy; ++lz; }
-      }
-    }
     // member constants (one thread per member) and the stack's PSF tables
     if (threadIdx.x < G.nm) {
       const MemberDev m = a.mem[G.m0 + threadIdx.x];
@@ -285,9 +272,35 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       const f2 qcxy = pk(f.qc[0], f.qc[1]);
       const float qcz = f.qc[2];
       const f2 mag = pk(kMagic, kMagic);
-      const float* sXo = sX + f.ob[2] * dxy + f.ob[1] * dx + f.ob[0];
       const float2* tpc = s_tpc + (f.skew ? (iv & 3) : 0);
       float acc = 0.0f;
+      if (MODE == 1) {
+        // coverage: the trilinear interpolant of the grid indicator is separable, per axis
+        // (1 - f) [i in grid] + f [i + 1 in grid] at the floor i and fraction f of the forward's
+        // own sample positions -- no tile, no shared loads
+        const int gx = G.lo[0] + f.ob[0], gy = G.lo[1] + f.ob[1], gz = G.lo[2] + f.ob[2];
+#pragma unroll kFwdUnroll
+        for (int k = 0; k < ntp; ++k) {
+          const float2 q = tpc[k];
+          const f2 rxy = fma2s(q.y, qcxy, rxy0);
+          const float rzc = fmaf(q.y, qcz, rz);
+          const f2 txy = add2_rd(rxy, mag);
+          const float tz = __fadd_rd(rzc, kMagic);
+          const int ix = gx + __float_as_int(lo2(txy)) - kMagicBits;
+          const int iy = gy + __float_as_int(hi2(txy)) - kMagicBits;
+          const int iz = gz + __float_as_int(tz) - kMagicBits;
+          const f2 fxy = sub2(rxy, sub2(txy, mag));
+          const float fz = rzc - __fsub_rn(tz, kMagic);
+          const float fx = lo2(fxy), fy = hi2(fxy);
+          const float wx = ((unsigned)ix < (unsigned)n.x ? 1.0f - fx : 0.0f) + ((unsigned)(ix + 1) < (unsigned)n.x ? fx : 0.0f);
+          const float wy = ((unsigned)iy < (unsigned)n.y ? 1.0f - fy : 0.0f) + ((unsigned)(iy + 1) < (unsigned)n.y ? fy : 0.0f);
+          const float wz = ((unsigned)iz < (unsigned)n.z ? 1.0f - fz : 0.0f) + ((unsigned)(iz + 1) < (unsigned)n.z ? fz : 0.0f);
+          acc = fmaf(q.x, wx * wy * wz, acc);
+        }
+        sT[f.t0 + iv * f.LU + iu] = acc;
+        continue;
+      }
+      const float* sXo = sX + f.ob[2] * dxy + f.ob[1] * dx + f.ob[0];
 #pragma unroll kFwdUnroll
       for (int k = 0; k < ntp; ++k) {
         const float2 q = tpc[k];
@@ -1012,7 +1025,8 @@ static const DevConfig& configure() {
 void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, float* kap,
                      double* partials) {
   (void)configure();
-  const int smem = (t_floats + x_floats) * 4;
+  (void)x_floats;  // coverage interpolates the grid indicator analytically: no X tile
+  const int smem = t_floats * 4;
   k_lattice_fwd<1><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, nullptr, nullptr, nullptr, kap,
                                                         partials, nullptr);
 }
