@@ -130,6 +130,8 @@ struct Trace {
 struct pvr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;       // set_transforms: the backprojection tables, beside coverage
+  cudaEvent_t ev_geo = nullptr, ev_tab = nullptr;
   bool own_stream = false;
   int3 dims;
   int nxp = 0;  // row pitch of X and (A, C): nx rounded up to a multiple of 4 (TMA: 16-byte rows)
@@ -161,6 +163,7 @@ struct pvr_ctx {
   struct Plan {
     int TU = 16, TV = 16, nseg = 1;
     int ngroups = 0, nsplit = 0;
+    int max_nm = kMaxGroupMembers;  // most members in one group (the table kernel's segment width)
     int tile_words = 0, r_bytes = 0, t_floats = 0;
     MemberDev* mem = nullptr;
     GroupDev* grp = nullptr;
@@ -1058,6 +1061,8 @@ pvr_status upload_plan(pvr_ctx* c, pvr_ctx::Plan& pl, const PlanBuild& pb, size_
   pl.nmem = (int64_t)pb.mem.size();
   ++c->geo_epoch;
   pl.nsplit = pb.nsplit;
+  pl.max_nm = 1;
+  for (const GroupDev& gd : pb.grp) pl.max_nm = std::max(pl.max_nm, (int)gd.nm);
   pl.tile_words = (int)((pb.max_tile_vox + 3) & ~int64_t(3));
   pl.r_bytes = (int)((pb.max_r_bytes + 15) & ~int64_t(15));
   pl.t_floats = (int)((pb.max_t_floats + 31) & ~int64_t(31));  // 128-byte aligned X tile after it
@@ -1246,6 +1251,12 @@ pvr_status pvr_destroy(pvr_ctx* c) {
   if (c->host_buf) cudaFreeHost(c->host_buf);
   if (c->pd_host) cudaFreeHost(c->pd_host);
   if (c->pd_copied) cudaEventDestroy(c->pd_copied);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+  }
+  if (c->ev_geo) cudaEventDestroy(c->ev_geo);
+  if (c->ev_tab) cudaEventDestroy(c->ev_tab);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return PVR_OK;
@@ -1718,6 +1729,7 @@ pvr_status pvr_get_patches(const pvr_ctx* c, int32_t* out) {
 }
 
 static pvr_status replan_on_device(pvr_ctx* c);
+static pvr_status prebuild_bp_table(pvr_ctx* c);
 
 pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   GUARD(c);
@@ -1801,6 +1813,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   ++c->geo_epoch;  // the backprojection tables are rebuilt by the next backprojection
   tr.mark("compose patches", c->stream);
   pvr_status r = PVR_OK;
+  int nblk = kStatBlocks;  // per-block partials written by the coverage pass
   if (c->psf_mode == 2) {
     // volume-space PSF (reading Q34): per patch the fp64 pixel-centre map, the inverse map of
     // index offsets to slice-frame offsets and the support box; no lattice plans
@@ -1891,13 +1904,16 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   r = encode_tmaps(c);
   if (r != PVR_OK) return r;
   tr.mark("tensor maps");
+  r = prebuild_bp_table(c);
+  if (r != PVR_OK) return r;
   // coverage kappa (geometry only) + live-y range, then the EM reset
   const LatticeArgs la = lattice_args(c, c->fplan);
-  launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
+  nblk = launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
   CHECK_LAUNCH(c);
+  if (c->bplan.ngroups > 0) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_tab, 0));  // the tables
   tr.mark("coverage", c->stream);
   }
-  launch_em_reduce(c->stream, c->partials, kStatBlocks, c->em);
+  launch_em_reduce(c->stream, c->partials, nblk, c->em);
   CHECK_LAUNCH(c);
   r = allreduce_stats(c);
   if (r != PVR_OK) return r;
@@ -1936,8 +1952,8 @@ pvr_status pvr_set_volume(pvr_ctx* c, const float* x, size_t nvox) {
 }
 
 // Backprojection with the plan's member tables, rebuilt first when the geometry changed.
-pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const LatticeArgs& lb, const float* w,
-                       int init) {
+// The plan's member-table buffer (k_bp_table's output), grown on demand.
+static pvr_status ensure_btab(pvr_ctx* c, pvr_ctx::Plan& pl) {
   size_t goff = 0;
   const size_t bytes = bp_table_bytes(pl.nmem, pl.ngroups, &goff);
   if (bytes > pl.btab_cap) {
@@ -1950,8 +1966,38 @@ pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const Latt
   }
   if (pl.btab_goff != goff) pl.btab_epoch = 0;
   pl.btab_goff = goff;
+  return PVR_OK;
+}
+
+// set_transforms: build the iteration plan's member tables on the auxiliary stream (after the
+// geometry upload and re-plan on the main stream), so that they overlap the coverage pass;
+// the main stream joins them (ev_tab) before set_transforms returns.
+static pvr_status prebuild_bp_table(pvr_ctx* c) {
+  pvr_ctx::Plan& pl = c->bplan;
+  if (pl.ngroups <= 0) return PVR_OK;
+  pvr_status r = ensure_btab(c, pl);
+  if (r != PVR_OK) return r;
+  if (!c->aux) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  if (!c->ev_geo) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_geo, cudaEventDisableTiming));
+  if (!c->ev_tab) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_tab, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventRecord(c->ev_geo, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->aux, c->ev_geo, 0));
+  launch_bp_table(c->aux, lattice_args(c, pl), pl.btab, pl.btab_goff, pl.max_nm);
+  CHECK_LAUNCH(c);
+  CUDA_TRY(c, cudaEventRecord(c->ev_tab, c->aux));
+  pl.btab_epoch = c->geo_epoch;
+  c->st.kernel_launches += 1;
+  return PVR_OK;
+}
+
+pvr_status backproject(pvr_ctx* c, cudaStream_t s, pvr_ctx::Plan& pl, const LatticeArgs& lb, const float* w,
+                       int init) {
+  pvr_status r = ensure_btab(c, pl);
+  if (r != PVR_OK) return r;
+  const size_t goff = pl.btab_goff;
   const bool build = pl.btab_epoch != c->geo_epoch;
-  launch_backproject(s, lb, pl.tile_words, pl.r_bytes, pl.btab, goff, build, c->kap, c->e, c->p, w, init, c->AC);
+  launch_backproject(s, lb, pl.tile_words, pl.r_bytes, pl.btab, goff, build, pl.max_nm, c->kap, c->e, c->p, w, init,
+                     c->AC);
   CHECK_LAUNCH(c);
   if (build) {
     pl.btab_epoch = c->geo_epoch;

@@ -154,14 +154,15 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
           "l"(tm), "r"(Gt.lo[0]), "r"(Gt.lo[1]), "r"(Gt.lo[2] + z), "r"(bar)
           : "memory");
   };
-  // MODE 0 with PVR_FWD_DYN: thread 0 claims each CTA's next group from a launch counter (reset
-  // before the launch) when it issues that group's TMA copy; groups differ in cost, so a static
-  // stride leaves SMs idle at the end. s_gn is published by the barrier at the loop top.
-  constexpr bool kDyn = MODE == 0 && PVR_FWD_DYN;
+  // PVR_FWD_DYN: thread 0 claims each CTA's next group from a launch counter (reset before the
+  // launch; MODE 0: when it issues that group's TMA copy); groups differ in cost (coverage:
+  // interior groups skip the lattice pass), so a static stride leaves SMs idle at the end.
+  // s_gn is published by the barrier at the loop top.
+  constexpr bool kDyn = PVR_FWD_DYN;
   __shared__ int s_gn;
-  if (MODE == 0 && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     s_gn = kDyn ? atomicAdd(next, 1) : (int)blockIdx.x;
-    if (s_gn < a.ngroups) issue_tma(s_gn);
+    if (MODE == 0 && s_gn < a.ngroups) issue_tma(s_gn);
   }
 
   for (int g = blockIdx.x;; g += gridDim.x) {
@@ -327,9 +328,9 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       sT[f.t0 + iv * f.LU + iu] = acc;
     }
     __syncthreads();
-    if (MODE == 0 && threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
       s_gn = kDyn ? atomicAdd(next, 1) : g + (int)gridDim.x;
-      if (s_gn < a.ngroups) issue_tma(s_gn);
+      if (MODE == 0 && s_gn < a.ngroups) issue_tma(s_gn);
     }
     // pixels of all members: yhat = sum_ab ip(a,b) T(nu u + a, nv v + b) / kappa
     const int w2 = 2 * ps.ru + 1;
@@ -616,13 +617,17 @@ __device__ __forceinline__ void splat_line_win(unsigned tA, unsigned s_tp, const
 }
 
 // Member tables of all groups of a backprojection plan (geometry only: rebuilt after every
-// set_transforms / re-plan, reused by every iteration). One warp per group, one lane per
-// member; the flattened line / pixel ranges by warp scans.
+// set_transforms / re-plan, reused by every iteration). One W-lane segment of a warp per group
+// (W >= the plan's largest member count: c3 groups have ~3 members, so W = 4 puts 8 groups in
+// a warp), one lane per member; the flattened line / pixel ranges by segment scans.
+template <int W>
 __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* __restrict__ tm,
                                                       BpGroupHdr* __restrict__ th) {
-  const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x * (kThreads >> 5) + (threadIdx.x >> 5);
-  if (g >= a.ngroups) return;  // uniform per warp
+  static_assert(W >= 1 && W <= 32 && (W & (W - 1)) == 0, "segment width: a power of two <= 32");
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned seg = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
+  const int g = (int)((blockIdx.x * blockDim.x + threadIdx.x) / W);
+  if (g >= a.ngroups) return;  // uniform per segment
   const GroupDev G = a.grp[g];
   if (G.nm == 0) {  // emptied by a device re-plan split (engine.cu: replan_on_device)
     if (lane == 0) {
@@ -711,18 +716,18 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     flb = fminf(ceilf(2.0f / qm) + 2.0f, (float)M.ns + 1.0f) * nlines;
   }
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    nterm = fmaxf(nterm, __shfl_xor_sync(0xffffffffu, nterm, d));
-    hib += __shfl_xor_sync(0xffffffffu, hib, d);
-    flb += __shfl_xor_sync(0xffffffffu, flb, d);
+  for (int d = W / 2; d > 0; d >>= 1) {
+    nterm = fmaxf(nterm, __shfl_xor_sync(seg, nterm, d, W));
+    hib += __shfl_xor_sync(seg, hib, d, W);
+    flb += __shfl_xor_sync(seg, flb, d, W);
   }
   int sl = nl, sp = np;  // inclusive scans over the members
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int tl = __shfl_up_sync(0xffffffffu, sl, d), tp = __shfl_up_sync(0xffffffffu, sp, d);
+  for (int d = 1; d < W; d <<= 1) {
+    const int tl = __shfl_up_sync(seg, sl, d, W), tp = __shfl_up_sync(seg, sp, d, W);
     if (lane >= d) { sl += tl; sp += tp; }
   }
-  const int tl = __shfl_sync(0xffffffffu, sl, G.nm - 1), tpx = __shfl_sync(0xffffffffu, sp, G.nm - 1);
+  const int tl = __shfl_sync(seg, sl, G.nm - 1, W), tpx = __shfl_sync(seg, sp, G.nm - 1, W);
   if (lane < G.nm) {
     M.lbeg = sl - nl; M.lend = sl;
     M.pbeg = sp - np; M.pend = sp;
@@ -1022,13 +1027,16 @@ static const DevConfig& configure() {
   return g_dev[dev];
 }
 
-void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, float* kap,
-                     double* partials) {
+int launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, float* kap,
+                    double* partials) {
   (void)configure();
   (void)x_floats;  // coverage interpolates the grid indicator analytically: no X tile
   const int smem = t_floats * 4;
-  k_lattice_fwd<1><<<kStatBlocks, kThreads, smem, st>>>(a, t_floats, nullptr, nullptr, nullptr, kap,
-                                                        partials, nullptr);
+  int* next = reinterpret_cast<int*>(partials + kStatBlocks * 5);  // the launch's group counter
+  const int grid = kStatBlocks;
+  if (PVR_FWD_DYN) cudaMemsetAsync(next, 0, sizeof(int), st);
+  k_lattice_fwd<1><<<grid, kThreads, smem, st>>>(a, t_floats, nullptr, nullptr, nullptr, kap, partials, next);
+  return grid;
 }
 
 void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, const void* tmaps,
@@ -1047,16 +1055,31 @@ size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off) {
   return m + (size_t)ngroups * sizeof(BpGroupHdr) + 16;  // + the launch's group counter
 }
 
+void launch_bp_table(cudaStream_t st, const LatticeArgs& a, void* table, size_t group_off, int max_members) {
+  if (a.ngroups <= 0) return;
+  BpMember* tm = static_cast<BpMember*>(table);
+  BpGroupHdr* th = reinterpret_cast<BpGroupHdr*>(static_cast<char*>(table) + group_off);
+  const int64_t threads = (int64_t)a.ngroups * (max_members <= 4 ? 4 : max_members <= 8 ? 8 : max_members <= 16 ? 16 : 32);
+  const int grid = (int)((threads + kThreads - 1) / kThreads);
+  if (max_members <= 4)
+    k_bp_table<4><<<grid, kThreads, 0, st>>>(a, tm, th);
+  else if (max_members <= 8)
+    k_bp_table<8><<<grid, kThreads, 0, st>>>(a, tm, th);
+  else if (max_members <= 16)
+    k_bp_table<16><<<grid, kThreads, 0, st>>>(a, tm, th);
+  else
+    k_bp_table<32><<<grid, kThreads, 0, st>>>(a, tm, th);
+}
+
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
-                        void* table, size_t group_off, bool build_table, const float* kap,
+                        void* table, size_t group_off, bool build_table, int max_members, const float* kap,
                         const float* e, const float* p, const float* w, int init, float2* AC) {
   if (a.ngroups <= 0) return;
   const DevConfig& dc = configure();
   BpMember* tm = static_cast<BpMember*>(table);
   BpGroupHdr* th = reinterpret_cast<BpGroupHdr*>(static_cast<char*>(table) + group_off);
   int* next = reinterpret_cast<int*>(th + a.ngroups);
-  const int wpb = kThreads >> 5;
-  if (build_table) k_bp_table<<<(a.ngroups + wpb - 1) / wpb, kThreads, 0, st>>>(a, tm, th);
+  if (build_table) launch_bp_table(st, a, table, group_off, max_members);
 #if PVR_BP_DYN
   const int per = dc.nsm * (dc.resident > 0 ? dc.resident : 1);
   const int grid = a.ngroups < per ? a.ngroups : per;

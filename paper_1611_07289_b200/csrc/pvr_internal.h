@@ -185,8 +185,9 @@ void launch_volpsf(cudaStream_t st, int mode, const struct VolPatch* VP, int64_t
                    const float* X, float* kap, float* vin, const float* pprev, float* e, double* partials,
                    const float* w, const float* p, int init, float2* AC);
 // lattice.cu
-void launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
-                     float* kap, double* partials);
+// returns the grid it launched: the number of per-block partials to reduce
+int launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
+                    float* kap, double* partials);
 // tmaps: device array of CUtensorMap (128 B each), one per box shape (GroupDev::tmap), over
 // the X buffer to read
 void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats,
@@ -198,9 +199,12 @@ void launch_forward(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_f
 // group headers at byte `group_off`, then the launch's int group counter), geometry only:
 // rebuilt by this launch when `build_table` (after a set_transforms / re-plan), else reused.
 size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off);
+// Member tables of a backprojection plan alone (geometry only): set_transforms builds them on an
+// auxiliary stream, overlapped with the coverage pass.
+void launch_bp_table(cudaStream_t st, const LatticeArgs& a, void* table, size_t group_off, int max_members);
 // Each group's tile precision is GroupDev::exact (init / rigidity passes: always exact).
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
-                        void* table, size_t group_off, bool build_table, const float* kap,
+                        void* table, size_t group_off, bool build_table, int max_members, const float* kap,
                         const float* e, const float* p, const float* w, int init, float2* AC);
 // superpixels.cu (f3): SLIC labels [K][H][W] (device) of one stack (device), synchronous
 cudaError_t slic_stack(cudaStream_t st, const float* y, int W, int H, int K, int S, int m, int iters,
