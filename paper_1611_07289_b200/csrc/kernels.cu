@@ -392,30 +392,65 @@ __global__ void __launch_bounds__(256) k_update(const float* __restrict__ X0,
   const int bx = blockIdx.x * kUX - 1, by = blockIdx.y * kUY - 1, bz = zlo + blockIdx.z * kUZ - 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   bool cov = true;
-  for (int r = wid; r < kHY * kHZ; r += 8) {
-    const int hz = r / kHY, hy = r - hz * kHY;
-    const int j = by + hy, l = bz + hz;
-    const bool rin = (unsigned)j < (unsigned)n.y && (unsigned)l < (unsigned)n.z;
-    const int row = (l * n.y + j) * nxp;  // < 2^31 voxels
+  // halo rows: a warp takes rows wid, wid + 8, ... on the 32 interior columns, and thread t <
+  // 2 rows takes the halo column cell (row t / 2, side t % 2); every load is issued before any
+  // is used (the load phase was latency-bound with one row's loads in flight per warp: 70% of
+  // the kernel's stall samples)
+  constexpr int kRows = kHY * kHZ, kRW = (kRows + 7) / 8;
+  static_assert(2 * kRows <= 256, "one halo-column cell per thread");
+  float rx0[kRW], ra[kRW], rc[kRW];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (q == 1 && lane >= 2) break;
-      const int hx = q == 0 ? lane + 1 : (lane == 0 ? 0 : kHX - 1);
-      const int i = bx + hx;
-      float x0 = 0.0f, x1 = __int_as_float(0x7fc00000);
-      if (rin && (unsigned)i < (unsigned)n.x) {
-        x0 = X0[row + i];
-        const float2 ac = AC[row + i];
-        if (ac.y > prm.tau_C) {
-          float x = fmaf(alpha * ac.x, rcp_ftz(ac.y), x0);  // a6: X1 = clip(X0 + alpha A / C)
-          if (prm.clamp) x = fminf(fmaxf(x, lo), hi);
-          x1 = x;
-        }
-      }
-      cov = cov && (x1 == x1);
-      s0[r * kHX + hx] = x0;
-      s1[r * kHX + hx] = x1;
+  for (int t = 0; t < kRW; ++t) {
+    const int r = wid + 8 * t;
+    rx0[t] = 0.0f; ra[t] = 0.0f; rc[t] = 0.0f;
+    const int hz = r / kHY, hy = r - hz * kHY;
+    const int j = by + hy, l = bz + hz, i = bx + lane + 1;
+    if (r < kRows && (unsigned)j < (unsigned)n.y && (unsigned)l < (unsigned)n.z && (unsigned)i < (unsigned)n.x) {
+      const int row = (l * n.y + j) * nxp;  // < 2^31 voxels
+      rx0[t] = __ldg(X0 + row + i);
+      const float2 ac = __ldg(AC + row + i);
+      ra[t] = ac.x;
+      rc[t] = ac.y;
     }
+  }
+  const int hr = threadIdx.x >> 1, hxh = (threadIdx.x & 1) ? kHX - 1 : 0;
+  float hx0 = 0.0f, ha = 0.0f, hc = 0.0f;
+  {
+    const int hz = hr / kHY, hy = hr - hz * kHY;
+    const int j = by + hy, l = bz + hz, i = bx + hxh;
+    if (hr < kRows && (unsigned)j < (unsigned)n.y && (unsigned)l < (unsigned)n.z && (unsigned)i < (unsigned)n.x) {
+      const int row = (l * n.y + j) * nxp;
+      hx0 = __ldg(X0 + row + i);
+      const float2 ac = __ldg(AC + row + i);
+      ha = ac.x;
+      hc = ac.y;
+    }
+  }
+  // a6: X1 = clip(X0 + alpha A / C) where C > tau_C (>= 0), else NaN (uncovered;
+  // off-grid cells read C = 0)
+  auto x1_of = [&](float x0, float a, float c) {
+    float x = __int_as_float(0x7fc00000);
+    if (c > prm.tau_C) {
+      x = fmaf(alpha * a, rcp_ftz(c), x0);
+      if (prm.clamp) x = fminf(fmaxf(x, lo), hi);
+    }
+    return x;
+  };
+#pragma unroll
+  for (int t = 0; t < kRW; ++t) {
+    const int r = wid + 8 * t;
+    if (r < kRows) {
+      const float x1 = x1_of(rx0[t], ra[t], rc[t]);
+      cov = cov && (x1 == x1);
+      s0[r * kHX + lane + 1] = rx0[t];
+      s1[r * kHX + lane + 1] = x1;
+    }
+  }
+  if (hr < kRows) {
+    const float h1 = x1_of(hx0, ha, hc);
+    cov = cov && (h1 == h1);
+    s0[hr * kHX + hxh] = hx0;
+    s1[hr * kHX + hxh] = h1;
   }
   const bool allc = __syncthreads_and(cov);
   const float al = alpha * lambda;

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
   __shared__ float2 s_tpc[2 * kMaxTp + 4];  // (tp(i mod ntp), i mod ntp): phase-shifted c loops
   __shared__ FwdMember sm[kMaxMembers];
   __shared__ int s_nt, s_np;  // lattice points / pixels of the group
+  __shared__ float s_tpsum;   // coverage: sum of tp over a line's samples
   __shared__ __align__(8) uint64_t s_bar;  // TMA completion barrier (MODE 0)
   double acc_s[3] = {0.0, 0.0, 0.0};
   float acc_m[2] = {-FLT_MAX, -FLT_MAX};
@@ -229,6 +230,11 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       }
       s_nt = t;
       s_np = p;
+      if (MODE == 1) {  // the weight sum of a line whose samples all interpolate inside the grid
+        float ts = 0.0f;
+        for (int k2 = 0; k2 < 2 * a.psf[a.P[a.mem[G.m0].patch].stack].cmax + 1; ++k2) ts += s_tpc[k2].x;
+        s_tpsum = ts;
+      }
     }
     if (MODE == 0) {  // the X tile has landed
       unsigned done = 0;
@@ -280,6 +286,22 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         // (1 - f) [i in grid] + f [i + 1 in grid] at the floor i and fraction f of the forward's
         // own sample positions -- no tile, no shared loads
         const int gx = G.lo[0] + f.ob[0], gy = G.lo[1] + f.ob[1], gz = G.lo[2] + f.ob[2];
+        // a line is straight and fma(c, q, r) is monotone in c: when the floors of both end
+        // samples lie in [0, n - 2] on every axis, every sample's 8 corners are in the grid and
+        // the line's sum is sum tp (most lines of a group that merely touches the border)
+        {
+          const float c1 = (float)(ntp - 1);
+          const f2 e0 = add2_rd(rxy0, mag), e1 = add2_rd(fma2s(c1, qcxy, rxy0), mag);
+          const float z0 = __fadd_rd(rz, kMagic), z1 = __fadd_rd(fmaf(c1, qcz, rz), kMagic);
+          const int x0 = gx + __float_as_int(lo2(e0)) - kMagicBits, x1 = gx + __float_as_int(lo2(e1)) - kMagicBits;
+          const int y0 = gy + __float_as_int(hi2(e0)) - kMagicBits, y1 = gy + __float_as_int(hi2(e1)) - kMagicBits;
+          const int zz0 = gz + __float_as_int(z0) - kMagicBits, zz1 = gz + __float_as_int(z1) - kMagicBits;
+          if (min(x0, x1) >= 0 && max(x0, x1) <= n.x - 2 && min(y0, y1) >= 0 && max(y0, y1) <= n.y - 2 &&
+              min(zz0, zz1) >= 0 && max(zz0, zz1) <= n.z - 2) {
+            sT[f.t0 + iv * f.LU + iu] = s_tpsum;
+            continue;
+          }
+        }
 #pragma unroll kFwdUnroll
         for (int k = 0; k < ntp; ++k) {
           const float2 q = tpc[k];
