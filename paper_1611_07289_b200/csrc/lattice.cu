@@ -389,11 +389,12 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         }
       } else {
         const float kk = kap[j];
+        const float ppf = pprev[j];  // issued with kappa's load, not after its test
         float ev = 0.0f;
         if (kk >= a.prm.tau_obs) {
           ev = y - s / kk;
           if (kk >= a.prm.tau_live) {
-            const double pp = pprev[j];
+            const double pp = ppf;
             if (a.prm.det) {
               // deterministic mode: every term on a fixed grid (2^-4, 2^-24): the fp64 sums of
               // these integers (< 2^53) are exact in any order, on any number of ranks
@@ -802,18 +803,32 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
   // persistent CTAs (resident count per SM x SMs) take the next group from the plan's launch
   // counter (after the group headers, reset before every launch): groups differ in cost, and a
   // static stride left SMs idle at the end (bp 14.59 -> 14.22 ms at c3)
+  // The next group is claimed (and its header fetched into shared memory) by thread 0 as soon
+  // as the current group's phase A is done, so the claim's and the header loads' round trips
+  // overlap the splat instead of opening the next group.
   __shared__ int s_next;
+  __shared__ GroupDev s_G;
+  __shared__ BpGroupHdr s_H;
+  auto claim = [&]() {
+    const int gn = atomicAdd(next, 1);
+    if (gn < a.ngroups) {
+      s_G = a.grp[gn];
+      s_H = th[gn];
+    }
+    s_next = gn;
+  };
+  if (threadIdx.x == 0) claim();
   for (;;) {
-    __syncthreads();  // everyone has read s_next of the previous group
-    if (threadIdx.x == 0) s_next = atomicAdd(next, 1);
-    __syncthreads();
+    __syncthreads();  // s_next / s_G / s_H of this group are published; the previous group is done
     const int g = s_next;
     if (g >= a.ngroups) break;
+    const GroupDev G = s_G;
+    const BpGroupHdr H = s_H;
 #else
   for (int g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
-#endif
     const GroupDev G = a.grp[g];
     const BpGroupHdr H = th[g];
+#endif
     // CTA-uniform: this group's tile precision (deterministic mode: three words everywhere)
     const int prec = DET ? kPrecDet : (init || G.exact) ? kPrecHiLo : kPrecSingle;
     const bool ex = prec != kPrecSingle;
@@ -822,7 +837,9 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     int* cbase = ex ? base + QW : base + kCOff / 4;
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2];
     const int nvox = dx * dy * dz;
+#if !PVR_BP_DYN
     __syncthreads();  // previous group's flush is done with the tile / R / tables / sbm
+#endif                // (PVR_BP_DYN: the barrier at the loop top)
     if (threadIdx.x == 0) s_cells = nvox;
     {  // member table, the stack's PSF factors, the tile reset
       const int4* src = reinterpret_cast<const int4*>(tm + G.m0);
@@ -846,26 +863,24 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     float mA = 0.0f, mC = 0.0f;
     {
       const int np = H.np;
-      int mi = 0, wmi = -1;
-      float ws = 0.0f, vs = 1.0f;  // the member's patch weight (1 in the init / rigidity
-                                   // passes), and the rigidity pass's patch score pbar
+      int mi = 0;
       for (int i = threadIdx.x; i < np; i += kThreads) {
         while (i >= sbm[mi].pend) ++mi;
         const BpMember& M = sbm[mi];
-        if (mi != wmi) {
-          wmi = mi;
-          ws = init ? 1.0f : w[M.patch];
-          vs = init == 2 ? w[M.patch] : 1.0f;
-        }
         const int li = i - M.pbeg;
         const int vv = (int)(((float)li + 0.5f) * M.inv_rw);
         const int u = M.plu + (li - vv * M.rw), v = M.plv + vv;
         const int64_t j = M.pixz + (int64_t)v * M.sx + u;
         float rA = 0.0f, rC = 0.0f;
+        // every load is issued before the observed test (one round trip, not two): the
+        // patch weight w (1 in the init / rigidity passes; rigidity: vs = the patch score pbar)
+        const float wm = init == 1 ? 1.0f : w[M.patch];
+        const float ws = init ? 1.0f : wm, vs = init == 2 ? wm : 1.0f;
         const float k = kap[j];
+        const float pj = init == 1 ? 1.0f : p[j];
+        const float val = init == 1 ? a.ys[M.yz + (int64_t)v * M.W + u] : init == 2 ? pj * vs : e[j];
         if (ws != 0.0f && k >= a.prm.tau_obs) {
-          const float pv = init ? 1.0f : p[j];
-          const float val = init == 1 ? a.ys[M.yz + (int64_t)v * M.W + u] : init == 2 ? p[j] * vs : e[j];
+          const float pv = init ? 1.0f : pj;
           rC = ws * pv / k;
           rA = rC * val;
         }
@@ -881,6 +896,10 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
       s_red[1][wid] = mC;
     }
     __syncthreads();
+#if PVR_BP_DYN
+    // every thread holds G and H in registers by now: thread 0 may claim the next group
+    if (threadIdx.x == 0) claim();
+#endif
     float xA = 0.0f, xC = 0.0f;  // every thread forms the same group maxima and scales
 #pragma unroll
     for (int i = 0; i < (kThreads >> 5); ++i) {
