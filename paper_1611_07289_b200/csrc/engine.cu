@@ -421,7 +421,31 @@ LatticeArgs lattice_args(const pvr_ctx* c, const pvr_ctx::Plan& pl) {
   a.prm = make_params(c);
   a.det_scale = c->em ? c->em->det_scale : nullptr;
   a.ACd = c->ACd;
+  a.ftab = pl.btab;  // forward plan: its member rows (build_fwd_table); unused by the others
+  a.fgoff = pl.btab_goff;
   return a;
+}
+
+// The forward plan's member rows and group headers (k_fwd_table), rebuilt when the geometry or
+// the plan changed (the forward plan keeps them in its btab fields).
+pvr_status build_fwd_table(pvr_ctx* c) {
+  pvr_ctx::Plan& pl = c->fplan;
+  if (pl.ngroups <= 0 || pl.btab_epoch == c->geo_epoch) return PVR_OK;
+  size_t goff = 0;
+  const size_t bytes = fwd_table_bytes(pl.nmem, pl.ngroups, &goff);
+  if (bytes > pl.btab_cap) {
+    if (pl.btab) cudaFree(pl.btab);
+    pl.btab = nullptr;
+    pl.btab_cap = 0;
+    CUDA_TRY(c, cudaMalloc(&pl.btab, bytes));
+    pl.btab_cap = bytes;
+  }
+  pl.btab_goff = goff;
+  launch_fwd_table(c->stream, lattice_args(c, pl), pl.btab, goff, pl.max_nm);
+  CHECK_LAUNCH(c);
+  pl.btab_epoch = c->geo_epoch;
+  c->st.kernel_launches += 1;
+  return PVR_OK;
 }
 
 pvr_status nccl_check(pvr_ctx* c, ncclResult_t r, const char* what) {
@@ -556,7 +580,7 @@ void free_dev(pvr_ctx* c) {
     if (s.y_dev) cudaFree(s.y_dev), s.y_dev = nullptr;
   void* ptrs[] = {c->X[0], c->X[1], c->AC, c->e, c->p, c->kap, c->pbar, c->w, c->ys, c->tab,
                   c->psf, c->pdev, c->fplan.mem, c->fplan.grp, c->bplan.mem, c->bplan.grp,
-                  c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
+                  c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab, c->fplan.btab,
                   c->partials, c->em, c->tmaps, c->regP, c->rpart, c->replan_buf, c->fbox_dev, c->nlivep, c->mask,
                   c->ACd, c->vpat, c->vin};
   for (void* q : ptrs)
@@ -1439,7 +1463,7 @@ static pvr_status begin_extraction(pvr_ctx* c) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   void* ptrs[] = {c->e, c->p, c->kap, c->pbar, c->w, c->tab, c->psf, c->pdev, c->fplan.mem, c->fplan.grp,
                   c->bplan.mem, c->bplan.grp, c->iplan.mem, c->iplan.grp, c->bplan.btab, c->iplan.btab,
-                  c->regP, c->rpart, c->nlivep, c->mask, c->vpat, c->vin};
+                  c->fplan.btab, c->regP, c->rpart, c->nlivep, c->mask, c->vpat, c->vin};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   c->e = c->p = c->kap = c->pbar = c->w = c->tab = nullptr;
@@ -1907,6 +1931,8 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   r = prebuild_bp_table(c);
   if (r != PVR_OK) return r;
   // coverage kappa (geometry only) + live-y range, then the EM reset
+  r = build_fwd_table(c);
+  if (r != PVR_OK) return r;
   const LatticeArgs la = lattice_args(c, c->fplan);
   nblk = launch_coverage(c->stream, la, c->fplan.t_floats, c->fplan.tile_words, c->kap, c->partials);
   CHECK_LAUNCH(c);
@@ -2322,6 +2348,10 @@ pvr_status pvr_sr_iterate(pvr_ctx* c, int n, float alpha, float lambda) {
   GUARD(c);
   if (c->state < READY) return fail(c, PVR_ERR_STATE, "sr_iterate needs set_transforms");
   if (n < 0 || !(alpha >= 0) || !(lambda >= 0)) return fail(c, PVR_ERR_ARG, "n, alpha, lambda must be >= 0");
+  if (c->psf_mode != 2) {
+    pvr_status rt = build_fwd_table(c);
+    if (rt != PVR_OK) return rt;
+  }
   const LatticeArgs la = lattice_args(c, c->fplan), lb = lattice_args(c, c->bplan);
   const Params prm = la.prm;
   const bool prof = c->profile != 0;

@@ -93,16 +93,27 @@ constexpr int kMaxMembers = 16;
 #endif
 constexpr int kFwdUnroll = PVR_FWD_UNROLL;  // samples per iteration of the forward's c loop
 
-struct FwdMember {  // per-member constants in shared memory
+// Per-member constants of the forward / coverage, in global memory (k_fwd_table: once per
+// geometry) and copied into shared memory by each group's CTA.
+struct __align__(16) FwdMember {
   float of[3], qa[3], qb[3], qc[3];
   int ob[3];
   int LU, LV, t0, p0;  // lattice extent, offset into sT, first pixel index in the group order
   int patch, z, u0, v0, tu, tv;
-  int sh;              // lattice point order: strips of 2^sh U columns, V-major inside
-                       // (sh = 2 axial-like, 3 x-normal), 0 = rows (U fastest); see the lattice pass
-  int skew;            // x-normal members: the c loop of point (U, V) starts at phase V & 3
+  int sh;              // lattice point order (forward; coverage uses rows): strips of 2^sh U
+                       // columns, V-major inside (sh = 2 axial-like, 3 x-normal), 0 = rows
+  int skew;            // x-normal members (forward): the c loop of point (U, V) starts at phase V & 3
   float inv_LU, inv_s4;  // 1 / LU, 1 / (2^sh LV)
   float inv_tu;          // 1 / tu (pixel index decode)
+  int pad[2];
+};
+static_assert(sizeof(FwdMember) % 16 == 0, "FwdMember is copied as int4");
+
+struct __align__(16) FwdHdr {  // per-group totals and the group's stack PSF constants
+  int nt, np;          // lattice points / pixels of all members
+  int nu, nv, ru, rv, ip0, tp0, cmax;
+  float tpsum;         // sum of tp over a line's samples (coverage: a line inside the grid)
+  int pad[2];
 };
 
 #ifndef PVR_FWD_DYN
@@ -123,8 +134,6 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
   __shared__ float s_ip[kMaxIp];
   __shared__ float2 s_tpc[2 * kMaxTp + 4];  // (tp(i mod ntp), i mod ntp): phase-shifted c loops
   __shared__ FwdMember sm[kMaxMembers];
-  __shared__ int s_nt, s_np;  // lattice points / pixels of the group
-  __shared__ float s_tpsum;   // coverage: sum of tp over a line's samples
   __shared__ __align__(8) uint64_t s_bar;  // TMA completion barrier (MODE 0)
   double acc_s[3] = {0.0, 0.0, 0.0};
   float acc_m[2] = {-FLT_MAX, -FLT_MAX};
@@ -177,63 +186,19 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     // aligned); the box covers the group footprint (engine.cu: size_groups)
     const int dx = G.dim[0], dy = G.dim[1], dz = G.dim[2], dxy = (dx * dy + 31) & ~31;
     __syncthreads();  // the previous group's readers of sT / tables / sm are done
-    // member constants (one thread per member) and the stack's PSF tables
-    if (threadIdx.x < G.nm) {
-      const MemberDev m = a.mem[G.m0 + threadIdx.x];
-      const PatchDev& pt = a.P[m.patch];
-      const StackPsf ps = a.psf[pt.stack];
-      FwdMember& f = sm[threadIdx.x];
-      f.LU = ps.nu * (m.tu - 1) + 2 * ps.ru + 1;
-      f.LV = ps.nv * (m.tv - 1) + 2 * ps.rv + 1;
-      lattice_origin(pt, m.z, ps.nu * m.u0 - ps.ru, ps.nv * m.v0 - ps.rv, -ps.cmax, G.lo, f.ob, f.of);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        f.qa[d] = pt.Qa[d];
-        f.qb[d] = pt.Qb[d];
-        f.qc[d] = pt.Qc[d];
-      }
-      f.patch = m.patch; f.z = m.z; f.u0 = m.u0; f.v0 = m.v0; f.tu = m.tu; f.tv = m.tv;
-      // V along the tile's y axis (axial-like stacks): a warp of row-ordered points straddles
-      // two lattice rows one tile row (dx floats) apart -> bank conflicts; blocks of 4 U x 8 V
-      // points hit 32 distinct banks (rows 4 (mod 8) banks apart). x-normal stacks (c along
-      // x): lanes differ only in y and z, whose tile offsets are multiples of 4 floats (TMA row
-      // pitch), so a warp reaches 8 banks (4 wavefronts per load); blocks of 8 U x 4 V with the
-      // c loop of row V started at phase V & 3 spread the lanes over 4 x offsets
-      // (tools/banksim_forward.py: 4.0 -> 1.5 wavefronts). Other stacks keep rows.
-      const float ab0 = fabsf(pt.Qb[0]), ab1 = fabsf(pt.Qb[1]), ab2 = fabsf(pt.Qb[2]);
-      const float ac0 = fabsf(pt.Qc[0]), ac1 = fabsf(pt.Qc[1]), ac2 = fabsf(pt.Qc[2]);
-      const bool xn = MODE == 0 && ac0 >= ac1 && ac0 >= ac2;
-      f.sh = (MODE == 0 && ab1 >= ab0 && ab1 >= ab2 && f.LU >= 4) ? 2 : (xn && f.LU >= 8 ? 3 : 0);
-      f.skew = xn ? 1 : 0;
-      f.inv_LU = 1.0f / (float)f.LU;
-      f.inv_s4 = 1.0f / (float)((1 << f.sh) * f.LV);
-      f.inv_tu = 1.0f / (float)f.tu;
-    }
+    // member rows and the stack's PSF tables (k_fwd_table)
+    const FwdHdr H = reinterpret_cast<const FwdHdr*>(static_cast<const char*>(a.ftab) + a.fgoff)[g];
     {
-      const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
-      const int nip = (2 * ps.ru + 1) * (2 * ps.rv + 1);
-      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[ps.ip0 + i];
-      const int nt = 2 * ps.cmax + 1;
+      const int4* src = reinterpret_cast<const int4*>(static_cast<const FwdMember*>(a.ftab) + G.m0);
+      int4* dst = reinterpret_cast<int4*>(sm);
+      const int nq = G.nm * (int)(sizeof(FwdMember) / 16);
+      for (int i = threadIdx.x; i < nq; i += kThreads) dst[i] = __ldg(src + i);
+      const int nip = (2 * H.ru + 1) * (2 * H.rv + 1);
+      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[H.ip0 + i];
+      const int nt = 2 * H.cmax + 1;
       for (int i = threadIdx.x; i < 2 * nt + 4; i += kThreads) {
         const int c = i % nt;
-        s_tpc[i] = make_float2(a.tab[ps.tp0 + c], (float)c);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0, p = 0;
-      for (int k = 0; k < G.nm; ++k) {
-        sm[k].t0 = t;
-        sm[k].p0 = p;
-        t += sm[k].LU * sm[k].LV;
-        p += sm[k].tu * sm[k].tv;
-      }
-      s_nt = t;
-      s_np = p;
-      if (MODE == 1) {  // the weight sum of a line whose samples all interpolate inside the grid
-        float ts = 0.0f;
-        for (int k2 = 0; k2 < 2 * a.psf[a.P[a.mem[G.m0].patch].stack].cmax + 1; ++k2) ts += s_tpc[k2].x;
-        s_tpsum = ts;
+        s_tpc[i] = make_float2(a.tab[H.tp0 + c], (float)c);
       }
     }
     if (MODE == 0) {  // the X tile has landed
@@ -247,17 +212,16 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       phase ^= 1u;
     }
     __syncthreads();
-    const StackPsf ps = a.psf[a.P[a.mem[G.m0].patch].stack];
-    const int ntp = 2 * ps.cmax + 1;
+    const int ntp = 2 * H.cmax + 1;
     // lattice points of all members: T(U, V) = sum_c tp(c) trilerp(X, x(U, V, c))
     const bool skip = MODE == 1 && G.interior;
     int k = 0;  // the member of lattice point / pixel i (i only grows)
-    for (int i = skip ? s_nt : threadIdx.x; i < s_nt; i += kThreads) {
+    for (int i = skip ? H.nt : threadIdx.x; i < H.nt; i += kThreads) {
       while (k + 1 < G.nm && i >= sm[k + 1].t0) ++k;
       const FwdMember& f = sm[k];
       const int li = i - f.t0;
       int iu, iv;
-      if (f.sh) {  // strip sidx of 2^sh U columns (the last one narrower), V-major inside
+      if (MODE == 0 && f.sh) {  // strip sidx of 2^sh U columns (the last one narrower), V-major inside
         const int sw = 1 << f.sh;
         const int sidx = (int)(((float)li + 0.5f) * f.inv_s4);
         const int r = li - sidx * sw * f.LV;
@@ -279,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       const f2 qcxy = pk(f.qc[0], f.qc[1]);
       const float qcz = f.qc[2];
       const f2 mag = pk(kMagic, kMagic);
-      const float2* tpc = s_tpc + (f.skew ? (iv & 3) : 0);
+      const float2* tpc = s_tpc + ((MODE == 0 && f.skew) ? (iv & 3) : 0);
       float acc = 0.0f;
       if (MODE == 1) {
         // coverage: the trilinear interpolant of the grid indicator is separable, per axis
@@ -298,7 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
           const int zz0 = gz + __float_as_int(z0) - kMagicBits, zz1 = gz + __float_as_int(z1) - kMagicBits;
           if (min(x0, x1) >= 0 && max(x0, x1) <= n.x - 2 && min(y0, y1) >= 0 && max(y0, y1) <= n.y - 2 &&
               min(zz0, zz1) >= 0 && max(zz0, zz1) <= n.z - 2) {
-            sT[f.t0 + iv * f.LU + iu] = s_tpsum;
+            sT[f.t0 + iv * f.LU + iu] = H.tpsum;
             continue;
           }
         }
@@ -355,9 +319,9 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       if (MODE == 0 && s_gn < a.ngroups) issue_tma(s_gn);
     }
     // pixels of all members: yhat = sum_ab ip(a,b) T(nu u + a, nv v + b) / kappa
-    const int w2 = 2 * ps.ru + 1;
+    const int w2 = 2 * H.ru + 1;
     k = 0;
-    for (int i = threadIdx.x; i < s_np; i += kThreads) {
+    for (int i = threadIdx.x; i < H.np; i += kThreads) {
       while (k + 1 < G.nm && i >= sm[k + 1].p0) ++k;
       const FwdMember& f = sm[k];
       const int li = i - f.p0;
@@ -367,8 +331,8 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       if (skip) {
         s = 1.0f;  // every sample fully in the grid: kappa = sum psi = 1 (reading Q27)
       } else {
-        for (int b = 0; b <= 2 * ps.rv; ++b) {
-          const float* row = sT + f.t0 + (ps.nv * dv + b) * f.LU + ps.nu * du;
+        for (int b = 0; b <= 2 * H.rv; ++b) {
+          const float* row = sT + f.t0 + (H.nv * dv + b) * f.LU + H.nu * du;
           for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
         }
       }
@@ -1066,6 +1030,106 @@ static const DevConfig& configure() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.resident, k_lattice_bp<false>, kThreads, kBpTileBytes + kRBytes);
   });
   return g_dev[dev];
+}
+
+// Forward member rows of all groups of a plan (geometry only: rebuilt after every
+// set_transforms / re-plan, reused by every forward and coverage pass). One W-lane warp
+// segment per group, one lane per member; the lattice-point and pixel offsets by segment scans.
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_fwd_table(LatticeArgs a, FwdMember* __restrict__ fm,
+                                                       FwdHdr* __restrict__ fh) {
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned seg = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1)));
+  const int g = (int)((blockIdx.x * blockDim.x + threadIdx.x) / W);
+  if (g >= a.ngroups) return;  // uniform per segment
+  const GroupDev G = a.grp[g];
+  if (G.nm == 0) {  // emptied by a device re-plan split
+    if (lane == 0) {
+      FwdHdr h = {};
+      fh[g] = h;
+    }
+    return;
+  }
+  FwdMember f = {};
+  StackPsf ps = {};
+  int nt = 0, np = 0;
+  if (lane < G.nm) {
+    const MemberDev m = a.mem[G.m0 + lane];
+    const PatchDev& pt = a.P[m.patch];
+    ps = a.psf[pt.stack];
+    f.LU = ps.nu * (m.tu - 1) + 2 * ps.ru + 1;
+    f.LV = ps.nv * (m.tv - 1) + 2 * ps.rv + 1;
+    lattice_origin(pt, m.z, ps.nu * m.u0 - ps.ru, ps.nv * m.v0 - ps.rv, -ps.cmax, G.lo, f.ob, f.of);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      f.qa[d] = pt.Qa[d];
+      f.qb[d] = pt.Qb[d];
+      f.qc[d] = pt.Qc[d];
+    }
+    f.patch = m.patch; f.z = m.z; f.u0 = m.u0; f.v0 = m.v0; f.tu = m.tu; f.tv = m.tv;
+    // V along the tile's y axis (axial-like stacks): a warp of row-ordered points straddles
+    // two lattice rows one tile row (dx floats) apart -> bank conflicts; blocks of 4 U x 8 V
+    // points hit 32 distinct banks (rows 4 (mod 8) banks apart). x-normal stacks (c along
+    // x): lanes differ only in y and z, whose tile offsets are multiples of 4 floats (TMA row
+    // pitch), so a warp reaches 8 banks (4 wavefronts per load); blocks of 8 U x 4 V with the
+    // c loop of row V started at phase V & 3 spread the lanes over 4 x offsets
+    // (tools/banksim_forward.py: 4.0 -> 1.5 wavefronts). Other stacks keep rows. (Coverage
+    // reads no X tile and walks rows: k_lattice_fwd<1> ignores sh and skew.)
+    const float ab0 = fabsf(pt.Qb[0]), ab1 = fabsf(pt.Qb[1]), ab2 = fabsf(pt.Qb[2]);
+    const float ac0 = fabsf(pt.Qc[0]), ac1 = fabsf(pt.Qc[1]), ac2 = fabsf(pt.Qc[2]);
+    const bool xn = ac0 >= ac1 && ac0 >= ac2;
+    f.sh = (ab1 >= ab0 && ab1 >= ab2 && f.LU >= 4) ? 2 : (xn && f.LU >= 8 ? 3 : 0);
+    f.skew = xn ? 1 : 0;
+    f.inv_LU = 1.0f / (float)f.LU;
+    f.inv_s4 = 1.0f / (float)((1 << f.sh) * f.LV);
+    f.inv_tu = 1.0f / (float)f.tu;
+    nt = f.LU * f.LV;
+    np = f.tu * f.tv;
+  }
+  int st = nt, sp = np;  // inclusive scans over the members
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    const int tt = __shfl_up_sync(seg, st, d, W), tp = __shfl_up_sync(seg, sp, d, W);
+    if (lane >= d) { st += tt; sp += tp; }
+  }
+  const int tot_t = __shfl_sync(seg, st, G.nm - 1, W), tot_p = __shfl_sync(seg, sp, G.nm - 1, W);
+  if (lane < G.nm) {
+    f.t0 = st - nt;
+    f.p0 = sp - np;
+    fm[G.m0 + lane] = f;
+  }
+  if (lane == 0) {  // all members of a group share the stack (and its PSF)
+    FwdHdr h = {};
+    h.nt = tot_t; h.np = tot_p;
+    h.nu = ps.nu; h.nv = ps.nv; h.ru = ps.ru; h.rv = ps.rv;
+    h.ip0 = ps.ip0; h.tp0 = ps.tp0; h.cmax = ps.cmax;
+    float ts = 0.0f;  // in the order of the coverage's c loop
+    for (int c = 0; c < 2 * ps.cmax + 1; ++c) ts += a.tab[ps.tp0 + c];
+    h.tpsum = ts;
+    fh[g] = h;
+  }
+}
+
+size_t fwd_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off) {
+  const size_t m = (size_t)nmembers * sizeof(FwdMember);
+  if (group_off) *group_off = m;
+  return m + (size_t)ngroups * sizeof(FwdHdr);
+}
+
+void launch_fwd_table(cudaStream_t st, const LatticeArgs& a, void* table, size_t group_off, int max_members) {
+  if (a.ngroups <= 0) return;
+  FwdMember* fm = static_cast<FwdMember*>(table);
+  FwdHdr* fh = reinterpret_cast<FwdHdr*>(static_cast<char*>(table) + group_off);
+  const int W = max_members <= 4 ? 4 : max_members <= 8 ? 8 : max_members <= 16 ? 16 : 32;
+  const int grid = (int)(((int64_t)a.ngroups * W + kThreads - 1) / kThreads);
+  if (W == 4)
+    k_fwd_table<4><<<grid, kThreads, 0, st>>>(a, fm, fh);
+  else if (W == 8)
+    k_fwd_table<8><<<grid, kThreads, 0, st>>>(a, fm, fh);
+  else if (W == 16)
+    k_fwd_table<16><<<grid, kThreads, 0, st>>>(a, fm, fh);
+  else
+    k_fwd_table<32><<<grid, kThreads, 0, st>>>(a, fm, fh);
 }
 
 int launch_coverage(cudaStream_t st, const LatticeArgs& a, int t_floats, int x_floats, float* kap,

@@ -117,6 +117,10 @@ struct LatticeArgs {
   // {A hi, A lo 2^20 + lo2, C hi, C lo 2^20 + lo2} (k_det_to_float forms A, C)
   const double* det_scale;
   unsigned long long* ACd;
+  // forward / coverage: the plan's member rows and group headers (k_fwd_table, geometry only;
+  // the header array starts fgoff bytes into ftab)
+  const void* ftab;
+  size_t fgoff;
 };
 
 constexpr int kThreads = 256;      // CTA size of the lattice kernels
@@ -202,6 +206,10 @@ size_t bp_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off);
 // Member tables of a backprojection plan alone (geometry only): set_transforms builds them on an
 // auxiliary stream, overlapped with the coverage pass.
 void launch_bp_table(cudaStream_t st, const LatticeArgs& a, void* table, size_t group_off, int max_members);
+// Member rows and group headers of a forward plan (geometry only): built by set_transforms
+// before the coverage pass, read by every forward.
+size_t fwd_table_bytes(int64_t nmembers, int64_t ngroups, size_t* group_off);
+void launch_fwd_table(cudaStream_t st, const LatticeArgs& a, void* table, size_t group_off, int max_members);
 // Each group's tile precision is GroupDev::exact (init / rigidity passes: always exact).
 void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, int r_bytes,
                         void* table, size_t group_off, bool build_table, int max_members, const float* kap,
