@@ -749,6 +749,7 @@ struct PlanBuild {
   int nsplit = 0;              // natural groups split into single members
   bool all_fit = true;         // every single member fits the tile budget
   double fit_frac = 0.0;       // fraction of natural groups that fit whole
+  double half_frac = 0.0;      // ... that fit whole or as two groups of half-tile members
 };
 
 // Bounding boxes for the current transforms and the final group list of one plan.
@@ -920,6 +921,8 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     }
   };
   std::vector<int32_t> core;
+  std::vector<std::pair<std::vector<int32_t>, int>> hwork;  // (member list, halving depth)
+  int half = 0;
   for (int gi = 0; gi < ngrp; ++gi) {
     const int a = ng.start[gi], b = ng.start[gi + 1];
     if (status[gi] == 0) {
@@ -943,11 +946,71 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
       emit(g, vox, core.data(), (int)core.size());
       continue;
     }
+    // Backprojection: a group that does not fit is first halved as a whole -- every member's
+    // pixel tile split the same way along its longer axis, the halves of all members staying
+    // together -- so the group keeps its members' lines in one CTA (a 3-member group of 8 x 8
+    // tiles has 768 lines: three full rounds of 256 threads; single members of half tiles
+    // would leave half of a round idle). Two levels, then single members.
+    if (!fwd && (pool[core[0]].tu > 1 || pool[core[0]].tv > 1)) {
+      bool whole = true;  // every half (first level) fits
+      hwork.clear();
+      hwork.push_back({core, 0});
+      while (!hwork.empty()) {
+        auto item = std::move(hwork.back());
+        hwork.pop_back();
+        GroupDev hg;
+        const int64_t hv = group(item.first.data(), (int)item.first.size(), hg);
+        if (fits(hg, hv)) {
+          emit(hg, hv, item.first.data(), (int)item.first.size());
+          continue;
+        }
+        if (item.second > 0) whole = false;
+        const MemberDev& m0 = pool[item.first[0]];
+        if (item.second >= 2 || (m0.tu == 1 && m0.tv == 1)) {
+          whole = false;
+          for (int32_t i : item.first) emit_single(i);
+          continue;
+        }
+        const bool along_u = m0.tu >= m0.tv;
+        std::vector<int32_t> h0, h1;
+        for (int32_t i : item.first) {
+          const MemberDev m = pool[i];
+          MemberDev q0 = m, q1 = m;
+          if (along_u) {
+            const int hu = (m.tu + 1) / 2;
+            q0.tu = hu;
+            q1.u0 = m.u0 + hu;
+            q1.tu = m.tu - hu;
+          } else {
+            const int hv2 = (m.tv + 1) / 2;
+            q0.tv = hv2;
+            q1.v0 = m.v0 + hv2;
+            q1.tv = m.tv - hv2;
+          }
+          for (int h = 0; h < 2; ++h) {
+            const MemberDev& q = h ? q1 : q0;
+            if (q.tu <= 0 || q.tv <= 0) continue;
+            pool.push_back(q);
+            mlo.resize(3 * pool.size());
+            mhi.resize(3 * pool.size());
+            const int32_t k = (int32_t)pool.size() - 1;
+            bbox_of(q, &mlo[3 * k], &mhi[3 * k]);
+            (h ? h1 : h0).push_back(k);
+          }
+        }
+        if (!h0.empty()) hwork.push_back({std::move(h0), item.second + 1});
+        if (!h1.empty()) hwork.push_back({std::move(h1), item.second + 1});
+      }
+      ++out.nsplit;
+      if (whole) ++half;
+      continue;
+    }
     if (core.size() > 1) ++out.nsplit;
     for (int32_t i : core) emit_single(i);
   }
   gstart.push_back((int32_t)ix.size());
   out.fit_frac = ngrp ? (double)fit / ngrp : 1.0;
+  out.half_frac = ngrp ? (double)(fit + half) / ngrp : 1.0;
   tr.mark("    group boxes");
   // Order the CTAs' work along a Morton curve of the groups' bbox centres (16-voxel cells), so
   // that overlapping footprints of all stacks are processed close in time: the forward's X
@@ -1116,6 +1179,12 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
     ng.sample = smp;
     return ng;
   };
+  // a tile size is taken when >= 90% of the natural groups fit whole; the backprojection also
+  // takes it when >= 75% fit whole and >= 90% whole or halved (size_groups): c3 at the 56 KB
+  // tile, 8 x 8 (85% whole: the exact rim groups need 16 B per cell) rather than 8 x 4
+  auto accept = [](const PlanBuild& pb, bool fwd) {
+    return pb.all_fit && (pb.fit_frac >= 0.9 || (!fwd && pb.fit_frac >= 0.75 && pb.half_frac >= 0.9));
+  };
   Trace tr;
   for (int kind = kind_lo; kind < kind_hi; ++kind) {
     const bool fwd = kind == 0;
@@ -1132,13 +1201,17 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
       const bool previous = pl.ngroups > 0 && k == order[0] && order.size() > (size_t)ncand;
       if (!previous) {  // quick reject on the sample
         size_groups(c, geo, natural(cand[k][0], cand[k][1], cand[k][2], fwd, true), kind, pb);
-        if (!(pb.all_fit && pb.fit_frac >= 0.9)) continue;
+        if (tr.on)
+          fprintf(stderr, "[pvr]   plan kind %d tile %dx%dx%d (sample): fit %.3f (halved %.3f) all_fit %d\n", kind,
+                  cand[k][0], cand[k][1], cand[k][2], pb.fit_frac, pb.half_frac, (int)pb.all_fit);
+        if (!accept(pb, fwd)) continue;
       }
       size_groups(c, geo, natural(cand[k][0], cand[k][1], cand[k][2], fwd, false), kind, pb);
       if (tr.on)
-        fprintf(stderr, "[pvr]   plan kind %d tile %dx%dx%d: fit %.3f all_fit %d groups %zu split %d\n", kind,
-                cand[k][0], cand[k][1], cand[k][2], pb.fit_frac, (int)pb.all_fit, pb.grp.size(), pb.nsplit);
-      if (pb.all_fit && pb.fit_frac >= 0.9) { pick = k; break; }
+        fprintf(stderr, "[pvr]   plan kind %d tile %dx%dx%d: fit %.3f (halved %.3f) all_fit %d groups %zu split %d\n",
+                kind, cand[k][0], cand[k][1], cand[k][2], pb.fit_frac, pb.half_frac, (int)pb.all_fit, pb.grp.size(),
+                pb.nsplit);
+      if (accept(pb, fwd)) { pick = k; break; }
     }
     if (pick < 0) return fail(c, PVR_ERR_ARG, "no tiling fits the shared-memory budget (extreme transforms?)");
     pl.TU = cand[pick][0];
