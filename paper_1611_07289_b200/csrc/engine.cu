@@ -177,6 +177,8 @@ struct pvr_ctx {
   bool iplan_valid = false;     // the init plan is built lazily by pvr_init_volume
   std::vector<PatchGeo> geo;    // composed geometry of the local patches (last set_transforms)
   std::vector<double> Tloc;     // the local patches' transforms (last set_transforms), [nloc][12]
+  std::vector<PatchGeo> geo_next;  // set_transforms scratch, swapped with geo / Tloc
+  std::vector<double> T_next;
   RegPatch* regP = nullptr;     // f1: device per-patch registration geometry
   size_t regP_cap = 0;
   std::vector<std::unique_ptr<NaturalGroups>> ngcache;  // geometry-free group lists
@@ -1833,12 +1835,20 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   if (c->state < PATCHED) return fail(c, PVR_ERR_STATE, "set_transforms needs extract_patches");
   if (!T || n != c->M) return fail(c, PVR_ERR_ARG, "expected %lld transforms, got %lld", (long long)c->M, (long long)n);
   Trace tr;
-  std::vector<double> Th((size_t)12 * c->nloc);
+  // the local transforms and the composed geometry go into scratch vectors that are swapped
+  // with the context's at the end (no reallocation or zero fill per call: c5 has 876k patches)
+  std::vector<double>& Th = c->T_next;
+  Th.resize((size_t)12 * c->nloc);
   const double* Tl = T + 12 * c->first;
   if (is_device_ptr(T)) {
     CUDA_TRY(c, cudaMemcpy(Th.data(), Tl, Th.size() * sizeof(double), cudaMemcpyDeviceToHost));
   } else {
-    memcpy(Th.data(), Tl, Th.size() * sizeof(double));
+    const int64_t nchunk = 64, len = (int64_t)Th.size(), per = (len + nchunk - 1) / nchunk;
+#pragma omp parallel for schedule(static) if (len >= (1 << 20))
+    for (int64_t k = 0; k < nchunk; ++k) {
+      const int64_t a = k * per, b = std::min(len, a + per);
+      if (a < b) memcpy(Th.data() + a, Tl + a, (size_t)(b - a) * sizeof(double));
+    }
   }
   // compose, per patch, in fp64: voxel index of lattice point (a,b,c) of pixel (u,v,z) is
   // g(T_s(G (x0+u, y0+v, z0+z, 1) + a h_u u^ + b h_v v^ + c h_w w^)), g(x) = (x - o) / s
@@ -1852,7 +1862,8 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
     c->pd_host_n = c->nloc;
   }
   PatchDev* pd = c->pd_host;
-  std::vector<PatchGeo> geo(c->nloc);
+  std::vector<PatchGeo>& geo = c->geo_next;
+  geo.resize(c->nloc);
   const double is = 1.0 / c->s;
 #pragma omp parallel for schedule(static) if (c->nloc >= 2048)
   for (int64_t s = 0; s < c->nloc; ++s) {
@@ -1980,7 +1991,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
     CUDA_TRY(c, cudaMemcpyAsync(c->vpat, vp.data(), vp.size() * sizeof(VolPatch), cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // vp goes out of scope
     c->geo.swap(geo);
-    c->Tloc = Th;
+    c->Tloc.swap(Th);
     const LatticeArgs la = lattice_args(c, c->fplan);
     launch_volpsf(c->stream, 1, c->vpat, c->nloc, la, nullptr, c->kap, c->vin, nullptr, nullptr, c->partials,
                   nullptr, nullptr, 0, nullptr);
@@ -1996,7 +2007,7 @@ pvr_status pvr_set_transforms(pvr_ctx* c, const double* T, int64_t n) {
   if (r != PVR_OK) return r;
   c->iplan_valid = false;
   c->geo.swap(geo);
-  c->Tloc = Th;
+  c->Tloc.swap(Th);
   tr.mark("build plans", c->stream);
   r = encode_tmaps(c);
   if (r != PVR_OK) return r;

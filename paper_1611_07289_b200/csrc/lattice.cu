@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
 // DET: the deterministic mode's instance (three-word tiles, int64 accumulators); the default
 // instance carries only the single-word and hi/lo paths (fewer registers).
 template <bool DET>
-__global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeArgs a, int tile_words,
+__global__ void __launch_bounds__(kBpThreads, kBpCtasPerSm) k_lattice_bp(LatticeArgs a, int tile_words,
                                                          const BpMember* __restrict__ tm,
                                                          const BpGroupHdr* __restrict__ th,
                                                          const float* __restrict__ kap,
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
 
   float2* R = reinterpret_cast<float2*>(base + kBpTileBytes / 4);
   __shared__ float s_ip[kMaxIp], s_tp[kMaxTp];
-  __shared__ float s_red[2][kThreads >> 5];
+  __shared__ float s_red[2][kBpThreads >> 5];
   __shared__ BpMember sbm[kMaxMembers];
   const int3 n = a.n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -809,17 +809,17 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
       const int4* src = reinterpret_cast<const int4*>(tm + G.m0);
       int4* dst = reinterpret_cast<int4*>(sbm);
       const int nq = G.nm * (int)(sizeof(BpMember) / 16);
-      for (int i = threadIdx.x; i < nq; i += kThreads) dst[i] = __ldg(src + i);
+      for (int i = threadIdx.x; i < nq; i += kBpThreads) dst[i] = __ldg(src + i);
       const int nip = (2 * H.ru + 1) * (2 * H.rv + 1);
-      for (int i = threadIdx.x; i < nip; i += kThreads) s_ip[i] = a.tab[H.ip0 + i];
-      for (int i = threadIdx.x; i < H.ntp; i += kThreads) s_tp[i] = a.tab[H.tp0 + i];
+      for (int i = threadIdx.x; i < nip; i += kBpThreads) s_ip[i] = a.tab[H.ip0 + i];
+      for (int i = threadIdx.x; i < H.ntp; i += kBpThreads) s_tp[i] = a.tab[H.tp0 + i];
       const int4 z4 = make_int4(0, 0, 0, 0);
       const int nv4 = (nvox + 3) >> 2;  // tile_words is a multiple of 4
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         if (q >= NW) break;
         int4* t4 = reinterpret_cast<int4*>(ex ? base + q * QW : (q == 1 ? cbase : base));
-        for (int i = threadIdx.x; i < nv4; i += kThreads) t4[i] = z4;
+        for (int i = threadIdx.x; i < nv4; i += kBpThreads) t4[i] = z4;
       }
     }
     __syncthreads();
@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     {
       const int np = H.np;
       int mi = 0;
-      for (int i = threadIdx.x; i < np; i += kThreads) {
+      for (int i = threadIdx.x; i < np; i += kBpThreads) {
         while (i >= sbm[mi].pend) ++mi;
         const BpMember& M = sbm[mi];
         const int li = i - M.pbeg;
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
 #endif
     float xA = 0.0f, xC = 0.0f;  // every thread forms the same group maxima and scales
 #pragma unroll
-    for (int i = 0; i < (kThreads >> 5); ++i) {
+    for (int i = 0; i < (kBpThreads >> 5); ++i) {
       xA = fmaxf(xA, s_red[0][i]);
       xC = fmaxf(xC, s_red[1][i]);
     }
@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
       const int w2 = 2 * H.ru + 1;
       const float inv_nu = 1.0f / (float)H.nu, inv_nv = 1.0f / (float)H.nv;
       int mi = 0;
-      for (int i = threadIdx.x; i < nl; i += kThreads) {
+      for (int i = threadIdx.x; i < nl; i += kBpThreads) {
         while (i >= sbm[mi].lend) ++mi;
         const BpMember& M = sbm[mi];
         // colour-ordered lines: class (U mod 3, V mod 3), then rows of the class. The lanes of
@@ -954,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, kBpCtasPerSm) k_lattice_bp(LatticeAr
     // flat pair index i = (zl * dy + yl) * hx + pl, decoded by float reciprocals (exact for
     // these small integers); 32-bit voxel offsets (the volume has < 2^31 voxels)
     const int gbase = (G.lo[2] * n.y + G.lo[1]) * a.nxp + G.lo[0];
-    for (int i = threadIdx.x; i < npair; i += kThreads) {
+    for (int i = threadIdx.x; i < npair; i += kBpThreads) {
       const int row = (int)(((float)i + 0.5f) * inv_hx);
       const int pl = i - row * hx;
       const int zl = (int)(((float)row + 0.5f) * inv_dy);
@@ -1027,7 +1027,7 @@ static const DevConfig& configure() {
     cudaFuncSetAttribute(k_lattice_fwd<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_lattice_fwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.resident, k_lattice_bp<false>, kThreads, kBpTileBytes + kRBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.resident, k_lattice_bp<false>, kBpThreads, kBpTileBytes + kRBytes);
   });
   return g_dev[dev];
 }
@@ -1194,10 +1194,10 @@ void launch_backproject(cudaStream_t st, const LatticeArgs& a, int tile_words, i
   const int grid = a.ngroups < 148 * 16 ? a.ngroups : 148 * 16;
 #endif
   if (a.prm.det)
-    k_lattice_bp<true><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC,
+    k_lattice_bp<true><<<grid, kBpThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC,
                                                                        next);
   else
-    k_lattice_bp<false><<<grid, kThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC,
+    k_lattice_bp<false><<<grid, kBpThreads, kBpTileBytes + r_bytes, st>>>(a, tile_words, tm, th, kap, e, p, w, init, AC,
                                                                         next);
 }
 

@@ -135,7 +135,11 @@ constexpr int kBpTileBytes = PVR_BP_TILE_KB * 1024;
 // Backprojection tile precision (PVR_PARAM_BP_EXACT): 0 one word everywhere (a timing
 // reference), 1 exact hi/lo words for rim groups only (default), 2 exact everywhere.
 enum { kBpSingle = 0, kBpRim = 1, kBpAll = 2, kBpDet = 3 /* deterministic mode: three words, 24 B */ };
-constexpr int kBpCtasPerSm = PVR_BP_TILE_KB <= 56 ? 3 : 2;
+#ifndef PVR_BP_THREADS
+#define PVR_BP_THREADS 256
+#endif
+constexpr int kBpThreads = PVR_BP_THREADS;  // CTA size of the backprojection
+constexpr int kBpCtasPerSm = kBpThreads > 256 ? 2 : PVR_BP_TILE_KB <= 56 ? 3 : 2;
 constexpr int kBpDetPlane = (kBpTileBytes / 6) & ~15;  // deterministic mode: 6 planes
 #ifndef PVR_R_KB
 #define PVR_R_KB 12
