@@ -764,6 +764,9 @@ struct PlanBuild {
 #ifndef PVR_FWD_HALVE
 #define PVR_FWD_HALVE 1
 #endif
+#ifndef PVR_BP_HALVE_MIN
+#define PVR_BP_HALVE_MIN 0.75
+#endif
 #ifndef PVR_FWD_HALVE_MIN
 #define PVR_FWD_HALVE_MIN 0.6
 #endif
@@ -1194,7 +1197,7 @@ pvr_status build_plans(pvr_ctx* c, const std::vector<PatchGeo>& geo, int kind_lo
   // takes it when >= 75% fit whole and >= 90% whole or halved (size_groups): c3 at the 56 KB
   // tile, 8 x 8 (85% whole: the exact rim groups need 16 B per cell) rather than 8 x 4
   auto accept = [](const PlanBuild& pb, bool fwd) {
-    return pb.all_fit && (pb.fit_frac >= 0.9 || (!fwd && pb.fit_frac >= 0.75 && pb.half_frac >= 0.9) ||
+    return pb.all_fit && (pb.fit_frac >= 0.9 || (!fwd && pb.fit_frac >= PVR_BP_HALVE_MIN && pb.half_frac >= 0.9) ||
                           (fwd && PVR_FWD_HALVE && pb.fit_frac >= PVR_FWD_HALVE_MIN && pb.half_frac >= 0.9));
   };
   Trace tr;
