@@ -100,6 +100,11 @@ enum {
                                  three int32 words per value (24 B per cell) and int64 (A, C)
                                  accumulators. Slower (~1.5x the backprojection); the
                                  two-Gaussian patch mixture (f4) is not covered [0]           */
+  ,PVR_PARAM_PLAN_BUDGET = 20 /* (extract) fraction in [0.05, 1] of the shared-memory tile
+                                 budgets the planner sizes groups for (forward X tile,
+                                 backprojection tile); the kernels keep their full size. Below
+                                 1 the planner halves and splits groups as at a larger problem:
+                                 tests run those paths on small grids [1]                       */
   ,PVR_PARAM_BP_EXACT = 16    /* (extract) precision of the backprojection's shared tiles
                                  (DESIGN.md 7). 1 [default]: exact hi/lo int32 word pairs
                                  (~2^-41 of the group's largest splat term) for every group

@@ -146,6 +146,7 @@ struct pvr_ctx {
   int clamp = 1, psf_mode = 0, profile = 0;
   int bp_exact = kBpRim;  // backprojection tile precision (PVR_PARAM_BP_EXACT)
   int det = 0;            // PVR_PARAM_DETERMINISTIC
+  double plan_budget = 1.0;  // PVR_PARAM_PLAN_BUDGET: fraction of the tile budgets planned for
   unsigned long long* ACd = nullptr;  // deterministic mode: int64 (A, C) accumulators [4 Vp]
   VolPatch* vpat = nullptr;     // volume-space PSF mode: per local patch geometry
   float* vin = nullptr;         // volume-space PSF mode: per pixel row normaliser sum_{grid} psi
@@ -779,7 +780,8 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   // past it into single-member groups) before falling back here
   // shared-memory budget in bytes: forward 4 B per staged voxel; backprojection 16 B per cell
   // for exact groups (hi / lo words), 8 B for single-word groups; the init plan is all exact
-  const int64_t byte_budget = fwd ? kFwdTileBytes : kind == 1 ? (int64_t)kBpTileBytes * 9 / 10 : kBpTileBytes;
+  const int64_t byte_budget = (int64_t)(c->plan_budget *
+                                        (fwd ? kFwdTileBytes : kind == 1 ? (int64_t)kBpTileBytes * 9 / 10 : kBpTileBytes));
   // member pool: the natural members, then sub-members made by splitting a member whose own
   // footprint does not fit (below); mlo / mhi: their fp64 voxel bboxes
   std::vector<MemberDev> pool(ng.mem);
@@ -835,7 +837,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     return (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
   };
   auto fits = [&](const GroupDev& g, int64_t vox) {
-    if (!fwd && c->det) return vox * 4 <= (int64_t)kBpDetPlane * (kind == 1 ? 9 : 10) / 10;
+    if (!fwd && c->det) return vox * 4 <= (int64_t)(c->plan_budget * kBpDetPlane * (kind == 1 ? 9 : 10) / 10);
     return vox * (fwd ? 4 : g.exact ? 16 : 8) <= byte_budget;
   };
   // Outlying members of a natural group: a member whose footprint centre lies more than a
@@ -1447,7 +1449,8 @@ pvr_status pvr_comm_init_host(pvr_ctx* c, int nranks, int rank, pvr_host_collect
 pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
   GUARD(c);
   const bool extract_key = key == PVR_PARAM_PSF_MODE || key == PVR_PARAM_PSF_NSIGMA || key == PVR_PARAM_PSF_QUALITY ||
-                           key == PVR_PARAM_BP_EXACT || key == PVR_PARAM_DETERMINISTIC;
+                           key == PVR_PARAM_BP_EXACT || key == PVR_PARAM_DETERMINISTIC ||
+                           key == PVR_PARAM_PLAN_BUDGET;
   if (extract_key && c->state >= PATCHED)
     return fail(c, PVR_ERR_STATE, "parameter %d must be set before extract_patches", key);
   switch (key) {
@@ -1476,6 +1479,7 @@ pvr_status pvr_set_param(pvr_ctx* c, int key, double v) {
       break;
     case PVR_PARAM_COMM_TIMEOUT: if (!(v > 0)) goto bad; c->comm_timeout = v; break;
     case PVR_PARAM_DETERMINISTIC: if (v != 0 && v != 1) goto bad; c->det = (int)v; break;
+    case PVR_PARAM_PLAN_BUDGET: if (!(v >= 0.05 && v <= 1)) goto bad; c->plan_budget = v; break;
     default: return fail(c, PVR_ERR_ARG, "unknown parameter key %d", key);
   }
   return PVR_OK;

@@ -21,7 +21,8 @@ STATUS_NAMES = {0: "PVR_OK", 1: "PVR_ERR_ARG", 2: "PVR_ERR_STATE", 3: "PVR_ERR_O
 PARAM = {"delta": 0, "tau_patch": 1, "c0": 2, "tau_live": 3, "tau_C": 4, "tau_obs": 5,
          "clamp": 6, "psf_mode": 7, "sigma2_floor": 9, "psf_nsigma": 10, "profile": 11, "psf_quality": 12,
          "em_rounds": 13, "em_tol": 14, "patch_mixture": 15,
-         "bp_exact": 16, "exchange": 17, "comm_timeout": 18, "deterministic": 19}
+         "bp_exact": 16, "exchange": 17, "comm_timeout": 18, "deterministic": 19,
+         "plan_budget": 20}
 EXCHANGE = {"allreduce": 0, "slabs": 1, "average": 2}
 COLL_ALLREDUCE_SUM, COLL_ALLREDUCE_MAX, COLL_ALLGATHER = 0, 1, 2
 DT_F32, DT_F64, DT_I64 = 0, 1, 2

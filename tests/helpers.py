@@ -43,11 +43,13 @@ def tau_c_tie_band(Co, tau_C, dims):
     env = ndimage.uniform_filter(C, size=3, mode="constant") * 27.0
     near = np.abs(C - tau_C) <= 3.0 * 2.0 ** -16 * env
     return near, ndimage.binary_dilation(near, np.ones((3, 3, 3), bool))
+
+
 def make_oracle(prob, params=None):
     from oracle import Oracle
     orc = Oracle(prob["dims"], prob["spacing"], prob["origin"])
     for k, v in (params or {}).items():
-        if k not in ("profile", "bp_exact", "deterministic", "exchange", "comm_timeout"):  # product-only
+        if k not in ("profile", "bp_exact", "deterministic", "exchange", "comm_timeout", "plan_budget"):  # product-only
             orc.set_param(k, v)
     for st in prob["stacks"]:
         orc.add_stack(st["slices"], st["G"], st["thickness"])

@@ -306,6 +306,22 @@ def test_explicit_masked_patches(thr):
         ctx.close()
 
 
+@pytest.mark.parametrize("budget", [0.4, 0.25])
+def test_planner_halving_and_splits(budget):
+    """PVR_PARAM_PLAN_BUDGET: the planner sizes groups for a fraction of the tile budget, so a
+    small problem takes the paths of a large one -- groups halved as a whole (every member's
+    tile split alike), single members, member subdivision -- in both plans (engine.cu
+    size_groups); same parity bars at SURVEY's thresholds."""
+    prob = synth.make_problem("c3", scale=(96, 96, 12), size=32, stride=16)
+    ctx = make_gpu(prob, {"plan_budget": budget})
+    st = ctx.stats()
+    ctx.close()
+    print("plan:", {k: st[k] for k in ("fwd_tile", "bp_tile", "fwd_groups", "bp_groups", "fwd_split", "bp_split",
+                                        "bp_exact_groups")})
+    assert st["bp_split"] > 0
+    run_pair(prob, 2, {"plan_budget": budget})
+
+
 @SETS
 def test_odd_volume_dims_small_patches(thr):
     """Edge shapes: a 37^3 volume (rows padded to 40 floats for the TMA pitch), 29x29 stacks
