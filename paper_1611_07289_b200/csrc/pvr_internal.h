@@ -139,7 +139,10 @@ enum { kBpSingle = 0, kBpRim = 1, kBpAll = 2, kBpDet = 3 /* deterministic mode: 
 #define PVR_BP_THREADS 256
 #endif
 constexpr int kBpThreads = PVR_BP_THREADS;  // CTA size of the backprojection
-constexpr int kBpCtasPerSm = kBpThreads > 256 ? 2 : PVR_BP_TILE_KB <= 56 ? 3 : 2;
+#ifndef PVR_BP_CTAS
+#define PVR_BP_CTAS (kBpThreads > 256 ? 2 : PVR_BP_TILE_KB <= 56 ? 3 : 2)
+#endif
+constexpr int kBpCtasPerSm = PVR_BP_CTAS;  // __launch_bounds__ minimum CTAs per SM
 constexpr int kBpDetPlane = (kBpTileBytes / 6) & ~15;  // deterministic mode: 6 planes
 #ifndef PVR_R_KB
 #define PVR_R_KB 12
