@@ -787,18 +787,36 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
   std::vector<MemberDev> pool(ng.mem);
   const int64_t nm = (int64_t)ng.mem.size();
   std::vector<int32_t> mlo(3 * nm), mhi(3 * nm);
-  auto bbox_of = [&](const MemberDev& m, int* lo, int* hi) {
+  std::vector<uint8_t> msup(nm);  // backprojection: the full PSF support of every pixel feeding the member is in the grid
+  const int n3[3] = {c->dims.x, c->dims.y, c->dims.z};
+  auto bbox_of = [&](const MemberDev& m, int* lo, int* hi) -> uint8_t {
     const HostPatch& hp = c->patches[c->first + m.patch];
-    member_bbox(m, hp, c->stacks[hp.stack].psf, geo[m.patch], fwd, lo, hi);
+    const StackPsf& ps = c->stacks[hp.stack].psf;
+    member_bbox(m, hp, ps, geo[m.patch], fwd, lo, hi);
+    if (fwd) return 1;
+    // the pixels feeding the member's lines reach one pixel past its tile (R range, lattice.cu
+    // owned_range); their whole supports (every in-plane and through-plane sample) in the grid
+    // means kappa = 1 for all of them, so no term of the group carries a 1/kappa > 1
+    MemberDev e = m;
+    e.u0 = std::max(0, m.u0 - 1);
+    e.tu = std::min(hp.sx, m.u0 + m.tu + 1) - e.u0;
+    e.v0 = std::max(0, m.v0 - 1);
+    e.tv = std::min(hp.sy, m.v0 + m.tv + 1) - e.v0;
+    e.c0 = -ps.cmax;
+    e.c1 = ps.cmax;
+    int sl[3], sh[3];
+    member_bbox(e, hp, ps, geo[m.patch], true, sl, sh);
+    for (int d = 0; d < 3; ++d)
+      if (sl[d] < 0 || sh[d] > n3[d] - 1) return 0;
+    return 1;
   };
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < nm; ++i) bbox_of(ng.mem[i], &mlo[3 * i], &mhi[3 * i]);
+  for (int64_t i = 0; i < nm; ++i) msup[i] = bbox_of(ng.mem[i], &mlo[3 * i], &mhi[3 * i]);
   tr.mark("    member bboxes");
-  const int n3[3] = {c->dims.x, c->dims.y, c->dims.z};
   // union bbox of the pool members listed in ix[0, n) -> tile box g (m0 / nm set by the caller)
   auto group = [&](const int32_t* ix, int n, GroupDev& g) {
     int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
-    int rim = 0;
+    int rim = 0, sup = 1;
     for (int k = 0; k < n; ++k) {
       const int i = ix[k];
       for (int d = 0; d < 3; ++d) {
@@ -806,6 +824,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
         hi[d] = std::max(hi[d], mhi[3 * i + d]);
       }
       rim |= pool[i].flags & kMemberRim;
+      sup &= msup[i];
     }
     g.m0 = 0;
     g.nm = n;
@@ -813,7 +832,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     g.interior = 1;
     for (int d = 0; d < 3; ++d)
       if (lo[d] < 0 || hi[d] > n3[d] - 1) g.interior = 0;
-    g.exact = !fwd && (kind == 2 || c->det || c->bp_exact == kBpAll || (c->bp_exact == kBpRim && (rim || !g.interior)));
+    g.exact = !fwd && (kind == 2 || c->det || c->bp_exact == kBpAll || (c->bp_exact == kBpRim && (rim || !sup)));
     if (fwd) {
       // TMA-staged X tile (lattice.cu): the box's x coordinate must be 16-byte aligned
       // (measured: a box starting at an x not a multiple of 4 floats faults with an illegal
@@ -930,7 +949,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
           mlo.resize(3 * pool.size());
           mhi.resize(3 * pool.size());
           const int32_t k = (int32_t)pool.size() - 1;
-          bbox_of(q, &mlo[3 * k], &mhi[3 * k]);
+          msup.push_back(bbox_of(q, &mlo[3 * k], &mhi[3 * k]));
           work.push_back(k);
         }
       ++out.nsplit;
@@ -967,6 +986,12 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
     // together -- so the group keeps its members' lines in one CTA (a 3-member group of 8 x 8
     // tiles has 768 lines: three full rounds of 256 threads; single members of half tiles
     // would leave half of a round idle). Two levels, then single members.
+    // Splitting never lowers a backprojection group's tile precision: when the group as a whole
+    // is exact (a rim member, or a footprint that leaves the grid, whose partly observed pixels
+    // carry 1/kappa-amplified terms), its halves and single members stay exact even where their
+    // own box is interior (a half's boundary lines are fed by the other half's pixels).
+    if (!fwd && g.exact)
+      for (int32_t i : core) pool[i].flags |= kMemberRim;
     if ((!fwd || PVR_FWD_HALVE) && (pool[core[0]].tu > 1 || pool[core[0]].tv > 1)) {
       bool whole = true;  // every half (first level) fits
       hwork.clear();
@@ -1010,7 +1035,7 @@ void size_groups(const pvr_ctx* c, const std::vector<PatchGeo>& geo, const Natur
             mlo.resize(3 * pool.size());
             mhi.resize(3 * pool.size());
             const int32_t k = (int32_t)pool.size() - 1;
-            bbox_of(q, &mlo[3 * k], &mhi[3 * k]);
+            msup.push_back(bbox_of(q, &mlo[3 * k], &mhi[3 * k]));
             (h ? h1 : h0).push_back(k);
           }
         }

@@ -575,6 +575,21 @@ __device__ int replan_interior(const int (&lo)[3], const int (&hi)[3], int3 n) {
   return 1;
 }
 
+// Backprojection member: the whole PSF support of every pixel feeding its lines (its tile and
+// one pixel around, all through-plane samples) is in the grid (engine.cu: size_groups)
+__device__ int replan_support_interior(const MemberDev& m, const PatchDev& pt, const StackPsf& ps, int3 n) {
+  MemberDev e = m;
+  e.u0 = max(0, m.u0 - 1);
+  e.tu = min(pt.sx, m.u0 + m.tu + 1) - e.u0;
+  e.v0 = max(0, m.v0 - 1);
+  e.tv = min(pt.sy, m.v0 + m.tv + 1) - e.v0;
+  e.c0 = -ps.cmax;
+  e.c1 = ps.cmax;
+  int lo[3], hi[3];
+  replan_member_box(e, pt, ps, 1, lo, hi);
+  return replan_interior(lo, hi, n);
+}
+
 // Device re-plan of one plan for new transforms: same groups and order, new boxes. Forward:
 // the smallest existing TMA box shape that holds the new footprint (else fail). Backprojection
 // (`nappend` != NULL): a group whose box outgrew the tile budget is emptied (nm = 0) and its
@@ -590,13 +605,14 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
   GroupDev G = grp[g];
   if (G.nm == 0) return;  // emptied by an earlier split
   int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
-  int rim = 0;
+  int rim = 0, sup = 1;
   for (int i = G.m0; i < G.m0 + G.nm; ++i) {
     const MemberDev m = mem[i];
     const PatchDev& pt = P[m.patch];
     int ml[3], mh[3];
     replan_member_box(m, pt, psf[pt.stack], fwd, ml, mh);
     rim |= m.flags & kMemberRim;
+    if (!fwd && bp_mode == kBpRim) sup &= replan_support_interior(m, pt, psf[pt.stack], n);
     for (int d = 0; d < 3; ++d) {
       lo[d] = min(lo[d], ml[d]);
       hi[d] = max(hi[d], mh[d]);
@@ -605,7 +621,7 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
   G.interior = replan_interior(lo, hi, n);
   // backprojection tile precision (engine.cu: size_groups): exact for rim members and
   // footprints that leave the grid; the byte budget then buys half the cells
-  G.exact = !fwd && (bp_mode >= kBpAll || (bp_mode == kBpRim && (rim || !G.interior)));
+  G.exact = !fwd && (bp_mode >= kBpAll || (bp_mode == kBpRim && (rim || !sup)));
   // (deterministic mode: 4 B per cell in each of 6 planes of kBpDetPlane bytes)
   const int64_t cell_bytes = bp_mode == kBpDet ? 24 : G.exact ? 16 : 8;
   int64_t vox;
@@ -640,7 +656,8 @@ __global__ void k_replan(const MemberDev* __restrict__ mem, GroupDev* __restrict
         S.nm = 1;
         S.tmap = 0;
         S.interior = replan_interior(ml, mh, n);
-        S.exact = bp_mode >= kBpAll || (bp_mode == kBpRim && ((m.flags & kMemberRim) || !S.interior));
+        // a split never lowers precision: the singles of an exact group stay exact
+        S.exact = G.exact;
         const int64_t sv = replan_bp_box(ml, mh, S);
         const int k = atomicAdd(nappend, 1);
         if (sv * (bp_mode == kBpDet ? 24 : S.exact ? 16 : 8) > vox_budget ||
