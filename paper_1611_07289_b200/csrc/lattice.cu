@@ -31,6 +31,7 @@
 #include <cfloat>
 #include <cmath>
 #include <mutex>
+#include <type_traits>
 
 #include "device_util.cuh"
 #include "pvr_internal.h"
@@ -954,17 +955,17 @@ __global__ void __launch_bounds__(kBpThreads, kBpCtasPerSm) k_lattice_bp(Lattice
     // flat pair index i = (zl * dy + yl) * hx + pl, decoded by float reciprocals (exact for
     // these small integers); 32-bit voxel offsets (the volume has < 2^31 voxels)
     const int gbase = (G.lo[2] * n.y + G.lo[1]) * a.nxp + G.lo[0];
-    for (int i = threadIdx.x; i < npair; i += kBpThreads) {
-      const int row = (int)(((float)i + 0.5f) * inv_hx);
-      const int pl = i - row * hx;
-      const int zl = (int)(((float)row + 0.5f) * inv_dy);
-      const int yl = row - zl * dy;
-      const int gy = G.lo[1] + yl, gz = G.lo[2] + zl, gx = G.lo[0] + 2 * pl;
-      if ((unsigned)gy >= (unsigned)n.y || (unsigned)gz >= (unsigned)n.z || (unsigned)gx >= (unsigned)a.nxp)
-        continue;
-      const int k = row * dx + 2 * pl;
-      const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
-      if (DET) {
+    if (DET) {
+      for (int i = threadIdx.x; i < npair; i += kBpThreads) {
+        const int row = (int)(((float)i + 0.5f) * inv_hx);
+        const int pl = i - row * hx;
+        const int zl = (int)(((float)row + 0.5f) * inv_dy);
+        const int yl = row - zl * dy;
+        const int gy = G.lo[1] + yl, gz = G.lo[2] + zl, gx = G.lo[0] + 2 * pl;
+        if ((unsigned)gy >= (unsigned)n.y || (unsigned)gz >= (unsigned)n.z || (unsigned)gx >= (unsigned)a.nxp)
+          continue;
+        const int k = row * dx + 2 * pl;
+        const bool two = 2 * pl + 1 < dx;  // odd pitch: the last pair has one tile cell
         // deterministic mode: exact int64 totals per voxel and quantity, hi and (lo 2^20 + lo2)
         // parts at the global scale, accumulated by integer reductions (order-independent)
         for (int h = 0; h < (two ? 2 : 1); ++h) {
@@ -979,28 +980,55 @@ __global__ void __launch_bounds__(kBpThreads, kBpCtasPerSm) k_lattice_bp(Lattice
           for (int qn = 0; qn < 4; ++qn)
             if (v[qn]) atomicAdd(d + qn, (unsigned long long)v[qn]);
         }
-        continue;
       }
-      const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
-      int al0 = 0, al1 = 0, cl0 = 0, cl1 = 0;
-      if (ex) {
-        al0 = T.al[k]; al1 = two ? T.al[k + 1] : 0;
-        cl0 = T.cl[k]; cl1 = two ? T.cl[k + 1] : 0;
-      }
-      if ((ah0 | ah1 | ch0 | ch1 | al0 | al1 | cl0 | cl1) == 0) continue;
-      float A0, A1, C0, C1;
-      if (ex) {
-        A0 = (float)(((double)ah0 + (double)al0 * ilo) * iA);
-        A1 = (float)(((double)ah1 + (double)al1 * ilo) * iA);
-        C0 = (float)(((double)ch0 + (double)cl0 * ilo) * iC);
-        C1 = (float)(((double)ch1 + (double)cl1 * ilo) * iC);
-      } else {
-        A0 = (float)ah0 * fA; A1 = (float)ah1 * fA;
-        C0 = (float)ch0 * fC; C1 = (float)ch1 * fC;
-      }
-      PVR_CHECK(gbase + (zl * n.y + yl) * a.nxp + 2 * pl + 1 < n.z * n.y * a.nxp + 2);
-      red_v4(AC + (gbase + (zl * n.y + yl) * a.nxp + 2 * pl), A0, C0, A1, C1);
+      continue;
     }
+    // (row, pl) of a thread's successive pairs advance by (kBpThreads / hx, kBpThreads % hx)
+    // with one carry; one loop per tile precision (CTA-uniform), the single-word one free of
+    // the lo words
+    const int dq = kBpThreads / hx, dr = kBpThreads - dq * hx;
+    const int row0 = (int)(((float)threadIdx.x + 0.5f) * inv_hx), pl0 = (int)threadIdx.x - row0 * hx;
+    auto flush_tile = [&](auto exact_words) {
+      constexpr bool EXW = decltype(exact_words)::value;
+      int row = row0, pl = pl0;
+      for (int i = threadIdx.x; i < npair; i += kBpThreads) {
+        const int r = row, q = pl;
+        pl += dr;
+        row += dq;
+        if (pl >= hx) {
+          pl -= hx;
+          ++row;
+        }
+        const int zl = (int)(((float)r + 0.5f) * inv_dy);
+        const int yl = r - zl * dy;
+        const int gy = G.lo[1] + yl, gz = G.lo[2] + zl, gx = G.lo[0] + 2 * q;
+        if ((unsigned)gy >= (unsigned)n.y || (unsigned)gz >= (unsigned)n.z || (unsigned)gx >= (unsigned)a.nxp)
+          continue;
+        const int k = r * dx + 2 * q;
+        const bool two = 2 * q + 1 < dx;  // odd pitch: the last pair has one tile cell
+        const int ah0 = T.ah[k], ah1 = two ? T.ah[k + 1] : 0, ch0 = T.ch[k], ch1 = two ? T.ch[k + 1] : 0;
+        float A0, A1, C0, C1;
+        if (EXW) {
+          const int al0 = T.al[k], al1 = two ? T.al[k + 1] : 0;
+          const int cl0 = T.cl[k], cl1 = two ? T.cl[k + 1] : 0;
+          if ((ah0 | ah1 | ch0 | ch1 | al0 | al1 | cl0 | cl1) == 0) continue;
+          A0 = (float)(((double)ah0 + (double)al0 * ilo) * iA);
+          A1 = (float)(((double)ah1 + (double)al1 * ilo) * iA);
+          C0 = (float)(((double)ch0 + (double)cl0 * ilo) * iC);
+          C1 = (float)(((double)ch1 + (double)cl1 * ilo) * iC);
+        } else {
+          if ((ah0 | ah1 | ch0 | ch1) == 0) continue;
+          A0 = (float)ah0 * fA; A1 = (float)ah1 * fA;
+          C0 = (float)ch0 * fC; C1 = (float)ch1 * fC;
+        }
+        PVR_CHECK(gbase + (zl * n.y + yl) * a.nxp + 2 * q + 1 < n.z * n.y * a.nxp + 2);
+        red_v4(AC + (gbase + (zl * n.y + yl) * a.nxp + 2 * q), A0, C0, A1, C1);
+      }
+    };
+    if (ex)
+      flush_tile(std::true_type{});
+    else
+      flush_tile(std::false_type{});
   }
 }
 
