@@ -19,15 +19,19 @@
 // group's voxel footprint of X is staged once in shared memory, zero outside the grid, so the
 // inner loop is 8 shared loads + 7 lerps with 32-bit addressing and no bounds logic (dropping
 // out-of-grid corners == reading zeros there). Coverage is the same pass over the grid's
-// indicator function.
+// indicator function, interpolated analytically (separable tents, no tile). The per-member
+// constants of both (and of the backprojection) are built once per geometry by k_fwd_table /
+// k_bp_table (one warp segment per group) and copied by each group's CTA.
 //
 // Backprojection: one CTA per group. Splats accumulate in a shared tile of the group's voxel
 // bounding box as int32 fixed point on a per-group grid (one word per quantity on a 2^-21
-// grid in the iterations; exact hi/lo word pairs, 2^-41, in the init pass) with native
-// ATOMS.ADD: fp32 shared atomics are CAS loops on sm_100a (5-10x slower under contention,
-// profiles/r01_ubench_atomics2.txt). Precision and thresholds: DESIGN.md §7. Each thread walks
-// a lattice line along c. The tile is flushed with
-// coalesced red.global.add.v4.f32 (voxel pairs), skipping cells outside the grid.
+// grid for interior groups; exact hi/lo word pairs, 2^-41, for groups that can reach the rim
+// of the coverage or carry 1/kappa-amplified terms, and in the init / rigidity passes) with
+// native ATOMS.ADD: fp32 shared atomics are CAS loops on sm_100a (5-10x slower under
+// contention, profiles/r01_ubench_atomics2.txt). Precision and thresholds: DESIGN.md §7. Each
+// thread walks a lattice line along its dominant axis with a two-plane register window. The
+// tile is flushed with coalesced red.global.add.v4.f32 (voxel pairs), skipping cells outside
+// the grid. Persistent CTAs claim groups dynamically (the next claim overlaps the splat).
 #include <cfloat>
 #include <cmath>
 #include <mutex>
