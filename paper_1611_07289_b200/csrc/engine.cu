@@ -641,7 +641,9 @@ void member_bbox(const MemberDev& m, const HostPatch& hp, const StackPsf& ps, co
 }
 
 int64_t r_bytes_of(const MemberDev& m, const StackPsf& ps) {
-  return (int64_t)(m.tu + 2 * ps.ru / ps.nu + 2) * (m.tv + 2 * ps.rv / ps.nv + 2) * 8;
+  // the member's feeding pixels (its tile and up to ru / nu + 1 around) and the R block's
+  // one-pixel zero border (lattice.cu k_bp_table)
+  return (int64_t)(m.tu + 2 * ps.ru / ps.nu + 4) * (m.tv + 2 * ps.rv / ps.nv + 4) * 8;
 }
 
 void build_natural(const pvr_ctx* c, const std::vector<int64_t>& which, int TU, int TV, int nseg, bool fwd,

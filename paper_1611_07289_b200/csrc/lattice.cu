@@ -669,7 +669,9 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
     M.inv_nUV3 = 1.0f / (float)M.nUV3;
     M.inv_nU = 1.0f / (float)M.nU;
     M.plu = o.plu; M.phu = o.phu; M.plv = o.plv; M.phv = o.phv;
-    M.rw = o.phu - o.plu + 1;
+    // R block of the member: its feeding pixels [plu, phu] x [plv, phv] with a zero border of
+    // one pixel, so the line gather reads its up to 4 taps without bounds tests
+    M.rw = o.phu - o.plu + 3;
     M.inv_rw = 1.0f / (float)M.rw;
     M.pixz = pt.pix0 + (int64_t)m.z * pt.sy * pt.sx;
     M.yz = pt.y0off + (int64_t)m.z * pt.HW;
@@ -681,7 +683,7 @@ __global__ void __launch_bounds__(kThreads) k_bp_table(LatticeArgs a, BpMember* 
 #else
     nl = M.nU * M.nV;
 #endif
-    np = M.rw * (o.phv - o.plv + 1);
+    np = M.rw * (o.phv - o.plv + 3);
   }
   // window bound: a flushed plane sums the terms of all samples whose floor along m is
   // m - 1 (<= ceil(1 / qm) of them, qm = the step along m >= |qc| / sqrt 3) and of one at
@@ -838,9 +840,14 @@ __global__ void __launch_bounds__(kBpThreads, kBpCtasPerSm) k_lattice_bp(Lattice
         const BpMember& M = sbm[mi];
         const int li = i - M.pbeg;
         const int vv = (int)(((float)li + 0.5f) * M.inv_rw);
-        const int u = M.plu + (li - vv * M.rw), v = M.plv + vv;
-        const int64_t j = M.pixz + (int64_t)v * M.sx + u;
+        const int uu = li - vv * M.rw;
+        const int u = M.plu - 1 + uu, v = M.plv - 1 + vv;
         float rA = 0.0f, rC = 0.0f;
+        if (u < M.plu || u > M.phu || v < M.plv || v > M.phv) {  // the zero border
+          R[i] = make_float2(0.0f, 0.0f);
+          continue;
+        }
+        const int64_t j = M.pixz + (int64_t)v * M.sx + u;
         // every load is issued before the observed test (one round trip, not two): the
         // patch weight w (1 in the init / rigidity passes; rigidity: vs = the patch score pbar)
         const float wm = init == 1 ? 1.0f : w[M.patch];
@@ -918,21 +925,25 @@ __global__ void __launch_bounds__(kBpThreads, kBpCtasPerSm) k_lattice_bp(Lattice
         // that is within [-ru, ru]); same along V. U >= -ru > -nu: the float floor is exact.
         const int ub = __float2int_rd(((float)U + 0.5f) * inv_nu), ra = U - ub * H.nu;
         const int vb = __float2int_rd(((float)V + 0.5f) * inv_nv), rb = V - vb * H.nv;
-        float LA = 0.0f, LC = 0.0f;
-#pragma unroll
-        for (int jb = 0; jb < 2; ++jb) {
-          const int b = jb ? rb - H.nv : rb, v = vb + jb;
-          if (b < -H.rv || b > H.rv || v < M.plv || v > M.phv) continue;
-#pragma unroll
-          for (int ja = 0; ja < 2; ++ja) {
-            const int aa = ja ? ra - H.nu : ra, u = ub + ja;
-            if (aa < -H.ru || aa > H.ru || u < M.plu || u > M.phu) continue;
-            const float wt = s_ip[(b + H.rv) * w2 + (aa + H.ru)];
-            const float2 rr = R[M.pbeg + (v - M.plv) * M.rw + (u - M.plu)];
-            LA += wt * rr.x;
-            LC += wt * rr.y;
-          }
-        }
+        // taps (ja, jb): a = ra - ja nu, b = rb - jb nv at pixel (ub + ja, vb + jb); with
+        // ru = nu - 1 (engine.cu build_psf) a = ra is always in [-ru, ru] and a = ra - nu is
+        // iff ra > 0; pixels outside [plu, phu] x [plv, phv] read the R block's zero border.
+        // Summed in the order of the tap loop (jb, then ja).
+        const bool a1 = ra > 0, b1 = rb > 0;
+        const float* ipr = s_ip + (rb + H.rv) * w2 + (ra + H.ru);
+        const float w00 = ipr[0];
+        const float w10 = a1 ? ipr[-H.nu] : 0.0f;
+        const float w01 = b1 ? ipr[-H.nv * w2] : 0.0f;
+        const float w11 = (a1 && b1) ? ipr[-H.nv * w2 - H.nu] : 0.0f;
+        const float2* rp0 = R + M.pbeg + (vb - M.plv + 1) * M.rw + (ub - M.plu + 1);
+        const float2 r00 = rp0[0], r10 = rp0[1], r01 = rp0[M.rw], r11 = rp0[M.rw + 1];
+        float LA = w00 * r00.x, LC = w00 * r00.y;
+        LA += w10 * r10.x;
+        LC += w10 * r10.y;
+        LA += w01 * r01.x;
+        LC += w01 * r01.y;
+        LA += w11 * r11.x;
+        LC += w11 * r11.y;
         if (LA == 0.0f && LC == 0.0f) continue;
         LA *= scA;
         LC *= scC;
