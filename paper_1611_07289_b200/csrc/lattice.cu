@@ -336,9 +336,18 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
       if (skip) {
         s = 1.0f;  // every sample fully in the grid: kappa = sum psi = 1 (reading Q27)
       } else {
-        for (int b = 0; b <= 2 * H.rv; ++b) {
-          const float* row = sT + f.t0 + (H.nv * dv + b) * f.LU + H.nu * du;
-          for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
+        if (H.ru == 1 && H.rv == 1) {  // n_u = n_v = 2 (every stack of c1-c5 at q = 1): 3 x 3 taps unrolled
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const float* row = sT + f.t0 + (H.nv * dv + b) * f.LU + H.nu * du;
+#pragma unroll
+            for (int aa = 0; aa < 3; ++aa) s += s_ip[b * 3 + aa] * row[aa];
+          }
+        } else {
+          for (int b = 0; b <= 2 * H.rv; ++b) {
+            const float* row = sT + f.t0 + (H.nv * dv + b) * f.LU + H.nu * du;
+            for (int aa = 0; aa < w2; ++aa) s += s_ip[b * w2 + aa] * row[aa];
+          }
         }
       }
       const PatchDev& pt = a.P[f.patch];
