@@ -97,6 +97,7 @@ constexpr int kMaxMembers = 16;
 #define PVR_FWD_UNROLL 4
 #endif
 constexpr int kFwdUnroll = PVR_FWD_UNROLL;  // samples per iteration of the forward's c loop
+constexpr int kFwdNtpFixed = 15;            // through-plane samples of the unrolled forward path
 
 // Per-member constants of the forward / coverage, in global memory (k_fwd_table: once per
 // geometry) and copied into shared memory by each group's CTA.
@@ -220,6 +221,9 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
     const int ntp = 2 * H.cmax + 1;
     // lattice points of all members: T(U, V) = sum_c tp(c) trilerp(X, x(U, V, c))
     const bool skip = MODE == 1 && G.interior;
+    float tpr[kFwdNtpFixed];  // the group's tp values when ntp == kFwdNtpFixed (forward)
+#pragma unroll
+    for (int c = 0; c < kFwdNtpFixed; ++c) tpr[c] = MODE == 0 ? s_tpc[c].x : 0.0f;
     int k = 0;  // the member of lattice point / pixel i (i only grows)
     for (int i = skip ? H.nt : threadIdx.x; i < H.nt; i += kThreads) {
       while (k + 1 < G.nm && i >= sm[k + 1].t0) ++k;
@@ -293,11 +297,10 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         continue;
       }
       const float* sXo = sX + f.ob[2] * dxy + f.ob[1] * dx + f.ob[0];
-#pragma unroll kFwdUnroll
-      for (int k = 0; k < ntp; ++k) {
-        const float2 q = tpc[k];
-        const f2 rxy = fma2s(q.y, qcxy, rxy0);
-        const float rzc = fmaf(q.y, qcz, rz);
+      // one sample at lattice step cq (tp value tpk) added to acc
+      auto sample = [&](float tpk, float cq, float acc_in) -> float {
+        const f2 rxy = fma2s(cq, qcxy, rxy0);
+        const float rzc = fmaf(cq, qcz, rz);
         const f2 txy = add2_rd(rxy, mag);
         const float tz = __fadd_rd(rzc, kMagic);
         const int ix = __float_as_int(lo2(txy)) - kMagicBits;
@@ -314,7 +317,19 @@ __global__ void __launch_bounds__(kThreads) k_lattice_fwd(LatticeArgs a, int t_f
         const f2 cy1 = fma2s(fx, sub2(x11, x01), x01);   // at y1
         const f2 cz = fma2s(fy, sub2(cy1, cy0), cy0);    // y-lerp: (z0, z1)
         const float c0 = lo2(cz), c1 = hi2(cz);
-        acc = fmaf(q.x, fmaf(fz, c1 - c0, c0), acc);
+        return fmaf(tpk, fmaf(fz, c1 - c0, c0), acc_in);
+      };
+      if (ntp == kFwdNtpFixed && !f.skew) {
+        // the common slice profile (c1-c5 at q = 1: 15 samples): fully unrolled, tp from
+        // registers instead of one shared load per sample
+#pragma unroll
+        for (int k = 0; k < kFwdNtpFixed; ++k) acc = sample(tpr[k], (float)k, acc);
+      } else {
+#pragma unroll kFwdUnroll
+        for (int k = 0; k < ntp; ++k) {
+          const float2 q = tpc[k];
+          acc = sample(q.x, q.y, acc);
+        }
       }
       sT[f.t0 + iv * f.LU + iu] = acc;
     }
